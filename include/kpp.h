@@ -1,0 +1,164 @@
+/*
+ * kpp.h -- C ABI of the B200-native Kaczmarz++ / CD++ hot path
+ * (Derezinski, Needell, Rebrova, Yang, arXiv 2501.11673; "the paper").
+ *
+ * Citations: P:n = line n of the paper's LaTeX source.
+ *
+ * Problem statement: solve a consistent system
+ * A x = b.  Kaczmarz++ takes a general m x n matrix (min-norm solution when
+ * under-determined); CD++ takes a symmetric positive semidefinite n x n matrix.
+ *
+ * Each kpp_solve runs, per block iteration t (Alg 5 P:1332-1360 with Proj replaced
+ * by the exact factor; Alg 3 P:740-770 for CD++):
+ *   1. block selection with online memoization
+ *   2. on a block's first visit ("Phase 1"): its memoized factor
+ *   3. r = A_S x - b_S
+ *   4. w = A_S^T (A_S A_S^T + lam I)^{-1} r   [K++, Eq (bk) P:94-102]
+ *      w = I_S^T (A_SS + lam I)^{-1} r        [CD++, Alg 3 l.11 P:756-757]
+ *   5. m <- (1-rho)/(1+rho) (m - w);  x <- x - w + eta m   (Eq (momentum))
+ *   6. residual-window estimate, stopping test E1 <= tol^2 ||b||^2, adaptive rho
+ *      (Eq (residual), Eq (weighted)).
+ * No RHT preprocessing (the inputs are assumed incoherent).
+ *
+ * Conventions
+ *  - All floating point is IEEE fp64.  Matrices are row-major with leading dimension
+ *    lda >= n (elements).  Index sets are int32, 0-based, sorted ascending.
+ *  - Memory: A is a DEVICE pointer on the current CUDA device and is BORROWED: it is
+ *    not copied, must outlive the context and must not change while it is in use.
+ *    b, x0, x_out may be DEVICE or HOST pointers (detected with
+ *    cudaPointerGetAttributes; host buffers are staged through the context's stream,
+ *    so a call with host buffers includes the host<->device copies).
+ *    res_hist and all introspection outputs are HOST pointers.
+ *  - Ownership: the caller owns every buffer it passes.  The context owns its
+ *    factor cache (memoized blocks), schedule, work vectors and NCCL communicator.
+ *  - Errors: status codes only; nothing is thrown across the ABI and nothing exits.
+ *    On KPP_EINVAL the outputs are untouched.  kpp_last_error() describes the last
+ *    failure of a context.  A context is not thread-safe; distinct contexts are.
+ *  - Determinism: identical (A, b, x0, s, lam, seed, options, device count) give
+ *    bit-identical x and history (no floating-point atomics anywhere).
+ *  - The memo cache persists across kpp_solve calls on one context: the k-th fresh
+ *    block is a function of (seed, k) only, so a later solve reuses earlier factors.
+ */
+#ifndef KPP_H
+#define KPP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kpp_ctx kpp_ctx; /* opaque; one per (A, s, lam, seed[, communicator]) */
+
+typedef enum {
+  KPP_OK = 0,
+  KPP_EINVAL = 1,    /* invalid argument (outputs untouched) */
+  KPP_ENOMEM = 2,    /* device or host allocation failed */
+  KPP_ECUDA = 3,     /* CUDA runtime error (see kpp_last_error) */
+  KPP_ENCCL = 4,     /* NCCL error */
+  KPP_ENOTPD = 5,    /* non-positive pivot in chol(A_S A_S^T + lam I) / chol(A_SS + lam I) */
+  KPP_EDIVERGED = 6, /* non-finite block residual */
+  KPP_EMAXITER = 7   /* informational: max_iters reached before the tolerance; x_out written */
+} kpp_status;
+
+/* Options for kpp_set_option (value is a double; integers are passed as doubles). */
+typedef enum {
+  KPP_OPT_ACCEL = 1,      /* 1 (default): eta = s/(2n); 0: eta = 0, plain block Kaczmarz */
+  KPP_OPT_MEMO = 2,       /* 1 (default): online memoization; 0: a fresh block every iteration */
+  KPP_OPT_ETA = 3,        /* < 0 (default): s/(2n); otherwise the momentum step eta */
+  KPP_OPT_RHO_FIXED = 4,  /* < 0 (default): adaptive rho; >= 0: fixed rho, never updated */
+  KPP_OPT_FACTOR = 5,     /* K++ factor route: 0 (default) shifted CholeskyQR2 of [A_S, sqrt(lam) I];
+                             1 literal Gram + Cholesky -- same R in exact arithmetic */
+  KPP_OPT_WINDOW = 6,     /* iterations per device window (default 8192; rounded to >= 1) */
+  KPP_OPT_PHASE1_MB = 7,  /* device workspace budget for a Phase-1 batch, MiB (default 4096) */
+  KPP_OPT_RESIDENT = 8    /* 1 (default): keep the block slab on chip across both passes when it
+                             fits; 0: always stream A_S from HBM/L2 */
+} kpp_option;
+
+/* ---- setup ------------------------------------------------------------------ */
+/* Kaczmarz++ context for general A (m x n).  1 <= block_size <= m, lambda >= 0.
+   No device work beyond allocation is done here. */
+kpp_status kpp_setup(kpp_ctx** out, const double* A, int64_t m, int64_t n, int64_t lda,
+                     int32_t block_size, double lambda, uint64_t seed);
+/* CD++ context for symmetric PSD A (n x n).  1 <= block_size <= n, lambda >= 0.
+   A must be exactly symmetric (A_SS is read from the stored rows). */
+kpp_status cdpp_setup(kpp_ctx** out, const double* A, int64_t n, int64_t lda,
+                      int32_t block_size, double lambda, uint64_t seed);
+
+/* ---- solve ------------------------------------------------------------------ */
+/* One solve.  b: m values (n for CD++).  x0: n values or NULL (= 0).  max_iters >= 0.
+   tol >= 0: stop at the first checkpoint with E1 <= tol^2 ||b||^2 (0 = run max_iters
+   unless the estimate is exactly zero).  x_out: n values.  res_hist (HOST, may be
+   NULL): per-checkpoint sqrt(E1/||b||^2), at most hist_cap entries; n_hist (may be
+   NULL) receives the number of checkpoints; iters_out (may be NULL) receives the
+   number of block iterations performed.
+   Returns KPP_OK (tolerance met), KPP_EMAXITER, or an error. */
+kpp_status kpp_solve(kpp_ctx* ctx, const double* b, const double* x0, int64_t max_iters, double tol,
+                     double* x_out, double* res_hist, int64_t hist_cap, int64_t* n_hist,
+                     int64_t* iters_out);
+/* Same entry point for CD++ contexts (kpp_solve accepts both kinds). */
+kpp_status cdpp_solve(kpp_ctx* ctx, const double* b, const double* x0, int64_t max_iters, double tol,
+                      double* x_out, double* res_hist, int64_t hist_cap, int64_t* n_hist,
+                      int64_t* iters_out);
+
+void kpp_destroy(kpp_ctx* ctx);
+const char* kpp_status_str(kpp_status s);
+const char* kpp_last_error(const kpp_ctx* ctx); /* owned by ctx; "" if none */
+
+/* Run the context's work on this cudaStream_t (default: the legacy default stream). */
+kpp_status kpp_set_stream(kpp_ctx* ctx, void* cuda_stream);
+kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double value);
+
+/* ---- introspection (parity tests, benchmarks) ------------------------------- */
+/* Schedule for t in [t0, t0+count): block id (fresh blocks numbered in creation
+   order) and fresh flag.  Computed on the device; HOST outputs. */
+kpp_status kpp_get_schedule(kpp_ctx* ctx, int64_t t0, int64_t count, int32_t* block_id,
+                            uint8_t* is_fresh);
+/* Index set of memoized block `block_id` (HOST, s ints).  The block must already exist
+   (created by a solve or by kpp_get_schedule/kpp_prepare). */
+kpp_status kpp_get_block(kpp_ctx* ctx, int64_t block_id, int32_t* S_out);
+/* Memoized projection operator of block `block_id`: M = (A_S A_S^T + lam I)^{-1}
+   (K++) or (A_SS + lam I)^{-1} (CD++), s x s row-major, HOST output.  Requires the
+   factor to exist (run kpp_prepare or a solve first). */
+kpp_status kpp_get_factor(kpp_ctx* ctx, int64_t block_id, double* M_out);
+/* Generate and factor (Phase 1) every fresh block needed by iterations [0, iters). */
+kpp_status kpp_prepare(kpp_ctx* ctx, int64_t iters);
+/* Rho history of the last solve (HOST, per checkpoint, the rho in force after it). */
+kpp_status kpp_get_rho_history(kpp_ctx* ctx, double* rho_hist, int64_t cap, int64_t* n);
+
+typedef struct {
+  double phase1_ms;      /* device time in schedule + block generation + factorisation */
+  double phase2_ms;      /* device time in the iteration kernel */
+  double iter_kernel_ms; /* same as phase2_ms, summed over the iteration-kernel launches */
+  int64_t n_blocks;      /* memoized blocks held by the context */
+  int64_t n_fresh_last;  /* blocks factored during the last solve */
+  int64_t iter_launches; /* iteration-kernel launches during the last solve */
+  int64_t kernel_launches; /* all kernel launches during the last solve */
+  int32_t grid_ctas;     /* CTAs of the persistent iteration kernel */
+  int32_t resident;      /* 1 if the last solve kept the block slab on chip */
+} kpp_stats;
+kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
+/* Reset the timing counters of kpp_get_stats. */
+kpp_status kpp_reset_stats(kpp_ctx* ctx);
+
+/* ---- column-sharded multi-GPU (one process per GPU) ------------------------- */
+/* 128-byte NCCL unique id; rank 0 creates it, the harness broadcasts it through its
+   own process group (torch.distributed), every rank passes it to *_setup_dist. */
+kpp_status kpp_get_unique_id(uint8_t id[128]);
+/* A_slab = A[:, col_begin:col_end] (m x (col_end-col_begin), row-major, lda >= width)
+   on this rank's device.  b is full and replicated; x0 / x_out are the local slab. */
+kpp_status kpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t m, int64_t n_global,
+                          int64_t col_begin, int64_t col_end, int64_t lda, int32_t block_size,
+                          double lambda, uint64_t seed, const uint8_t id[128], int32_t rank,
+                          int32_t nranks);
+kpp_status cdpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t n, int64_t col_begin,
+                           int64_t col_end, int64_t lda, int32_t block_size, double lambda,
+                           uint64_t seed, const uint8_t id[128], int32_t rank, int32_t nranks);
+
+/* Library version string. */
+const char* kpp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KPP_H */
