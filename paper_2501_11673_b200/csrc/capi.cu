@@ -1,0 +1,783 @@
+// capi.cu -- host runtime behind include/kpp.h.
+//
+// Owns a context per (A, s, lambda, seed[, communicator]): the memo cache of blocks
+// (index sets S_k and projection operators M_k), the schedule buffers, the work vectors
+// and the NCCL communicator.  A solve walks the iterations in windows:
+//   1. schedule kernels for the window (row 1)                        [schedule.cu]
+//   2. fresh-block generation + Phase-1 factorisation of the new blocks [schedule.cu,
+//      gemm.cu, factor.cu], batched under a workspace budget
+//   3. Phase 2 for the window: one cooperative persistent launch        [iterate.cu]
+//      or (multi-GPU / engine=graph) a replayed CUDA graph of step kernels with an
+//      NCCL allreduce per iteration                                     [steps.cu]
+//   4. read back the replicated state (stop flag) -- one small D2H per window.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/kpp.h"
+#include "kpp_internal.h"
+
+using namespace kpp;
+
+namespace {
+
+enum { KIND_KPP = 0, KIND_CDPP = 1 };
+enum { OPT_ENGINE = 9 };  // private: 0 persistent (default on 1 GPU), 1 graph
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct kpp_ctx {
+  int kind = KIND_KPP;
+  const double* A = nullptr;
+  long long m = 0, n = 0, lda = 0;   // local columns n (== n_global on one GPU)
+  long long n_global = 0, col_begin = 0, col_end = 0;
+  int s = 0;
+  double lam = 0.0;
+  uint64_t seed = 0;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  // options
+  int accel = 1, memo = 1, factor = 0, resident_opt = 1, engine = 0;
+  double eta_opt = -1.0, rho_fixed = -1.0;
+  long long window = 8192, phase1_mb = 4096;
+  cudaStream_t stream = nullptr;
+  int device = 0, num_sms = 0;
+  // derived
+  double C = 0.0;
+  long long zeta = 1;
+  long long pop = 0;
+  // memo cache
+  int32_t* S_pool = nullptr;
+  double* M_pool = nullptr;
+  long long pool_cap = 0, nb_gen = 0, nb_ready = 0;
+  // schedule workspace
+  uint32_t* word1 = nullptr;
+  uint8_t* fresh = nullptr;
+  int32_t* bid = nullptr;
+  long long sched_cap = 0;
+  // state / work
+  DevState* dstate = nullptr;
+  DevStep* dstep = nullptr;
+  long long* d_nb = nullptr;
+  double *x = nullptr, *mom = nullptr, *part = nullptr, *r = nullptr, *y = nullptr, *d_bb = nullptr,
+         *bstage = nullptr;
+  unsigned int* bar = nullptr;
+  double *hist_res = nullptr, *hist_rho = nullptr;
+  long long hist_capd = 0;
+  int grid = 0, slab = 0;
+  // phase-1 workspace
+  Buf p1;
+  int* d_info = nullptr;
+  long long info_cap = 0;
+  // graph engine
+  cudaGraphExec_t gexec = nullptr;
+  int graph_unroll = 0;
+  const void* gkey[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double gkeyv[3] = {0, 0, 0};
+  // events / stats
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  kpp_stats stats{};
+  std::vector<double> rho_hist;
+  std::string err;
+};
+
+namespace {
+
+kpp_status fail(kpp_ctx* c, kpp_status s, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return s;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? KPP_ENOMEM : KPP_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+
+#define CKN(call)                                                                             \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess)                                                                    \
+      return fail(ctx, KPP_ENCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
+  } while (0)
+
+#define CKS(call)                       \
+  do {                                  \
+    kpp_status s_ = (call);             \
+    if (s_ != KPP_OK) return s_;        \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+kpp_status dalloc(kpp_ctx* ctx, T** p, size_t count) {
+  if (*p) {
+    cudaFree(*p);
+    *p = nullptr;
+  }
+  if (count == 0) count = 1;
+  CK(cudaMalloc((void**)p, count * sizeof(T)));
+  return KPP_OK;
+}
+
+kpp_status ensure_buf(kpp_ctx* ctx, Buf& b, size_t bytes) {
+  if (b.bytes >= bytes) return KPP_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  CK(cudaMalloc(&b.p, bytes));
+  b.bytes = bytes;
+  return KPP_OK;
+}
+
+// Grow the memo pools to hold at least `need` blocks (contents preserved).
+kpp_status ensure_pool(kpp_ctx* ctx, long long need) {
+  if (need <= ctx->pool_cap) return KPP_OK;
+  long long cap = std::max<long long>(need, std::max<long long>(64, ctx->pool_cap * 2));
+  const size_t s = (size_t)ctx->s;
+  int32_t* S2 = nullptr;
+  double* M2 = nullptr;
+  CK(cudaMalloc((void**)&S2, (size_t)cap * s * sizeof(int32_t)));
+  cudaError_t e = cudaMalloc((void**)&M2, (size_t)cap * s * s * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaFree(S2);
+    cudaGetLastError();
+    // fall back to the exact need
+    cap = need;
+    CK(cudaMalloc((void**)&S2, (size_t)cap * s * sizeof(int32_t)));
+    CK(cudaMalloc((void**)&M2, (size_t)cap * s * s * sizeof(double)));
+  }
+  if (ctx->pool_cap > 0) {
+    CK(cudaMemcpyAsync(S2, ctx->S_pool, (size_t)ctx->nb_gen * s * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(M2, ctx->M_pool, (size_t)ctx->nb_ready * s * s * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->S_pool);
+    cudaFree(ctx->M_pool);
+  }
+  ctx->S_pool = S2;
+  ctx->M_pool = M2;
+  ctx->pool_cap = cap;
+  return KPP_OK;
+}
+
+kpp_status ensure_sched(kpp_ctx* ctx, long long count) {
+  if (count <= ctx->sched_cap) return KPP_OK;
+  CKS(dalloc(ctx, &ctx->word1, (size_t)count));
+  CKS(dalloc(ctx, &ctx->fresh, (size_t)count));
+  CKS(dalloc(ctx, &ctx->bid, (size_t)count));
+  ctx->sched_cap = count;
+  return KPP_OK;
+}
+
+kpp_status allreduce(kpp_ctx* ctx, double* buf, size_t count) {
+  if (ctx->nranks <= 1 && !ctx->comm) return KPP_OK;
+  CKN(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  return KPP_OK;
+}
+
+// ------------------------------------------------------------------ Phase 1
+// Factor blocks [k0, k1) (their index sets are in S_pool) into M_pool.
+kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
+  const int s = ctx->s;
+  const long long ss = (long long)s * s;
+  const long long n = ctx->n;
+  cudaStream_t st = ctx->stream;
+  const int32_t* S = ctx->S_pool + k0 * s;
+  double* Mout = ctx->M_pool + k0 * ss;
+  if ((long long)B > ctx->info_cap) {
+    CKS(dalloc(ctx, &ctx->d_info, (size_t)B));
+    ctx->info_cap = B;
+  }
+  // workspace carve-up
+  const int T = (s + 63) / 64;
+  const int tiles_up = T * (T + 1) / 2;
+  int Z = 1;
+  if (ctx->kind == KIND_KPP) {
+    const long long target = 4LL * ctx->num_sms;
+    Z = (int)std::max<long long>(1, (target + (long long)B * tiles_up - 1) / ((long long)B * tiles_up));
+    Z = (int)std::min<long long>(Z, std::max<long long>(1, n / 256));
+    Z = std::min(Z, 64);
+  }
+  const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor == 0;
+  size_t off = 0;
+  auto carve = [&](size_t count) {
+    size_t o = off;
+    off += ((count * sizeof(double) + 255) / 256) * 256;
+    return o;
+  };
+  const size_t o_part = carve((size_t)B * Z * ss);
+  const size_t o_G = carve((size_t)B * ss);
+  const size_t o_X1 = carve((size_t)B * ss);
+  const size_t o_L = cqr2 ? carve((size_t)B * ss) : 0;
+  const size_t o_X2 = cqr2 ? carve((size_t)B * ss) : 0;
+  const size_t o_X = cqr2 ? carve((size_t)B * ss) : 0;
+  const size_t o_Q = cqr2 ? carve((size_t)B * s * n) : 0;
+  CKS(ensure_buf(ctx, ctx->p1, off));
+  char* base = (char*)ctx->p1.p;
+  double* part = (double*)(base + o_part);
+  double* G = (double*)(base + o_G);
+  double* X1 = (double*)(base + o_X1);
+
+  if (ctx->kind == KIND_CDPP) {
+    // G = A_SS + lam I (Alg 3 l.8); multi-GPU: disjoint column supports summed exactly
+    launch_gather_principal(st, B, ctx->A, ctx->lda, S, s, ctx->nranks > 1 ? 0.0 : ctx->lam,
+                            ctx->col_begin, ctx->col_end, G);
+    if (ctx->nranks > 1) {
+      CKS(allreduce(ctx, G, (size_t)B * ss));
+      launch_add_diag(st, B, G, s, ctx->lam);
+    }
+    launch_chol_trtri(st, B, G, X1, s, ctx->d_info);
+    Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
+    launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0);  // M = X X^T
+  } else {
+    // G1 = A_S A_S^T (+ lam I): NT GEMM with row gathers on both operands, split-K
+    Operand a{ctx->A, ctx->lda, 0, S, s, 0}, b{ctx->A, ctx->lda, 0, S, s, 1};
+    const int z1 = launch_dgemm(st, B, s, s, (int)n, a, b, part, s, ss, Z, 1);
+    const bool dist = ctx->nranks > 1;
+    launch_splitk_reduce(st, B, s, s, z1, part, ss, dist ? 0.0 : ctx->lam, nullptr, 0.0, 0, G, ss, 1);
+    if (dist) {
+      CKS(allreduce(ctx, G, (size_t)B * ss));
+      launch_add_diag(st, B, G, s, ctx->lam);
+    }
+    launch_chol_trtri(st, B, G, X1, s, ctx->d_info);  // R1, X1 = R1^{-1}
+    if (!cqr2) {
+      Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
+      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0);
+    } else {
+      // shifted CholeskyQR2 of A_aug = [A_S, sqrt(lam) I]:
+      //   Q1 = R1^{-T} A_aug,  G2 = Q1 Q1^T = X1^T A_S A_S^T X1 + lam X1^T X1  (Q1 formed explicitly)
+      double* L = (double*)(base + o_L);
+      double* X2 = (double*)(base + o_X2);
+      double* X = (double*)(base + o_X);
+      double* Q = (double*)(base + o_Q);
+      Operand x1t{X1, s, ss, nullptr, 0, 1}, as{ctx->A, ctx->lda, 0, S, s, 0};
+      launch_dgemm(st, B, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0);  // Q1 = X1^T A_S
+      Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
+      const int z2 = launch_dgemm(st, B, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
+      Operand x1n{X1, s, ss, nullptr, 0, 0};
+      launch_dgemm(st, B, s, s, s, x1t, x1n, L, s, ss, 1, 0);  // X1^T X1
+      const double lscale = (dist && ctx->rank != 0) ? 0.0 : ctx->lam;
+      launch_splitk_reduce(st, B, s, s, z2, part, ss, 0.0, L, lscale, ss, G, ss, 1);
+      if (dist) CKS(allreduce(ctx, G, (size_t)B * ss));
+      launch_chol_trtri(st, B, G, X2, s, ctx->d_info + 0);  // R2, X2 = R2^{-1}
+      Operand x1a{X1, s, ss, nullptr, 0, 0}, x2b{X2, s, ss, nullptr, 0, 0};
+      launch_dgemm(st, B, s, s, s, x1a, x2b, X, s, ss, 1, 0);  // X = R^{-1} = X1 X2
+      Operand xa{X, s, ss, nullptr, 0, 0}, xb{X, s, ss, nullptr, 0, 1};
+      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0);  // M = X X^T
+    }
+  }
+  CK(cudaGetLastError());
+  std::vector<int> info((size_t)B);
+  CK(cudaMemcpyAsync(info.data(), ctx->d_info, (size_t)B * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int i = 0; i < B; ++i)
+    if (info[(size_t)i])
+      return fail(ctx, KPP_ENOTPD, "non-positive pivot %d in block %lld", info[(size_t)i] - 1, k0 + i);
+  ctx->stats.n_fresh_last += B;
+  return KPP_OK;
+}
+
+kpp_status phase1(kpp_ctx* ctx, long long k0, long long k1) {
+  const long long s = ctx->s, n = ctx->n;
+  const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor == 0;
+  const long long per_block = (long long)sizeof(double) *
+                              ((cqr2 ? 70 : 66) * s * s + (cqr2 ? s * n : 0));
+  long long Bmax = std::max<long long>(1, ctx->phase1_mb * (1LL << 20) / per_block);
+  Bmax = std::min<long long>(Bmax, 4096);
+  for (long long k = k0; k < k1; k += Bmax) {
+    const int B = (int)std::min(Bmax, k1 - k);
+    CKS(phase1_batch(ctx, k, B));
+  }
+  return KPP_OK;
+}
+
+// Schedule for [t0, t0+count) (needs d_nb = fresh count before t0); generates and factors
+// the new blocks.  On return bid[0..count) is valid and every referenced block is ready.
+kpp_status schedule_and_prepare(kpp_ctx* ctx, long long t0, long long count, bool factor) {
+  cudaStream_t st = ctx->stream;
+  CKS(ensure_sched(ctx, count));
+  launch_schedule(st, ctx->seed, ctx->C, ctx->memo, t0, (int)count, ctx->d_nb, ctx->word1, ctx->fresh, ctx->bid);
+  CK(cudaGetLastError());
+  long long nb = 0;
+  CK(cudaMemcpyAsync(&nb, ctx->d_nb, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (nb > ctx->nb_gen) {
+    CKS(ensure_pool(ctx, nb));
+    launch_fresh_blocks(st, ctx->seed, ctx->pop, ctx->s, ctx->nb_gen, nb, ctx->S_pool);
+    CK(cudaGetLastError());
+    ctx->nb_gen = nb;
+  }
+  if (factor && nb > ctx->nb_ready) {
+    CKS(phase1(ctx, ctx->nb_ready, nb));
+    ctx->nb_ready = nb;
+  }
+  return KPP_OK;
+}
+
+kpp_status setup_common(kpp_ctx* ctx) {
+  CK(cudaGetDevice(&ctx->device));
+  CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  ctx->pop = ctx->kind == KIND_CDPP ? ctx->n_global : ctx->m;
+  // Bernoulli constants as printed (reading Q5): K++ (min(m,n)/s) ln m; CD++ (n/s) ln n
+  if (ctx->kind == KIND_KPP)
+    ctx->C = ((double)std::min(ctx->m, ctx->n_global) / (double)ctx->s) * std::log((double)ctx->m);
+  else
+    ctx->C = ((double)ctx->n_global / (double)ctx->s) * std::log((double)ctx->n_global);
+  ctx->zeta = (ctx->pop + ctx->s - 1) / ctx->s;  // zeta = ceil(m/s) or ceil(n/s)
+  CKS(dalloc(ctx, &ctx->dstate, 1));
+  CKS(dalloc(ctx, &ctx->dstep, 1));
+  CKS(dalloc(ctx, &ctx->d_nb, 1));
+  CKS(dalloc(ctx, &ctx->x, (size_t)ctx->n));
+  CKS(dalloc(ctx, &ctx->mom, (size_t)ctx->n));
+  CKS(dalloc(ctx, &ctx->r, (size_t)ctx->s));
+  CKS(dalloc(ctx, &ctx->y, (size_t)ctx->s));
+  CKS(dalloc(ctx, &ctx->d_bb, 1));
+  CKS(dalloc(ctx, &ctx->bar, 1));
+  CKS(dalloc(ctx, &ctx->bstage, (size_t)ctx->m));
+  // persistent grid: one CTA per SM; slab = ceil(n / grid) rounded up to 4 columns
+  const size_t smem = iterate_smem_bytes(ctx->s, 0, 0);
+  ctx->grid = iterate_max_grid(ctx->device, smem);
+  if (ctx->grid <= 0) ctx->grid = ctx->num_sms;
+  long long slab = (ctx->n + ctx->grid - 1) / ctx->grid;
+  slab = (slab + 3) / 4 * 4;
+  if (slab < 4) slab = 4;
+  ctx->slab = (int)slab;
+  CKS(dalloc(ctx, &ctx->part, (size_t)ctx->grid * ctx->s));
+  CK(cudaEventCreate(&ctx->ev0));
+  CK(cudaEventCreate(&ctx->ev1));
+  ctx->stats.grid_ctas = ctx->grid;
+  return KPP_OK;
+}
+
+kpp_status validate_and_create(kpp_ctx** out, int kind, const double* A, long long m, long long n,
+                               long long nloc, long long lda, int s, double lam) {
+  if (!out) return KPP_EINVAL;
+  *out = nullptr;
+  const long long pop = kind == KIND_CDPP ? n : m;
+  if (!A || m < 1 || n < 1 || nloc < 1 || lda < nloc || s < 1 || s > pop || s > 1024 ||
+      !(lam >= 0.0) || !std::isfinite(lam))
+    return KPP_EINVAL;
+  if (!is_device_ptr(A)) return KPP_EINVAL;
+  return KPP_OK;
+}
+
+// Graph engine: (re)capture U iterations of step kernels (+ NCCL allreduce) once.
+kpp_status build_graph(kpp_ctx* ctx, const StepParams& sp, int U) {
+  if (ctx->gexec && ctx->graph_unroll == U) return KPP_OK;
+  if (ctx->gexec) {
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  cudaStream_t cs;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaStream_t saved = ctx->stream;
+  ctx->stream = cs;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  for (int u = 0; u < U; ++u) {
+    launch_step_partial(cs, sp);
+    launch_step_reduce(cs, sp);
+    if (ctx->comm) {
+      ncclResult_t rr = ncclAllReduce(sp.rsum, sp.rsum, (size_t)ctx->s, ncclDouble, ncclSum, ctx->comm, cs);
+      if (rr != ncclSuccess) {
+        cudaStreamEndCapture(cs, &g);
+        ctx->stream = saved;
+        return fail(ctx, KPP_ENCCL, "ncclAllReduce capture: %s", ncclGetErrorString(rr));
+      }
+    }
+    launch_step_solve(cs, sp);
+    launch_step_update(cs, sp);
+    launch_step_window(cs, sp);
+  }
+  CK(cudaStreamEndCapture(cs, &g));
+  ctx->stream = saved;
+  CK(cudaGraphInstantiate(&ctx->gexec, g, 0));
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  ctx->graph_unroll = U;
+  return KPP_OK;
+}
+
+kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long max_iters, double tol,
+                      double* x_out, double* res_hist, long long hist_cap, long long* n_hist,
+                      long long* iters_out) {
+  if (!ctx || !b || !x_out || max_iters < 0 || !(tol >= 0.0) || !std::isfinite(tol) || hist_cap < 0)
+    return KPP_EINVAL;
+  cudaStream_t st = ctx->stream;
+  const long long m = ctx->m, n = ctx->n;
+  ctx->stats.n_fresh_last = 0;
+  ctx->stats.iter_launches = 0;
+  ctx->stats.kernel_launches = 0;
+  // inputs: b (m, replicated), x0 (n local)
+  const double* b_dev = b;
+  if (!is_device_ptr(b)) {
+    CK(cudaMemcpyAsync(ctx->bstage, b, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, st));
+    b_dev = ctx->bstage;
+  }
+  if (x0) {
+    CK(cudaMemcpyAsync(ctx->x, x0, (size_t)n * sizeof(double), cudaMemcpyDefault, st));
+  } else {
+    CK(cudaMemsetAsync(ctx->x, 0, (size_t)n * sizeof(double), st));
+  }
+  CK(cudaMemsetAsync(ctx->mom, 0, (size_t)n * sizeof(double), st));
+  launch_sumsq(st, b_dev, m, ctx->d_bb);
+  // state
+  DevState hs{};
+  hs.rho = ctx->rho_fixed >= 0.0 ? ctx->rho_fixed : 0.0;  // rho_0 = 0
+  hs.rhat = 1.0;
+  CK(cudaMemcpyAsync(ctx->dstate, &hs, sizeof hs, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->d_nb, 0, sizeof(long long), st));
+  double bb = 0.0;
+  CK(cudaMemcpyAsync(&bb, ctx->d_bb, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // history capacity: one entry per checkpoint
+  const long long need_hist = max_iters / (2 * ctx->zeta) + 2;
+  if (need_hist > ctx->hist_capd) {
+    CKS(dalloc(ctx, &ctx->hist_res, (size_t)need_hist));
+    CKS(dalloc(ctx, &ctx->hist_rho, (size_t)need_hist));
+    ctx->hist_capd = need_hist;
+  }
+  const double eta = ctx->accel ? (ctx->eta_opt >= 0.0 ? ctx->eta_opt : (double)ctx->s / (2.0 * (double)ctx->n_global)) : 0.0;
+  const long long W = std::max<long long>(1, ctx->window);
+  const bool use_graph = ctx->engine == 1 || ctx->nranks > 1;
+  const size_t smem = iterate_smem_bytes(ctx->s, ctx->slab, 0);
+  float p1ms = 0.f, p2ms = 0.f;
+  DevState fin = hs;
+  for (long long t0 = 0; t0 < max_iters; t0 += W) {
+    const long long cnt = std::min(W, max_iters - t0);
+    CK(cudaEventRecord(ctx->ev0, st));
+    CKS(schedule_and_prepare(ctx, t0, cnt, true));
+    CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    p1ms += ms;
+    CK(cudaEventRecord(ctx->ev0, st));
+    if (!use_graph) {
+      IterParams p{};
+      p.A = ctx->A; p.lda = ctx->lda; p.m = m; p.n = n; p.s = ctx->s;
+      p.cd = ctx->kind == KIND_CDPP; p.col_base = ctx->col_begin;
+      p.b = b_dev; p.tol2bb = tol * tol * bb; p.bb = bb;
+      p.S_pool = ctx->S_pool; p.M_pool = ctx->M_pool; p.bid = ctx->bid;
+      p.t0 = t0; p.t1 = t0 + cnt;
+      p.x = ctx->x; p.mom = ctx->mom; p.eta = eta; p.zeta = ctx->zeta;
+      p.adaptive = ctx->rho_fixed < 0.0;
+      p.part = ctx->part; p.r = ctx->r; p.y = ctx->y; p.bar = ctx->bar; p.st = ctx->dstate;
+      p.hist_res = ctx->hist_res; p.hist_rho = ctx->hist_rho; p.hist_cap = ctx->hist_capd;
+      p.slab = ctx->slab; p.resident = 0;
+      CK(cudaMemsetAsync(ctx->bar, 0, sizeof(unsigned int), st));
+      CK(launch_iterate(st, p, ctx->grid, iterate_block_threads(), smem));
+      ctx->stats.iter_launches += 1;
+      ctx->stats.kernel_launches += 1;
+    } else {
+      StepParams sp{};
+      sp.A = ctx->A; sp.lda = ctx->lda; sp.m = m; sp.n = n; sp.s = ctx->s;
+      sp.cd = ctx->kind == KIND_CDPP; sp.grid = ctx->grid; sp.slab = ctx->slab;
+      sp.col_base = ctx->col_begin; sp.b = b_dev; sp.tol2bb = tol * tol * bb; sp.bb = bb;
+      sp.S_pool = ctx->S_pool; sp.M_pool = ctx->M_pool; sp.bid = ctx->bid;
+      sp.x = ctx->x; sp.mom = ctx->mom; sp.eta = eta; sp.zeta = ctx->zeta;
+      sp.adaptive = ctx->rho_fixed < 0.0; sp.writer = ctx->rank == 0;
+      sp.part = ctx->part; sp.rsum = ctx->r; sp.y = ctx->y; sp.st = ctx->dstate; sp.sp = ctx->dstep;
+      sp.hist_res = ctx->hist_res; sp.hist_rho = ctx->hist_rho; sp.hist_cap = ctx->hist_capd;
+      // the graph bakes in pointers and scalars: re-capture when any of them changed
+      const double keyv[3] = {sp.tol2bb, sp.eta, (double)sp.adaptive};
+      const void* key[5] = {ctx->S_pool, ctx->M_pool, b_dev, ctx->hist_res, ctx->bid};
+      if (ctx->gexec && (memcmp(key, ctx->gkey, sizeof key) != 0 || memcmp(keyv, ctx->gkeyv, sizeof keyv) != 0)) {
+        cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+      }
+      memcpy(ctx->gkey, key, sizeof key);
+      memcpy(ctx->gkeyv, keyv, sizeof keyv);
+      const int U = 64;
+      CKS(build_graph(ctx, sp, U));
+      DevStep dsp{t0, t0 + cnt, t0};
+      CK(cudaMemcpyAsync(ctx->dstep, &dsp, sizeof dsp, cudaMemcpyHostToDevice, st));
+      for (long long u = 0; u < cnt; u += U) {
+        CK(cudaGraphLaunch(ctx->gexec, st));
+        ctx->stats.iter_launches += 1;
+        ctx->stats.kernel_launches += 5LL * U;
+      }
+    }
+    CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaMemcpyAsync(&fin, ctx->dstate, sizeof fin, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    p2ms += ms;
+    if (fin.stopped) break;
+  }
+  if (max_iters == 0) fin = hs;
+  ctx->stats.phase1_ms += p1ms;
+  ctx->stats.phase2_ms += p2ms;
+  ctx->stats.iter_kernel_ms += p2ms;
+  ctx->stats.n_blocks = ctx->nb_ready;
+  // outputs
+  CK(cudaMemcpyAsync(x_out, ctx->x, (size_t)n * sizeof(double), cudaMemcpyDefault, st));
+  const long long nh = fin.nh;
+  const long long keep = std::min(nh, ctx->hist_capd);
+  ctx->rho_hist.assign((size_t)keep, 0.0);
+  if (keep > 0) CK(cudaMemcpyAsync(ctx->rho_hist.data(), ctx->hist_rho, (size_t)keep * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (res_hist && hist_cap > 0 && keep > 0)
+    CK(cudaMemcpyAsync(res_hist, ctx->hist_res, (size_t)std::min(keep, hist_cap) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (n_hist) *n_hist = nh;
+  if (iters_out) *iters_out = max_iters == 0 ? 0 : fin.t_done;
+  if (fin.stopped == 2) return fail(ctx, KPP_EDIVERGED, "non-finite block residual at iteration %lld", fin.t_done - 1);
+  if (fin.stopped == 1) return KPP_OK;
+  return KPP_EMAXITER;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kpp_version(void) { return "kpp-b200 0.1 (sm_100a)"; }
+
+const char* kpp_status_str(kpp_status s) {
+  switch (s) {
+    case KPP_OK: return "ok";
+    case KPP_EINVAL: return "invalid argument";
+    case KPP_ENOMEM: return "out of memory";
+    case KPP_ECUDA: return "CUDA error";
+    case KPP_ENCCL: return "NCCL error";
+    case KPP_ENOTPD: return "factor not positive definite";
+    case KPP_EDIVERGED: return "diverged (non-finite residual)";
+    case KPP_EMAXITER: return "maximum iterations reached";
+  }
+  return "unknown status";
+}
+
+const char* kpp_last_error(const kpp_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+static kpp_status setup_any(kpp_ctx** out, int kind, const double* A, long long m, long long n_global,
+                            long long cb, long long ce, long long lda, int s, double lam, uint64_t seed,
+                            const uint8_t* id, int rank, int nranks) {
+  const long long nloc = ce - cb;
+  kpp_status v = validate_and_create(out, kind, A, m, n_global, nloc, lda, s, lam);
+  if (v != KPP_OK) return v;
+  if (cb < 0 || ce > n_global || nranks < 1 || rank < 0 || rank >= nranks) return KPP_EINVAL;
+  kpp_ctx* ctx = new (std::nothrow) kpp_ctx();
+  if (!ctx) return KPP_ENOMEM;
+  ctx->kind = kind;
+  ctx->A = A;
+  ctx->m = m;
+  ctx->n = nloc;
+  ctx->n_global = n_global;
+  ctx->col_begin = cb;
+  ctx->col_end = ce;
+  ctx->lda = lda;
+  ctx->s = s;
+  ctx->lam = lam;
+  ctx->seed = seed;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  kpp_status st = setup_common(ctx);
+  if (st == KPP_OK && id) {
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof uid);
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, uid, rank);
+    if (r != ncclSuccess) st = fail(ctx, KPP_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  if (st != KPP_OK) {
+    kpp_destroy(ctx);
+    return st;
+  }
+  *out = ctx;
+  return KPP_OK;
+}
+
+kpp_status kpp_setup(kpp_ctx** out, const double* A, int64_t m, int64_t n, int64_t lda, int32_t block_size,
+                     double lambda, uint64_t seed) {
+  return setup_any(out, KIND_KPP, A, m, n, 0, n, lda, block_size, lambda, seed, nullptr, 0, 1);
+}
+
+kpp_status cdpp_setup(kpp_ctx** out, const double* A, int64_t n, int64_t lda, int32_t block_size,
+                      double lambda, uint64_t seed) {
+  return setup_any(out, KIND_CDPP, A, n, n, 0, n, lda, block_size, lambda, seed, nullptr, 0, 1);
+}
+
+kpp_status kpp_get_unique_id(uint8_t id[128]) {
+  if (!id) return KPP_EINVAL;
+  ncclUniqueId uid;
+  if (ncclGetUniqueId(&uid) != ncclSuccess) return KPP_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(id, &uid, 128);
+  return KPP_OK;
+}
+
+kpp_status kpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t m, int64_t n_global, int64_t col_begin,
+                          int64_t col_end, int64_t lda, int32_t block_size, double lambda, uint64_t seed,
+                          const uint8_t id[128], int32_t rank, int32_t nranks) {
+  if (!id) return KPP_EINVAL;
+  return setup_any(out, KIND_KPP, A_slab, m, n_global, col_begin, col_end, lda, block_size, lambda, seed, id,
+                   rank, nranks);
+}
+
+kpp_status cdpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t n, int64_t col_begin, int64_t col_end,
+                           int64_t lda, int32_t block_size, double lambda, uint64_t seed, const uint8_t id[128],
+                           int32_t rank, int32_t nranks) {
+  if (!id) return KPP_EINVAL;
+  return setup_any(out, KIND_CDPP, A_slab, n, n, col_begin, col_end, lda, block_size, lambda, seed, id, rank,
+                   nranks);
+}
+
+kpp_status kpp_solve(kpp_ctx* ctx, const double* b, const double* x0, int64_t max_iters, double tol,
+                     double* x_out, double* res_hist, int64_t hist_cap, int64_t* n_hist, int64_t* iters_out) {
+  long long nh = 0, it = 0;
+  kpp_status s = solve_impl(ctx, b, x0, max_iters, tol, x_out, res_hist, hist_cap, &nh, &it);
+  if (s != KPP_EINVAL) {
+    if (n_hist) *n_hist = nh;
+    if (iters_out) *iters_out = it;
+  }
+  return s;
+}
+
+kpp_status cdpp_solve(kpp_ctx* ctx, const double* b, const double* x0, int64_t max_iters, double tol,
+                      double* x_out, double* res_hist, int64_t hist_cap, int64_t* n_hist, int64_t* iters_out) {
+  if (!ctx || ctx->kind != KIND_CDPP) return KPP_EINVAL;
+  return kpp_solve(ctx, b, x0, max_iters, tol, x_out, res_hist, hist_cap, n_hist, iters_out);
+}
+
+void kpp_destroy(kpp_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  void* ptrs[] = {ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
+                  ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
+                  ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->d_info};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  delete ctx;
+}
+
+kpp_status kpp_set_stream(kpp_ctx* ctx, void* s) {
+  if (!ctx) return KPP_EINVAL;
+  ctx->stream = (cudaStream_t)s;
+  return KPP_OK;
+}
+
+kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
+  if (!ctx || !std::isfinite(v)) return KPP_EINVAL;
+  switch (key) {
+    case KPP_OPT_ACCEL: ctx->accel = v != 0.0; break;
+    case KPP_OPT_MEMO:
+      if ((v != 0.0) != (ctx->memo != 0)) {  // a different schedule: drop the cache
+        ctx->nb_gen = ctx->nb_ready = 0;
+      }
+      ctx->memo = v != 0.0;
+      break;
+    case KPP_OPT_ETA: ctx->eta_opt = v; break;
+    case KPP_OPT_RHO_FIXED:
+      if (v > 1.0) return KPP_EINVAL;
+      ctx->rho_fixed = v;
+      break;
+    case KPP_OPT_FACTOR:
+      if (v != 0.0 && v != 1.0) return KPP_EINVAL;
+      if ((int)v != ctx->factor) ctx->nb_ready = 0;  // recompute factors
+      ctx->factor = (int)v;
+      break;
+    case KPP_OPT_WINDOW:
+      if (v < 1) return KPP_EINVAL;
+      ctx->window = (long long)v;
+      break;
+    case KPP_OPT_PHASE1_MB:
+      if (v < 1) return KPP_EINVAL;
+      ctx->phase1_mb = (long long)v;
+      break;
+    case KPP_OPT_RESIDENT: ctx->resident_opt = v != 0.0; break;
+    case OPT_ENGINE:
+      if (v != 0.0 && v != 1.0) return KPP_EINVAL;
+      ctx->engine = (int)v;
+      break;
+    default: return KPP_EINVAL;
+  }
+  return KPP_OK;
+}
+
+kpp_status kpp_get_schedule(kpp_ctx* ctx, int64_t t0, int64_t count, int32_t* block_id, uint8_t* is_fresh) {
+  if (!ctx || t0 < 0 || count < 0 || (count > 0 && (!block_id || !is_fresh))) return KPP_EINVAL;
+  if (count == 0) return KPP_OK;
+  cudaStream_t st = ctx->stream;
+  // fresh count before t0: run the schedule from 0 (cheap: a few kernels)
+  CK(cudaMemsetAsync(ctx->d_nb, 0, sizeof(long long), st));
+  if (t0 > 0) CKS(schedule_and_prepare(ctx, 0, t0, false));
+  CKS(schedule_and_prepare(ctx, t0, count, false));
+  CK(cudaMemcpyAsync(block_id, ctx->bid, (size_t)count * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(is_fresh, ctx->fresh, (size_t)count, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return KPP_OK;
+}
+
+kpp_status kpp_prepare(kpp_ctx* ctx, int64_t iters) {
+  if (!ctx || iters < 0) return KPP_EINVAL;
+  if (iters == 0) return KPP_OK;
+  CK(cudaMemsetAsync(ctx->d_nb, 0, sizeof(long long), ctx->stream));
+  return schedule_and_prepare(ctx, 0, iters, true);
+}
+
+kpp_status kpp_get_block(kpp_ctx* ctx, int64_t block_id, int32_t* S_out) {
+  if (!ctx || !S_out || block_id < 0 || block_id >= ctx->nb_gen) return KPP_EINVAL;
+  CK(cudaMemcpy(S_out, ctx->S_pool + block_id * ctx->s, (size_t)ctx->s * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  return KPP_OK;
+}
+
+kpp_status kpp_get_factor(kpp_ctx* ctx, int64_t block_id, double* M_out) {
+  if (!ctx || !M_out || block_id < 0 || block_id >= ctx->nb_ready) return KPP_EINVAL;
+  const size_t ss = (size_t)ctx->s * ctx->s;
+  CK(cudaMemcpy(M_out, ctx->M_pool + block_id * ss, ss * sizeof(double), cudaMemcpyDeviceToHost));
+  return KPP_OK;
+}
+
+kpp_status kpp_get_rho_history(kpp_ctx* ctx, double* rho_hist, int64_t cap, int64_t* n) {
+  if (!ctx) return KPP_EINVAL;
+  const long long k = (long long)ctx->rho_hist.size();
+  if (n) *n = k;
+  if (rho_hist && cap > 0) memcpy(rho_hist, ctx->rho_hist.data(), (size_t)std::min<long long>(k, cap) * sizeof(double));
+  return KPP_OK;
+}
+
+kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out) {
+  if (!ctx || !out) return KPP_EINVAL;
+  *out = ctx->stats;
+  out->n_blocks = ctx->nb_ready;
+  return KPP_OK;
+}
+
+kpp_status kpp_reset_stats(kpp_ctx* ctx) {
+  if (!ctx) return KPP_EINVAL;
+  ctx->stats.phase1_ms = ctx->stats.phase2_ms = ctx->stats.iter_kernel_ms = 0.0;
+  return KPP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,146 @@
+// kpp_internal.h -- declarations shared by the host runtime and the kernels of libkpp.
+// Product code: shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kpp {
+
+// Replicated solver state of one solve, persisted in device memory between
+// iteration-kernel launches (windows).  Every CTA of the persistent kernel keeps an
+// identical copy; CTA 0 writes it back at the end of a launch.
+struct DevState {
+  double rho;    // momentum parameter in force (Eq (momentum))
+  double rhat;   // weighted ratio average (Eq (weighted))
+  double E0, E1; // residual window sums (Eq (residual))
+  long long ichk;    // checkpoints passed
+  long long nh;      // history entries written
+  long long t_done;  // iterations completed
+  long long nb;      // fresh blocks created by the schedule in [0, t_sched)
+  int stopped;       // 0 running, 1 tolerance met, 2 non-finite residual
+  int pad;
+};
+
+// ------------------------------------------------------------------ schedule.cu
+// Bernoulli / reuse decisions for t in [t0, t0+count) and the block ids; reads the
+// fresh-block count before t0 from *nb_io and writes the count after the window.
+void launch_schedule(cudaStream_t st, uint64_t seed, double C, int memo, long long t0, int count,
+                     long long* nb_io, uint32_t* word1_ws, uint8_t* fresh_out, int32_t* bid_out);
+// Index sets of fresh blocks k in [k0, k1): S_pool[k*s .. k*s+s) sorted ascending.
+void launch_fresh_blocks(cudaStream_t st, uint64_t seed, long long pop, int s, long long k0,
+                         long long k1, int32_t* S_pool);
+
+// ------------------------------------------------------------------ gemm.cu
+// Batched fp64 GEMM on FP64 tensor cores (mma.sync m8n8k4 -> DMMA):
+//   C[b*Z + z] = sum_{k in chunk z} opA_b(i,k) * opB_b(k,j)
+// Operand memory is row-major with leading dimension ld; `trans` selects the logical view
+// (A: 0 -> (i,k) = mem(i,k), 1 -> (i,k) = mem(k,i); B: 0 -> (k,j) = mem(k,j),
+// 1 -> (k,j) = mem(j,k)); `idx` (optional) gathers memory rows.
+struct Operand {
+  const double* ptr;
+  long long ld;
+  long long bstride;      // elements between batch entries
+  const int32_t* idx;     // optional memory-row gather (nullptr: identity)
+  long long idx_bstride;  // ints between batch entries of idx
+  int trans;
+};
+// Returns the effective split count Z (K chunks are rounded to the K step).
+int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand& a,
+                 const Operand& b, double* C, long long ldc, long long c_bstride, int Z,
+                 int upper_only);
+// out[b] = sum_z part[b*Z+z] (+ diag_add on the diagonal) (+ add_scale * add[b]);
+// with upper_only, element (i,j), i>j, is taken from (j,i).
+void launch_splitk_reduce(cudaStream_t st, int batch, int M, int N, int Z, const double* part,
+                          long long p_bstride, double diag_add, const double* add,
+                          double add_scale, long long add_bstride, double* out,
+                          long long o_bstride, int upper_only);
+
+// ------------------------------------------------------------------ factor.cu
+// G[b] (s x s, row-major) <- A[S_b, S_b] + lam I   (CD++ principal block, Alg 3 l.8)
+// Multi-GPU: only columns S_l in [col_begin, col_end) of the local slab contribute (others 0).
+void launch_gather_principal(cudaStream_t st, int batch, const double* A, long long lda,
+                             const int32_t* S, int s, double lam, long long col_begin,
+                             long long col_end, double* G);
+// G[b] += lam on the diagonal
+void launch_add_diag(cudaStream_t st, int batch, double* G, int s, double lam);
+// In place: G[b] -> R[b] upper with R^T R = G (lower part zeroed); X[b] = R^{-1}.
+// info[b] = 0 on success, 1 + pivot index on a non-positive pivot.
+void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info);
+
+// ------------------------------------------------------------------ iterate.cu
+struct IterParams {
+  const double* A;
+  long long lda, m, n;   // A is m x n_local (this rank's columns)
+  int s;
+  int cd;                // 1: CD++ (w = I_S^T y), 0: K++ (w = A_S^T y)
+  long long col_base;    // global index of local column 0 (CD++ scatter, multi-GPU)
+  const double* b;       // length m (replicated)
+  double tol2bb;         // tol^2 * ||b||^2
+  double bb;             // ||b||^2
+  const int32_t* S_pool; // block k at S_pool + k*s
+  const double* M_pool;  // block k at M_pool + k*s*s: (A_S A_S^T + lam I)^{-1} or (A_SS + lam I)^{-1}
+  const int32_t* bid;    // block id of iteration t0 + i
+  long long t0, t1;
+  double* x;             // local iterate (n_local)
+  double* mom;           // local momentum (n_local)
+  double eta;
+  long long zeta;
+  int adaptive;          // 0: rho fixed
+  double* part;          // [grid][s] partial block residuals
+  double* r;             // [s]
+  double* y;             // [s]
+  unsigned int* bar;     // grid barrier counter (zeroed before launch)
+  DevState* st;
+  double* hist_res;      // [hist_cap]
+  double* hist_rho;
+  long long hist_cap;
+  int slab;              // columns per CTA (multiple of 4)
+  int resident;          // keep the block slab in shared memory across both passes
+};
+cudaError_t launch_iterate(cudaStream_t st, const IterParams& p, int grid, int block, size_t smem);
+int iterate_block_threads();
+int iterate_max_grid(int device, size_t smem);  // one CTA per SM if it fits, else 0
+size_t iterate_smem_bytes(int s, int slab, int resident);
+
+// ------------------------------------------------------------------ steps.cu (engine "graph")
+// Iteration cursor of the step kernels (device memory), so a captured graph is reusable.
+struct DevStep {
+  long long t_cur;   // next iteration
+  long long t_end;   // end of the current window
+  long long t_base;  // iteration of bid[0]
+};
+struct StepParams {
+  const double* A;
+  long long lda, m, n;
+  int s, cd, grid, slab;
+  long long col_base;
+  const double* b;
+  double tol2bb, bb;
+  const int32_t* S_pool;
+  const double* M_pool;
+  const int32_t* bid;
+  double* x;
+  double* mom;
+  double eta;
+  long long zeta;
+  int adaptive;
+  int writer;          // this rank writes the history
+  double* part;        // [grid][s]
+  double* rsum;        // [s] local partial sums, allreduced in place between kernels
+  double* y;           // [s]
+  DevState* st;
+  DevStep* sp;
+  double* hist_res;
+  double* hist_rho;
+  long long hist_cap;
+};
+void launch_step_partial(cudaStream_t st, const StepParams& p);
+void launch_step_reduce(cudaStream_t st, const StepParams& p);   // rsum = sum_g part[g]
+void launch_step_solve(cudaStream_t st, const StepParams& p);    // y = M (rsum - b_S)
+void launch_step_update(cudaStream_t st, const StepParams& p);   // w, momentum, x
+void launch_step_window(cudaStream_t st, const StepParams& p);   // e, checkpoint, t_cur++
+
+// sum of squares of b (single CTA, fixed order) -> *out
+void launch_sumsq(cudaStream_t st, const double* b, long long m, double* out);
+
+}  // namespace kpp

@@ -1,0 +1,287 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star): block schedule bit-exact; ||x_gpu - x_cpu|| / ||x_cpu||
+<= 1e-10 after 200 iterations; final relative residuals within 1e-12 absolute.
+The oracle uses Householder factors; the GPU uses shifted CholeskyQR2 + the memoized
+inverse M = (A_S A_S^T + lam I)^{-1}.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def kpp():
+    import paper_2501_11673_b200 as k
+    from paper_2501_11673_b200 import build
+    build.build()
+    k.load_library()
+    assert torch.cuda.is_available()
+    return k
+
+
+DEV = "cuda:0"
+
+
+def run_pair(kpp, ora, cfg, T, seed=0, x0=None, tol=0.0, **opts):
+    A, b, _ = synth.make_problem(cfg)
+    An, bn = A.numpy(), b.numpy()
+    s = cfg.s
+    if cfg.kind == "cdpp":
+        ref = ora.cdpp_run(An, bn, s, lam=cfg.lam, seed=seed, max_iters=T, tol=tol, x0=x0, threads=8)
+        ctx = kpp.cdpp_setup(A.to(DEV), s, cfg.lam, seed)
+    else:
+        ref = ora.kpp_run(An, bn, s, lam=cfg.lam, seed=seed, max_iters=T, tol=tol, x0=x0, threads=8)
+        ctx = kpp.kpp_setup(A.to(DEV), s, cfg.lam, seed)
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    res = ctx.solve(b.to(DEV), None if x0 is None else torch.from_numpy(x0).to(DEV), max_iters=T, tol=tol)
+    return An, bn, ref, res, ctx
+
+
+# ----------------------------------------------------------------- schedule
+@pytest.mark.parametrize("m,n,s,T", [(256, 256, 32, 500), (8192, 8192, 128, 200000), (65536, 65536, 512, 50000)])
+def test_schedule_bit_exact(kpp, ora, m, n, s, T):
+    nc = min(n, 8192)  # only the schedule is used; C depends on min(m, n)
+    ctx = kpp.kpp_setup(torch.zeros(m, nc, dtype=torch.float64, device=DEV), s, 1e-8, 7)
+    bid, fresh = ctx.schedule(0, T)
+    C = ora.kpp_C(m, nc, s)
+    rb, rf, nb = ora.schedule(7, C, T)
+    assert np.array_equal(bid.numpy(), rb) and np.array_equal(fresh.numpy(), rf)
+    # windows starting mid-stream agree too
+    bid2, fresh2 = ctx.schedule(T // 3, T // 5)
+    assert np.array_equal(bid2.numpy(), rb[T // 3: T // 3 + T // 5])
+    # fresh index sets, bit-exact
+    for k in list(range(min(nb, 50))) + [nb - 1]:
+        assert np.array_equal(ctx.block(k).numpy(), ora.fresh_block(7, m, s, k)), k
+
+
+def test_philox_against_curand(ora):
+    """Both Philox implementations against the toolkit's curand_Philox4x32_10 (test-only)."""
+    from torch.utils.cpp_extension import load_inline
+    src = r"""
+#include <curand_philox4x32_x.h>
+__global__ void k(const uint4* c, const uint2* key, uint4* o, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = curand_Philox4x32_10(c[i], key[i]);
+}
+torch::Tensor run(torch::Tensor c, torch::Tensor key) {
+  auto o = torch::empty_like(c);
+  int n = c.size(0);
+  k<<<(n + 127) / 128, 128>>>((const uint4*)c.data_ptr(), (const uint2*)key.data_ptr(), (uint4*)o.data_ptr(), n);
+  return o;
+}
+"""
+    try:
+        mod = load_inline("philox_kat", cpp_sources="torch::Tensor run(torch::Tensor c, torch::Tensor key);",
+                          cuda_sources=src, functions=["run"],
+                          extra_cuda_cflags=["-gencode", "arch=compute_100a,code=sm_100a"])
+    except Exception as e:  # pragma: no cover - toolchain problem, not a parity failure
+        pytest.skip(f"inline extension unavailable: {e}")
+    rng = np.random.default_rng(0)
+    c = rng.integers(0, 2**32, size=(256, 4), dtype=np.uint64).astype(np.uint32)
+    kk = rng.integers(0, 2**32, size=(256, 2), dtype=np.uint64).astype(np.uint32)
+    out = mod.run(torch.from_numpy(c.view(np.int32)).to(DEV), torch.from_numpy(kk.view(np.int32)).to(DEV))
+    out = out.cpu().numpy().view(np.uint32)
+    for i in range(256):
+        assert np.array_equal(out[i], ora.philox(c[i], kk[i]))
+
+
+# ----------------------------------------------------------------- Phase-1 operator
+@pytest.mark.parametrize("factor", [0, 1])
+def test_factor_operator(kpp, ora, factor):
+    """M_k = (A_S A_S^T + lam I)^{-1} from the GPU against the oracle's Householder R
+    (M = R^{-1} R^{-T}); error bound ~ u kappa(G)."""
+    cfg = synth.twin("c2", 1024, 1024, 128)
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), 128, 1e-8, 3)
+    ctx.set_option(kpp.OPT_FACTOR, factor)
+    ctx.prepare(20)
+    An = A.numpy()
+    for k in (0, 5, 13):
+        S = ctx.block(k).numpy()
+        assert np.array_equal(S, ora.fresh_block(3, 1024, 128, k))
+        M = ctx.factor(k).numpy()
+        R = ora.kpp_factor(An, S, 1e-8)
+        Ri = np.linalg.inv(R)
+        Mref = Ri @ Ri.T
+        G = An[S] @ An[S].T + 1e-8 * np.eye(128)
+        kap = np.linalg.cond(G)
+        assert rel(M, Mref) < 200 * 2.2e-16 * kap, (k, rel(M, Mref), kap)
+        assert np.allclose(M, M.T, rtol=0, atol=1e-12 * np.abs(M).max())
+
+
+def test_cdpp_factor_operator(kpp, ora):
+    cfg = synth.twin("c5", 1024, 1024, 128, k=25)
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.cdpp_setup(A.to(DEV), 128, 1e-8, 1)
+    ctx.prepare(10)
+    An = A.numpy()
+    for k in (0, 4):
+        S = ctx.block(k).numpy()
+        M = ctx.factor(k).numpy()
+        R = ora.cdpp_factor(An, S, 1e-8)
+        Ri = np.linalg.inv(R)
+        assert rel(M, Ri @ Ri.T) < 1e-11
+
+
+# ----------------------------------------------------------------- end-to-end parity
+def test_c1_parity_200(kpp, ora):
+    """BASELINE configs[0] at its exact size: x after 200 iterations within 1e-10."""
+    _, _, ref, res, _ = run_pair(kpp, ora, synth.CONFIGS["c1"], 200)
+    assert res.iters == 200
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+
+
+def test_c1_final_residual_500(kpp, ora):
+    """configs[0]: 500 iterations; final relative residuals within 1e-12 absolute; history agrees."""
+    An, bn, ref, res, ctx = run_pair(kpp, ora, synth.CONFIGS["c1"], 500)
+    xg = res.x.cpu().numpy()
+    rg = np.linalg.norm(An @ xg - bn) / np.linalg.norm(bn)
+    rc = np.linalg.norm(An @ ref.x - bn) / np.linalg.norm(bn)
+    assert abs(rg - rc) <= 1e-12
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=0)
+    assert np.allclose(ctx.rho_history().numpy(), ref.hist_rho, rtol=1e-6, atol=1e-12)
+
+
+TWINS = [
+    synth.twin("c2", 2048, 2048, 128, k=64),       # square, spiked bulk
+    synth.twin("c3", 8192, 512, 256),              # over-determined
+    synth.twin("c4", 512, 8192, 256),              # under-determined
+    synth.twin("c3", 1000, 777, 50, k=8),          # ragged: nothing a multiple of a tile
+    synth.twin("c4", 300, 5003, 37, k=8),          # ragged under-determined
+    synth.twin("c5", 2048, 2048, 512, k=100),      # CD++ at the real block size
+    synth.twin("c5", 1001, 1001, 77, k=16),        # CD++ ragged
+]
+
+
+@pytest.mark.parametrize("cfg", TWINS, ids=[c.name for c in TWINS])
+def test_twin_parity_200(kpp, ora, cfg):
+    _, _, ref, res, _ = run_pair(kpp, ora, cfg, 200)
+    assert res.iters == 200
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+
+
+def test_engines_bitwise_equal(kpp, ora):
+    """Persistent kernel and step-kernel graph (the multi-GPU engine at P=1) give the same bits."""
+    cfg = synth.twin("c3", 4096, 512, 64, k=16)
+    A, b, _ = synth.make_problem(cfg)
+    outs = []
+    for eng in (0, 1):
+        ctx = kpp.kpp_setup(A.to(DEV), 64, 1e-8, 0)
+        ctx.set_option(kpp.OPT_ENGINE, eng)
+        outs.append(ctx.solve(b.to(DEV), max_iters=300).x.cpu())
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_deterministic_and_warm_cache(kpp):
+    """Same inputs -> same bits; a second solve on the same context reuses the memo cache."""
+    cfg = synth.twin("c2", 1024, 1024, 64, k=16)
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), 64, 1e-8, 0)
+    x1 = ctx.solve(b.to(DEV), max_iters=400).x.clone()
+    nf1 = ctx.stats()["n_fresh_last"]
+    x2 = ctx.solve(b.to(DEV), max_iters=400).x.clone()
+    assert ctx.stats()["n_fresh_last"] == 0 and nf1 > 0
+    assert torch.equal(x1, x2)
+    ctx2 = kpp.kpp_setup(A.to(DEV), 64, 1e-8, 0)
+    ctx2.set_option(kpp.OPT_WINDOW, 37)  # window boundaries do not change the result
+    assert torch.equal(ctx2.solve(b.to(DEV), max_iters=400).x, x1)
+
+
+def test_host_buffers_equal_device_buffers(kpp):
+    cfg = synth.twin("c3", 2048, 256, 32)
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), 32, 1e-8, 0)
+    xd = ctx.solve(b.to(DEV), max_iters=100).x.cpu()
+    xh = ctx.solve(b.pin_memory(), max_iters=100, x_out=torch.empty(256, dtype=torch.float64).pin_memory()).x
+    assert torch.equal(xd, xh)
+
+
+def test_stop_matches_oracle(kpp, ora):
+    """Tolerance stop (Alg 5 l.15): same stopping checkpoint as the oracle on a case whose
+    estimate crosses the threshold with margin; x within the parity bar there."""
+    cfg = synth.twin("c3", 4096, 256, 64, k=8)
+    An, bn, ref, res, _ = run_pair(kpp, ora, cfg, 20000, tol=1e-6)
+    assert ref.status == ora.OK and res.status == 0
+    assert res.iters == ref.iters
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+
+
+def test_x0_and_options(kpp, ora):
+    """x0 given; momentum off; memoization off; fixed rho -- each against the oracle."""
+    cfg = synth.twin("c3", 2048, 300, 40, k=8)
+    A, b, _ = synth.make_problem(cfg)
+    An, bn = A.numpy(), b.numpy()
+    x0 = np.random.default_rng(1).standard_normal(300)
+    cases = [
+        (dict(), dict()),
+        (dict(accel=False), {kpp.OPT_ACCEL: 0}),
+        (dict(memo=False), {kpp.OPT_MEMO: 0}),
+        (dict(rho_fixed=0.2), {kpp.OPT_RHO_FIXED: 0.2}),
+        (dict(eta=0.05), {kpp.OPT_ETA: 0.05}),
+    ]
+    for okw, gopts in cases:
+        ref = ora.kpp_run(An, bn, 40, lam=1e-8, seed=2, max_iters=150, x0=x0, **okw)
+        ctx = kpp.kpp_setup(A.to(DEV), 40, 1e-8, 2)
+        for k, v in gopts.items():
+            ctx.set_option(k, v)
+        res = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=150)
+        assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10, okw
+
+
+def test_edge_cases(kpp, ora):
+    # s = m (one full block), s = 1, max_iters = 0
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((48, 64))
+    b = rng.standard_normal(48)
+    for s in (48, 1, 7):
+        ref = ora.kpp_run(A, b, s, lam=1e-8, seed=0, max_iters=60)
+        ctx = kpp.kpp_setup(torch.from_numpy(A).to(DEV), s, 1e-8, 0)
+        res = ctx.solve(torch.from_numpy(b).to(DEV), max_iters=60)
+        assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10, s
+    res = ctx.solve(torch.from_numpy(b).to(DEV), max_iters=0)
+    assert res.iters == 0 and float(res.x.abs().max()) == 0.0
+    # identity, full block, lam = 0, no momentum: exact in one step
+    I = torch.eye(64, dtype=torch.float64, device=DEV)
+    bb = torch.from_numpy(rng.standard_normal(64)).to(DEV)
+    ctx = kpp.kpp_setup(I, 64, 0.0, 0)
+    ctx.set_option(kpp.OPT_ACCEL, 0)
+    assert torch.allclose(ctx.solve(bb, max_iters=1).x, bb, rtol=1e-15, atol=1e-15)
+
+
+def test_errors(kpp):
+    A = torch.ones(4, 4, dtype=torch.float64, device=DEV)
+    with pytest.raises(kpp.KppError) as e:
+        kpp.kpp_setup(A, 5)
+    assert e.value.status == kpp.EINVAL
+    ctx = kpp.kpp_setup(A, 2, 0.0, 0)  # rank-1 rows, lam = 0 -> not positive definite
+    with pytest.raises(kpp.KppError) as e:
+        ctx.solve(torch.ones(4, dtype=torch.float64, device=DEV), max_iters=5)
+    assert e.value.status == kpp.ENOTPD
+    B = torch.full((8, 8), float("nan"), dtype=torch.float64, device=DEV)
+    ctx = kpp.kpp_setup(torch.eye(8, dtype=torch.float64, device=DEV), 4, 1e-8, 0)
+    with pytest.raises(kpp.KppError) as e:
+        ctx.solve(torch.full((8,), float("inf"), dtype=torch.float64, device=DEV), max_iters=4)
+    assert e.value.status == kpp.EDIVERGED
+    del B
+
+
+def test_cdpp_identity_and_scalar(kpp, ora):
+    rng = np.random.default_rng(6)
+    X = rng.standard_normal((40, 40))
+    A = X @ X.T + np.eye(40)
+    A = (A + A.T) / 2
+    b = rng.standard_normal(40)
+    x0 = rng.standard_normal(40)
+    ref = ora.cdpp_run(A, b, 1, lam=0.0, seed=4, max_iters=30, x0=x0, accel=False)
+    ctx = kpp.cdpp_setup(torch.from_numpy(A).to(DEV), 1, 0.0, 4)
+    ctx.set_option(kpp.OPT_ACCEL, 0)
+    res = ctx.solve(torch.from_numpy(b).to(DEV), torch.from_numpy(x0).to(DEV), max_iters=30)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-12
