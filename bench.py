@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark of the Kaczmarz++ / CD++ hot path (BASELINE.json metric:
+"block-iters/s & HBM GB/s vs 8 TB/s (fp64); time to 1e-8 rel. residual").
+
+One *step* = one cold kpp_solve of `--iters` block iterations on a context whose memo
+cache was cleared first, so every step runs every hot-path row (schedule, Phase-1
+factorisation of each fresh block, Phase-2 iterations with the adaptive momentum).
+Inputs (A, b) are resident in HBM before the timed region; A (512 MiB for c2) is larger
+than L2, and each step touches every row of it.
+
+Default workload (N=1): BASELINE configs[1] = c2, Kaczmarz++ m=n=8192, s=128.
+N>1 (torchrun): the same problem column-sharded across ranks (NCCL allreduce of the
+s-vector per iteration), strong scaling.
+
+`--impl reference` times the CPU oracle (oracle/) on the host cores on a bounded sample
+of the same workload (this tier has no reference implementation to install).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "block-iters/s & HBM GB/s vs 8 TB/s (fp64); time to 1e-8 rel. residual"
+UNIT = "block-iters/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=list(synth.CONFIGS))
+    ap.add_argument("--iters", type=int, default=0, help="block iterations per step (0: config default)")
+    ap.add_argument("--ttt", action="store_true", help="also measure time to the 1e-8 tolerance")
+    ap.add_argument("--ttt-cap", type=int, default=2_000_000)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--engine", type=int, default=-1)
+    return ap.parse_args()
+
+
+DEFAULT_ITERS = {"c1": 500, "c2": 8192, "c3": 4096, "c4": 1024, "c5": 2048}
+
+
+def bytes_per_iter(cfg, n_local=None):
+    """Algorithmic HBM bytes of one block iteration: A_S once (8 s n),
+    the memoized s x s operator, s-vectors and the x / m read+write (32 n)."""
+    s = cfg.s
+    n = cfg.n if n_local is None else n_local
+    return 8 * s * n + 8 * s * s + 12 * s + 32 * n
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(cfg_name):
+    """dram bytes per launch of the iteration kernel from the committed ncu capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        e = d.get(cfg_name, {}).get("iterate_kernel")
+        return e.get("dram_bytes_per_iter") if e else None
+    except Exception:
+        return None
+
+
+def cpu_oracle_sample(cfg, A_host, b_host, seconds):
+    """Time the oracle, as it stands, on the host cores: iterations 0..T-1 of the same cold
+    solve, T grown until the call takes about `seconds`."""
+    import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    T = 8
+    while True:
+        t0 = time.perf_counter()
+        if cfg.kind == "cdpp":
+            oracle.cdpp_run(A_host, b_host, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=threads)
+        else:
+            oracle.kpp_run(A_host, b_host, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=threads)
+        dt = time.perf_counter() - t0
+        if dt >= seconds / 3 or T >= 1 << 20:
+            break
+        T = int(T * min(8.0, max(2.0, seconds / 3 / max(dt, 1e-3))))
+    return {"value": T / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{cfg.name}: iterations 0..{T - 1} of a cold solve (first-visit Householder "
+                      f"factors included), {threads} OpenMP threads over independent outputs, {dt:.1f} s"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    A, b, _ = synth.make_problem(cfg, seed=0, device="cuda" if torch.cuda.is_available() else "cpu")
+    A_host, b_host = A.cpu().numpy(), b.cpu().numpy()
+    del A, b
+    per_step = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(cfg, A_host, b_host, args.cpu_seconds / max(1, args.steps))
+        if i >= args.warmup:
+            per_step.append(r["value"])
+            cb = r
+    v = float(np.median(per_step))
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg.name},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import paper_2501_11673_b200 as kpp
+    from paper_2501_11673_b200 import build as kbuild
+    kbuild.build()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=dev)
+    iters = args.iters or DEFAULT_ITERS[cfg.name]
+
+    A, b, _ = synth.make_problem(cfg, seed=0, device=dev)
+    n = cfg.n
+    if dist:
+        cb, ce = kpp.column_slabs(n, world)[rank]
+        A_loc = A[:, cb:ce].contiguous()
+        uid = [kpp.kpp_get_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        if cfg.kind == "cdpp":
+            ctx = kpp.cdpp_setup_dist(A_loc, n, cb, ce, cfg.s, cfg.lam, 0, uid[0], rank, world)
+        else:
+            ctx = kpp.kpp_setup_dist(A_loc, cfg.m, n, cb, ce, cfg.s, cfg.lam, 0, uid[0], rank, world)
+        A_keep = A_loc
+        del A
+        n_local = ce - cb
+    else:
+        ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A, cfg.s, cfg.lam, 0)
+        A_keep = A
+        n_local = n
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream)
+    if args.engine >= 0:
+        ctx.set_option(kpp.OPT_ENGINE, args.engine)
+    x_out = torch.empty(n_local, dtype=torch.float64, device=dev)
+
+    def step():
+        ctx.clear_cache()
+        return ctx.solve(b, max_iters=iters, tol=0.0, x_out=x_out)
+
+    def barrier():
+        if dist:
+            tdist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    ctx.reset_stats()
+    launches = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = step()
+            launches += ctx.stats()["kernel_launches"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = ctx.stats()
+    if dist:
+        t = torch.tensor([ms, st["phase2_ms"]], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms, p2max = float(t[0]), float(t[1])
+    else:
+        p2max = st["phase2_ms"]
+    total_iters = args.steps * iters
+    value = total_iters / (ms / 1e3)
+
+    # warm Phase-2 rate (memo cache full): one more solve without clearing
+    ctx.reset_stats()
+    ctx.solve(b, max_iters=iters, tol=0.0, x_out=x_out)
+    warm = ctx.stats()
+    warm_rate = iters / (warm["phase2_ms"] / 1e3) if warm["phase2_ms"] > 0 else None
+
+    # end to end through the C ABI with HOST buffers: H2D of b, D2H of x inside the timed region
+    b_host = b.cpu().pin_memory()
+    x_host = torch.empty(n_local, dtype=torch.float64).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.clear_cache()
+        ctx.solve(b_host, max_iters=iters, tol=0.0, x_out=x_host)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e = {"value": total_iters / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * cfg.m,
+           "d2h_bytes_per_step": 8 * n_local}
+
+    ttt = None
+    if args.ttt:
+        ctx.clear_cache()
+        ctx.reset_stats()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = ctx.solve(b, max_iters=args.ttt_cap, tol=cfg.tol if cfg.tol > 0 else 1e-8, x_out=x_out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tms = e0.elapsed_time(e1)
+        true_res = None
+        if not dist:
+            true_res = float(torch.linalg.vector_norm(A_keep @ x_out - b) / torch.linalg.vector_norm(b))
+        ttt = {"seconds": tms / 1e3, "iters": r.iters, "converged": r.status == kpp.OK,
+               "est_rel_res": float(r.res_hist[-1]) if len(r.res_hist) else None,
+               "true_rel_res": true_res, "tol": 1e-8}
+
+    if rank != 0:
+        if dist:
+            tdist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    peak_note = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if hbm_peak else "fallback 6650 GB/s"
+    hbm_peak = hbm_peak or 6650.0
+    bpi = bytes_per_iter(cfg, n_local)
+    achieved = bpi * total_iters / (p2max / 1e3) / 1e9 if p2max > 0 else None
+    tr = ncu_traffic(cfg.name)
+    roof = {"bound": "hbm", "kernel": "iterate_kernel (persistent Phase 2)", "achieved": achieved,
+            "peak": hbm_peak, "unit": "GB/s", "frac": (achieved / hbm_peak) if achieved else None,
+            "traffic": tr, "peak_source": peak_note,
+            "bytes_per_iter": bpi, "iter_kernel_share": p2max / ms if ms > 0 else None}
+    cpu = None
+    if not args.no_cpu and not dist:
+        cpu = cpu_oracle_sample(cfg, A_keep.cpu().numpy(), b.cpu().numpy(), args.cpu_seconds)
+    elif not args.no_cpu and dist and rank == 0:
+        cpu = None  # N>1: the oracle baseline is reported by the N=1 run only
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {'CD++' if cfg.kind == 'cdpp' else 'Kaczmarz++'} "
+                               f"m={cfg.m} n={cfg.n} s={cfg.s} lam={cfg.lam:g}",
+                   "iters_per_step": iters, "step": "cold solve (memo cache cleared)",
+                   "parallelism": f"column-sharded x{world}" if dist else "1 GPU",
+                   "l2": f"inputs larger than L2 (A = {cfg.m * cfg.n * 8 / 2**20:.0f} MiB)"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "phase1_ms_per_step": st["phase1_ms"] / args.steps,
+        "phase2_ms_per_step": st["phase2_ms"] / args.steps,
+        "warm_block_iters_per_s": warm_rate,
+        "hbm_gbs_alg_warm": (bpi * iters / (warm["phase2_ms"] / 1e3) / 1e9) if warm["phase2_ms"] > 0 else None,
+        "time_to_tol": ttt,
+        "n_blocks_per_step": warm["n_blocks"],
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

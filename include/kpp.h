@@ -121,6 +121,8 @@ kpp_status kpp_get_block(kpp_ctx* ctx, int64_t block_id, int32_t* S_out);
    (K++) or (A_SS + lam I)^{-1} (CD++), s x s row-major, HOST output.  Requires the
    factor to exist (run kpp_prepare or a solve first). */
 kpp_status kpp_get_factor(kpp_ctx* ctx, int64_t block_id, double* M_out);
+/* Drop every memoized block (the next solve regenerates and refactors them: a cold solve). */
+kpp_status kpp_clear_cache(kpp_ctx* ctx);
 /* Generate and factor (Phase 1) every fresh block needed by iterations [0, iters). */
 kpp_status kpp_prepare(kpp_ctx* ctx, int64_t iters);
 /* Rho history of the last solve (HOST, per checkpoint, the rho in force after it). */

@@ -68,6 +68,7 @@ def load_library():
         "kpp_get_block": ([P, i64, P], i32),
         "kpp_get_factor": ([P, i64, P], i32),
         "kpp_prepare": ([P, i64], i32),
+        "kpp_clear_cache": ([P], i32),
         "kpp_get_rho_history": ([P, P, i64, P], i32),
         "kpp_get_stats": ([P, P], i32),
         "kpp_reset_stats": ([P], i32),
@@ -154,6 +155,10 @@ class Ctx:
 
     def prepare(self, iters: int):
         _check(load_library().kpp_prepare(self.handle, iters), self.handle)
+
+    def clear_cache(self):
+        """Forget every memoized block: the next solve is cold (Phase 1 for every fresh block)."""
+        _check(load_library().kpp_clear_cache(self.handle), self.handle)
 
     def block(self, k: int) -> torch.Tensor:
         S = torch.zeros(self.s, dtype=torch.int32)

@@ -27,6 +27,13 @@
 
 using namespace kpp;
 
+#include <atomic>
+namespace kpp {
+static std::atomic<long long> g_launches{0};
+void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+long long launches_total() { return g_launches.load(std::memory_order_relaxed); }
+}  // namespace kpp
+
 namespace {
 
 enum { KIND_KPP = 0, KIND_CDPP = 1 };
@@ -221,13 +228,11 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   // workspace carve-up
   const int T = (s + 63) / 64;
   const int tiles_up = T * (T + 1) / 2;
+  // split-K count depends on n only, so the summation order (and the bits of M) does not
+  // depend on how fresh blocks happen to be batched
+  (void)tiles_up;
   int Z = 1;
-  if (ctx->kind == KIND_KPP) {
-    const long long target = 4LL * ctx->num_sms;
-    Z = (int)std::max<long long>(1, (target + (long long)B * tiles_up - 1) / ((long long)B * tiles_up));
-    Z = (int)std::min<long long>(Z, std::max<long long>(1, n / 256));
-    Z = std::min(Z, 64);
-  }
+  if (ctx->kind == KIND_KPP) Z = (int)std::min<long long>(64, std::max<long long>(1, (n + 511) / 512));
   const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor == 0;
   size_t off = 0;
   auto carve = [&](size_t count) {
@@ -438,6 +443,8 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   ctx->stats.n_fresh_last = 0;
   ctx->stats.iter_launches = 0;
   ctx->stats.kernel_launches = 0;
+  const long long launches0 = launches_total();
+  long long graph_kernels = 0;
   // inputs: b (m, replicated), x0 (n local)
   const double* b_dev = b;
   if (!is_device_ptr(b)) {
@@ -498,7 +505,6 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       CK(cudaMemsetAsync(ctx->bar, 0, sizeof(unsigned int), st));
       CK(launch_iterate(st, p, ctx->grid, iterate_block_threads(), smem));
       ctx->stats.iter_launches += 1;
-      ctx->stats.kernel_launches += 1;
     } else {
       StepParams sp{};
       sp.A = ctx->A; sp.lda = ctx->lda; sp.m = m; sp.n = n; sp.s = ctx->s;
@@ -525,7 +531,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       for (long long u = 0; u < cnt; u += U) {
         CK(cudaGraphLaunch(ctx->gexec, st));
         ctx->stats.iter_launches += 1;
-        ctx->stats.kernel_launches += 5LL * U;
+        graph_kernels += 5LL * U;
       }
     }
     CK(cudaEventRecord(ctx->ev1, st));
@@ -536,6 +542,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     if (fin.stopped) break;
   }
   if (max_iters == 0) fin = hs;
+  ctx->stats.kernel_launches = launches_total() - launches0 + graph_kernels;
   ctx->stats.phase1_ms += p1ms;
   ctx->stats.phase2_ms += p2ms;
   ctx->stats.iter_kernel_ms += p2ms;
@@ -736,6 +743,12 @@ kpp_status kpp_get_schedule(kpp_ctx* ctx, int64_t t0, int64_t count, int32_t* bl
   CK(cudaMemcpyAsync(block_id, ctx->bid, (size_t)count * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(is_fresh, ctx->fresh, (size_t)count, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return KPP_OK;
+}
+
+kpp_status kpp_clear_cache(kpp_ctx* ctx) {
+  if (!ctx) return KPP_EINVAL;
+  ctx->nb_gen = ctx->nb_ready = 0;
   return KPP_OK;
 }
 

@@ -102,6 +102,7 @@ __global__ void sumsq_kernel(const double* b, long long m, double* out) {
 void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info) {
   if (batch <= 0) return;
   chol_trtri_kernel<<<batch, CT, 0, st>>>(G, X, s, info);
+  count_launches(1);
 }
 
 void launch_gather_principal(cudaStream_t st, int batch, const double* A, long long lda,
@@ -110,15 +111,18 @@ void launch_gather_principal(cudaStream_t st, int batch, const double* A, long l
   if (batch <= 0) return;
   dim3 grid(s, batch);
   gather_principal_kernel<<<grid, 128, 0, st>>>(A, lda, S, s, lam, col_begin, col_end, G);
+  count_launches(1);
 }
 
 void launch_add_diag(cudaStream_t st, int batch, double* G, int s, double lam) {
   if (batch <= 0) return;
   add_diag_kernel<<<batch, 256, 0, st>>>(G, s, lam);
+  count_launches(1);
 }
 
 void launch_sumsq(cudaStream_t st, const double* b, long long m, double* out) {
   sumsq_kernel<<<1, 1024, 0, st>>>(b, m, out);
+  count_launches(1);
 }
 
 }  // namespace kpp

@@ -166,6 +166,7 @@ int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand&
     dgemm_kernel<true, false><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
   else
     dgemm_kernel<true, true><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
+  count_launches(1);
   return Z;
 }
 
@@ -179,6 +180,7 @@ void launch_splitk_reduce(cudaStream_t st, int batch, int M, int N, int Z, const
   dim3 grid(gx, batch);
   splitk_reduce_kernel<<<grid, 256, 0, st>>>(M, N, Z, part, p_bstride, diag_add, add, add_scale,
                                              add_bstride, out, o_bstride, upper_only);
+  count_launches(1);
 }
 
 }  // namespace kpp

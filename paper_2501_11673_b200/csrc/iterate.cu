@@ -177,6 +177,7 @@ cudaError_t launch_iterate(cudaStream_t stream, const IterParams& p, int grid, i
     cudaError_t e = cudaFuncSetAttribute(iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
+  count_launches(1);
   return cudaLaunchCooperativeKernel((const void*)iterate_kernel, dim3(grid), dim3(block), args, smem, stream);
 }
 

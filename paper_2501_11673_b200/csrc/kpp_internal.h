@@ -6,6 +6,10 @@
 
 namespace kpp {
 
+// Number of kernels this library has launched (process-wide; read by kpp_get_stats).
+void count_launches(long long k);
+long long launches_total();
+
 // Replicated solver state of one solve, persisted in device memory between
 // iteration-kernel launches (windows).  Every CTA of the persistent kernel keeps an
 // identical copy; CTA 0 writes it back at the end of a launch.

@@ -164,6 +164,7 @@ void launch_schedule(cudaStream_t st, uint64_t seed, double C, int memo, long lo
   if (count <= 0) return;
   sched_flags_kernel<<<(count + 255) / 256, 256, 0, st>>>(seed, C, memo, t0, count, fresh_out, word1_ws);
   sched_scan_kernel<<<1, 1024, 0, st>>>(count, nb_io, fresh_out, word1_ws, bid_out);
+  count_launches(2);
 }
 
 void launch_fresh_blocks(cudaStream_t st, uint64_t seed, long long pop, int s, long long k0,
@@ -173,6 +174,7 @@ void launch_fresh_blocks(cudaStream_t st, uint64_t seed, long long pop, int s, l
   while (nblk > 0) {
     const int g = (int)(nblk > 65535 ? 65535 : nblk);
     fresh_blocks_kernel<<<g, FB_THREADS, 0, st>>>(seed, pop, s, k0, S_pool);
+    count_launches(1);
     k0 += g;
     nblk -= g;
   }

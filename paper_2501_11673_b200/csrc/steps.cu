@@ -150,20 +150,25 @@ size_t step_update_smem(int s) { return (size_t)s * (sizeof(double) + sizeof(int
 
 void launch_step_partial(cudaStream_t st, const StepParams& p) {
   step_partial_kernel<<<p.grid, ST_THREADS, 0, st>>>(p);
+  count_launches(1);
 }
 void launch_step_reduce(cudaStream_t st, const StepParams& p) {
   step_reduce_kernel<<<(p.s + ST_WARPS - 1) / ST_WARPS, ST_THREADS, 0, st>>>(p);
+  count_launches(1);
 }
 void launch_step_solve(cudaStream_t st, const StepParams& p) {
   step_solve_kernel<<<(p.s + ST_WARPS - 1) / ST_WARPS, ST_THREADS, 0, st>>>(p);
+  count_launches(1);
 }
 void launch_step_update(cudaStream_t st, const StepParams& p) {
   const size_t sm = step_update_smem(p.s);
   if (sm > 48 * 1024) cudaFuncSetAttribute(step_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   step_update_kernel<<<p.grid, ST_THREADS, sm, st>>>(p);
+  count_launches(1);
 }
 void launch_step_window(cudaStream_t st, const StepParams& p) {
   step_window_kernel<<<1, 32, 0, st>>>(p);
+  count_launches(1);
 }
 
 }  // namespace kpp
