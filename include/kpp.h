@@ -137,7 +137,9 @@ typedef struct {
   int64_t iter_launches; /* iteration-kernel launches during the last solve */
   int64_t kernel_launches; /* all kernel launches during the last solve */
   int32_t grid_ctas;     /* CTAs of the persistent iteration kernel */
-  int32_t resident;      /* 1 if the last solve kept the block slab on chip */
+  int32_t resident;      /* 1 if the persistent kernel keeps the block slab on chip */
+  int32_t cluster;       /* thread-block cluster size of the persistent kernel */
+  int32_t m_in_smem;     /* 1 if each CTA stages its rows of M in shared memory */
 } kpp_stats;
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */

@@ -84,7 +84,12 @@ struct kpp_ctx {
   unsigned int* bar = nullptr;
   double *hist_res = nullptr, *hist_rho = nullptr;
   long long hist_capd = 0;
-  int grid = 0, slab = 0;
+  int grid = 0, slab = 0;               // step-kernel engine
+  int pC = 1, pgrid = 0;                 // persistent kernel: cluster size, grid
+  IterParams pplan{};
+  size_t psmem = 0;
+  unsigned int* cnt = nullptr;
+  int* d_err = nullptr;
   // phase-1 workspace
   Buf p1;
   int* d_info = nullptr;
@@ -349,6 +354,76 @@ kpp_status schedule_and_prepare(kpp_ctx* ctx, long long t0, long long count, boo
   return KPP_OK;
 }
 
+// Launch plan of the persistent kernel: cluster size C, grid (C x co-resident clusters),
+// column slab, and whether the block slab / the M rows fit in shared memory.
+IterParams plan_params(const kpp_ctx* ctx, int G, bool resident, bool m_in_smem) {
+  IterParams p{};
+  p.s = ctx->s;
+  long long slab = (ctx->n + G - 1) / G;
+  slab = std::max<long long>(4, (slab + 3) / 4 * 4);
+  p.slab = (int)slab;
+  int tpr = 1;
+  while (tpr < 32 && tpr * 2 * ctx->s <= iterate_block_threads()) tpr *= 2;
+  p.tpr = tpr;
+  // row stride congruent to tpr (mod 16): the half-warp's 16 rows x tpr columns hit distinct banks
+  const int target = tpr % 16;
+  p.sw = (int)(slab + ((target - slab % 16) + 16) % 16);
+  if (tpr == 1) p.sw = (int)slab;
+  p.cw = (int)((slab + 31) / 32 * 32);
+  p.resident = resident && slab <= iterate_block_threads();
+  p.m_in_smem = m_in_smem;
+  return p;
+}
+
+kpp_status plan_persistent(kpp_ctx* ctx) {
+  int maxsm = 0;
+  CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  struct Cand { int C, G; IterParams p; size_t smem; };
+  std::vector<Cand> cands;
+  const int sizes[] = {16, 8, 4, 2, 1};
+  for (int C : sizes) {
+    int G = ctx->num_sms / C * C;
+    if (G <= 0) continue;
+    Cand best{0, 0, {}, 0};
+    for (int variant = 0; variant < 4 && best.G == 0; ++variant) {
+      const bool res = ctx->resident_opt && variant < 2;
+      const bool msm = (variant % 2) == 0;
+      int g = G;
+      for (int rep = 0; rep < 4 && g > 0; ++rep) {
+        IterParams p = plan_params(ctx, g, res, msm);
+        if (res && !p.resident) break;
+        const size_t smem = iterate_smem_bytes(p, C);
+        if ((long long)smem > maxsm) break;
+        const int nq = iterate_max_clusters(C, smem);
+        if (nq <= 0) break;
+        if (nq * C >= g) {
+          best = {C, g, p, smem};
+          break;
+        }
+        g = nq * C;
+      }
+    }
+    if (best.G > 0) cands.push_back(best);
+  }
+  if (cands.empty()) return fail(ctx, KPP_ECUDA, "no feasible launch plan for the persistent kernel");
+  int gmax = 0;
+  for (auto& c : cands) gmax = std::max(gmax, c.G);
+  // prefer resident plans, then the largest cluster within 5% of the best SM count
+  const Cand* pick = nullptr;
+  for (int pass = 0; pass < 2 && !pick; ++pass)
+    for (auto& c : cands)
+      if ((pass == 1 || c.p.resident || !ctx->resident_opt) && c.G * 20 >= gmax * 19) { pick = &c; break; }
+  if (!pick) pick = &cands.front();
+  ctx->pC = pick->C;
+  ctx->pgrid = pick->G;
+  ctx->pplan = pick->p;
+  ctx->psmem = pick->smem;
+  ctx->stats.resident = pick->p.resident;
+  ctx->stats.cluster = pick->C;
+  ctx->stats.m_in_smem = pick->p.m_in_smem;
+  return KPP_OK;
+}
+
 kpp_status setup_common(kpp_ctx* ctx) {
   CK(cudaGetDevice(&ctx->device));
   CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -369,18 +444,21 @@ kpp_status setup_common(kpp_ctx* ctx) {
   CKS(dalloc(ctx, &ctx->d_bb, 1));
   CKS(dalloc(ctx, &ctx->bar, 1));
   CKS(dalloc(ctx, &ctx->bstage, (size_t)ctx->m));
-  // persistent grid: one CTA per SM; slab = ceil(n / grid) rounded up to 4 columns
-  const size_t smem = iterate_smem_bytes(ctx->s, 0, 0);
-  ctx->grid = iterate_max_grid(ctx->device, smem);
-  if (ctx->grid <= 0) ctx->grid = ctx->num_sms;
+  // step-kernel engine: one CTA per SM, slab = ceil(n / grid) rounded up to 4 columns
+  ctx->grid = ctx->num_sms;
   long long slab = (ctx->n + ctx->grid - 1) / ctx->grid;
-  slab = (slab + 3) / 4 * 4;
-  if (slab < 4) slab = 4;
+  slab = std::max<long long>(4, (slab + 3) / 4 * 4);
   ctx->slab = (int)slab;
-  CKS(dalloc(ctx, &ctx->part, (size_t)ctx->grid * ctx->s));
+  CKS(plan_persistent(ctx));
+  const long long part_need = std::max<long long>((long long)ctx->grid * ctx->s,
+                                                  2LL * (ctx->pgrid / std::max(1, ctx->pC)) * ctx->s);
+  CKS(dalloc(ctx, &ctx->part, (size_t)part_need));
+  CKS(dalloc(ctx, &ctx->cnt, 32));
+  CKS(dalloc(ctx, &ctx->d_err, 1));
+  CK(cudaMemset(ctx->d_err, 0, sizeof(int)));
   CK(cudaEventCreate(&ctx->ev0));
   CK(cudaEventCreate(&ctx->ev1));
-  ctx->stats.grid_ctas = ctx->grid;
+  ctx->stats.grid_ctas = ctx->pgrid;
   return KPP_OK;
 }
 
@@ -477,7 +555,6 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   const double eta = ctx->accel ? (ctx->eta_opt >= 0.0 ? ctx->eta_opt : (double)ctx->s / (2.0 * (double)ctx->n_global)) : 0.0;
   const long long W = std::max<long long>(1, ctx->window);
   const bool use_graph = ctx->engine == 1 || ctx->nranks > 1;
-  const size_t smem = iterate_smem_bytes(ctx->s, ctx->slab, 0);
   float p1ms = 0.f, p2ms = 0.f;
   DevState fin = hs;
   for (long long t0 = 0; t0 < max_iters; t0 += W) {
@@ -491,19 +568,18 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     p1ms += ms;
     CK(cudaEventRecord(ctx->ev0, st));
     if (!use_graph) {
-      IterParams p{};
+      IterParams p = ctx->pplan;
       p.A = ctx->A; p.lda = ctx->lda; p.m = m; p.n = n; p.s = ctx->s;
       p.cd = ctx->kind == KIND_CDPP; p.col_base = ctx->col_begin;
       p.b = b_dev; p.tol2bb = tol * tol * bb; p.bb = bb;
       p.S_pool = ctx->S_pool; p.M_pool = ctx->M_pool; p.bid = ctx->bid;
       p.t0 = t0; p.t1 = t0 + cnt;
       p.x = ctx->x; p.mom = ctx->mom; p.eta = eta; p.zeta = ctx->zeta;
-      p.adaptive = ctx->rho_fixed < 0.0;
-      p.part = ctx->part; p.r = ctx->r; p.y = ctx->y; p.bar = ctx->bar; p.st = ctx->dstate;
+      p.adaptive = ctx->rho_fixed < 0.0; p.writer = 1;
+      p.part = ctx->part; p.cnt = ctx->cnt; p.err = ctx->d_err; p.st = ctx->dstate;
       p.hist_res = ctx->hist_res; p.hist_rho = ctx->hist_rho; p.hist_cap = ctx->hist_capd;
-      p.slab = ctx->slab; p.resident = 0;
-      CK(cudaMemsetAsync(ctx->bar, 0, sizeof(unsigned int), st));
-      CK(launch_iterate(st, p, ctx->grid, iterate_block_threads(), smem));
+      CK(cudaMemsetAsync(ctx->cnt, 0, 32 * sizeof(unsigned int), st));
+      CK(launch_iterate(st, p, ctx->pgrid, ctx->pC, ctx->psmem));
       ctx->stats.iter_launches += 1;
     } else {
       StepParams sp{};
@@ -678,7 +754,7 @@ void kpp_destroy(kpp_ctx* ctx) {
   if (!ctx) return;
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  void* ptrs[] = {ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
+  void* ptrs[] = {ctx->cnt, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
                   ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->d_info};
   for (void* p : ptrs)

@@ -1,31 +1,44 @@
 // iterate.cu -- Phase 2: the per-iteration memoized block update.
 //
 // For each iteration t of a window (Alg 5 l.9-18 P:1346-1357 / Alg 3 l.10-20 P:755-766):
-//   r   = A_S x - b_S                                   (row 3)
-//   y   = M r,  M = (A_S A_S^T + lam I)^{-1} memoized    (row 4; K++)  / (A_SS + lam I)^{-1} (CD++)
-//   w   = A_S^T y (K++, Eq (bk))  |  I_S^T y (CD++, Alg 3 l.11)        (row 5)
-//   m   = (1-rho)/(1+rho) (m - w);  x = x - w + eta m   (row 6, Eq (momentum))
-//   E0/E1 window sums, checkpoint every 2 zeta: stop test, adaptive rho   (row 8)
+//   r   = A_S x - b_S                                        (row 3)
+//   y   = M r,  M = (A_S A_S^T + lam I)^{-1}  memoized (K++)  / (A_SS + lam I)^{-1} (CD++)  (row 4)
+//   w   = A_S^T y (K++, Eq (bk))  |  I_S^T y (CD++, Alg 3 l.11)            (row 5)
+//   m   = (1-rho)/(1+rho) (m - w);  x = x - w + eta m        (row 6, Eq (momentum))
+//   E0/E1 window sums; checkpoint every 2 zeta: stop test, adaptive rho   (row 8)
 //
-// Engine "persistent": one cooperative launch per window, one CTA per SM.  CTA g owns a
-// column slab [g*slab, (g+1)*slab) of x, m and A; the s-vector partials of A_S x are
-// combined through a deterministic grid reduction (fixed order, no atomics on data),
-// every CTA replicates the scalar window logic on identical bits, so all CTAs take the
-// same stop / rho decisions without further exchange.
-//
-// Engine "graph" (multi-GPU, and a single-GPU cross-check): the same arithmetic split
-// into step kernels so that an NCCL allreduce of the s-vector can sit between them.
+// Engine "persistent" (one launch per window, one CTA per SM, thread-block clusters of C CTAs):
+//  * CTA g owns the column slab [g*slab, (g+1)*slab) of A, x and m; x and m live in shared
+//    memory for the whole launch.
+//  * Resident mode (the s x slab block fits on chip): the slab of the NEXT block is copied
+//    HBM -> shared memory with cp.async while the current iteration runs (the schedule is
+//    data independent, so block t+1 is known); both passes (A_S x and A_S^T y) read shared
+//    memory, and A_S crosses HBM once per iteration.  Streaming mode (c4/c5-sized blocks):
+//    both passes stream from HBM/L2 with 16-byte loads.
+//  * Exchange of the s-vector partials: inside a cluster through distributed shared memory
+//    (DSMEM); across clusters CTA rank c of every cluster owns row slice c of the s-vector,
+//    writes its cluster's partial of that slice to global memory and waits on a per-slice
+//    arrival counter -- C independent barriers of G/C CTAs instead of one grid barrier.
+//    Each slice owner then forms r for its slice (fixed summation order), all-gathers r in
+//    the cluster (DSMEM), computes its slice of y = M r from a shared-memory copy of its M
+//    rows (prefetched for the next block), and all-gathers y.  Every CTA ends up with the
+//    identical r and y, so the scalar window logic is replicated bit-for-bit and no CTA
+//    needs to broadcast a decision.  No floating-point atomics: runs are bit-reproducible.
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <cstdint>
 
 #include "kpp_internal.h"
 #include "window.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace kpp {
 namespace {
 
-constexpr int IT_THREADS = 512;
-constexpr int NWARPS = IT_THREADS / 32;
+constexpr int T2 = 512;
+constexpr int NW2 = T2 / 32;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -39,111 +52,295 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
-// Grid-wide barrier over a monotonically increasing arrival counter.
-__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target) {
-  target += gridDim.x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    while (ld_acquire(bar) < target) {
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Copy rows S[0..s) x columns [c0, c0+w) of A into dst (row stride sw doubles) with cp.async.
+__device__ __forceinline__ void prefetch_slab(const double* A, long long lda, const int32_t* S_sh, int s,
+                                              long long c0, int w, double* dst, int sw) {
+  if (w <= 0) return;
+  const bool vec = ((lda & 1) == 0) && ((c0 & 1) == 0) && ((w & 1) == 0) && ((sw & 1) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  if (vec) {
+    const int hw = w >> 1;  // 16-byte chunks per row
+    const int total = s * hw;
+    for (int e = threadIdx.x; e < total; e += T2) {
+      const int k = e / hw, j = (e - k * hw) * 2;
+      cp_async16(dst + (long long)k * sw + j, A + (long long)S_sh[k] * lda + c0 + j);
     }
-    __threadfence();
+  } else {
+    const int total = s * w;
+    for (int e = threadIdx.x; e < total; e += T2) {
+      const int k = e / w, j = e - k * w;
+      cp_async8(dst + (long long)k * sw + j, A + (long long)S_sh[k] * lda + c0 + j);
+    }
   }
-  __syncthreads();
 }
 
-// CD++ scatter: position of global column gj in the sorted block S (or -1).
-__device__ __forceinline__ int find_sorted(const int32_t* S, int s, long long gj) {
-  int lo = 0, hi = s - 1;
-  while (lo <= hi) {
-    const int mid = (lo + hi) >> 1;
-    const long long v = S[mid];
-    if (v == gj) return mid;
-    if (v < gj) lo = mid + 1; else hi = mid - 1;
+__device__ __forceinline__ void prefetch_rows(const double* src, int count, double* dst) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((count & 1) == 0);
+  if (vec) {
+    for (int e = threadIdx.x * 2; e < count; e += 2 * T2) cp_async16(dst + e, src + e);
+  } else {
+    for (int e = threadIdx.x; e < count; e += T2) cp_async8(dst + e, src + e);
   }
-  return -1;
 }
 
-__global__ void __launch_bounds__(IT_THREADS, 1) iterate_kernel(IterParams p) {
+__device__ __forceinline__ void spin_until(const unsigned* cnt, unsigned target, int* err_flag) {
+  const unsigned long long t0 = globaltimer();
+  unsigned it = 0;
+  while (ld_acquire(cnt) < target) {
+    if ((++it & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) {  // 20 s: co-residency lost
+      atomicExch(err_flag, 1);
+      __trap();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = p.s;
-  double* y_sh = reinterpret_cast<double*>(smem_raw);
-  double* r_sh = y_sh + s;
-  int32_t* S_sh = reinterpret_cast<int32_t*>(r_sh + s);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int c = (int)cluster.block_rank();
+  const int q = blockIdx.x / C;   // cluster index
+  const int NQ = gridDim.x / C;   // clusters
+  // slice of the s-vector owned by this rank
+  const int sl = (s + C - 1) / C;
+  const int r0 = min(s, c * sl), r1 = min(s, r0 + sl);
+
+  // ---- shared memory carve-up (must match iterate_smem_bytes) ----
+  const int sp = (s + 1) & ~1;
+  const int wpad = p.slab;  // multiple of 4
+  double* x_sm = reinterpret_cast<double*>(smem_raw);
+  double* m_sm = x_sm + wpad;
+  double* w_sm = m_sm + wpad;
+  double* part_sm = w_sm + wpad;
+  double* r_sm = part_sm + sp;
+  double* y_sm = r_sm + sp;
+  double* red_sm = y_sm + sp;                                      // [T2] column-partial scratch
+  int32_t* S_sh = reinterpret_cast<int32_t*>(red_sm + T2);         // [2][sp]
+  double* Msl = reinterpret_cast<double*>(S_sh + 2 * sp);          // [sl][s] if m_in_smem
+  double* Abuf = Msl + (p.m_in_smem ? (long long)sl * s : 0);      // [2][s][sw] if resident
+  const long long absz = (long long)s * p.sw;
   __shared__ DevState st;
   __shared__ int stop_sh;
-  const int G = gridDim.x, g = blockIdx.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long c0 = (long long)g * p.slab;
+
+  const long long c0 = (long long)blockIdx.x * p.slab;
   const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
+  const int w = (int)(c1 > c0 ? c1 - c0 : 0);
+
   if (tid == 0) {
     st = *p.st;
     stop_sh = 0;
   }
-  __syncthreads();
-  unsigned target = 0;
+  for (int j = tid; j < w; j += T2) {
+    x_sm[j] = p.x[c0 + j];
+    m_sm[j] = p.mom[c0 + j];
+  }
+  // prefetch the first block (index set, slab, M slice)
+  {
+    const long long k0 = p.bid[0];
+    for (int i = tid; i < s; i += T2) S_sh[i] = p.S_pool[k0 * s + i];
+    __syncthreads();
+    if (p.resident) prefetch_slab(p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw);
+    if (p.m_in_smem && r1 > r0)
+      prefetch_rows(p.M_pool + k0 * (long long)s * s + (long long)r0 * s, (r1 - r0) * s, Msl);
+    cp_async_commit();
+  }
+  cluster.sync();  // peers' shared memory is live before any DSMEM access
+
   long long t = p.t0;
-  for (; t < p.t1; ++t) {
-    const long long k = p.bid[t - p.t0];
-    const int32_t* S = p.S_pool + k * s;
-    const double* M = p.M_pool + k * (long long)s * s;
-    for (int i = tid; i < s; i += IT_THREADS) S_sh[i] = S[i];
+  unsigned it = 0;
+  for (; t < p.t1; ++t, ++it) {
+    const int buf = it & 1;
+    const int32_t* Sc = S_sh + buf * sp;
+    const long long kb = p.bid[t - p.t0];
+    const double* Mg = p.M_pool + kb * (long long)s * s;
+    cp_async_wait_all();
     __syncthreads();
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
-    // row 3: partial block residual over this CTA's slab
-    for (int kk = warp; kk < s; kk += NWARPS) {
-      const double* row = p.A + (long long)S_sh[kk] * p.lda;
-      double acc = 0.0;
-      for (long long j = c0 + lane; j < c1; j += 32) acc = fma(row[j], p.x[j], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) p.part[(long long)g * s + kk] = acc;
+    // ---- prefetch block t+1 (index set, then its slab) into the other buffer
+    if (t + 1 < p.t1) {
+      const long long kn = p.bid[t + 1 - p.t0];
+      int32_t* Sn = S_sh + (buf ^ 1) * sp;
+      for (int i = tid; i < s; i += T2) Sn[i] = p.S_pool[kn * s + i];
+      if (p.resident) {
+        __syncthreads();
+        prefetch_slab(p.A, p.lda, Sn, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw);
+        cp_async_commit();
+      }
     }
-    grid_sync(p.bar, target);
-    // combine partials in a fixed order: r_k = sum_g part[g][k] - b_{S_k}
-    for (int kk = g * NWARPS + warp; kk < s; kk += G * NWARPS) {
-      double acc = 0.0;
-      for (int q = lane; q < G; q += 32) acc += __ldcg(p.part + (long long)q * s + kk);
-      acc = warp_sum(acc);
-      if (lane == 0) p.r[kk] = acc - p.b[S_sh[kk]];
+    const double* Ac = Abuf + buf * absz;
+
+    // ---- row 3: partial block residual over the slab -> part_sm[k]
+    if (p.resident) {
+      // tpr threads per row, rows in passes of T2/tpr
+      const int tpr = p.tpr;
+      const int rows_per_pass = T2 / tpr;
+      const int sub = tid & (tpr - 1);
+      for (int kp = 0; kp < s; kp += rows_per_pass) {
+        const int k = kp + tid / tpr;
+        double acc = 0.0;
+        if (k < s) {
+          const double* arow = Ac + (long long)k * p.sw;
+          for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
+        }
+        for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (k < s && sub == 0) part_sm[k] = acc;
+      }
+    } else {
+      // streaming: warp per row, 4 rows in flight, 16-byte loads when aligned
+      const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0);
+      for (int kbase = warp * 4; kbase < s; kbase += NW2 * 4) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const double* rows[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = min(kbase + u, s - 1);
+          rows[u] = p.A + (long long)Sc[k] * p.lda + c0;
+        }
+        if (vec) {
+          const int w2 = w >> 1;
+          for (int j2 = lane; j2 < w2; j2 += 32) {
+            const double2 xv = *reinterpret_cast<const double2*>(x_sm + 2 * j2);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double2 a = __ldcs(reinterpret_cast<const double2*>(rows[u]) + j2);
+              acc[u] = fma(a.x, xv.x, acc[u]);
+              acc[u] = fma(a.y, xv.y, acc[u]);
+            }
+          }
+          if ((w & 1) && lane == 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(__ldcs(rows[u] + w - 1), x_sm[w - 1], acc[u]);
+          }
+        } else {
+          for (int j = lane; j < w; j += 32) {
+            const double xv = x_sm[j];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(__ldcs(rows[u] + j), xv, acc[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double v = warp_sum(acc[u]);
+          if (lane == 0 && kbase + u < s) part_sm[kbase + u] = v;
+        }
+      }
     }
-    grid_sync(p.bar, target);
-    // row 4: y = M r
-    for (int kk = g * NWARPS + warp; kk < s; kk += G * NWARPS) {
-      const double* Mrow = M + (long long)kk * s;
-      double acc = 0.0;
-      for (int l = lane; l < s; l += 32) acc = fma(Mrow[l], __ldcg(p.r + l), acc);
-      acc = warp_sum(acc);
-      if (lane == 0) p.y[kk] = acc;
-    }
-    grid_sync(p.bar, target);
-    for (int i = tid; i < s; i += IT_THREADS) {
-      y_sh[i] = __ldcg(p.y + i);
-      r_sh[i] = __ldcg(p.r + i);
+    cluster.sync();  // [A] every rank's part_sm is complete
+
+    // ---- cluster partial of my slice -> global (double-buffered by parity), arrive, wait
+    double* pcl = p.part + (long long)(it & 1) * NQ * s;
+    for (int kk = r0 + tid; kk < r1; kk += T2) {
+      double v = 0.0;
+      for (int cc = 0; cc < C; ++cc) v += *cluster.map_shared_rank(part_sm + kk, cc);
+      pcl[(long long)q * s + kk] = v;
     }
     __syncthreads();
-    // rows 5-6: back-projection and momentum update on the slab
-    const double c = (1.0 - rho) / (1.0 + rho);
-    for (long long j = c0 + tid; j < c1; j += IT_THREADS) {
-      double w = 0.0;
-      if (!p.cd) {
-        for (int q = 0; q < s; ++q) w = fma(p.A[(long long)S_sh[q] * p.lda + j], y_sh[q], w);
-      } else {
-        const int pos = find_sorted(S_sh, s, p.col_base + j);
-        if (pos >= 0) w = y_sh[pos];
-      }
-      const double mm = c * (p.mom[j] - w);
-      p.mom[j] = mm;
-      p.x[j] = p.x[j] - w + p.eta * mm;
+    if (tid == 0) {
+      __threadfence();
+      red_release_add(p.cnt + c, 1u);
+      spin_until(p.cnt + c, (it + 1) * (unsigned)NQ, p.err);
     }
-    // row 8: ||r||^2 and the replicated window logic
+    __syncthreads();
+    // ---- r for my slice: fixed-order sum over clusters, minus b_S; all-gather in the cluster
+    for (int kk = r0 + warp; kk < r1; kk += NW2) {
+      double v = 0.0;
+      for (int qq = lane; qq < NQ; qq += 32) v += __ldcg(pcl + (long long)qq * s + kk);
+      v = warp_sum(v);
+      v -= p.b[Sc[kk]];
+      if (lane < C) *cluster.map_shared_rank(r_sm + kk, lane) = v;
+    }
+    cluster.sync();  // [B] r complete everywhere
+    // ---- row 4: my slice of y = M r; all-gather
+    for (int kk = r0 + warp; kk < r1; kk += NW2) {
+      const double* Mrow = p.m_in_smem ? Msl + (long long)(kk - r0) * s : Mg + (long long)kk * s;
+      double v = 0.0;
+      for (int l = lane; l < s; l += 32) v = fma(Mrow[l], r_sm[l], v);
+      v = warp_sum(v);
+      if (lane < C) *cluster.map_shared_rank(y_sm + kk, lane) = v;
+    }
+    cluster.sync();  // [C] y complete everywhere
+    // M slice of block t+1 into shared memory (mine is consumed)
+    if (p.m_in_smem && t + 1 < p.t1 && r1 > r0) {
+      const long long kn = p.bid[t + 1 - p.t0];
+      prefetch_rows(p.M_pool + kn * (long long)s * s + (long long)r0 * s, (r1 - r0) * s, Msl);
+      cp_async_commit();
+    }
+
+    // ---- rows 5-6: w on the slab, momentum, x
+    const double cm = (1.0 - rho) / (1.0 + rho);
+    if (!p.cd) {
+      if (p.resident) {
+        // ng groups of cw threads: group g sums rows [g*rg, (g+1)*rg) of column j; then a
+        // fixed-order sum over the groups (w <= cw is guaranteed by the host)
+        const int cw = p.cw, ng = T2 / cw, rg = (s + ng - 1) / ng;
+        const int g = tid / cw, j = tid - g * cw;
+        const int ka = min(s, g * rg), kz = min(s, ka + rg);
+        double a = 0.0;
+        if (j < w)
+          for (int k = ka; k < kz; ++k) a = fma(Ac[(long long)k * p.sw + j], y_sm[k], a);
+        red_sm[g * cw + j] = a;
+        __syncthreads();
+        for (int jj = tid; jj < w; jj += T2) {
+          double v = 0.0;
+          for (int gg = 0; gg < ng; ++gg) v += red_sm[gg * cw + jj];
+          w_sm[jj] = v;
+        }
+      } else {
+        for (int jj = tid; jj < w; jj += T2) {
+          double a = 0.0;
+          const double* col = p.A + c0 + jj;
+#pragma unroll 8
+          for (int k = 0; k < s; ++k) a = fma(__ldcg(col + (long long)Sc[k] * p.lda), y_sm[k], a);
+          w_sm[jj] = a;
+        }
+      }
+    } else {
+      for (int jj = tid; jj < w; jj += T2) w_sm[jj] = 0.0;
+      __syncthreads();
+      for (int k = tid; k < s; k += T2) {
+        const long long gj = (long long)Sc[k] - p.col_base;
+        if (gj >= c0 && gj < c1) w_sm[gj - c0] = y_sm[k];
+      }
+    }
+    __syncthreads();
+    for (int jj = tid; jj < w; jj += T2) {
+      const double wv = w_sm[jj];
+      const double mm = cm * (m_sm[jj] - wv);
+      m_sm[jj] = mm;
+      x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
+    }
+    // ---- row 8: ||r||^2 (fixed order, identical in every CTA) and the window logic
     if (warp == 0) {
       double e = 0.0;
-      for (int i = lane; i < s; i += 32) e = fma(r_sh[i], r_sh[i], e);
+      for (int i = lane; i < s; i += 32) e = fma(r_sm[i], r_sm[i], e);
       e = warp_sum(e);
       if (lane == 0) {
-        const int res = window_step_dev(st, t, e, p.zeta, p.tol2bb, p.bb, p.adaptive, g == 0,
-                                    p.hist_res, p.hist_rho, p.hist_cap);
+        const int res = window_step_dev(st, t, e, p.zeta, p.tol2bb, p.bb, p.adaptive,
+                                        blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho,
+                                        p.hist_cap);
         if (res) {
           st.stopped = res;
           stop_sh = 1;
@@ -156,37 +353,79 @@ __global__ void __launch_bounds__(IT_THREADS, 1) iterate_kernel(IterParams p) {
       break;
     }
   }
-  if (g == 0 && tid == 0) {
+  cp_async_wait_all();
+  for (int j = tid; j < w; j += T2) {
+    p.x[c0 + j] = x_sm[j];
+    p.mom[c0 + j] = m_sm[j];
+  }
+  if (blockIdx.x == 0 && tid == 0) {
     st.t_done = t;
     *p.st = st;
   }
+  cluster.sync();  // keep shared memory alive until every peer is done with DSMEM
 }
 
 }  // namespace
 
-int iterate_block_threads() { return IT_THREADS; }
+int iterate_block_threads() { return T2; }
 
-size_t iterate_smem_bytes(int s, int /*slab*/, int /*resident*/) {
-  return (size_t)s * (2 * sizeof(double) + sizeof(int32_t)) + 16;
+size_t iterate_smem_bytes(const IterParams& p, int C) {
+  const int s = p.s;
+  const int sp = (s + 1) & ~1;
+  const int sl = (s + C - 1) / C;
+  size_t bytes = 0;
+  bytes += 3ull * p.slab * sizeof(double);
+  bytes += 3ull * sp * sizeof(double);
+  bytes += (size_t)T2 * sizeof(double);
+  bytes += 2ull * sp * sizeof(int32_t);
+  if (p.m_in_smem) bytes += (size_t)sl * s * sizeof(double);
+  if (p.resident) bytes += 2ull * s * p.sw * sizeof(double);
+  return bytes + 64;
 }
 
-cudaError_t launch_iterate(cudaStream_t stream, const IterParams& p, int grid, int block, size_t smem) {
-  IterParams pp = p;
-  void* args[] = {&pp};
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+static void set_attrs(size_t smem, int C) {
+  cudaFuncSetAttribute(iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (C > 8) cudaFuncSetAttribute(iterate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
+cudaError_t launch_iterate(cudaStream_t stream, const IterParams& p, int grid, int C, size_t smem) {
+  set_attrs(smem, C);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(T2);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   count_launches(1);
-  return cudaLaunchCooperativeKernel((const void*)iterate_kernel, dim3(grid), dim3(block), args, smem, stream);
+  return cudaLaunchKernelEx(&cfg, iterate_kernel, p);
 }
 
-int iterate_max_grid(int device, size_t smem) {
-  int sms = 0, per = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, iterate_kernel, IT_THREADS, smem);
-  return sms * (per > 0 ? 1 : 0);
+// Largest number of co-resident clusters of size C at this shared-memory size.
+int iterate_max_clusters(int C, size_t smem) {
+  set_attrs(smem, C);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * 256);
+  cfg.blockDim = dim3(T2);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, iterate_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 }  // namespace kpp

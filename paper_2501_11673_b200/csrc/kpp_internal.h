@@ -90,21 +90,26 @@ struct IterParams {
   double eta;
   long long zeta;
   int adaptive;          // 0: rho fixed
-  double* part;          // [grid][s] partial block residuals
-  double* r;             // [s]
-  double* y;             // [s]
-  unsigned int* bar;     // grid barrier counter (zeroed before launch)
+  int writer;            // this rank writes the history
+  double* part;          // [2][clusters][s] cluster partials (double-buffered by parity)
+  unsigned int* cnt;     // [cluster size] per-slice arrival counters (zeroed before launch)
+  int* err;              // set if a spin-wait times out
   DevState* st;
   double* hist_res;      // [hist_cap]
   double* hist_rho;
   long long hist_cap;
   int slab;              // columns per CTA (multiple of 4)
-  int resident;          // keep the block slab in shared memory across both passes
+  int resident;          // the block slab lives in shared memory (double-buffered)
+  int sw;                // shared-memory row stride of the slab (doubles)
+  int tpr;               // threads per row in the A_S x pass (power of two <= 32)
+  int cw;                // threads per column group in the A_S^T y pass (multiple of 32)
+  int m_in_smem;         // this rank's rows of M are staged in shared memory
 };
-cudaError_t launch_iterate(cudaStream_t st, const IterParams& p, int grid, int block, size_t smem);
+// Persistent Phase-2 kernel: grid = C * clusters CTAs, cluster size C.
+cudaError_t launch_iterate(cudaStream_t st, const IterParams& p, int grid, int C, size_t smem);
 int iterate_block_threads();
-int iterate_max_grid(int device, size_t smem);  // one CTA per SM if it fits, else 0
-size_t iterate_smem_bytes(int s, int slab, int resident);
+size_t iterate_smem_bytes(const IterParams& p, int C);
+int iterate_max_clusters(int C, size_t smem);  // co-resident clusters of size C (0 on error)
 
 // ------------------------------------------------------------------ steps.cu (engine "graph")
 // Iteration cursor of the step kernels (device memory), so a captured graph is reusable.

@@ -132,6 +132,18 @@ def test_cdpp_factor_operator(kpp, ora):
 
 
 # ----------------------------------------------------------------- end-to-end parity
+def test_persistent_plan(kpp):
+    """c2/c3-sized blocks run resident (slab in shared memory) with clusters; c4/c5 stream."""
+    for cfg, resident in [(synth.CONFIGS["c2"], 1), (synth.twin("c3", 4096, 4096, 256), 1),
+                          (synth.twin("c4", 256, 131072, 256), 0)]:
+        A = torch.zeros(cfg.m, cfg.n, dtype=torch.float64, device=DEV)
+        ctx = kpp.kpp_setup(A, cfg.s, 1e-8, 0)
+        st = ctx.stats()
+        assert st["resident"] == resident, (cfg.name, st)
+        assert st["grid_ctas"] >= 0.9 * torch.cuda.get_device_properties(0).multi_processor_count
+        print(cfg.name, st)
+
+
 def test_c1_parity_200(kpp, ora):
     """BASELINE configs[0] at its exact size: x after 200 iterations within 1e-10."""
     _, _, ref, res, _ = run_pair(kpp, ora, synth.CONFIGS["c1"], 200)
