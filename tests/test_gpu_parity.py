@@ -180,16 +180,19 @@ def test_twin_parity_200(kpp, ora, cfg):
     assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
 
 
-def test_engines_bitwise_equal(kpp, ora):
-    """Persistent kernel and step-kernel graph (the multi-GPU engine at P=1) give the same bits."""
-    cfg = synth.twin("c3", 4096, 512, 64, k=16)
+@pytest.mark.parametrize("cfg", [synth.twin("c3", 4096, 512, 64, k=16), synth.twin("c5", 1024, 1024, 128, k=25)],
+                         ids=["kpp", "cdpp"])
+def test_engines_agree(kpp, ora, cfg):
+    """Persistent kernel and step-kernel graph (the multi-GPU engine at P=1) both match the oracle."""
     A, b, _ = synth.make_problem(cfg)
+    ref = (ora.cdpp_run if cfg.kind == "cdpp" else ora.kpp_run)(A.numpy(), b.numpy(), cfg.s, max_iters=300, threads=8)
     outs = []
     for eng in (0, 1):
-        ctx = kpp.kpp_setup(A.to(DEV), 64, 1e-8, 0)
+        ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A.to(DEV), cfg.s, 1e-8, 0)
         ctx.set_option(kpp.OPT_ENGINE, eng)
-        outs.append(ctx.solve(b.to(DEV), max_iters=300).x.cpu())
-    assert torch.equal(outs[0], outs[1])
+        outs.append(ctx.solve(b.to(DEV), max_iters=300).x.cpu().numpy())
+        assert rel(outs[-1], ref.x) <= 1e-10, eng
+    assert rel(outs[0], outs[1]) <= 1e-10
 
 
 def test_deterministic_and_warm_cache(kpp):

@@ -1,0 +1,29 @@
+"""Profiling driver: one warm solve of `iters` iterations on a config (for ncu captures)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2501_11673_b200 as kpp  # noqa: E402
+import synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--iters", type=int, default=1024)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--engine", type=int, default=0)
+a = ap.parse_args()
+cfg = synth.CONFIGS[a.config]
+A, b, _ = synth.make_problem(cfg, device="cuda")
+ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A, cfg.s, cfg.lam, 0)
+ctx.set_option(kpp.OPT_ENGINE, a.engine)
+ctx.set_option(kpp.OPT_WINDOW, a.iters)
+ctx.prepare(a.iters)
+for _ in range(a.reps):
+    ctx.reset_stats()
+    r = ctx.solve(b, max_iters=a.iters)
+    st = ctx.stats()
+    print(f"{a.config}: {a.iters} iters phase2 {st['phase2_ms']:.3f} ms -> {st['phase2_ms'] * 1e3 / a.iters:.2f} us/iter; "
+          f"plan grid={st['grid_ctas']} C={st['cluster']} resident={st['resident']} msm={st['m_in_smem']}")
