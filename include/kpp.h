@@ -71,8 +71,12 @@ typedef enum {
                              1 literal Gram + Cholesky -- same R in exact arithmetic */
   KPP_OPT_WINDOW = 6,     /* iterations per device window (default 8192; rounded to >= 1) */
   KPP_OPT_PHASE1_MB = 7,  /* device workspace budget for a Phase-1 batch, MiB (default 4096) */
-  KPP_OPT_RESIDENT = 8    /* 1 (default): keep the block slab on chip across both passes when it
+  KPP_OPT_RESIDENT = 8,   /* 1 (default): keep the block slab on chip across both passes when it
                              fits; 0: always stream A_S from HBM/L2 */
+  KPP_OPT_ENGINE = 9,     /* 0 (default on one GPU): persistent cluster kernel; 1: replayed CUDA
+                             graph of step kernels (the multi-GPU engine, NCCL between steps) */
+  KPP_OPT_CLUSTER = 10    /* 0 (default): choose the thread-block cluster size automatically;
+                             1, 2, 4, 8 or 16: force it (the grid shrinks to co-resident clusters) */
 } kpp_option;
 
 /* ---- setup ------------------------------------------------------------------ */

@@ -37,7 +37,6 @@ long long launches_total() { return g_launches.load(std::memory_order_relaxed); 
 namespace {
 
 enum { KIND_KPP = 0, KIND_CDPP = 1 };
-enum { OPT_ENGINE = 9 };  // private: 0 persistent (default on 1 GPU), 1 graph
 
 struct Buf {
   void* p = nullptr;
@@ -57,7 +56,7 @@ struct kpp_ctx {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   // options
-  int accel = 1, memo = 1, factor = 0, resident_opt = 1, engine = 0;
+  int accel = 1, memo = 1, factor = 0, resident_opt = 1, engine = 0, cluster_opt = 0;
   double eta_opt = -1.0, rho_fixed = -1.0;
   long long window = 8192, phase1_mb = 4096;
   cudaStream_t stream = nullptr;
@@ -382,6 +381,7 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
   std::vector<Cand> cands;
   const int sizes[] = {16, 8, 4, 2, 1};
   for (int C : sizes) {
+    if (ctx->cluster_opt && C != ctx->cluster_opt) continue;
     int G = ctx->num_sms / C * C;
     if (G <= 0) continue;
     Cand best{0, 0, {}, 0};
@@ -450,8 +450,7 @@ kpp_status setup_common(kpp_ctx* ctx) {
   slab = std::max<long long>(4, (slab + 3) / 4 * 4);
   ctx->slab = (int)slab;
   CKS(plan_persistent(ctx));
-  const long long part_need = std::max<long long>((long long)ctx->grid * ctx->s,
-                                                  2LL * (ctx->pgrid / std::max(1, ctx->pC)) * ctx->s);
+  const long long part_need = std::max<long long>((long long)ctx->grid * ctx->s, 2LL * ctx->num_sms * ctx->s);
   CKS(dalloc(ctx, &ctx->part, (size_t)part_need));
   CKS(dalloc(ctx, &ctx->cnt, 32));
   CKS(dalloc(ctx, &ctx->d_err, 1));
@@ -798,8 +797,14 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
       if (v < 1) return KPP_EINVAL;
       ctx->phase1_mb = (long long)v;
       break;
-    case KPP_OPT_RESIDENT: ctx->resident_opt = v != 0.0; break;
-    case OPT_ENGINE:
+    case KPP_OPT_RESIDENT:
+      ctx->resident_opt = v != 0.0;
+      return plan_persistent(ctx);
+    case KPP_OPT_CLUSTER:
+      if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8 && v != 16) return KPP_EINVAL;
+      ctx->cluster_opt = (int)v;
+      return plan_persistent(ctx);
+    case KPP_OPT_ENGINE:
       if (v != 0.0 && v != 1.0) return KPP_EINVAL;
       ctx->engine = (int)v;
       break;

@@ -73,24 +73,26 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* g) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// Copy rows S[0..s) x columns [c0, c0+w) of A into dst (row stride sw doubles) with cp.async.
+// Copy rows S[0..s) x columns [c0, c0+w) of A into dst (row stride sw doubles) with cp.async:
+// warp per row, lanes over 16-byte chunks (8-byte chunks when the row is not 16-byte aligned).
 __device__ __forceinline__ void prefetch_slab(const double* A, long long lda, const int32_t* S_sh, int s,
                                               long long c0, int w, double* dst, int sw) {
   if (w <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool vec = ((lda & 1) == 0) && ((c0 & 1) == 0) && ((w & 1) == 0) && ((sw & 1) == 0) &&
                    ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   if (vec) {
     const int hw = w >> 1;  // 16-byte chunks per row
-    const int total = s * hw;
-    for (int e = threadIdx.x; e < total; e += T2) {
-      const int k = e / hw, j = (e - k * hw) * 2;
-      cp_async16(dst + (long long)k * sw + j, A + (long long)S_sh[k] * lda + c0 + j);
+    for (int k = warp; k < s; k += T2 / 32) {
+      const double* src = A + (long long)S_sh[k] * lda + c0;
+      double* d = dst + (long long)k * sw;
+      for (int j = lane; j < hw; j += 32) cp_async16(d + 2 * j, src + 2 * j);
     }
   } else {
-    const int total = s * w;
-    for (int e = threadIdx.x; e < total; e += T2) {
-      const int k = e / w, j = e - k * w;
-      cp_async8(dst + (long long)k * sw + j, A + (long long)S_sh[k] * lda + c0 + j);
+    for (int k = warp; k < s; k += T2 / 32) {
+      const double* src = A + (long long)S_sh[k] * lda + c0;
+      double* d = dst + (long long)k * sw;
+      for (int j = lane; j < w; j += 32) cp_async8(d + j, src + j);
     }
   }
 }
@@ -264,22 +266,55 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
       spin_until(p.cnt + c, (it + 1) * (unsigned)NQ, p.err);
     }
     __syncthreads();
-    // ---- r for my slice: fixed-order sum over clusters, minus b_S; all-gather in the cluster
-    for (int kk = r0 + warp; kk < r1; kk += NW2) {
-      double v = 0.0;
-      for (int qq = lane; qq < NQ; qq += 32) v += __ldcg(pcl + (long long)qq * s + kk);
-      v = warp_sum(v);
-      v -= p.b[Sc[kk]];
-      if (lane < C) *cluster.map_shared_rank(r_sm + kk, lane) = v;
+    // ---- r for my slice: fixed-order sum over clusters, minus b_S; all-gather in the cluster.
+    // Every (row, cluster-group) pair loads at once; groups are then summed in a fixed order.
+    const int R = r1 - r0;
+    if (R > 0) {
+      const int G2 = R <= T2 ? T2 / R : 1;
+      for (int e = tid; e < R * G2 && e < T2; e += T2) {
+        const int row = e % R, grp = e / R;
+        double v = 0.0;
+        for (int qq = grp; qq < NQ; qq += G2) v += __ldcg(pcl + (long long)qq * s + r0 + row);
+        red_sm[grp * R + row] = v;
+      }
+      if (R > T2) {  // very large slices (s > T2 * C): one thread per row, all clusters
+        for (int row = tid; row < R; row += T2) {
+          double v = 0.0;
+          for (int qq = 0; qq < NQ; qq += 1) v += __ldcg(pcl + (long long)qq * s + r0 + row);
+          r_sm[r0 + row] = v;  // local staging; subtract b and scatter below
+        }
+      }
+      __syncthreads();
+      for (int row = tid; row < R; row += T2) {
+        double v;
+        if (R <= T2) {
+          v = 0.0;
+          for (int grp = 0; grp < G2; ++grp) v += red_sm[grp * R + row];
+        } else {
+          v = r_sm[r0 + row];
+        }
+        v -= p.b[Sc[r0 + row]];
+        for (int cc = 0; cc < C; ++cc) *cluster.map_shared_rank(r_sm + r0 + row, cc) = v;
+      }
     }
     cluster.sync();  // [B] r complete everywhere
-    // ---- row 4: my slice of y = M r; all-gather
-    for (int kk = r0 + warp; kk < r1; kk += NW2) {
-      const double* Mrow = p.m_in_smem ? Msl + (long long)(kk - r0) * s : Mg + (long long)kk * s;
-      double v = 0.0;
-      for (int l = lane; l < s; l += 32) v = fma(Mrow[l], r_sm[l], v);
-      v = warp_sum(v);
-      if (lane < C) *cluster.map_shared_rank(y_sm + kk, lane) = v;
+    // ---- row 4: my slice of y = M r (tq threads per row, shuffle-combined); all-gather
+    if (R > 0) {
+      int tq = 1;
+      while (tq < 32 && tq * 2 * R <= T2) tq *= 2;
+      const int rows_per_pass = T2 / tq;
+      const int sub = tid & (tq - 1);
+      for (int rp = 0; rp < R; rp += rows_per_pass) {
+        const int row = rp + tid / tq;
+        double v = 0.0;
+        if (row < R) {
+          const double* Mrow = p.m_in_smem ? Msl + (long long)row * s : Mg + (long long)(r0 + row) * s;
+          for (int l = sub; l < s; l += tq) v = fma(Mrow[l], r_sm[l], v);
+        }
+        for (int o = tq >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (row < R)
+          for (int cc = sub; cc < C; cc += tq) *cluster.map_shared_rank(y_sm + r0 + row, cc) = v;
+      }
     }
     cluster.sync();  // [C] y complete everywhere
     // M slice of block t+1 into shared memory (mine is consumed)

@@ -14,11 +14,13 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--iters", type=int, default=1024)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--engine", type=int, default=0)
+ap.add_argument("--cluster", type=int, default=0)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 A, b, _ = synth.make_problem(cfg, device="cuda")
 ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A, cfg.s, cfg.lam, 0)
 ctx.set_option(kpp.OPT_ENGINE, a.engine)
+ctx.set_option(kpp.OPT_CLUSTER, a.cluster)
 ctx.set_option(kpp.OPT_WINDOW, a.iters)
 ctx.prepare(a.iters)
 for _ in range(a.reps):
