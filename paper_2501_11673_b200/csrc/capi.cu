@@ -419,6 +419,7 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
   ctx->pplan = pick->p;
   ctx->psmem = pick->smem;
   ctx->stats.resident = pick->p.resident;
+  ctx->stats.grid_ctas = pick->G;
   ctx->stats.cluster = pick->C;
   ctx->stats.m_in_smem = pick->p.m_in_smem;
   return KPP_OK;

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
   double* red_sm = y_sm + sp;                                      // [T2] column-partial scratch
   int32_t* S_sh = reinterpret_cast<int32_t*>(red_sm + T2);         // [2][sp]
   double* Msl = reinterpret_cast<double*>(S_sh + 2 * sp);          // [sl][s] if m_in_smem
-  double* Abuf = Msl + (p.m_in_smem ? (long long)sl * s : 0);      // [2][s][sw] if resident
+  double* Abuf = Msl + (p.m_in_smem ? (((long long)sl * s + 1) & ~1LL) : 0);  // [2][s][sw] if resident (16B aligned)
   const long long absz = (long long)s * p.sw;
   __shared__ DevState st;
   __shared__ int stop_sh;
@@ -413,7 +413,7 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   bytes += 3ull * sp * sizeof(double);
   bytes += (size_t)T2 * sizeof(double);
   bytes += 2ull * sp * sizeof(int32_t);
-  if (p.m_in_smem) bytes += (size_t)sl * s * sizeof(double);
+  if (p.m_in_smem) bytes += (size_t)(((long long)sl * s + 1) & ~1LL) * sizeof(double);
   if (p.resident) bytes += 2ull * s * p.sw * sizeof(double);
   return bytes + 64;
 }
