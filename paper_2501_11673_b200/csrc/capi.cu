@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -89,6 +90,7 @@ struct kpp_ctx {
   size_t psmem = 0;
   unsigned int* cnt = nullptr;
   int* d_err = nullptr;
+  long long* d_prof = nullptr;
   // phase-1 workspace
   Buf p1;
   int* d_info = nullptr;
@@ -579,6 +581,13 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       p.part = ctx->part; p.cnt = ctx->cnt; p.err = ctx->d_err; p.st = ctx->dstate;
       p.hist_res = ctx->hist_res; p.hist_rho = ctx->hist_rho; p.hist_cap = ctx->hist_capd;
       CK(cudaMemsetAsync(ctx->cnt, 0, 32 * sizeof(unsigned int), st));
+      if (getenv("KPP_PHASE_PROFILE")) {
+        if (!ctx->d_prof) {
+          CKS(dalloc(ctx, &ctx->d_prof, 8));
+          CK(cudaMemset(ctx->d_prof, 0, 8 * sizeof(long long)));
+        }
+        p.prof = ctx->d_prof;
+      }
       CK(launch_iterate(st, p, ctx->pgrid, ctx->pC, ctx->psmem));
       ctx->stats.iter_launches += 1;
     } else {
@@ -634,6 +643,16 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   CK(cudaStreamSynchronize(st));
   if (n_hist) *n_hist = nh;
   if (iters_out) *iters_out = max_iters == 0 ? 0 : fin.t_done;
+  if (ctx->d_prof && fin.t_done > 0) {
+    long long pr[8];
+    CK(cudaMemcpy(pr, ctx->d_prof, sizeof pr, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(ctx->d_prof, 0, sizeof pr));
+    const char* names[8] = {"wait_prefetch", "issue_prefetch", "rows3_Ax", "barA_clpart", "xcluster_wait",
+                            "r_gather_barB", "y_barC", "rows56_window"};
+    fprintf(stderr, "[kpp phase cycles/iter, CTA 0]");
+    for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
+    fprintf(stderr, "\n");
+  }
   if (fin.stopped == 2) return fail(ctx, KPP_EDIVERGED, "non-finite block residual at iteration %lld", fin.t_done - 1);
   if (fin.stopped == 1) return KPP_OK;
   return KPP_EMAXITER;
@@ -754,7 +773,7 @@ void kpp_destroy(kpp_ctx* ctx) {
   if (!ctx) return;
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  void* ptrs[] = {ctx->cnt, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
+  void* ptrs[] = {ctx->d_prof, ctx->cnt, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
                   ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->d_info};
   for (void* p : ptrs)

@@ -117,6 +117,16 @@ __device__ __forceinline__ void spin_until(const unsigned* cnt, unsigned target,
   }
 }
 
+// Optional phase timers (CTA 0, thread 0): cumulative clock64 cycles per phase -> p.prof[8].
+#define PHASE_MARK(i)                                   \
+  do {                                                  \
+    if (prof_on) {                                      \
+      const long long now_ = clock64();                 \
+      prof_acc[i] += now_ - prof_last;                  \
+      prof_last = now_;                                 \
+    }                                                   \
+  } while (0)
+
 __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = p.s;
@@ -171,6 +181,9 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
   }
   cluster.sync();  // peers' shared memory is live before any DSMEM access
 
+  const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_last = prof_on ? clock64() : 0;
   long long t = p.t0;
   unsigned it = 0;
   for (; t < p.t1; ++t, ++it) {
@@ -180,6 +193,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
     const double* Mg = p.M_pool + kb * (long long)s * s;
     cp_async_wait_all();
     __syncthreads();
+    PHASE_MARK(0);  // wait for this iteration's prefetched slab + previous iteration tail
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
     // ---- prefetch block t+1 (index set, then its slab) into the other buffer
     if (t + 1 < p.t1) {
@@ -193,6 +207,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
       }
     }
     const double* Ac = Abuf + buf * absz;
+    PHASE_MARK(1);  // issue of the next prefetch
 
     // ---- row 3: partial block residual over the slab -> part_sm[k]
     if (p.resident) {
@@ -250,6 +265,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
         }
       }
     }
+    PHASE_MARK(2);  // row 3 (A_S x partials)
     cluster.sync();  // [A] every rank's part_sm is complete
 
     // ---- cluster partial of my slice -> global (double-buffered by parity), arrive, wait
@@ -262,8 +278,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
     __syncthreads();
     if (tid == 0) {
       __threadfence();
+      PHASE_MARK(3);  // cluster barrier A + cluster partial of the slice
       red_release_add(p.cnt + c, 1u);
       spin_until(p.cnt + c, (it + 1) * (unsigned)NQ, p.err);
+      PHASE_MARK(4);  // cross-cluster arrival wait
     }
     __syncthreads();
     // ---- r for my slice: fixed-order sum over clusters, minus b_S; all-gather in the cluster.
@@ -298,6 +316,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
       }
     }
     cluster.sync();  // [B] r complete everywhere
+    PHASE_MARK(5);  // r slice gather + all-gather + barrier B
     // ---- row 4: my slice of y = M r (tq threads per row, shuffle-combined); all-gather
     if (R > 0) {
       int tq = 1;
@@ -317,6 +336,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
       }
     }
     cluster.sync();  // [C] y complete everywhere
+    PHASE_MARK(6);  // y slice + all-gather + barrier C
     // M slice of block t+1 into shared memory (mine is consumed)
     if (p.m_in_smem && t + 1 < p.t1 && r1 > r0) {
       const long long kn = p.bid[t + 1 - p.t0];
@@ -383,11 +403,14 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
       }
     }
     __syncthreads();
+    PHASE_MARK(7);  // rows 5-6 (A_S^T y, momentum) + window logic
     if (stop_sh) {
       ++t;
       break;
     }
   }
+  if (prof_on)
+    for (int i = 0; i < 8; ++i) p.prof[i] += prof_acc[i];
   cp_async_wait_all();
   for (int j = tid; j < w; j += T2) {
     p.x[c0 + j] = x_sm[j];
