@@ -88,7 +88,8 @@ struct kpp_ctx {
   int pC = 1, pgrid = 0;                 // persistent kernel: cluster size, grid
   IterParams pplan{};
   size_t psmem = 0;
-  unsigned int* cnt = nullptr;
+  unsigned long long* d_ll = nullptr;
+  size_t ll_bytes = 0;
   int* d_err = nullptr;
   long long* d_prof = nullptr;
   // phase-1 workspace
@@ -455,7 +456,8 @@ kpp_status setup_common(kpp_ctx* ctx) {
   CKS(plan_persistent(ctx));
   const long long part_need = std::max<long long>((long long)ctx->grid * ctx->s, 2LL * ctx->num_sms * ctx->s);
   CKS(dalloc(ctx, &ctx->part, (size_t)part_need));
-  CKS(dalloc(ctx, &ctx->cnt, 32));
+  ctx->ll_bytes = (size_t)2 * ctx->num_sms * ctx->s * 2 * sizeof(unsigned long long);
+  CKS(dalloc(ctx, &ctx->d_ll, ctx->ll_bytes / sizeof(unsigned long long)));
   CKS(dalloc(ctx, &ctx->d_err, 1));
   CK(cudaMemset(ctx->d_err, 0, sizeof(int)));
   CK(cudaEventCreate(&ctx->ev0));
@@ -578,9 +580,9 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       p.t0 = t0; p.t1 = t0 + cnt;
       p.x = ctx->x; p.mom = ctx->mom; p.eta = eta; p.zeta = ctx->zeta;
       p.adaptive = ctx->rho_fixed < 0.0; p.writer = 1;
-      p.part = ctx->part; p.cnt = ctx->cnt; p.err = ctx->d_err; p.st = ctx->dstate;
+      p.ll = ctx->d_ll; p.err = ctx->d_err; p.st = ctx->dstate;
       p.hist_res = ctx->hist_res; p.hist_rho = ctx->hist_rho; p.hist_cap = ctx->hist_capd;
-      CK(cudaMemsetAsync(ctx->cnt, 0, 32 * sizeof(unsigned int), st));
+      CK(cudaMemsetAsync(ctx->d_ll, 0, ctx->ll_bytes, st));
       if (getenv("KPP_PHASE_PROFILE")) {
         if (!ctx->d_prof) {
           CKS(dalloc(ctx, &ctx->d_prof, 8));
@@ -773,7 +775,7 @@ void kpp_destroy(kpp_ctx* ctx) {
   if (!ctx) return;
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  void* ptrs[] = {ctx->d_prof, ctx->cnt, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
+  void* ptrs[] = {ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
                   ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->d_info};
   for (void* p : ptrs)

@@ -7,23 +7,26 @@
 //   m   = (1-rho)/(1+rho) (m - w);  x = x - w + eta m        (row 6, Eq (momentum))
 //   E0/E1 window sums; checkpoint every 2 zeta: stop test, adaptive rho   (row 8)
 //
-// Engine "persistent" (one launch per window, one CTA per SM, thread-block clusters of C CTAs):
-//  * CTA g owns the column slab [g*slab, (g+1)*slab) of A, x and m; x and m live in shared
+// Engine "persistent": one launch per window, one CTA per SM, thread-block clusters of C CTAs.
+//  * CTA g owns the column slab [g*slab, (g+1)*slab) of A, x and m; x and m stay in shared
 //    memory for the whole launch.
-//  * Resident mode (the s x slab block fits on chip): the slab of the NEXT block is copied
-//    HBM -> shared memory with cp.async while the current iteration runs (the schedule is
-//    data independent, so block t+1 is known); both passes (A_S x and A_S^T y) read shared
-//    memory, and A_S crosses HBM once per iteration.  Streaming mode (c4/c5-sized blocks):
-//    both passes stream from HBM/L2 with 16-byte loads.
-//  * Exchange of the s-vector partials: inside a cluster through distributed shared memory
-//    (DSMEM); across clusters CTA rank c of every cluster owns row slice c of the s-vector,
-//    writes its cluster's partial of that slice to global memory and waits on a per-slice
-//    arrival counter -- C independent barriers of G/C CTAs instead of one grid barrier.
-//    Each slice owner then forms r for its slice (fixed summation order), all-gathers r in
-//    the cluster (DSMEM), computes its slice of y = M r from a shared-memory copy of its M
-//    rows (prefetched for the next block), and all-gathers y.  Every CTA ends up with the
-//    identical r and y, so the scalar window logic is replicated bit-for-bit and no CTA
-//    needs to broadcast a decision.  No floating-point atomics: runs are bit-reproducible.
+//  * Resident mode (the s x slab block fits on chip): the block schedule is data independent,
+//    so while iteration t runs, the TMA engine (cp.async.bulk, one bulk copy per row segment,
+//    completion on an mbarrier) brings the slab of block t+1 into the other half of a
+//    double buffer, and the M rows this CTA needs for t+1 into a staging buffer.  Both
+//    passes (A_S x and A_S^T y) read shared memory and A_S crosses HBM once per iteration.
+//    Streaming mode (c4/c5-sized blocks): both passes stream 16-byte loads from HBM/L2.
+//  * The one all-reduce of the iteration (the s-vector A_S x) is a barrier-free dataflow
+//    exchange.  Every value travels as two 8-byte words, each carrying 32 data bits and a
+//    32-bit iteration tag (the "LL" protocol of NCCL): an 8-byte store is single-copy
+//    atomic, so a consumer that polls a word and sees the current tag has the data -- no
+//    flag round trip, no cluster barrier on the critical path.
+//      partials --DSMEM--> slice owner in the cluster (rank c owns rows slice c)
+//      cluster partial of the slice --L2--> the slice owners of every cluster
+//      r slice (fixed-order sum, - b_S) --DSMEM--> every CTA of the cluster
+//      y slice = M[slice] r --DSMEM--> every CTA of the cluster
+//    Every CTA then holds identical r and y, so the scalar window logic is replicated
+//    bit-for-bit and nobody broadcasts a decision.  No floating-point atomics anywhere.
 #include <cooperative_groups.h>
 
 #include <cmath>
@@ -46,113 +49,163 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
+// ------------------------------------------------------------------ LL words
+// value v with tag g -> two words (g << 32 | lo32(v)), (g << 32 | hi32(v))
+__device__ __forceinline__ void ll_store(unsigned long long* dst, double v, unsigned tag) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long t = (unsigned long long)tag << 32;
+  volatile unsigned long long* d = dst;
+  d[0] = t | (u & 0xffffffffull);
+  d[1] = t | (u >> 32);
 }
+__device__ __forceinline__ void ll_store_global(unsigned long long* dst, double v, unsigned tag) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long t = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(dst), "l"(t | (u & 0xffffffffull)),
+               "l"(t | (u >> 32))
+               : "memory");
+}
+__device__ __noinline__ void spin_fail(int* err) {
+  atomicExch(err, 1);
+  __trap();
+}
+// poll a word pair in (local) shared memory until both carry `tag`
+__device__ __forceinline__ double ll_wait_shared(const unsigned long long* src, unsigned tag, int* err) {
+  volatile const unsigned long long* s = src;
+  unsigned long long a = s[0], b = s[1];
+  if ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
+    const unsigned long long t0 = globaltimer();
+    unsigned n = 0;
+    while ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
+      a = s[0];
+      b = s[1];
+      if ((++n & 4095u) == 0 && globaltimer() - t0 > 20000000000ull) spin_fail(err);
+    }
+  }
+  return __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
+}
+__device__ __forceinline__ double ll_wait_global(const unsigned long long* src, unsigned tag, int* err) {
+  unsigned long long a, b;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+  if ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
+    const unsigned long long t0 = globaltimer();
+    unsigned n = 0;
+    while ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
+      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+      if ((++n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) spin_fail(err);
+    }
+  }
+  return __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
+}
+
+// ------------------------------------------------------------------ TMA bulk copies + mbarriers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// cp.async fallback (rows that are not 16-byte aligned)
 __device__ __forceinline__ void cp_async8(void* smem, const void* g) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// Copy rows S[0..s) x columns [c0, c0+w) of A into dst (row stride sw doubles) with cp.async:
-// warp per row, lanes over 16-byte chunks (8-byte chunks when the row is not 16-byte aligned).
-__device__ __forceinline__ void prefetch_slab(const double* A, long long lda, const int32_t* S_sh, int s,
-                                              long long c0, int w, double* dst, int sw) {
-  if (w <= 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool vec = ((lda & 1) == 0) && ((c0 & 1) == 0) && ((w & 1) == 0) && ((sw & 1) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-  if (vec) {
-    const int hw = w >> 1;  // 16-byte chunks per row
-    for (int k = warp; k < s; k += T2 / 32) {
-      const double* src = A + (long long)S_sh[k] * lda + c0;
-      double* d = dst + (long long)k * sw;
-      for (int j = lane; j < hw; j += 32) cp_async16(d + 2 * j, src + 2 * j);
-    }
+// Warp 0: load s row segments of the slab (and optionally `mcount` doubles of M rows).
+// bulk: TMA bulk copies completing on `bar` (lane 0 registers the byte count first);
+// otherwise 8-byte cp.async (waited with cp.async.wait_group by warp 0).
+__device__ __forceinline__ void issue_loads(bool bulk, const double* A, long long lda, const int32_t* S, int s,
+                                            long long c0, int w, double* adst, int sw, bool slab,
+                                            const double* msrc, int mcount, double* mdst,
+                                            unsigned long long* bar) {
+  const int lane = threadIdx.x & 31;
+  if (bulk) {
+    unsigned bytes = 0;
+    if (slab && w > 0) bytes += (unsigned)s * (unsigned)w * 8u;
+    if (msrc && mcount > 0) bytes += (unsigned)mcount * 8u;
+    if (lane == 0) mbar_expect_tx(bar, bytes);
+    __syncwarp();
+    if (slab && w > 0)
+      for (int k = lane; k < s; k += 32)
+        bulk_g2s(adst + (long long)k * sw, A + (long long)S[k] * lda + c0, (unsigned)w * 8u, bar);
+    if (msrc && mcount > 0 && lane == 0) bulk_g2s(mdst, msrc, (unsigned)mcount * 8u, bar);
   } else {
-    for (int k = warp; k < s; k += T2 / 32) {
-      const double* src = A + (long long)S_sh[k] * lda + c0;
-      double* d = dst + (long long)k * sw;
-      for (int j = lane; j < w; j += 32) cp_async8(d + j, src + j);
-    }
+    if (slab)
+      for (int k = 0; k < s; ++k) {
+        const double* src = A + (long long)S[k] * lda + c0;
+        double* d = adst + (long long)k * sw;
+        for (int j = lane; j < w; j += 32) cp_async8(d + j, src + j);
+      }
+    if (msrc)
+      for (int e = lane; e < mcount; e += 32) cp_async8(mdst + e, msrc + e);
+    cp_async_commit();
   }
 }
 
-__device__ __forceinline__ void prefetch_rows(const double* src, int count, double* dst) {
-  const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((count & 1) == 0);
-  if (vec) {
-    for (int e = threadIdx.x * 2; e < count; e += 2 * T2) cp_async16(dst + e, src + e);
-  } else {
-    for (int e = threadIdx.x; e < count; e += T2) cp_async8(dst + e, src + e);
-  }
-}
-
-__device__ __forceinline__ void spin_until(const unsigned* cnt, unsigned target, int* err_flag) {
-  const unsigned long long t0 = globaltimer();
-  unsigned it = 0;
-  while (ld_acquire(cnt) < target) {
-    if ((++it & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) {  // 20 s: co-residency lost
-      atomicExch(err_flag, 1);
-      __trap();
-    }
-  }
-}
-
-// Optional phase timers (CTA 0, thread 0): cumulative clock64 cycles per phase -> p.prof[8].
-#define PHASE_MARK(i)                                   \
-  do {                                                  \
-    if (prof_on) {                                      \
-      const long long now_ = clock64();                 \
-      prof_acc[i] += now_ - prof_last;                  \
-      prof_last = now_;                                 \
-    }                                                   \
+#define PHASE_MARK(i)                   \
+  do {                                  \
+    if (prof_on) {                      \
+      const long long now_ = clock64(); \
+      prof_acc[i] += now_ - prof_last;  \
+      prof_last = now_;                 \
+    }                                   \
   } while (0)
 
 __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int s = p.s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
   const int c = (int)cluster.block_rank();
-  const int q = blockIdx.x / C;   // cluster index
-  const int NQ = gridDim.x / C;   // clusters
-  // slice of the s-vector owned by this rank
-  const int sl = (s + C - 1) / C;
+  const int q = blockIdx.x / C;    // cluster index
+  const int NQ = gridDim.x / C;    // clusters
+  const int sl = (s + C - 1) / C;  // rank cc owns rows [cc*sl, min(s, cc*sl + sl))
   const int r0 = min(s, c * sl), r1 = min(s, r0 + sl);
+  const int R = r1 - r0;
 
   // ---- shared memory carve-up (must match iterate_smem_bytes) ----
   const int sp = (s + 1) & ~1;
-  const int wpad = p.slab;  // multiple of 4
-  double* x_sm = reinterpret_cast<double*>(smem_raw);
-  double* m_sm = x_sm + wpad;
-  double* w_sm = m_sm + wpad;
-  double* part_sm = w_sm + wpad;
-  double* r_sm = part_sm + sp;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // [4] mbarriers
+  unsigned long long* rp_ll = bars + 4;                 // [2][C][sl][2]  partials for my slice
+  unsigned long long* r_ll = rp_ll + 4LL * C * sl;      // [2][s][2]
+  unsigned long long* y_ll = r_ll + 4LL * s;            // [2][s][2]
+  double* x_sm = reinterpret_cast<double*>(y_ll + 4LL * s);
+  double* m_sm = x_sm + p.slab;
+  double* w_sm = m_sm + p.slab;
+  double* r_sm = w_sm + p.slab;
   double* y_sm = r_sm + sp;
-  double* red_sm = y_sm + sp;                                      // [T2] column-partial scratch
-  int32_t* S_sh = reinterpret_cast<int32_t*>(red_sm + T2);         // [2][sp]
-  double* Msl = reinterpret_cast<double*>(S_sh + 2 * sp);          // [sl][s] if m_in_smem
-  double* Abuf = Msl + (p.m_in_smem ? (((long long)sl * s + 1) & ~1LL) : 0);  // [2][s][sw] if resident (16B aligned)
+  double* red_sm = y_sm + sp;                               // [T2]
+  int32_t* S_sh = reinterpret_cast<int32_t*>(red_sm + T2);  // [3][sp]
+  unsigned char* tail = reinterpret_cast<unsigned char*>(S_sh + 3 * sp);
+  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  double* Msl = reinterpret_cast<double*>(tail);                                   // [sl][s]
+  double* Abuf = Msl + (p.m_in_smem ? (((long long)sl * s + 1) & ~1LL) : 0);      // [2][s][sw]
   const long long absz = (long long)s * p.sw;
   __shared__ DevState st;
   __shared__ int stop_sh;
@@ -160,58 +213,77 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
   const long long c0 = (long long)blockIdx.x * p.slab;
   const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
   const int w = (int)(c1 > c0 ? c1 - c0 : 0);
+  // TMA eligibility: 16-byte aligned row segments of a multiple of 16 bytes, aligned M slices
+  const bool bulkA = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((w & 1) == 0) && ((p.sw & 1) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
+  const bool bulkM = ((s & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.M_pool) & 15) == 0);
+  const bool bulk = (!p.resident || bulkA) && (!p.m_in_smem || bulkM);
+  const long long ss = (long long)s * s;
+  const bool stageM = p.m_in_smem && R > 0;
 
   if (tid == 0) {
     st = *p.st;
     stop_sh = 0;
+    for (int i = 0; i < 4; ++i) mbar_init(bars + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  for (long long i = tid; i < 4LL * C * sl + 8LL * s; i += T2) rp_ll[i] = 0ull;  // tags start at 1
   for (int j = tid; j < w; j += T2) {
     x_sm[j] = p.x[c0 + j];
     m_sm[j] = p.mom[c0 + j];
   }
-  // prefetch the first block (index set, slab, M slice)
-  {
-    const long long k0 = p.bid[0];
-    for (int i = tid; i < s; i += T2) S_sh[i] = p.S_pool[k0 * s + i];
-    __syncthreads();
-    if (p.resident) prefetch_slab(p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw);
-    if (p.m_in_smem && r1 > r0)
-      prefetch_rows(p.M_pool + k0 * (long long)s * s + (long long)r0 * s, (r1 - r0) * s, Msl);
-    cp_async_commit();
-  }
-  cluster.sync();  // peers' shared memory is live before any DSMEM access
+  for (int i = tid; i < s; i += T2) S_sh[i] = p.S_pool[(long long)p.bid[0] * s + i];
+  if (p.t0 + 1 < p.t1)
+    for (int i = tid; i < s; i += T2) S_sh[sp + i] = p.S_pool[(long long)p.bid[1] * s + i];
+  __syncthreads();
+  if (warp == 0)  // block t0: slab + M rows on bars[0]
+    issue_loads(bulk, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, p.resident,
+                stageM ? p.M_pool + (long long)p.bid[0] * ss + (long long)r0 * s : nullptr, R * s, Msl, bars + 0);
+  cluster.sync();  // every peer's LL buffers are zeroed before any DSMEM store
 
   const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long prof_last = prof_on ? clock64() : 0;
   long long t = p.t0;
   unsigned it = 0;
+  unsigned phA0 = 0, phA1 = 0;  // mbarrier parities of bars[0], bars[1]
   for (; t < p.t1; ++t, ++it) {
     const int buf = it & 1;
-    const int32_t* Sc = S_sh + buf * sp;
+    const int par = it & 1;
+    const unsigned tag = it + 1;
+    const int32_t* Sc = S_sh + (it % 3) * sp;
     const long long kb = p.bid[t - p.t0];
-    const double* Mg = p.M_pool + kb * (long long)s * s;
-    cp_async_wait_all();
+    const double* Mg = p.M_pool + kb * ss;
+    // ---- this iteration's slab has landed (iteration 0: + its M rows)
+    if (bulk) {
+      if (it == 0 || p.resident) {  // bars[buf] is armed at launch (block t0) and per resident prefetch
+        if (buf == 0) { mbar_wait(bars + 0, phA0); phA0 ^= 1u; }
+        else          { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
+      }
+    } else if (warp == 0) {
+      cp_async_wait_all();
+    }
     __syncthreads();
-    PHASE_MARK(0);  // wait for this iteration's prefetched slab + previous iteration tail
+    PHASE_MARK(0);
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
-    // ---- prefetch block t+1 (index set, then its slab) into the other buffer
-    if (t + 1 < p.t1) {
-      const long long kn = p.bid[t + 1 - p.t0];
-      int32_t* Sn = S_sh + (buf ^ 1) * sp;
-      for (int i = tid; i < s; i += T2) Sn[i] = p.S_pool[kn * s + i];
-      if (p.resident) {
-        __syncthreads();
-        prefetch_slab(p.A, p.lda, Sn, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw);
-        cp_async_commit();
+    // ---- warp 0: slab of block t+1 into the other buffer; index set of block t+2
+    if (warp == 0) {
+      if (t + 1 < p.t1 && p.resident) {
+        fence_proxy_async();
+        issue_loads(bulk, p.A, p.lda, S_sh + ((it + 1) % 3) * sp, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw,
+                    true, nullptr, 0, nullptr, bars + (buf ^ 1));
+      }
+      if (t + 2 < p.t1) {
+        const long long k2 = p.bid[t + 2 - p.t0];
+        int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
+        for (int i = lane; i < s; i += 32) S2[i] = p.S_pool[k2 * s + i];
       }
     }
     const double* Ac = Abuf + buf * absz;
-    PHASE_MARK(1);  // issue of the next prefetch
+    PHASE_MARK(1);
 
-    // ---- row 3: partial block residual over the slab -> part_sm[k]
+    // ---- row 3: partial block residual over the slab; each value goes (LL) to its slice owner
     if (p.resident) {
-      // tpr threads per row, rows in passes of T2/tpr
       const int tpr = p.tpr;
       const int rows_per_pass = T2 / tpr;
       const int sub = tid & (tpr - 1);
@@ -223,19 +295,19 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
           for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
         }
         for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (k < s && sub == 0) part_sm[k] = acc;
+        if (k < s && sub == 0) {
+          const int owner = k / sl;
+          unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
+          ll_store(cluster.map_shared_rank(dst, owner), acc, tag);
+        }
       }
     } else {
-      // streaming: warp per row, 4 rows in flight, 16-byte loads when aligned
-      const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0);
+      const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
       for (int kbase = warp * 4; kbase < s; kbase += NW2 * 4) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         const double* rows[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = min(kbase + u, s - 1);
-          rows[u] = p.A + (long long)Sc[k] * p.lda + c0;
-        }
+        for (int u = 0; u < 4; ++u) rows[u] = p.A + (long long)Sc[min(kbase + u, s - 1)] * p.lda + c0;
         if (vec) {
           const int w2 = w >> 1;
           for (int j2 = lane; j2 < w2; j2 += 32) {
@@ -261,63 +333,63 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const double v = warp_sum(acc[u]);
-          if (lane == 0 && kbase + u < s) part_sm[kbase + u] = v;
+          const int k = kbase + u;
+          if (lane == 0 && k < s) {
+            const int owner = k / sl;
+            unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
+            ll_store(cluster.map_shared_rank(dst, owner), v, tag);
+          }
         }
       }
     }
-    PHASE_MARK(2);  // row 3 (A_S x partials)
-    cluster.sync();  // [A] every rank's part_sm is complete
+    PHASE_MARK(2);
 
-    // ---- cluster partial of my slice -> global (double-buffered by parity), arrive, wait
-    double* pcl = p.part + (long long)(it & 1) * NQ * s;
-    for (int kk = r0 + tid; kk < r1; kk += T2) {
+    // ---- slice owner: cluster partial of my slice -> L2 (LL) for every cluster's owner
+    unsigned long long* gll = p.ll + (long long)par * NQ * s * 2;
+    for (int row = tid; row < R; row += T2) {
       double v = 0.0;
-      for (int cc = 0; cc < C; ++cc) v += *cluster.map_shared_rank(part_sm + kk, cc);
-      pcl[(long long)q * s + kk] = v;
+      for (int cc = 0; cc < C; ++cc) v += ll_wait_shared(rp_ll + (((long long)par * C + cc) * sl + row) * 2, tag, p.err);
+      ll_store_global(gll + ((long long)q * s + r0 + row) * 2, v, tag);
     }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      PHASE_MARK(3);  // cluster barrier A + cluster partial of the slice
-      red_release_add(p.cnt + c, 1u);
-      spin_until(p.cnt + c, (it + 1) * (unsigned)NQ, p.err);
-      PHASE_MARK(4);  // cross-cluster arrival wait
-    }
-    __syncthreads();
-    // ---- r for my slice: fixed-order sum over clusters, minus b_S; all-gather in the cluster.
-    // Every (row, cluster-group) pair loads at once; groups are then summed in a fixed order.
-    const int R = r1 - r0;
-    if (R > 0) {
-      const int G2 = R <= T2 ? T2 / R : 1;
-      for (int e = tid; e < R * G2 && e < T2; e += T2) {
-        const int row = e % R, grp = e / R;
+    PHASE_MARK(3);
+    // ---- r slice: every (row, cluster-group) polls at once; fixed-order combine; - b_S;
+    //      all-gather in the cluster (LL over DSMEM)
+    const int G2 = (R > 0 && R <= T2) ? T2 / R : 1;
+    if (R > 0 && R <= T2) {
+      if (tid < R * G2) {
+        const int row = tid % R, grp = tid / R;
         double v = 0.0;
-        for (int qq = grp; qq < NQ; qq += G2) v += __ldcg(pcl + (long long)qq * s + r0 + row);
+        for (int qq = grp; qq < NQ; qq += G2) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
         red_sm[grp * R + row] = v;
       }
-      if (R > T2) {  // very large slices (s > T2 * C): one thread per row, all clusters
-        for (int row = tid; row < R; row += T2) {
-          double v = 0.0;
-          for (int qq = 0; qq < NQ; qq += 1) v += __ldcg(pcl + (long long)qq * s + r0 + row);
-          r_sm[r0 + row] = v;  // local staging; subtract b and scatter below
-        }
-      }
-      __syncthreads();
+    } else if (R > T2) {
       for (int row = tid; row < R; row += T2) {
-        double v;
-        if (R <= T2) {
-          v = 0.0;
-          for (int grp = 0; grp < G2; ++grp) v += red_sm[grp * R + row];
-        } else {
-          v = r_sm[r0 + row];
-        }
-        v -= p.b[Sc[r0 + row]];
-        for (int cc = 0; cc < C; ++cc) *cluster.map_shared_rank(r_sm + r0 + row, cc) = v;
+        double v = 0.0;
+        for (int qq = 0; qq < NQ; ++qq) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
+        y_sm[r0 + row] = v;  // staging (y_sm is rewritten below)
       }
     }
-    cluster.sync();  // [B] r complete everywhere
-    PHASE_MARK(5);  // r slice gather + all-gather + barrier B
-    // ---- row 4: my slice of y = M r (tq threads per row, shuffle-combined); all-gather
+    __syncthreads();
+    PHASE_MARK(4);
+    for (int row = tid; row < R; row += T2) {
+      double v;
+      if (R <= T2) {
+        v = 0.0;
+        for (int grp = 0; grp < G2; ++grp) v += red_sm[grp * R + row];
+      } else {
+        v = y_sm[r0 + row];
+      }
+      v -= p.b[Sc[r0 + row]];
+      for (int cc = 0; cc < C; ++cc)
+        ll_store(cluster.map_shared_rank(r_ll + ((long long)par * s + r0 + row) * 2, cc), v, tag);
+    }
+    // ---- every CTA: collect r
+    for (int l = tid; l < s; l += T2) r_sm[l] = ll_wait_shared(r_ll + ((long long)par * s + l) * 2, tag, p.err);
+    if (stageM && it > 0 && bulk) mbar_wait(bars + 2, (it - 1) & 1u);  // M rows of block t (issued at t-1)
+    if (stageM && it > 0 && !bulk && warp == 0) cp_async_wait_all();
+    __syncthreads();
+    PHASE_MARK(5);
+    // ---- row 4: my slice of y = M r (tq threads per row); all-gather (LL over DSMEM)
     if (R > 0) {
       int tq = 1;
       while (tq < 32 && tq * 2 * R <= T2) tq *= 2;
@@ -332,24 +404,26 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
         }
         for (int o = tq >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (row < R)
-          for (int cc = sub; cc < C; cc += tq) *cluster.map_shared_rank(y_sm + r0 + row, cc) = v;
+          for (int cc = sub; cc < C; cc += tq)
+            ll_store(cluster.map_shared_rank(y_ll + ((long long)par * s + r0 + row) * 2, cc), v, tag);
       }
     }
-    cluster.sync();  // [C] y complete everywhere
-    PHASE_MARK(6);  // y slice + all-gather + barrier C
-    // M slice of block t+1 into shared memory (mine is consumed)
-    if (p.m_in_smem && t + 1 < p.t1 && r1 > r0) {
+    __syncthreads();  // Msl consumed
+    // ---- warp 0: M rows of block t+1 (on bars[2]; waited before the y step of t+1)
+    if (stageM && t + 1 < p.t1 && warp == 0) {
       const long long kn = p.bid[t + 1 - p.t0];
-      prefetch_rows(p.M_pool + kn * (long long)s * s + (long long)r0 * s, (r1 - r0) * s, Msl);
-      cp_async_commit();
+      fence_proxy_async();
+      issue_loads(bulk, p.A, p.lda, nullptr, 0, c0, 0, nullptr, p.sw, false,
+                  p.M_pool + kn * ss + (long long)r0 * s, R * s, Msl, bars + 2);
     }
+    for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_shared(y_ll + ((long long)par * s + l) * 2, tag, p.err);
+    __syncthreads();
+    PHASE_MARK(6);
 
     // ---- rows 5-6: w on the slab, momentum, x
     const double cm = (1.0 - rho) / (1.0 + rho);
     if (!p.cd) {
       if (p.resident) {
-        // ng groups of cw threads: group g sums rows [g*rg, (g+1)*rg) of column j; then a
-        // fixed-order sum over the groups (w <= cw is guaranteed by the host)
         const int cw = p.cw, ng = T2 / cw, rg = (s + ng - 1) / ng;
         const int g = tid / cw, j = tid - g * cw;
         const int ka = min(s, g * rg), kz = min(s, ka + rg);
@@ -394,8 +468,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
       e = warp_sum(e);
       if (lane == 0) {
         const int res = window_step_dev(st, t, e, p.zeta, p.tol2bb, p.bb, p.adaptive,
-                                        blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho,
-                                        p.hist_cap);
+                                        blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
         if (res) {
           st.stopped = res;
           stop_sh = 1;
@@ -403,15 +476,19 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
       }
     }
     __syncthreads();
-    PHASE_MARK(7);  // rows 5-6 (A_S^T y, momentum) + window logic
+    PHASE_MARK(7);
     if (stop_sh) {
       ++t;
       break;
     }
   }
-  if (prof_on)
-    for (int i = 0; i < 8; ++i) p.prof[i] += prof_acc[i];
-  cp_async_wait_all();
+  // drain copies still in flight after an early stop (their mbarriers must complete before exit)
+  if (bulk && t < p.t1) {
+    const int nb = it & 1;  // iteration `it` issued the slab of block t into buffer nb^1
+    if (p.resident) mbar_wait(bars + (nb ^ 1), nb ^ 1 ? phA1 : phA0);
+    if (stageM) mbar_wait(bars + 2, it & 1u);
+  }
+  if (!bulk) cp_async_wait_all();
   for (int j = tid; j < w; j += T2) {
     p.x[c0 + j] = x_sm[j];
     p.mom[c0 + j] = m_sm[j];
@@ -420,6 +497,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
     st.t_done = t;
     *p.st = st;
   }
+  if (prof_on)
+    for (int i = 0; i < 8; ++i) p.prof[i] += prof_acc[i];
   cluster.sync();  // keep shared memory alive until every peer is done with DSMEM
 }
 
@@ -428,17 +507,20 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
 int iterate_block_threads() { return T2; }
 
 size_t iterate_smem_bytes(const IterParams& p, int C) {
-  const int s = p.s;
-  const int sp = (s + 1) & ~1;
-  const int sl = (s + C - 1) / C;
-  size_t bytes = 0;
-  bytes += 3ull * p.slab * sizeof(double);
-  bytes += 3ull * sp * sizeof(double);
-  bytes += (size_t)T2 * sizeof(double);
-  bytes += 2ull * sp * sizeof(int32_t);
-  if (p.m_in_smem) bytes += (size_t)(((long long)sl * s + 1) & ~1LL) * sizeof(double);
-  if (p.resident) bytes += 2ull * s * p.sw * sizeof(double);
-  return bytes + 64;
+  const long long s = p.s;
+  const long long sp = (s + 1) & ~1LL;
+  const long long sl = (s + C - 1) / C;
+  long long bytes = 4 * 8;              // mbarriers
+  bytes += 4LL * C * sl * 8;            // rp_ll
+  bytes += 8LL * s * 8;                 // r_ll, y_ll
+  bytes += 3LL * p.slab * 8;            // x, m, w
+  bytes += 2LL * sp * 8;                // r, y
+  bytes += (long long)T2 * 8;           // red
+  bytes += 3LL * sp * 4;                // S (triple-buffered)
+  bytes = (bytes + 15) & ~15LL;
+  if (p.m_in_smem) bytes += ((sl * s + 1) & ~1LL) * 8;
+  if (p.resident) bytes += 2LL * s * p.sw * 8;
+  return (size_t)bytes + 128;
 }
 
 static void set_attrs(size_t smem, int C) {
@@ -464,7 +546,6 @@ cudaError_t launch_iterate(cudaStream_t stream, const IterParams& p, int grid, i
   return cudaLaunchKernelEx(&cfg, iterate_kernel, p);
 }
 
-// Largest number of co-resident clusters of size C at this shared-memory size.
 int iterate_max_clusters(int C, size_t smem) {
   set_attrs(smem, C);
   cudaLaunchConfig_t cfg = {};

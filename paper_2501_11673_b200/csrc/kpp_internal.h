@@ -91,8 +91,7 @@ struct IterParams {
   long long zeta;
   int adaptive;          // 0: rho fixed
   int writer;            // this rank writes the history
-  double* part;          // [2][clusters][s] cluster partials (double-buffered by parity)
-  unsigned int* cnt;     // [cluster size] per-slice arrival counters (zeroed before launch)
+  unsigned long long* ll; // [2][clusters][s][2] tagged cluster partials (zeroed before launch)
   int* err;              // set if a spin-wait times out
   DevState* st;
   double* hist_res;      // [hist_cap]
