@@ -144,6 +144,7 @@ typedef struct {
   int32_t resident;      /* 1 if the persistent kernel keeps the block slab on chip */
   int32_t cluster;       /* thread-block cluster size of the persistent kernel */
   int32_t m_in_smem;     /* 1 if each CTA stages its rows of M in shared memory */
+  int32_t tma;           /* 1 if resident slabs are gathered by TMA (tile::gather4) */
 } kpp_stats;
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */

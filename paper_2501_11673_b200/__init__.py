@@ -42,7 +42,8 @@ class _Stats(ctypes.Structure):
                 ("iter_kernel_ms", ctypes.c_double), ("n_blocks", ctypes.c_int64),
                 ("n_fresh_last", ctypes.c_int64), ("iter_launches", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("grid_ctas", ctypes.c_int32),
-                ("resident", ctypes.c_int32), ("cluster", ctypes.c_int32), ("m_in_smem", ctypes.c_int32)]
+                ("resident", ctypes.c_int32), ("cluster", ctypes.c_int32), ("m_in_smem", ctypes.c_int32),
+                ("tma", ctypes.c_int32)]
 
 
 def load_library():

@@ -12,6 +12,7 @@
 //   4. read back the replicated state (stop flag) -- one small D2H per window.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -364,13 +365,12 @@ IterParams plan_params(const kpp_ctx* ctx, int G, bool resident, bool m_in_smem)
   long long slab = (ctx->n + G - 1) / G;
   slab = std::max<long long>(4, (slab + 3) / 4 * 4);
   p.slab = (int)slab;
-  int tpr = 1;
+  int tpr = 4;  // >= 4: keeps the row stride a multiple of 4 doubles (TMA 128-byte destinations)
   while (tpr < 32 && tpr * 2 * ctx->s <= iterate_block_threads()) tpr *= 2;
   p.tpr = tpr;
-  // row stride congruent to tpr (mod 16): the half-warp's 16 rows x tpr columns hit distinct banks
+  // row stride congruent to tpr (mod 16): a half-warp's 16/tpr rows x tpr columns hit distinct banks
   const int target = tpr % 16;
   p.sw = (int)(slab + ((target - slab % 16) + 16) % 16);
-  if (tpr == 1) p.sw = (int)slab;
   p.cw = (int)((slab + 31) / 32 * 32);
   p.resident = resident && slab <= iterate_block_threads();
   p.m_in_smem = m_in_smem;
@@ -420,6 +420,31 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
   ctx->pC = pick->C;
   ctx->pgrid = pick->G;
   ctx->pplan = pick->p;
+  // TMA gather4 descriptor over A (cols x rows, box {sw, 1}) for resident slabs
+  ctx->pplan.tma = 0;
+  if (pick->p.resident && (ctx->lda % 2) == 0 && (reinterpret_cast<uintptr_t>(ctx->A) % 16) == 0 &&
+      pick->p.sw <= 256 && !getenv("KPP_NO_TMA")) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult qr;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+          qr == cudaDriverEntryPointSuccess)
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      cudaGetLastError();
+    }
+    if (encode) {
+      cuuint64_t dims[2] = {(cuuint64_t)ctx->n, (cuuint64_t)ctx->m};
+      cuuint64_t strides[1] = {(cuuint64_t)ctx->lda * sizeof(double)};
+      cuuint32_t box[2] = {(cuuint32_t)pick->p.sw, 1u};
+      cuuint32_t estr[2] = {1u, 1u};
+      CUresult r = encode(&ctx->pplan.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)ctx->A, dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r == CUDA_SUCCESS) ctx->pplan.tma = 1;
+    }
+  }
+  ctx->stats.tma = ctx->pplan.tma;
   ctx->psmem = pick->smem;
   ctx->stats.resident = pick->p.resident;
   ctx->stats.grid_ctas = pick->G;
@@ -572,7 +597,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     p1ms += ms;
     CK(cudaEventRecord(ctx->ev0, st));
     if (!use_graph) {
-      IterParams p = ctx->pplan;
+      IterParams p = ctx->pplan;  // carries the tensor map
       p.A = ctx->A; p.lda = ctx->lda; p.m = m; p.n = n; p.s = ctx->s;
       p.cd = ctx->kind == KIND_CDPP; p.col_base = ctx->col_begin;
       p.b = b_dev; p.tol2bb = tol * tol * bb; p.bb = bb;

@@ -127,6 +127,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA gather4: 4 rows (r0..r3) x box columns starting at column c0 -> dst (dense rows)
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int c0, int r0, int r1, int r2, int r3,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // cp.async fallback (rows that are not 16-byte aligned)
@@ -139,20 +148,30 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Warp 0: load s row segments of the slab (and optionally `mcount` doubles of M rows).
 // bulk: TMA bulk copies completing on `bar` (lane 0 registers the byte count first);
 // otherwise 8-byte cp.async (waited with cp.async.wait_group by warp 0).
-__device__ __forceinline__ void issue_loads(bool bulk, const double* A, long long lda, const int32_t* S, int s,
-                                            long long c0, int w, double* adst, int sw, bool slab,
-                                            const double* msrc, int mcount, double* mdst,
+__device__ __forceinline__ void issue_loads(bool bulk, const CUtensorMap* tm, const double* A, long long lda,
+                                            const int32_t* S, int s, long long c0, int w, double* adst, int sw,
+                                            bool slab, const double* msrc, int mcount, double* mdst,
                                             unsigned long long* bar) {
   const int lane = threadIdx.x & 31;
   if (bulk) {
+    const int nops = (s + 3) >> 2;  // gather4 ops (TMA path)
     unsigned bytes = 0;
-    if (slab && w > 0) bytes += (unsigned)s * (unsigned)w * 8u;
+    if (slab && w > 0) bytes += tm ? (unsigned)nops * 4u * (unsigned)sw * 8u : (unsigned)s * (unsigned)w * 8u;
     if (msrc && mcount > 0) bytes += (unsigned)mcount * 8u;
     if (lane == 0) mbar_expect_tx(bar, bytes);
     __syncwarp();
-    if (slab && w > 0)
-      for (int k = lane; k < s; k += 32)
-        bulk_g2s(adst + (long long)k * sw, A + (long long)S[k] * lda + c0, (unsigned)w * 8u, bar);
+    if (slab && w > 0) {
+      if (tm) {
+        for (int j = lane; j < nops; j += 32) {
+          const int k = 4 * j;
+          tma_gather4(adst + (long long)k * sw, tm, (int)c0, S[k], S[min(k + 1, s - 1)], S[min(k + 2, s - 1)],
+                      S[min(k + 3, s - 1)], bar);
+        }
+      } else {
+        for (int k = lane; k < s; k += 32)
+          bulk_g2s(adst + (long long)k * sw, A + (long long)S[k] * lda + c0, (unsigned)w * 8u, bar);
+      }
+    }
     if (msrc && mcount > 0 && lane == 0) bulk_g2s(mdst, msrc, (unsigned)mcount * 8u, bar);
   } else {
     if (slab)
@@ -176,7 +195,7 @@ __device__ __forceinline__ void issue_loads(bool bulk, const double* A, long lon
     }                                   \
   } while (0)
 
-__global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
+__global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ IterParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int s = p.s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -203,10 +222,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
   double* red_sm = y_sm + sp;                               // [T2]
   int32_t* S_sh = reinterpret_cast<int32_t*>(red_sm + T2);  // [3][sp]
   unsigned char* tail = reinterpret_cast<unsigned char*>(S_sh + 3 * sp);
-  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
-  double* Msl = reinterpret_cast<double*>(tail);                                   // [sl][s]
-  double* Abuf = Msl + (p.m_in_smem ? (((long long)sl * s + 1) & ~1LL) : 0);      // [2][s][sw]
-  const long long absz = (long long)s * p.sw;
+  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 127) & ~uintptr_t(127));
+  double* Abuf = reinterpret_cast<double*>(tail);                                 // [2][s4][sw] (128B aligned)
+  const long long absz = (long long)((s + 3) & ~3) * p.sw;
+  double* Msl = Abuf + (p.resident ? 2 * absz : 0);                               // [sl][s]
   __shared__ DevState st;
   __shared__ int stop_sh;
 
@@ -217,7 +236,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
   const bool bulkA = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((w & 1) == 0) && ((p.sw & 1) == 0) &&
                      ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
   const bool bulkM = ((s & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.M_pool) & 15) == 0);
-  const bool bulk = (!p.resident || bulkA) && (!p.m_in_smem || bulkM);
+  const bool bulk = (!p.resident || bulkA || p.tma) && (!p.m_in_smem || bulkM);
+  const CUtensorMap* tm = p.tma ? &p.tmA : nullptr;
   const long long ss = (long long)s * s;
   const bool stageM = p.m_in_smem && R > 0;
 
@@ -237,7 +257,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
     for (int i = tid; i < s; i += T2) S_sh[sp + i] = p.S_pool[(long long)p.bid[1] * s + i];
   __syncthreads();
   if (warp == 0)  // block t0: slab + M rows on bars[0]
-    issue_loads(bulk, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, p.resident,
+    issue_loads(bulk, tm, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, p.resident,
                 stageM ? p.M_pool + (long long)p.bid[0] * ss + (long long)r0 * s : nullptr, R * s, Msl, bars + 0);
   cluster.sync();  // every peer's LL buffers are zeroed before any DSMEM store
 
@@ -270,7 +290,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
     if (warp == 0) {
       if (t + 1 < p.t1 && p.resident) {
         fence_proxy_async();
-        issue_loads(bulk, p.A, p.lda, S_sh + ((it + 1) % 3) * sp, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw,
+        issue_loads(bulk, tm, p.A, p.lda, S_sh + ((it + 1) % 3) * sp, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw,
                     true, nullptr, 0, nullptr, bars + (buf ^ 1));
       }
       if (t + 2 < p.t1) {
@@ -287,12 +307,30 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
       const int tpr = p.tpr;
       const int rows_per_pass = T2 / tpr;
       const int sub = tid & (tpr - 1);
+      constexpr int XR = 16;  // x values cached in registers when w <= XR * tpr
+      const bool xreg = w <= XR * tpr;
+      double xr[XR];
+      if (xreg) {
+#pragma unroll
+        for (int u = 0; u < XR; ++u) {
+          const int j = sub + u * tpr;
+          xr[u] = j < w ? x_sm[j] : 0.0;
+        }
+      }
       for (int kp = 0; kp < s; kp += rows_per_pass) {
         const int k = kp + tid / tpr;
         double acc = 0.0;
         if (k < s) {
           const double* arow = Ac + (long long)k * p.sw;
-          for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
+          if (xreg) {
+#pragma unroll
+            for (int u = 0; u < XR; ++u) {
+              const int j = sub + u * tpr;
+              if (j < w) acc = fma(arow[j], xr[u], acc);
+            }
+          } else {
+            for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
+          }
         }
         for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (k < s && sub == 0) {
@@ -413,7 +451,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(IterParams p) {
     if (stageM && t + 1 < p.t1 && warp == 0) {
       const long long kn = p.bid[t + 1 - p.t0];
       fence_proxy_async();
-      issue_loads(bulk, p.A, p.lda, nullptr, 0, c0, 0, nullptr, p.sw, false,
+      issue_loads(bulk, nullptr, p.A, p.lda, nullptr, 0, c0, 0, nullptr, p.sw, false,
                   p.M_pool + kn * ss + (long long)r0 * s, R * s, Msl, bars + 2);
     }
     for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_shared(y_ll + ((long long)par * s + l) * 2, tag, p.err);
@@ -517,9 +555,9 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   bytes += 2LL * sp * 8;                // r, y
   bytes += (long long)T2 * 8;           // red
   bytes += 3LL * sp * 4;                // S (triple-buffered)
-  bytes = (bytes + 15) & ~15LL;
+  bytes = (bytes + 127) & ~127LL;
+  if (p.resident) bytes += 2LL * ((s + 3) & ~3LL) * p.sw * 8;
   if (p.m_in_smem) bytes += ((sl * s + 1) & ~1LL) * 8;
-  if (p.resident) bytes += 2LL * s * p.sw * 8;
   return (size_t)bytes + 128;
 }
 

@@ -1,6 +1,7 @@
 // kpp_internal.h -- declarations shared by the host runtime and the kernels of libkpp.
 // Product code: shares nothing with oracle/.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -72,7 +73,9 @@ void launch_add_diag(cudaStream_t st, int batch, double* G, int s, double lam);
 void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info);
 
 // ------------------------------------------------------------------ iterate.cu
-struct IterParams {
+struct alignas(64) IterParams {
+  CUtensorMap tmA;       // 2D tensor map of A (cols x rows, box {sw, 1}) for TMA gather4, if tma
+  int tma;               // 1: resident slabs are gathered with cp.async.bulk.tensor ... gather4
   const double* A;
   long long lda, m, n;   // A is m x n_local (this rank's columns)
   int s;
