@@ -397,7 +397,7 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
         if (res && !p.resident) break;
         const size_t smem = iterate_smem_bytes(p, C);
         if ((long long)smem > maxsm) break;
-        const int nq = iterate_max_clusters(C, smem);
+        const int nq = iterate_max_clusters(p, C, smem);
         if (nq <= 0) break;
         if (nq * C >= g) {
           best = {C, g, p, smem};

@@ -142,6 +142,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void cp_async8(void* smem, const void* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(g) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -195,6 +198,8 @@ __device__ __forceinline__ void issue_loads(bool bulk, const CUtensorMap* tm, co
     }                                   \
   } while (0)
 
+// XR x NP register tile of the resident A_S x / A_S^T y passes (0 x 0: shared-memory path).
+template <int XR, int NP>
 __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ IterParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int s = p.s;
@@ -219,8 +224,9 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   double* w_sm = m_sm + p.slab;
   double* r_sm = w_sm + p.slab;
   double* y_sm = r_sm + sp;
-  double* red_sm = y_sm + sp;                               // [T2]
-  int32_t* S_sh = reinterpret_cast<int32_t*>(red_sm + T2);  // [3][sp]
+  double* red_sm = y_sm + sp;                                   // [2*T2] reduction scratch
+  double* bS_sh = red_sm + 2 * T2;                              // [3][sp] b_S of blocks t, t+1, t+2
+  int32_t* S_sh = reinterpret_cast<int32_t*>(bS_sh + 3 * sp);   // [3][sp]
   unsigned char* tail = reinterpret_cast<unsigned char*>(S_sh + 3 * sp);
   tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 127) & ~uintptr_t(127));
   double* Abuf = reinterpret_cast<double*>(tail);                                 // [2][s4][sw] (128B aligned)
@@ -252,9 +258,17 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     x_sm[j] = p.x[c0 + j];
     m_sm[j] = p.mom[c0 + j];
   }
-  for (int i = tid; i < s; i += T2) S_sh[i] = p.S_pool[(long long)p.bid[0] * s + i];
+  for (int i = tid; i < s; i += T2) {
+    const int32_t v = p.S_pool[(long long)p.bid[0] * s + i];
+    S_sh[i] = v;
+    bS_sh[i] = p.b[v];
+  }
   if (p.t0 + 1 < p.t1)
     for (int i = tid; i < s; i += T2) S_sh[sp + i] = p.S_pool[(long long)p.bid[1] * s + i];
+  // warp 0 keeps the block ids of t+1 and t+2 in registers (each loaded an iteration early)
+  long long qb1 = (p.t0 + 1 < p.t1) ? p.bid[1] : 0;
+  long long qb2 = (p.t0 + 2 < p.t1) ? p.bid[2] : 0;
+  long long qb3 = 0;
   __syncthreads();
   if (warp == 0)  // block t0: slab + M rows on bars[0]
     issue_loads(bulk, tm, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, p.resident,
@@ -272,8 +286,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     const int par = it & 1;
     const unsigned tag = it + 1;
     const int32_t* Sc = S_sh + (it % 3) * sp;
-    const long long kb = p.bid[t - p.t0];
-    const double* Mg = p.M_pool + kb * ss;
+    const double* bSc = bS_sh + (it % 3) * sp;
     // ---- this iteration's slab has landed (iteration 0: + its M rows)
     if (bulk) {
       if (it == 0 || p.resident) {  // bars[buf] is armed at launch (block t0) and per resident prefetch
@@ -286,57 +299,85 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     __syncthreads();
     PHASE_MARK(0);
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
-    // ---- warp 0: slab of block t+1 into the other buffer; index set of block t+2
+    // ---- warp 0 (producer): slab of block t+1 -> other buffer (TMA); b_S of block t+1 and the
+    //      index set of block t+2 -> shared memory (cp.async); block id of t+3 -> register.
+    //      Nothing here waits on memory, so the producer stays off the critical path.
     if (warp == 0) {
-      if (t + 1 < p.t1 && p.resident) {
-        fence_proxy_async();
-        issue_loads(bulk, tm, p.A, p.lda, S_sh + ((it + 1) % 3) * sp, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw,
-                    true, nullptr, 0, nullptr, bars + (buf ^ 1));
+      cp_async_wait_all();  // S(t+1) (issued at t-1) has landed
+      __syncwarp();
+      const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
+      if (t + 1 < p.t1) {
+        if (p.resident) {
+          fence_proxy_async();
+          issue_loads(bulk, tm, p.A, p.lda, S1, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw, true, nullptr, 0,
+                      nullptr, bars + (buf ^ 1));
+        }
+        double* b1 = bS_sh + ((it + 1) % 3) * sp;
+        for (int i = lane; i < s; i += 32) cp_async8(b1 + i, p.b + S1[i]);
       }
       if (t + 2 < p.t1) {
-        const long long k2 = p.bid[t + 2 - p.t0];
         int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
-        for (int i = lane; i < s; i += 32) S2[i] = p.S_pool[k2 * s + i];
+        const int32_t* src = p.S_pool + qb2 * s;
+        for (int i = lane; i < s; i += 32) cp_async4(S2 + i, src + i);
       }
+      cp_async_commit();
+      if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
     }
     const double* Ac = Abuf + buf * absz;
     PHASE_MARK(1);
 
     // ---- row 3: partial block residual over the slab; each value goes (LL) to its slice owner
+    // register path: a thread keeps its A elements (row k of each pass, columns sub + u*tpr)
+    // in registers between the A_S x pass and the A_S^T y pass
+    const int tpr = p.tpr;
+    const int rows_per_pass = T2 / tpr;
+    const int sub = tid & (tpr - 1);
+    const bool regpath = XR > 0 && p.resident && w <= XR * tpr && s <= NP * rows_per_pass && NW2 * p.slab <= 2 * T2;
+    double ar[NP > 0 ? NP : 1][XR > 0 ? XR : 1];
     if (p.resident) {
-      const int tpr = p.tpr;
-      const int rows_per_pass = T2 / tpr;
-      const int sub = tid & (tpr - 1);
-      constexpr int XR = 16;  // x values cached in registers when w <= XR * tpr
-      const bool xreg = w <= XR * tpr;
-      double xr[XR];
-      if (xreg) {
+      double xr[XR > 0 ? XR : 1];
+      if (regpath) {
 #pragma unroll
         for (int u = 0; u < XR; ++u) {
           const int j = sub + u * tpr;
           xr[u] = j < w ? x_sm[j] : 0.0;
         }
-      }
-      for (int kp = 0; kp < s; kp += rows_per_pass) {
-        const int k = kp + tid / tpr;
-        double acc = 0.0;
-        if (k < s) {
-          const double* arow = Ac + (long long)k * p.sw;
-          if (xreg) {
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+          const int k = pp * rows_per_pass + tid / tpr;
+          double acc = 0.0;
+          if (k < s) {
+            const double* arow = Ac + (long long)k * p.sw;
 #pragma unroll
             for (int u = 0; u < XR; ++u) {
               const int j = sub + u * tpr;
-              if (j < w) acc = fma(arow[j], xr[u], acc);
+              ar[pp][u] = j < w ? arow[j] : 0.0;
+              acc = fma(ar[pp][u], xr[u], acc);
             }
-          } else {
-            for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
+          }
+          if (pp * rows_per_pass < s) {
+            for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (k < s && sub == 0) {
+              const int owner = k / sl;
+              unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
+              ll_store(cluster.map_shared_rank(dst, owner), acc, tag);
+            }
           }
         }
-        for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (k < s && sub == 0) {
-          const int owner = k / sl;
-          unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
-          ll_store(cluster.map_shared_rank(dst, owner), acc, tag);
+      } else {
+        for (int kp = 0; kp < s; kp += rows_per_pass) {
+          const int k = kp + tid / tpr;
+          double acc = 0.0;
+          if (k < s) {
+            const double* arow = Ac + (long long)k * p.sw;
+            for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
+          }
+          for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (k < s && sub == 0) {
+            const int owner = k / sl;
+            unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
+            ll_store(cluster.map_shared_rank(dst, owner), acc, tag);
+          }
         }
       }
     } else {
@@ -417,7 +458,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       } else {
         v = y_sm[r0 + row];
       }
-      v -= p.b[Sc[r0 + row]];
+      v -= bSc[r0 + row];
       for (int cc = 0; cc < C; ++cc)
         ll_store(cluster.map_shared_rank(r_ll + ((long long)par * s + r0 + row) * 2, cc), v, tag);
     }
@@ -437,7 +478,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         const int row = rp + tid / tq;
         double v = 0.0;
         if (row < R) {
-          const double* Mrow = p.m_in_smem ? Msl + (long long)row * s : Mg + (long long)(r0 + row) * s;
+          const double* Mrow = p.m_in_smem ? Msl + (long long)row * s
+                                           : p.M_pool + (long long)p.bid[t - p.t0] * ss + (long long)(r0 + row) * s;
           for (int l = sub; l < s; l += tq) v = fma(Mrow[l], r_sm[l], v);
         }
         for (int o = tq >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -449,7 +491,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     __syncthreads();  // Msl consumed
     // ---- warp 0: M rows of block t+1 (on bars[2]; waited before the y step of t+1)
     if (stageM && t + 1 < p.t1 && warp == 0) {
-      const long long kn = p.bid[t + 1 - p.t0];
+      const long long kn = qb1;
       fence_proxy_async();
       issue_loads(bulk, nullptr, p.A, p.lda, nullptr, 0, c0, 0, nullptr, p.sw, false,
                   p.M_pool + kn * ss + (long long)r0 * s, R * s, Msl, bars + 2);
@@ -461,7 +503,38 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     // ---- rows 5-6: w on the slab, momentum, x
     const double cm = (1.0 - rho) / (1.0 + rho);
     if (!p.cd) {
-      if (p.resident) {
+      if (regpath) {
+        // w_j = sum_k A[k][j] y_k: products from the registers of row 3, xor-shuffle over the
+        // lanes holding the same columns (fixed tree), then a fixed-order sum over the warps
+        double wa[XR > 0 ? XR : 1];
+#pragma unroll
+        for (int u = 0; u < XR; ++u) wa[u] = 0.0;
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+          const int k = pp * rows_per_pass + tid / tpr;
+          if (k < s) {
+            const double yk = y_sm[k];
+#pragma unroll
+            for (int u = 0; u < XR; ++u) wa[u] = fma(ar[pp][u], yk, wa[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < XR; ++u)
+          for (int o = tpr; o < 32; o <<= 1) wa[u] += __shfl_xor_sync(0xffffffffu, wa[u], o);
+        if (lane < tpr) {
+#pragma unroll
+          for (int u = 0; u < XR; ++u) {
+            const int j = sub + u * tpr;
+            if (j < w) red_sm[warp * p.slab + j] = wa[u];
+          }
+        }
+        __syncthreads();
+        for (int jj = tid; jj < w; jj += T2) {
+          double v = 0.0;
+          for (int ww = 0; ww < NW2; ++ww) v += red_sm[ww * p.slab + jj];
+          w_sm[jj] = v;
+        }
+      } else if (p.resident) {
         const int cw = p.cw, ng = T2 / cw, rg = (s + ng - 1) / ng;
         const int g = tid / cw, j = tid - g * cw;
         const int ka = min(s, g * rg), kz = min(s, ka + rg);
@@ -515,6 +588,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     __syncthreads();
     PHASE_MARK(7);
+    qb1 = qb2;
+    qb2 = qb3;
     if (stop_sh) {
       ++t;
       break;
@@ -553,7 +628,8 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   bytes += 8LL * s * 8;                 // r_ll, y_ll
   bytes += 3LL * p.slab * 8;            // x, m, w
   bytes += 2LL * sp * 8;                // r, y
-  bytes += (long long)T2 * 8;           // red
+  bytes += 2LL * T2 * 8;                // red
+  bytes += 3LL * sp * 8;                // b_S (triple-buffered)
   bytes += 3LL * sp * 4;                // S (triple-buffered)
   bytes = (bytes + 127) & ~127LL;
   if (p.resident) bytes += 2LL * ((s + 3) & ~3LL) * p.sw * 8;
@@ -561,44 +637,54 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   return (size_t)bytes + 128;
 }
 
-static void set_attrs(size_t smem, int C) {
-  cudaFuncSetAttribute(iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (C > 8) cudaFuncSetAttribute(iterate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+using KernelFn = void (*)(const IterParams);
+
+// register tile for the resident passes: enough registers for w <= XR * tpr and s <= NP * (T2/tpr)
+static KernelFn pick_kernel(const IterParams& p) {
+  if (p.resident) {
+    const int rpp = T2 / p.tpr;
+    if (p.slab <= 16 * p.tpr && p.s <= rpp) return iterate_kernel<16, 1>;
+    if (p.slab <= 8 * p.tpr && p.s <= 2 * rpp) return iterate_kernel<8, 2>;
+  }
+  return iterate_kernel<0, 0>;
 }
 
-cudaError_t launch_iterate(cudaStream_t stream, const IterParams& p, int grid, int C, size_t smem) {
-  set_attrs(smem, C);
+static void set_attrs(KernelFn fn, size_t smem, int C) {
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (C > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
+static cudaLaunchConfig_t make_cfg(int grid, int C, size_t smem, cudaStream_t stream, cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(T2);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  count_launches(1);
-  return cudaLaunchKernelEx(&cfg, iterate_kernel, p);
+  return cfg;
 }
 
-int iterate_max_clusters(int C, size_t smem) {
-  set_attrs(smem, C);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C * 256);
-  cfg.blockDim = dim3(T2);
-  cfg.dynamicSmemBytes = smem;
+cudaError_t launch_iterate(cudaStream_t stream, const IterParams& p, int grid, int C, size_t smem) {
+  KernelFn fn = pick_kernel(p);
+  set_attrs(fn, smem, C);
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cudaLaunchConfig_t cfg = make_cfg(grid, C, smem, stream, attr);
+  count_launches(1);
+  return cudaLaunchKernelEx(&cfg, fn, p);
+}
+
+int iterate_max_clusters(const IterParams& p, int C, size_t smem) {
+  KernelFn fn = pick_kernel(p);
+  set_attrs(fn, smem, C);
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = make_cfg(C * 256, C, smem, nullptr, attr);
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, iterate_kernel, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, (const void*)fn, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }

@@ -112,7 +112,7 @@ struct alignas(64) IterParams {
 cudaError_t launch_iterate(cudaStream_t st, const IterParams& p, int grid, int C, size_t smem);
 int iterate_block_threads();
 size_t iterate_smem_bytes(const IterParams& p, int C);
-int iterate_max_clusters(int C, size_t smem);  // co-resident clusters of size C (0 on error)
+int iterate_max_clusters(const IterParams& p, int C, size_t smem);  // co-resident clusters of size C
 
 // ------------------------------------------------------------------ steps.cu (engine "graph")
 // Iteration cursor of the step kernels (device memory), so a captured graph is reusable.
