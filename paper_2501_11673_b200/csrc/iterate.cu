@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   cluster.sync();  // every peer's LL buffers are zeroed before any DSMEM store
 
   const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-  long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long prof_last = prof_on ? clock64() : 0;
   long long t = p.t0;
   unsigned it = 0;
@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     if (warp == 0) {
       cp_async_wait_all();  // S(t+1) (issued at t-1) has landed
       __syncwarp();
+      PHASE_MARK(8);
       const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
       if (t + 1 < p.t1) {
         if (p.resident) {
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
           issue_loads(bulk, tm, p.A, p.lda, S1, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw, true, nullptr, 0,
                       nullptr, bars + (buf ^ 1));
         }
+        PHASE_MARK(9);
         double* b1 = bS_sh + ((it + 1) % 3) * sp;
         for (int i = lane; i < s; i += 32) cp_async8(b1 + i, p.b + S1[i]);
       }
@@ -321,6 +323,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         for (int i = lane; i < s; i += 32) cp_async4(S2 + i, src + i);
       }
       cp_async_commit();
+      PHASE_MARK(10);
       if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
     }
     const double* Ac = Abuf + buf * absz;
@@ -518,9 +521,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
             for (int u = 0; u < XR; ++u) wa[u] = fma(ar[pp][u], yk, wa[u]);
           }
         }
+        for (int o = tpr; o < 32; o <<= 1) {  // XR independent shuffles per step (pipelined)
 #pragma unroll
-        for (int u = 0; u < XR; ++u)
-          for (int o = tpr; o < 32; o <<= 1) wa[u] += __shfl_xor_sync(0xffffffffu, wa[u], o);
+          for (int u = 0; u < XR; ++u) wa[u] += __shfl_xor_sync(0xffffffffu, wa[u], o);
+        }
         if (lane < tpr) {
 #pragma unroll
           for (int u = 0; u < XR; ++u) {
@@ -611,7 +615,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     *p.st = st;
   }
   if (prof_on)
-    for (int i = 0; i < 8; ++i) p.prof[i] += prof_acc[i];
+    for (int i = 0; i < 12; ++i) p.prof[i] += prof_acc[i];
   cluster.sync();  // keep shared memory alive until every peer is done with DSMEM
 }
 
