@@ -610,8 +610,8 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       CK(cudaMemsetAsync(ctx->d_ll, 0, ctx->ll_bytes, st));
       if (getenv("KPP_PHASE_PROFILE")) {
         if (!ctx->d_prof) {
-          CKS(dalloc(ctx, &ctx->d_prof, 12));
-          CK(cudaMemset(ctx->d_prof, 0, 12 * sizeof(long long)));
+          CKS(dalloc(ctx, &ctx->d_prof, 16));
+          CK(cudaMemset(ctx->d_prof, 0, 16 * sizeof(long long)));
         }
         p.prof = ctx->d_prof;
       }
@@ -671,13 +671,13 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   if (n_hist) *n_hist = nh;
   if (iters_out) *iters_out = max_iters == 0 ? 0 : fin.t_done;
   if (ctx->d_prof && fin.t_done > 0) {
-    long long pr[12];
+    long long pr[16];
     CK(cudaMemcpy(pr, ctx->d_prof, sizeof pr, cudaMemcpyDeviceToHost));
     CK(cudaMemset(ctx->d_prof, 0, sizeof pr));
-    const char* names[12] = {"wait_prefetch", "issue_prefetch", "rows3_Ax", "clpart", "xcluster_wait",
-                             "r_gather", "y", "rows56_window", "(p:cpwait)", "(p:tma)", "(p:cpasync)", "-"};
+    const char* names[13] = {"wait", "pf_rest", "rows3_Ax", "clpart", "xcluster_wait", "r_gather", "y",
+                             "window", "-", "pf_tma", "pf_cpasync", "w", "mom"};
     fprintf(stderr, "[kpp phase cycles/iter, CTA 0]");
-    for (int i = 0; i < 11; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
+    for (int i = 0; i < 13; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
     fprintf(stderr, "\n");
   }
   if (fin.stopped == 2) return fail(ctx, KPP_EDIVERGED, "non-finite block residual at iteration %lld", fin.t_done - 1);

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   cluster.sync();  // every peer's LL buffers are zeroed before any DSMEM store
 
   const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-  long long prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_acc[16] = {};
   long long prof_last = prof_on ? clock64() : 0;
   long long t = p.t0;
   unsigned it = 0;
@@ -287,42 +287,60 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     const unsigned tag = it + 1;
     const int32_t* Sc = S_sh + (it % 3) * sp;
     const double* bSc = bS_sh + (it % 3) * sp;
-    // ---- this iteration's slab has landed (iteration 0: + its M rows)
+    // ---- this iteration's slab has landed (iteration 0: + its M rows); this thread's cp.async
+    //      loads of the previous iteration (S, b_S) have landed
     if (bulk) {
       if (it == 0 || p.resident) {  // bars[buf] is armed at launch (block t0) and per resident prefetch
         if (buf == 0) { mbar_wait(bars + 0, phA0); phA0 ^= 1u; }
         else          { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
       }
-    } else if (warp == 0) {
-      cp_async_wait_all();
     }
+    cp_async_wait_all();
+    const bool pf_slab = t + 1 < p.t1 && p.resident;
+    const int nops = (s + 3) >> 2;
+    const bool tma_slab = pf_slab && bulk && tm != nullptr;
+    // the next slab's byte count is registered before any thread issues its gather4
+    if (tid == 0 && tma_slab) mbar_expect_tx(bars + (buf ^ 1), (unsigned)nops * 4u * (unsigned)p.sw * 8u);
     __syncthreads();
     PHASE_MARK(0);
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
-    // ---- warp 0 (producer): slab of block t+1 -> other buffer (TMA); b_S of block t+1 and the
-    //      index set of block t+2 -> shared memory (cp.async); block id of t+3 -> register.
-    //      Nothing here waits on memory, so the producer stays off the critical path.
-    if (warp == 0) {
-      cp_async_wait_all();  // S(t+1) (issued at t-1) has landed
-      __syncwarp();
-      PHASE_MARK(8);
+    // ---- prefetch, spread over all threads so no warp is delayed by TMA issue latency:
+    //      slab of block t+1 (gather4 ops), b_S of block t+1, index set of block t+2
+    {
       const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
-      if (t + 1 < p.t1) {
-        if (p.resident) {
-          fence_proxy_async();
-          issue_loads(bulk, tm, p.A, p.lda, S1, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw, true, nullptr, 0,
-                      nullptr, bars + (buf ^ 1));
+      if (tma_slab) {
+        const int stride = T2 / nops >= 1 ? T2 / nops : 1;
+        if (tid % stride == 0 && tid / stride < nops) {
+          for (int j = tid / stride; j < nops; j += T2 / stride) {
+            const int k = 4 * j;
+            fence_proxy_async();
+            tma_gather4(Abuf + (buf ^ 1) * absz + (long long)k * p.sw, tm, (int)c0, S1[k], S1[min(k + 1, s - 1)],
+                        S1[min(k + 2, s - 1)], S1[min(k + 3, s - 1)], bars + (buf ^ 1));
+          }
         }
-        PHASE_MARK(9);
+      } else if (pf_slab && warp == 0) {
+        fence_proxy_async();
+        issue_loads(bulk, nullptr, p.A, p.lda, S1, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw, true, nullptr, 0,
+                    nullptr, bars + (buf ^ 1));
+      }
+      PHASE_MARK(9);
+      bool any = false;
+      if (t + 1 < p.t1) {
         double* b1 = bS_sh + ((it + 1) % 3) * sp;
-        for (int i = lane; i < s; i += 32) cp_async8(b1 + i, p.b + S1[i]);
+        for (int i = tid; i < s; i += T2) {
+          cp_async8(b1 + i, p.b + S1[i]);
+          any = true;
+        }
       }
       if (t + 2 < p.t1) {
         int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
         const int32_t* src = p.S_pool + qb2 * s;
-        for (int i = lane; i < s; i += 32) cp_async4(S2 + i, src + i);
+        for (int i = tid; i < s; i += T2) {
+          cp_async4(S2 + i, src + i);
+          any = true;
+        }
       }
-      cp_async_commit();
+      if (any) cp_async_commit();
       PHASE_MARK(10);
       if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
     }
@@ -504,6 +522,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     PHASE_MARK(6);
 
     // ---- rows 5-6: w on the slab, momentum, x
+    PHASE_MARK(6);
     const double cm = (1.0 - rho) / (1.0 + rho);
     if (!p.cd) {
       if (regpath) {
@@ -570,12 +589,14 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       }
     }
     __syncthreads();
+    PHASE_MARK(11);
     for (int jj = tid; jj < w; jj += T2) {
       const double wv = w_sm[jj];
       const double mm = cm * (m_sm[jj] - wv);
       m_sm[jj] = mm;
       x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
     }
+    PHASE_MARK(12);
     // ---- row 8: ||r||^2 (fixed order, identical in every CTA) and the window logic
     if (warp == 0) {
       double e = 0.0;
@@ -615,7 +636,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     *p.st = st;
   }
   if (prof_on)
-    for (int i = 0; i < 12; ++i) p.prof[i] += prof_acc[i];
+    for (int i = 0; i < 16; ++i) p.prof[i] += prof_acc[i];
   cluster.sync();  // keep shared memory alive until every peer is done with DSMEM
 }
 
