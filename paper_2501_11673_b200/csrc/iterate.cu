@@ -198,8 +198,36 @@ __device__ __forceinline__ void issue_loads(bool bulk, const CUtensorMap* tm, co
     }                                   \
   } while (0)
 
-// XR x NP register tile of the resident A_S x / A_S^T y passes (0 x 0: shared-memory path).
-template <int XR, int NP>
+// Butterfly reduce-scatter of RPW per-lane values over the 32 lanes of a warp: afterwards
+// v[0] of lane l is the full warp sum of value index rs_row<RPW>(l) (fixed order: deterministic).
+template <int RPW>
+__device__ __forceinline__ void warp_reduce_scatter(double (&v)[RPW], int lane) {
+  int o = 16;
+#pragma unroll
+  for (int cnt = RPW; cnt > 1; cnt >>= 1, o >>= 1) {
+    const int half = cnt >> 1;
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = upper ? v[i] : v[i + half];
+      const double keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  for (; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+}
+template <int RPW>
+__device__ __forceinline__ int rs_row(int lane) {
+  int r = 0, o = 16;
+#pragma unroll
+  for (int cnt = RPW; cnt > 1; cnt >>= 1, o >>= 1)
+    if (lane & o) r += cnt >> 1;
+  return r;
+}
+
+// Register tile of the resident A_S x / A_S^T y passes: warp wi holds rows wi + 16 i (i < RPW),
+// lane l holds columns l + 32 c (c < CPL).  RPW = 0: shared-memory path.
+template <int RPW, int CPL>
 __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ IterParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int s = p.s;
@@ -348,44 +376,39 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     PHASE_MARK(1);
 
     // ---- row 3: partial block residual over the slab; each value goes (LL) to its slice owner
-    // register path: a thread keeps its A elements (row k of each pass, columns sub + u*tpr)
-    // in registers between the A_S x pass and the A_S^T y pass
-    const int tpr = p.tpr;
-    const int rows_per_pass = T2 / tpr;
-    const int sub = tid & (tpr - 1);
-    const bool regpath = XR > 0 && p.resident && w <= XR * tpr && s <= NP * rows_per_pass && NW2 * p.slab <= 2 * T2;
-    double ar[NP > 0 ? NP : 1][XR > 0 ? XR : 1];
+    // register path: rows wi + 16 i of the slab, columns lane + 32 c, kept in registers between
+    // the A_S x pass and the A_S^T y pass
+    const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL;
+    double ar[RPW > 0 ? RPW : 1][CPL > 0 ? CPL : 1];
     if (p.resident) {
-      double xr[XR > 0 ? XR : 1];
       if (regpath) {
+        double xr[CPL > 0 ? CPL : 1];
 #pragma unroll
-        for (int u = 0; u < XR; ++u) {
-          const int j = sub + u * tpr;
-          xr[u] = j < w ? x_sm[j] : 0.0;
+        for (int cc = 0; cc < CPL; ++cc) xr[cc] = (lane + 32 * cc < w) ? x_sm[lane + 32 * cc] : 0.0;
+        double v[RPW > 0 ? RPW : 1];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+          const int k = warp + 16 * i;
+          const double* arow = Ac + (long long)k * p.sw;
+          v[i] = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) {
+            ar[i][cc] = (k < s && lane + 32 * cc < w) ? arow[lane + 32 * cc] : 0.0;
+            v[i] = fma(ar[i][cc], xr[cc], v[i]);
+          }
         }
-#pragma unroll
-        for (int pp = 0; pp < NP; ++pp) {
-          const int k = pp * rows_per_pass + tid / tpr;
-          double acc = 0.0;
-          if (k < s) {
-            const double* arow = Ac + (long long)k * p.sw;
-#pragma unroll
-            for (int u = 0; u < XR; ++u) {
-              const int j = sub + u * tpr;
-              ar[pp][u] = j < w ? arow[j] : 0.0;
-              acc = fma(ar[pp][u], xr[u], acc);
-            }
-          }
-          if (pp * rows_per_pass < s) {
-            for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (k < s && sub == 0) {
-              const int owner = k / sl;
-              unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
-              ll_store(cluster.map_shared_rank(dst, owner), acc, tag);
-            }
-          }
+        if constexpr (RPW > 0) warp_reduce_scatter<RPW>(v, lane);
+        const int ri = rs_row<RPW>(lane);
+        const int k = warp + 16 * ri;
+        if ((lane & (32 / RPW - 1)) == 0 && k < s) {
+          const int owner = k / sl;
+          unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
+          ll_store(cluster.map_shared_rank(dst, owner), v[0], tag);
         }
       } else {
+        const int tpr = p.tpr;
+        const int rows_per_pass = T2 / tpr;
+        const int sub = tid & (tpr - 1);
         for (int kp = 0; kp < s; kp += rows_per_pass) {
           const int k = kp + tid / tpr;
           double acc = 0.0;
@@ -526,30 +549,16 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     const double cm = (1.0 - rho) / (1.0 + rho);
     if (!p.cd) {
       if (regpath) {
-        // w_j = sum_k A[k][j] y_k: products from the registers of row 3, xor-shuffle over the
-        // lanes holding the same columns (fixed tree), then a fixed-order sum over the warps
-        double wa[XR > 0 ? XR : 1];
+        // w_j = sum_k A[k][j] y_k: the warp's rows from registers, then a fixed-order sum over warps
 #pragma unroll
-        for (int u = 0; u < XR; ++u) wa[u] = 0.0;
+        for (int cc = 0; cc < CPL; ++cc) {
+          double a = 0.0;
 #pragma unroll
-        for (int pp = 0; pp < NP; ++pp) {
-          const int k = pp * rows_per_pass + tid / tpr;
-          if (k < s) {
-            const double yk = y_sm[k];
-#pragma unroll
-            for (int u = 0; u < XR; ++u) wa[u] = fma(ar[pp][u], yk, wa[u]);
+          for (int i = 0; i < RPW; ++i) {
+            const int k = warp + 16 * i;
+            if (k < s) a = fma(ar[i][cc], y_sm[k], a);
           }
-        }
-        for (int o = tpr; o < 32; o <<= 1) {  // XR independent shuffles per step (pipelined)
-#pragma unroll
-          for (int u = 0; u < XR; ++u) wa[u] += __shfl_xor_sync(0xffffffffu, wa[u], o);
-        }
-        if (lane < tpr) {
-#pragma unroll
-          for (int u = 0; u < XR; ++u) {
-            const int j = sub + u * tpr;
-            if (j < w) red_sm[warp * p.slab + j] = wa[u];
-          }
+          if (lane + 32 * cc < w) red_sm[warp * p.slab + lane + 32 * cc] = a;
         }
         __syncthreads();
         for (int jj = tid; jj < w; jj += T2) {
@@ -666,10 +675,20 @@ using KernelFn = void (*)(const IterParams);
 
 // register tile for the resident passes: enough registers for w <= XR * tpr and s <= NP * (T2/tpr)
 static KernelFn pick_kernel(const IterParams& p) {
-  if (p.resident) {
-    const int rpp = T2 / p.tpr;
-    if (p.slab <= 16 * p.tpr && p.s <= rpp) return iterate_kernel<16, 1>;
-    if (p.slab <= 8 * p.tpr && p.s <= 2 * rpp) return iterate_kernel<8, 2>;
+  if (p.resident && NW2 * p.slab <= 2 * T2) {
+    int rpw = 1;
+    while (16 * rpw < p.s) rpw *= 2;
+    const int cpl = (p.slab + 31) / 32;
+    if (cpl == 1) {
+      if (rpw <= 2) return iterate_kernel<2, 1>;
+      if (rpw == 4) return iterate_kernel<4, 1>;
+      if (rpw == 8) return iterate_kernel<8, 1>;
+      if (rpw == 16) return iterate_kernel<16, 1>;
+    } else if (cpl == 2) {
+      if (rpw <= 2) return iterate_kernel<2, 2>;
+      if (rpw == 4) return iterate_kernel<4, 2>;
+      if (rpw == 8) return iterate_kernel<8, 2>;
+    }
   }
   return iterate_kernel<0, 0>;
 }
