@@ -257,11 +257,13 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   int32_t* S_sh = reinterpret_cast<int32_t*>(bS_sh + 3 * sp);   // [3][sp]
   unsigned char* tail = reinterpret_cast<unsigned char*>(S_sh + 3 * sp);
   tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 127) & ~uintptr_t(127));
-  double* Abuf = reinterpret_cast<double*>(tail);                                 // [2][s4][sw] (128B aligned)
+  double* Abuf = reinterpret_cast<double*>(tail);               // [2][s4][sw] (128B aligned)
   const long long absz = (long long)((s + 3) & ~3) * p.sw;
-  double* Msl = Abuf + (p.resident ? 2 * absz : 0);                               // [sl][s]
+  const long long mslz = ((long long)sl * s + 15) & ~15LL;
+  double* Mbuf = Abuf + (p.resident ? 2 * absz : 0);           // [2][sl][s] staged rows of M
   __shared__ DevState st;
   __shared__ int stop_sh;
+  __shared__ long long tmod_sh;
 
   const long long c0 = (long long)blockIdx.x * p.slab;
   const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
@@ -274,10 +276,19 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   const CUtensorMap* tm = p.tma ? &p.tmA : nullptr;
   const long long ss = (long long)s * s;
   const bool stageM = p.m_in_smem && R > 0;
+  const int nops = (s + 3) >> 2;
+  // bytes landing on bars[buf] per iteration: the slab (resident) + this rank's M rows (staged)
+  const unsigned slab_bytes = p.resident ? (tm ? (unsigned)nops * 4u * (unsigned)p.sw * 8u : (unsigned)s * (unsigned)w * 8u) : 0u;
+  const unsigned m_bytes = stageM ? (unsigned)(R * s) * 8u : 0u;
+  // warps that issue the prefetch (the others do the slice-owner work in the same window)
+  const int own_warps = (R + 31) / 32;
+  const int pf_tid = tid - 32 * own_warps;
+  const int pf_n = T2 - 32 * own_warps;
 
   if (tid == 0) {
     st = *p.st;
     stop_sh = 0;
+    tmod_sh = p.t0 % (2 * p.zeta);
     for (int i = 0; i < 4; ++i) mbar_init(bars + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -293,15 +304,16 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   }
   if (p.t0 + 1 < p.t1)
     for (int i = tid; i < s; i += T2) S_sh[sp + i] = p.S_pool[(long long)p.bid[1] * s + i];
-  // warp 0 keeps the block ids of t+1 and t+2 in registers (each loaded an iteration early)
+  // block ids of t+1 and t+2 in registers (each loaded an iteration before it is needed)
   long long qb1 = (p.t0 + 1 < p.t1) ? p.bid[1] : 0;
   long long qb2 = (p.t0 + 2 < p.t1) ? p.bid[2] : 0;
   long long qb3 = 0;
   __syncthreads();
   if (warp == 0)  // block t0: slab + M rows on bars[0]
     issue_loads(bulk, tm, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, p.resident,
-                stageM ? p.M_pool + (long long)p.bid[0] * ss + (long long)r0 * s : nullptr, R * s, Msl, bars + 0);
+                stageM ? p.M_pool + (long long)p.bid[0] * ss + (long long)r0 * s : nullptr, R * s, Mbuf, bars + 0);
   cluster.sync();  // every peer's LL buffers are zeroed before any DSMEM store
+  long long tmod = tmod_sh;
 
   const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   long long prof_acc[16] = {};
@@ -315,73 +327,27 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     const unsigned tag = it + 1;
     const int32_t* Sc = S_sh + (it % 3) * sp;
     const double* bSc = bS_sh + (it % 3) * sp;
-    // ---- this iteration's slab has landed (iteration 0: + its M rows); this thread's cp.async
-    //      loads of the previous iteration (S, b_S) have landed
+    const double* Ac = Abuf + buf * absz;
+    const double* Msl = Mbuf + buf * mslz;
+    const bool pf = t + 1 < p.t1;
+    // ---- top: this iteration's slab and M rows have landed; this thread's cp.async loads
+    //      (S, b_S) of the previous iteration have landed; arm the barrier of the next buffer
     if (bulk) {
-      if (it == 0 || p.resident) {  // bars[buf] is armed at launch (block t0) and per resident prefetch
-        if (buf == 0) { mbar_wait(bars + 0, phA0); phA0 ^= 1u; }
-        else          { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
-      }
+      if (buf == 0) { mbar_wait(bars + 0, phA0); phA0 ^= 1u; }
+      else          { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
     }
     cp_async_wait_all();
-    const bool pf_slab = t + 1 < p.t1 && p.resident;
-    const int nops = (s + 3) >> 2;
-    const bool tma_slab = pf_slab && bulk && tm != nullptr;
-    // the next slab's byte count is registered before any thread issues its gather4
-    if (tid == 0 && tma_slab) mbar_expect_tx(bars + (buf ^ 1), (unsigned)nops * 4u * (unsigned)p.sw * 8u);
+    if (tid == 0 && pf && bulk) mbar_expect_tx(bars + (buf ^ 1), slab_bytes + m_bytes);
     __syncthreads();
     PHASE_MARK(0);
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
-    // ---- prefetch, spread over all threads so no warp is delayed by TMA issue latency:
-    //      slab of block t+1 (gather4 ops), b_S of block t+1, index set of block t+2
-    {
-      const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
-      if (tma_slab) {
-        const int stride = T2 / nops >= 1 ? T2 / nops : 1;
-        if (tid % stride == 0 && tid / stride < nops) {
-          for (int j = tid / stride; j < nops; j += T2 / stride) {
-            const int k = 4 * j;
-            fence_proxy_async();
-            tma_gather4(Abuf + (buf ^ 1) * absz + (long long)k * p.sw, tm, (int)c0, S1[k], S1[min(k + 1, s - 1)],
-                        S1[min(k + 2, s - 1)], S1[min(k + 3, s - 1)], bars + (buf ^ 1));
-          }
-        }
-      } else if (pf_slab && warp == 0) {
-        fence_proxy_async();
-        issue_loads(bulk, nullptr, p.A, p.lda, S1, s, c0, w, Abuf + (buf ^ 1) * absz, p.sw, true, nullptr, 0,
-                    nullptr, bars + (buf ^ 1));
-      }
-      PHASE_MARK(9);
-      bool any = false;
-      if (t + 1 < p.t1) {
-        double* b1 = bS_sh + ((it + 1) % 3) * sp;
-        for (int i = tid; i < s; i += T2) {
-          cp_async8(b1 + i, p.b + S1[i]);
-          any = true;
-        }
-      }
-      if (t + 2 < p.t1) {
-        int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
-        const int32_t* src = p.S_pool + qb2 * s;
-        for (int i = tid; i < s; i += T2) {
-          cp_async4(S2 + i, src + i);
-          any = true;
-        }
-      }
-      if (any) cp_async_commit();
-      PHASE_MARK(10);
-      if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
-    }
-    const double* Ac = Abuf + buf * absz;
-    PHASE_MARK(1);
 
     // ---- row 3: partial block residual over the slab; each value goes (LL) to its slice owner
-    // register path: rows wi + 16 i of the slab, columns lane + 32 c, kept in registers between
-    // the A_S x pass and the A_S^T y pass
     const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL;
     double ar[RPW > 0 ? RPW : 1][CPL > 0 ? CPL : 1];
     if (p.resident) {
       if (regpath) {
+        // register tile: rows wi + 16 i, columns lane + 32 c, kept until the A_S^T y pass
         double xr[CPL > 0 ? CPL : 1];
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) xr[cc] = (lane + 32 * cc < w) ? x_sm[lane + 32 * cc] : 0.0;
@@ -398,9 +364,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
           }
         }
         if constexpr (RPW > 0) warp_reduce_scatter<RPW>(v, lane);
-        const int ri = rs_row<RPW>(lane);
-        const int k = warp + 16 * ri;
-        if ((lane & (32 / RPW - 1)) == 0 && k < s) {
+        const int k = warp + 16 * rs_row<RPW>(lane);
+        if ((lane & (32 / (RPW > 0 ? RPW : 1) - 1)) == 0 && k < s) {
           const int owner = k / sl;
           unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
           ll_store(cluster.map_shared_rank(dst, owner), v[0], tag);
@@ -467,16 +432,67 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     PHASE_MARK(2);
 
-    // ---- slice owner: cluster partial of my slice -> L2 (LL) for every cluster's owner
     unsigned long long* gll = p.ll + (long long)par * NQ * s * 2;
-    for (int row = tid; row < R; row += T2) {
-      double v = 0.0;
-      for (int cc = 0; cc < C; ++cc) v += ll_wait_shared(rp_ll + (((long long)par * C + cc) * sl + row) * 2, tag, p.err);
-      ll_store_global(gll + ((long long)q * s + r0 + row) * 2, v, tag);
+    if (pf_tid < 0) {
+      // ---- slice owner warps: cluster partial of my slice -> L2 (LL) for every cluster's owner
+      for (int row = tid; row < R; row += 32 * own_warps) {
+        double v = 0.0;
+        for (int cc = 0; cc < C; ++cc) v += ll_wait_shared(rp_ll + (((long long)par * C + cc) * sl + row) * 2, tag, p.err);
+        ll_store_global(gll + ((long long)q * s + r0 + row) * 2, v, tag);
+      }
+    } else {
+      // ---- the other warps: prefetch block t+1 (slab by TMA gather4, M rows by one bulk copy)
+      //      and b_S(t+1), S(t+2) by cp.async -- spread so no warp serialises many TMA issues
+      const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
+      if (pf) {
+        double* adst = Abuf + (buf ^ 1) * absz;
+        if (p.resident) {
+          if (bulk && tm) {
+            const int stride = pf_n / nops >= 1 ? pf_n / nops : 1;
+            if (pf_tid % stride == 0)
+              for (int j = pf_tid / stride; j < nops; j += pf_n / stride) {
+                const int k = 4 * j;
+                fence_proxy_async();
+                tma_gather4(adst + (long long)k * p.sw, tm, (int)c0, S1[k], S1[min(k + 1, s - 1)],
+                            S1[min(k + 2, s - 1)], S1[min(k + 3, s - 1)], bars + (buf ^ 1));
+              }
+          } else if (bulk) {
+            for (int k = pf_tid; k < s; k += pf_n) {
+              fence_proxy_async();
+              bulk_g2s(adst + (long long)k * p.sw, p.A + (long long)S1[k] * p.lda + c0, (unsigned)w * 8u, bars + (buf ^ 1));
+            }
+          } else {
+            for (long long e = pf_tid; e < (long long)s * w; e += pf_n) {
+              const int k = (int)(e / w), j = (int)(e - (long long)k * w);
+              cp_async8(adst + (long long)k * p.sw + j, p.A + (long long)S1[k] * p.lda + c0 + j);
+            }
+          }
+        }
+        if (stageM) {
+          const double* msrc = p.M_pool + qb1 * ss + (long long)r0 * s;
+          double* mdst = Mbuf + (buf ^ 1) * mslz;
+          if (bulk) {
+            if (pf_tid == pf_n - 1) {
+              fence_proxy_async();
+              bulk_g2s(mdst, msrc, m_bytes, bars + (buf ^ 1));
+            }
+          } else {
+            for (int e = pf_tid; e < R * s; e += pf_n) cp_async8(mdst + e, msrc + e);
+          }
+        }
+        double* b1 = bS_sh + ((it + 1) % 3) * sp;
+        for (int i = pf_tid; i < s; i += pf_n) cp_async8(b1 + i, p.b + S1[i]);
+      }
+      if (t + 2 < p.t1) {
+        int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
+        const int32_t* src = p.S_pool + qb2 * s;
+        for (int i = pf_tid; i < s; i += pf_n) cp_async4(S2 + i, src + i);
+      }
+      cp_async_commit();
     }
+    if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
     PHASE_MARK(3);
-    // ---- r slice: every (row, cluster-group) polls at once; fixed-order combine; - b_S;
-    //      all-gather in the cluster (LL over DSMEM)
+    // ---- r slice: every (row, cluster-group) polls at once; fixed-order combine over the groups
     const int G2 = (R > 0 && R <= T2) ? T2 / R : 1;
     if (R > 0 && R <= T2) {
       if (tid < R * G2) {
@@ -494,6 +510,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     __syncthreads();
     PHASE_MARK(4);
+    // ---- r = A_S x - b_S for my slice; all-gather to the cluster (LL over DSMEM)
     for (int row = tid; row < R; row += T2) {
       double v;
       if (R <= T2) {
@@ -506,12 +523,25 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       for (int cc = 0; cc < C; ++cc)
         ll_store(cluster.map_shared_rank(r_ll + ((long long)par * s + r0 + row) * 2, cc), v, tag);
     }
-    // ---- every CTA: collect r
     for (int l = tid; l < s; l += T2) r_sm[l] = ll_wait_shared(r_ll + ((long long)par * s + l) * 2, tag, p.err);
-    if (stageM && it > 0 && bulk) mbar_wait(bars + 2, (it - 1) & 1u);  // M rows of block t (issued at t-1)
-    if (stageM && it > 0 && !bulk && warp == 0) cp_async_wait_all();
     __syncthreads();
     PHASE_MARK(5);
+    // ---- row 8 (off the critical path of the others): ||r||^2 in a fixed order (identical in
+    //      every CTA) and the replicated window logic; rho for t+1 is read after the next barrier
+    if (warp == NW2 - 1) {
+      double e = 0.0;
+      for (int i = lane; i < s; i += 32) e = fma(r_sm[i], r_sm[i], e);
+      e = warp_sum(e);
+      if (lane == 0) {
+        const int res = window_step_dev(st, tmod, e, p.zeta, p.tol2bb, p.bb, p.adaptive,
+                                        blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
+        if (res) {
+          st.stopped = res;
+          stop_sh = 1;
+        }
+      }
+    }
+    tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
     // ---- row 4: my slice of y = M r (tq threads per row); all-gather (LL over DSMEM)
     if (R > 0) {
       int tq = 1;
@@ -532,110 +562,89 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
             ll_store(cluster.map_shared_rank(y_ll + ((long long)par * s + r0 + row) * 2, cc), v, tag);
       }
     }
-    __syncthreads();  // Msl consumed
-    // ---- warp 0: M rows of block t+1 (on bars[2]; waited before the y step of t+1)
-    if (stageM && t + 1 < p.t1 && warp == 0) {
-      const long long kn = qb1;
-      fence_proxy_async();
-      issue_loads(bulk, nullptr, p.A, p.lda, nullptr, 0, c0, 0, nullptr, p.sw, false,
-                  p.M_pool + kn * ss + (long long)r0 * s, R * s, Msl, bars + 2);
-    }
     for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_shared(y_ll + ((long long)par * s + l) * 2, tag, p.err);
     __syncthreads();
     PHASE_MARK(6);
 
-    // ---- rows 5-6: w on the slab, momentum, x
-    PHASE_MARK(6);
+    // ---- rows 5-6: w on the slab, momentum, x (the next iteration's first barrier orders
+    //      these shared-memory updates before its A_S x pass)
     const double cm = (1.0 - rho) / (1.0 + rho);
-    if (!p.cd) {
-      if (regpath) {
-        // w_j = sum_k A[k][j] y_k: the warp's rows from registers, then a fixed-order sum over warps
+    if (!p.cd && regpath) {
+      // w_j = sum_k A[k][j] y_k: the warp's rows from registers, then a fixed-order sum over warps
 #pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-          double a = 0.0;
-#pragma unroll
-          for (int i = 0; i < RPW; ++i) {
-            const int k = warp + 16 * i;
-            if (k < s) a = fma(ar[i][cc], y_sm[k], a);
-          }
-          if (lane + 32 * cc < w) red_sm[warp * p.slab + lane + 32 * cc] = a;
-        }
-        __syncthreads();
-        for (int jj = tid; jj < w; jj += T2) {
-          double v = 0.0;
-          for (int ww = 0; ww < NW2; ++ww) v += red_sm[ww * p.slab + jj];
-          w_sm[jj] = v;
-        }
-      } else if (p.resident) {
-        const int cw = p.cw, ng = T2 / cw, rg = (s + ng - 1) / ng;
-        const int g = tid / cw, j = tid - g * cw;
-        const int ka = min(s, g * rg), kz = min(s, ka + rg);
+      for (int cc = 0; cc < CPL; ++cc) {
         double a = 0.0;
-        if (j < w)
-          for (int k = ka; k < kz; ++k) a = fma(Ac[(long long)k * p.sw + j], y_sm[k], a);
-        red_sm[g * cw + j] = a;
-        __syncthreads();
-        for (int jj = tid; jj < w; jj += T2) {
-          double v = 0.0;
-          for (int gg = 0; gg < ng; ++gg) v += red_sm[gg * cw + jj];
-          w_sm[jj] = v;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+          const int k = warp + 16 * i;
+          if (k < s) a = fma(ar[i][cc], y_sm[k], a);
         }
-      } else {
-        for (int jj = tid; jj < w; jj += T2) {
-          double a = 0.0;
-          const double* col = p.A + c0 + jj;
-#pragma unroll 8
-          for (int k = 0; k < s; ++k) a = fma(__ldcg(col + (long long)Sc[k] * p.lda), y_sm[k], a);
-          w_sm[jj] = a;
-        }
+        if (lane + 32 * cc < w) red_sm[warp * p.slab + lane + 32 * cc] = a;
+      }
+      __syncthreads();
+      PHASE_MARK(11);
+      for (int jj = tid; jj < w; jj += T2) {
+        double wv = 0.0;
+        for (int ww = 0; ww < NW2; ++ww) wv += red_sm[ww * p.slab + jj];
+        const double mm = cm * (m_sm[jj] - wv);
+        m_sm[jj] = mm;
+        x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
       }
     } else {
-      for (int jj = tid; jj < w; jj += T2) w_sm[jj] = 0.0;
-      __syncthreads();
-      for (int k = tid; k < s; k += T2) {
-        const long long gj = (long long)Sc[k] - p.col_base;
-        if (gj >= c0 && gj < c1) w_sm[gj - c0] = y_sm[k];
-      }
-    }
-    __syncthreads();
-    PHASE_MARK(11);
-    for (int jj = tid; jj < w; jj += T2) {
-      const double wv = w_sm[jj];
-      const double mm = cm * (m_sm[jj] - wv);
-      m_sm[jj] = mm;
-      x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
-    }
-    PHASE_MARK(12);
-    // ---- row 8: ||r||^2 (fixed order, identical in every CTA) and the window logic
-    if (warp == 0) {
-      double e = 0.0;
-      for (int i = lane; i < s; i += 32) e = fma(r_sm[i], r_sm[i], e);
-      e = warp_sum(e);
-      if (lane == 0) {
-        const int res = window_step_dev(st, t, e, p.zeta, p.tol2bb, p.bb, p.adaptive,
-                                        blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
-        if (res) {
-          st.stopped = res;
-          stop_sh = 1;
+      if (!p.cd) {
+        if (p.resident) {
+          const int cw = p.cw, ng = T2 / cw, rg = (s + ng - 1) / ng;
+          const int g = tid / cw, j = tid - g * cw;
+          const int ka = min(s, g * rg), kz = min(s, ka + rg);
+          double a = 0.0;
+          if (j < w)
+            for (int k = ka; k < kz; ++k) a = fma(Ac[(long long)k * p.sw + j], y_sm[k], a);
+          red_sm[g * cw + j] = a;
+          __syncthreads();
+          for (int jj = tid; jj < w; jj += T2) {
+            double v = 0.0;
+            for (int gg = 0; gg < ng; ++gg) v += red_sm[gg * cw + jj];
+            w_sm[jj] = v;
+          }
+        } else {
+          for (int jj = tid; jj < w; jj += T2) {
+            double a = 0.0;
+            const double* col = p.A + c0 + jj;
+#pragma unroll 8
+            for (int k = 0; k < s; ++k) a = fma(__ldcg(col + (long long)Sc[k] * p.lda), y_sm[k], a);
+            w_sm[jj] = a;
+          }
+        }
+      } else {
+        for (int jj = tid; jj < w; jj += T2) w_sm[jj] = 0.0;
+        __syncthreads();
+        for (int k = tid; k < s; k += T2) {
+          const long long gj = (long long)Sc[k] - p.col_base;
+          if (gj >= c0 && gj < c1) w_sm[gj - c0] = y_sm[k];
         }
       }
+      __syncthreads();
+      for (int jj = tid; jj < w; jj += T2) {
+        const double wv = w_sm[jj];
+        const double mm = cm * (m_sm[jj] - wv);
+        m_sm[jj] = mm;
+        x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
+      }
     }
-    __syncthreads();
     PHASE_MARK(7);
     qb1 = qb2;
     qb2 = qb3;
-    if (stop_sh) {
+    if (stop_sh) {  // written before the y barrier of this iteration: every thread sees it
       ++t;
       break;
     }
   }
-  // drain copies still in flight after an early stop (their mbarriers must complete before exit)
+  // drain copies still in flight after an early stop (their barriers must complete before exit)
   if (bulk && t < p.t1) {
-    const int nb = it & 1;  // iteration `it` issued the slab of block t into buffer nb^1
-    if (p.resident) mbar_wait(bars + (nb ^ 1), nb ^ 1 ? phA1 : phA0);
-    if (stageM) mbar_wait(bars + 2, it & 1u);
+    if (it & 1) mbar_wait(bars + 0, phA0); else mbar_wait(bars + 1, phA1);
   }
-  if (!bulk) cp_async_wait_all();
+  cp_async_wait_all();
+  __syncthreads();
   for (int j = tid; j < w; j += T2) {
     p.x[c0 + j] = x_sm[j];
     p.mom[c0 + j] = m_sm[j];
@@ -667,7 +676,7 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   bytes += 3LL * sp * 4;                // S (triple-buffered)
   bytes = (bytes + 127) & ~127LL;
   if (p.resident) bytes += 2LL * ((s + 3) & ~3LL) * p.sw * 8;
-  if (p.m_in_smem) bytes += ((sl * s + 1) & ~1LL) * 8;
+  if (p.m_in_smem) bytes += 2LL * ((sl * s + 15) & ~15LL) * 8;
   return (size_t)bytes + 128;
 }
 

@@ -135,7 +135,7 @@ __global__ void step_window_kernel(StepParams p) {
   e = wsum(e);
   if (lane == 0) {
     DevState st = *p.st;
-    const int res = window_step_dev(st, t, e, p.zeta, p.tol2bb, p.bb, p.adaptive, p.writer,
+    const int res = window_step_dev(st, t % (2 * p.zeta), e, p.zeta, p.tol2bb, p.bb, p.adaptive, p.writer,
                                     p.hist_res, p.hist_rho, p.hist_cap);
     if (res) st.stopped = res;
     st.t_done = t + 1;

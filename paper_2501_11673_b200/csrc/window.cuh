@@ -11,12 +11,12 @@ namespace kpp {
 // stop test E1 <= tol^2 ||b||^2, else the adaptive rho update of Eq (weighted)
 // with omega_i = a_{i-1}/a_i, a_i = (i+1)^{ln(i+1)} (reading Q8), rho = 1 - rhat^{1/zeta}
 // clamped to [0, 0.99] (Q9).  Returns 0 continue, 1 tolerance met, 2 non-finite residual.
-__device__ __forceinline__ int window_step_dev(DevState& st, long long t, double e, long long zeta,
+// tm = t mod 2 zeta is passed in (the persistent kernel keeps it incrementally: no 64-bit division).
+__device__ __forceinline__ int window_step_dev(DevState& st, long long tm, double e, long long zeta,
                                                double tol2bb, double bb, int adaptive, bool writer,
                                                double* hist_res, double* hist_rho,
                                                long long hist_cap) {
   if (!isfinite(e)) return 2;
-  const long long tm = t % (2 * zeta);
   if (tm < zeta) st.E0 += e; else st.E1 += e;
   if (tm != 2 * zeta - 1) return 0;
   st.ichk += 1;
