@@ -368,9 +368,16 @@ IterParams plan_params(const kpp_ctx* ctx, int G, bool resident, bool m_in_smem)
   int tpr = 4;  // >= 4: keeps the row stride a multiple of 4 doubles (TMA 128-byte destinations)
   while (tpr < 32 && tpr * 2 * ctx->s <= iterate_block_threads()) tpr *= 2;
   p.tpr = tpr;
-  // row stride congruent to tpr (mod 16): a half-warp's 16/tpr rows x tpr columns hit distinct banks
-  const int target = tpr % 16;
-  p.sw = (int)(slab + ((target - slab % 16) + 16) % 16);
+  // row stride: the register-tile path (s <= 256, slab <= 64) reads rows with consecutive lanes,
+  // so a multiple of 4 doubles suffices (TMA gather4 writes 4 rows = 32*sw bytes, 128B aligned);
+  // the generic path keeps the stride congruent to tpr (mod 16) so tpr-strided reads are
+  // bank-conflict free
+  if (ctx->s <= 256 && slab <= 64) {
+    p.sw = (int)((slab + 3) / 4 * 4);
+  } else {
+    const int target = tpr % 16;
+    p.sw = (int)(slab + ((target - slab % 16) + 16) % 16);
+  }
   p.cw = (int)((slab + 31) / 32 * 32);
   p.resident = resident && slab <= iterate_block_threads();
   p.m_in_smem = m_in_smem;

@@ -28,4 +28,4 @@ for _ in range(a.reps):
     r = ctx.solve(b, max_iters=a.iters)
     st = ctx.stats()
     print(f"{a.config}: {a.iters} iters phase2 {st['phase2_ms']:.3f} ms -> {st['phase2_ms'] * 1e3 / a.iters:.2f} us/iter; "
-          f"plan grid={st['grid_ctas']} C={st['cluster']} resident={st['resident']} msm={st['m_in_smem']}")
+          f"plan grid={st['grid_ctas']} C={st['cluster']} resident={st['resident']} msm={st['m_in_smem']} tma={st['tma']}")
