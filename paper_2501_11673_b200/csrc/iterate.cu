@@ -17,14 +17,15 @@
 //    passes (A_S x and A_S^T y) read shared memory and A_S crosses HBM once per iteration.
 //    Streaming mode (c4/c5-sized blocks): both passes stream 16-byte loads from HBM/L2.
 //  * The one all-reduce of the iteration (the s-vector A_S x) is a barrier-free dataflow
-//    exchange.  Every value travels as two 8-byte words, each carrying 32 data bits and a
-//    32-bit iteration tag (the "LL" protocol of NCCL): an 8-byte store is single-copy
-//    atomic, so a consumer that polls a word and sees the current tag has the data -- no
-//    flag round trip, no cluster barrier on the critical path.
-//      partials --DSMEM--> slice owner in the cluster (rank c owns rows slice c)
-//      cluster partial of the slice --L2--> the slice owners of every cluster
-//      r slice (fixed-order sum, - b_S) --DSMEM--> every CTA of the cluster
-//      y slice = M[slice] r --DSMEM--> every CTA of the cluster
+//    exchange.  Inside a cluster values move by st.async (DSMEM stores that complete bytes on
+//    the receiver's mbarrier, so the receiver sleeps on its barrier instead of polling);
+//    across clusters through L2 as two 8-byte words, each carrying 32 data bits and a 32-bit
+//    iteration tag (the "LL" protocol of NCCL): an 8-byte store is single-copy atomic, so a
+//    consumer that sees the current tag has the data -- no flag round trip.
+//      partials --st.async--> slice owner in the cluster (rank c owns rows slice c)
+//      cluster partial of the slice --L2 (LL)--> the slice owners of every cluster
+//      r slice (fixed-order sum, - b_S) --st.async--> every CTA of the cluster
+//      y slice = M[slice] r --st.async--> every CTA of the cluster
 //    Every CTA then holds identical r and y, so the scalar window logic is replicated
 //    bit-for-bit and nobody broadcasts a decision.  No floating-point atomics anywhere.
 #include <cooperative_groups.h>
@@ -57,13 +58,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // ------------------------------------------------------------------ LL words
 // value v with tag g -> two words (g << 32 | lo32(v)), (g << 32 | hi32(v))
-__device__ __forceinline__ void ll_store(unsigned long long* dst, double v, unsigned tag) {
-  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
-  const unsigned long long t = (unsigned long long)tag << 32;
-  volatile unsigned long long* d = dst;
-  d[0] = t | (u & 0xffffffffull);
-  d[1] = t | (u >> 32);
-}
 __device__ __forceinline__ void ll_store_global(unsigned long long* dst, double v, unsigned tag) {
   const unsigned long long u = (unsigned long long)__double_as_longlong(v);
   const unsigned long long t = (unsigned long long)tag << 32;
@@ -74,21 +68,6 @@ __device__ __forceinline__ void ll_store_global(unsigned long long* dst, double 
 __device__ __noinline__ void spin_fail(int* err) {
   atomicExch(err, 1);
   __trap();
-}
-// poll a word pair in (local) shared memory until both carry `tag`
-__device__ __forceinline__ double ll_wait_shared(const unsigned long long* src, unsigned tag, int* err) {
-  volatile const unsigned long long* s = src;
-  unsigned long long a = s[0], b = s[1];
-  if ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
-    const unsigned long long t0 = globaltimer();
-    unsigned n = 0;
-    while ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
-      a = s[0];
-      b = s[1];
-      if ((++n & 4095u) == 0 && globaltimer() - t0 > 20000000000ull) spin_fail(err);
-    }
-  }
-  return __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
 }
 __device__ __forceinline__ double ll_wait_global(const unsigned long long* src, unsigned tag, int* err) {
   unsigned long long a, b;
@@ -134,6 +113,27 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+// DSMEM: remote shared::cluster address of a local shared variable in CTA `rank`
+__device__ __forceinline__ unsigned mapa_u32(unsigned la, int rank) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(rank));
+  return ra;
+}
+// asynchronous remote store that completes `8` transaction bytes on the remote mbarrier
+__device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(raddr), "d"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
@@ -243,11 +243,11 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
 
   // ---- shared memory carve-up (must match iterate_smem_bytes) ----
   const int sp = (s + 1) & ~1;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // [4] mbarriers
-  unsigned long long* rp_ll = bars + 4;                 // [2][C][sl][2]  partials for my slice
-  unsigned long long* r_ll = rp_ll + 4LL * C * sl;      // [2][s][2]
-  unsigned long long* y_ll = r_ll + 4LL * s;            // [2][s][2]
-  double* x_sm = reinterpret_cast<double*>(y_ll + 4LL * s);
+  // mbarriers: [0],[1] slab buffers (TMA); [2] partials of my slice arrived; [3] r arrived;
+  // [4] y arrived (the DSMEM exchanges are st.async stores completing bytes on these)
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);
+  double* rp_sm = reinterpret_cast<double*>(bars + 8);  // [C][sl] partials of my slice, from each rank
+  double* x_sm = rp_sm + ((C * sl + 1) & ~1);
   double* m_sm = x_sm + p.slab;
   double* w_sm = m_sm + p.slab;
   double* r_sm = w_sm + p.slab;
@@ -289,10 +289,9 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     st = *p.st;
     stop_sh = 0;
     tmod_sh = p.t0 % (2 * p.zeta);
-    for (int i = 0; i < 4; ++i) mbar_init(bars + i, 1);
+    for (int i = 0; i < 5; ++i) mbar_init(bars + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (long long i = tid; i < 4LL * C * sl + 8LL * s; i += T2) rp_ll[i] = 0ull;  // tags start at 1
   for (int j = tid; j < w; j += T2) {
     x_sm[j] = p.x[c0 + j];
     m_sm[j] = p.mom[c0 + j];
@@ -315,6 +314,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   cluster.sync();  // every peer's LL buffers are zeroed before any DSMEM store
   long long tmod = tmod_sh;
 
+  const unsigned la_rp = smem_u32(rp_sm), la_r = smem_u32(r_sm), la_y = smem_u32(y_sm);
+  const unsigned lb_rp = smem_u32(bars + 2), lb_r = smem_u32(bars + 3), lb_y = smem_u32(bars + 4);
   const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   long long prof_acc[16] = {};
   long long prof_last = prof_on ? clock64() : 0;
@@ -337,7 +338,13 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       else          { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
     }
     cp_async_wait_all();
-    if (tid == 0 && pf && bulk) mbar_expect_tx(bars + (buf ^ 1), slab_bytes + m_bytes);
+    if (tid == 0) {
+      if (pf && bulk) mbar_expect_tx(bars + (buf ^ 1), slab_bytes + m_bytes);
+      // this iteration's DSMEM exchanges (phase `it` of bars[2..4])
+      if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
+      mbar_expect_tx(bars + 3, (unsigned)s * 8u);
+      mbar_expect_tx(bars + 4, (unsigned)s * 8u);
+    }
     __syncthreads();
     PHASE_MARK(0);
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
@@ -367,8 +374,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         const int k = warp + 16 * rs_row<RPW>(lane);
         if ((lane & (32 / (RPW > 0 ? RPW : 1) - 1)) == 0 && k < s) {
           const int owner = k / sl;
-          unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
-          ll_store(cluster.map_shared_rank(dst, owner), v[0], tag);
+          st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), v[0], mapa_u32(lb_rp, owner));
         }
       } else {
         const int tpr = p.tpr;
@@ -384,8 +390,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
           for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
           if (k < s && sub == 0) {
             const int owner = k / sl;
-            unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
-            ll_store(cluster.map_shared_rank(dst, owner), acc, tag);
+            st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), acc, mapa_u32(lb_rp, owner));
           }
         }
       }
@@ -424,8 +429,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
           const int k = kbase + u;
           if (lane == 0 && k < s) {
             const int owner = k / sl;
-            unsigned long long* dst = rp_ll + (((long long)par * C + c) * sl + (k - owner * sl)) * 2;
-            ll_store(cluster.map_shared_rank(dst, owner), v, tag);
+            st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), v, mapa_u32(lb_rp, owner));
           }
         }
       }
@@ -435,9 +439,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     unsigned long long* gll = p.ll + (long long)par * NQ * s * 2;
     if (pf_tid < 0) {
       // ---- slice owner warps: cluster partial of my slice -> L2 (LL) for every cluster's owner
+      if (R > 0) mbar_wait_cluster(bars + 2, it & 1u);
       for (int row = tid; row < R; row += 32 * own_warps) {
         double v = 0.0;
-        for (int cc = 0; cc < C; ++cc) v += ll_wait_shared(rp_ll + (((long long)par * C + cc) * sl + row) * 2, tag, p.err);
+        for (int cc = 0; cc < C; ++cc) v += rp_sm[cc * sl + row];
         ll_store_global(gll + ((long long)q * s + r0 + row) * 2, v, tag);
       }
     } else {
@@ -505,7 +510,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       for (int row = tid; row < R; row += T2) {
         double v = 0.0;
         for (int qq = 0; qq < NQ; ++qq) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
-        y_sm[r0 + row] = v;  // staging (y_sm is rewritten below)
+        red_sm[row] = v;  // R <= 2 * T2
       }
     }
     __syncthreads();
@@ -517,14 +522,12 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         v = 0.0;
         for (int grp = 0; grp < G2; ++grp) v += red_sm[grp * R + row];
       } else {
-        v = y_sm[r0 + row];
+        v = red_sm[row];
       }
       v -= bSc[r0 + row];
-      for (int cc = 0; cc < C; ++cc)
-        ll_store(cluster.map_shared_rank(r_ll + ((long long)par * s + r0 + row) * 2, cc), v, tag);
+      for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_r, cc));
     }
-    for (int l = tid; l < s; l += T2) r_sm[l] = ll_wait_shared(r_ll + ((long long)par * s + l) * 2, tag, p.err);
-    __syncthreads();
+    mbar_wait_cluster(bars + 3, it & 1u);  // r complete (every rank's slice)
     PHASE_MARK(5);
     // ---- row 8 (off the critical path of the others): ||r||^2 in a fixed order (identical in
     //      every CTA) and the replicated window logic; rho for t+1 is read after the next barrier
@@ -559,11 +562,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         for (int o = tq >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (row < R)
           for (int cc = sub; cc < C; cc += tq)
-            ll_store(cluster.map_shared_rank(y_ll + ((long long)par * s + r0 + row) * 2, cc), v, tag);
+            st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_y, cc));
       }
     }
-    for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_shared(y_ll + ((long long)par * s + l) * 2, tag, p.err);
-    __syncthreads();
+    mbar_wait_cluster(bars + 4, it & 1u);  // y complete
     PHASE_MARK(6);
 
     // ---- rows 5-6: w on the slab, momentum, x (the next iteration's first barrier orders
@@ -666,9 +668,8 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   const long long s = p.s;
   const long long sp = (s + 1) & ~1LL;
   const long long sl = (s + C - 1) / C;
-  long long bytes = 4 * 8;              // mbarriers
-  bytes += 4LL * C * sl * 8;            // rp_ll
-  bytes += 8LL * s * 8;                 // r_ll, y_ll
+  long long bytes = 8 * 8;              // mbarriers
+  bytes += ((C * sl + 1) & ~1LL) * 8;   // rp
   bytes += 3LL * p.slab * 8;            // x, m, w
   bytes += 2LL * sp * 8;                // r, y
   bytes += 2LL * T2 * 8;                // red
