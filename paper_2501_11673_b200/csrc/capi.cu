@@ -93,6 +93,7 @@ struct kpp_ctx {
   size_t ll_bytes = 0;
   int* d_err = nullptr;
   long long* d_prof = nullptr;
+  long long* d_trace = nullptr;
   // phase-1 workspace
   Buf p1;
   int* d_info = nullptr;
@@ -615,6 +616,14 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       p.ll = ctx->d_ll; p.err = ctx->d_err; p.st = ctx->dstate;
       p.hist_res = ctx->hist_res; p.hist_rho = ctx->hist_rho; p.hist_cap = ctx->hist_capd;
       CK(cudaMemsetAsync(ctx->d_ll, 0, ctx->ll_bytes, st));
+      p.dbg_skip = getenv("KPP_DBG_SKIP") ? 1 : 0;
+      if (getenv("KPP_TRACE")) {
+        static long long* dtr = nullptr;
+        if (!dtr) CK(cudaMalloc((void**)&dtr, 16LL * ctx->pgrid * 8 * sizeof(long long)));
+        CK(cudaMemsetAsync(dtr, 0, 16LL * ctx->pgrid * 8 * sizeof(long long), st));
+        p.trace = dtr;
+        ctx->d_trace = dtr;
+      }
       if (getenv("KPP_PHASE_PROFILE")) {
         if (!ctx->d_prof) {
           CKS(dalloc(ctx, &ctx->d_prof, 16));
@@ -677,6 +686,17 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   CK(cudaStreamSynchronize(st));
   if (n_hist) *n_hist = nh;
   if (iters_out) *iters_out = max_iters == 0 ? 0 : fin.t_done;
+  if (ctx->d_trace) {
+    std::vector<long long> tr(16LL * ctx->pgrid * 8);
+    CK(cudaMemcpy(tr.data(), ctx->d_trace, tr.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    FILE* f = fopen(getenv("KPP_TRACE"), "wb");
+    if (f) {
+      long long hdr[2] = {16, ctx->pgrid};
+      fwrite(hdr, sizeof hdr, 1, f);
+      fwrite(tr.data(), sizeof(long long), tr.size(), f);
+      fclose(f);
+    }
+  }
   if (ctx->d_prof && fin.t_done > 0) {
     long long pr[16];
     CK(cudaMemcpy(pr, ctx->d_prof, sizeof pr, cudaMemcpyDeviceToHost));

@@ -189,6 +189,12 @@ __device__ __forceinline__ void issue_loads(bool bulk, const CUtensorMap* tm, co
   }
 }
 
+#define TRACE(e)                                                                              \
+  do {                                                                                        \
+    if (p.trace && tid == 0 && it >= 64 && it < 64 + 16)                                      \
+      p.trace[(((long long)(it - 64) * gridDim.x) + blockIdx.x) * 8 + (e)] = (long long)globaltimer(); \
+  } while (0)
+
 #define PHASE_MARK(i)                   \
   do {                                  \
     if (prof_on) {                      \
@@ -347,10 +353,11 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     __syncthreads();
     PHASE_MARK(0);
+    TRACE(0);
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
 
     // ---- row 3: partial block residual over the slab; each value goes (LL) to its slice owner
-    const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL;
+    const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL && !p.dbg_skip;
     double ar[RPW > 0 ? RPW : 1][CPL > 0 ? CPL : 1];
     if (p.resident) {
       if (regpath) {
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         for (int kp = 0; kp < s; kp += rows_per_pass) {
           const int k = kp + tid / tpr;
           double acc = 0.0;
-          if (k < s) {
+          if (k < s && !p.dbg_skip) {
             const double* arow = Ac + (long long)k * p.sw;
             for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
           }
@@ -435,11 +442,13 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       }
     }
     PHASE_MARK(2);
+    TRACE(1);
 
     unsigned long long* gll = p.ll + (long long)par * NQ * s * 2;
     if (pf_tid < 0) {
       // ---- slice owner warps: cluster partial of my slice -> L2 (LL) for every cluster's owner
       if (R > 0) mbar_wait_cluster(bars + 2, it & 1u);
+      TRACE(2);
       for (int row = tid; row < R; row += 32 * own_warps) {
         double v = 0.0;
         for (int cc = 0; cc < C; ++cc) v += rp_sm[cc * sl + row];
@@ -497,6 +506,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
     PHASE_MARK(3);
+    TRACE(3);
     // ---- r slice: every (row, cluster-group) polls at once; fixed-order combine over the groups
     const int G2 = (R > 0 && R <= T2) ? T2 / R : 1;
     if (R > 0 && R <= T2) {
@@ -515,6 +525,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     __syncthreads();
     PHASE_MARK(4);
+    TRACE(4);
     // ---- r = A_S x - b_S for my slice; all-gather to the cluster (LL over DSMEM)
     for (int row = tid; row < R; row += T2) {
       double v;
@@ -529,6 +540,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     mbar_wait_cluster(bars + 3, it & 1u);  // r complete (every rank's slice)
     PHASE_MARK(5);
+    TRACE(5);
     // ---- row 8 (off the critical path of the others): ||r||^2 in a fixed order (identical in
     //      every CTA) and the replicated window logic; rho for t+1 is read after the next barrier
     if (warp == NW2 - 1) {
@@ -554,7 +566,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       for (int rp = 0; rp < R; rp += rows_per_pass) {
         const int row = rp + tid / tq;
         double v = 0.0;
-        if (row < R) {
+        if (row < R && !p.dbg_skip) {
           const double* Mrow = p.m_in_smem ? Msl + (long long)row * s
                                            : p.M_pool + (long long)p.bid[t - p.t0] * ss + (long long)(r0 + row) * s;
           for (int l = sub; l < s; l += tq) v = fma(Mrow[l], r_sm[l], v);
@@ -567,6 +579,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     mbar_wait_cluster(bars + 4, it & 1u);  // y complete
     PHASE_MARK(6);
+    TRACE(6);
 
     // ---- rows 5-6: w on the slab, momentum, x (the next iteration's first barrier orders
     //      these shared-memory updates before its A_S x pass)
@@ -634,6 +647,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       }
     }
     PHASE_MARK(7);
+    TRACE(7);
     qb1 = qb2;
     qb2 = qb3;
     if (stop_sh) {  // written before the y barrier of this iteration: every thread sees it

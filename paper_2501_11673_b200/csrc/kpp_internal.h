@@ -106,7 +106,9 @@ struct alignas(64) IterParams {
   int tpr;               // threads per row in the A_S x pass (power of two <= 32)
   int cw;                // threads per column group in the A_S^T y pass (multiple of 32)
   int m_in_smem;         // this rank's rows of M are staged in shared memory
-  long long* prof;       // optional [8] phase cycle counters (CTA 0), nullptr = off
+  long long* prof;       // optional [16] phase cycle counters (CTA 0), nullptr = off
+  long long* trace;      // debug: [16][grid][8] globaltimer event stamps (iterations 64..79)
+  int dbg_skip;          // debug: 1 skips the arithmetic of rows 3-5 (exchange-latency floor)
 };
 // Persistent Phase-2 kernel: grid = C * clusters CTAs, cluster size C.
 cudaError_t launch_iterate(cudaStream_t st, const IterParams& p, int grid, int C, size_t smem);
