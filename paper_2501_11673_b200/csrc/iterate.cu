@@ -83,6 +83,44 @@ __device__ __forceinline__ double ll_wait_global(const unsigned long long* src, 
   return __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
 }
 
+// Sum of LL values at src[q * stride] for q = q0, q0 + dq, ... < nq (fixed order), with every
+// load of the thread in flight at once: one L2 round trip once the data is there.
+template <int KQ>
+__device__ __forceinline__ double ll_gather_sum(const unsigned long long* src, long long stride, int q0, int dq, int nq,
+                                                unsigned tag, int* err) {
+  unsigned long long a[KQ], b[KQ];
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < KQ; ++i) {
+    const int qq = q0 + i * dq;
+    if (qq < nq) {
+      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a[i]), "=l"(b[i]) : "l"(src + qq * stride) : "memory");
+      cnt = i + 1;
+    } else {
+      a[i] = b[i] = (unsigned long long)tag << 32;
+    }
+  }
+  const unsigned long long t0 = globaltimer();
+  unsigned n = 0;
+  for (;;) {
+    bool all = true;
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) {
+      if ((unsigned)(a[i] >> 32) != tag || (unsigned)(b[i] >> 32) != tag) {
+        all = false;
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a[i]), "=l"(b[i]) : "l"(src + (q0 + i * dq) * stride) : "memory");
+      }
+    }
+    if (all) break;
+    if ((++n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) spin_fail(err);
+  }
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < KQ; ++i)
+    if (i < cnt) v += __longlong_as_double((long long)((a[i] & 0xffffffffull) | (b[i] << 32)));
+  return v;
+}
+
 // ------------------------------------------------------------------ TMA bulk copies + mbarriers
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -343,6 +381,19 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       if (buf == 0) { mbar_wait(bars + 0, phA0); phA0 ^= 1u; }
       else          { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
     }
+    // register tile of the slab (rows wi + 16 i, columns lane + 32 c): loaded as soon as the slab
+    // has landed, before the barrier (it does not depend on x)
+    const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL && !p.dbg_skip;
+    double ar[RPW > 0 ? RPW : 1][CPL > 0 ? CPL : 1];
+    if (regpath) {
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int k = warp + 16 * i;
+        const double* arow = Ac + (long long)k * p.sw;
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) ar[i][cc] = (k < s && lane + 32 * cc < w) ? arow[lane + 32 * cc] : 0.0;
+      }
+    }
     cp_async_wait_all();
     if (tid == 0) {
       if (pf && bulk) mbar_expect_tx(bars + (buf ^ 1), slab_bytes + m_bytes);
@@ -357,8 +408,6 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
 
     // ---- row 3: partial block residual over the slab; each value goes (LL) to its slice owner
-    const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL && !p.dbg_skip;
-    double ar[RPW > 0 ? RPW : 1][CPL > 0 ? CPL : 1];
     if (p.resident) {
       if (regpath) {
         // register tile: rows wi + 16 i, columns lane + 32 c, kept until the A_S^T y pass
@@ -368,14 +417,9 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         double v[RPW > 0 ? RPW : 1];
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-          const int k = warp + 16 * i;
-          const double* arow = Ac + (long long)k * p.sw;
           v[i] = 0.0;
 #pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) {
-            ar[i][cc] = (k < s && lane + 32 * cc < w) ? arow[lane + 32 * cc] : 0.0;
-            v[i] = fma(ar[i][cc], xr[cc], v[i]);
-          }
+          for (int cc = 0; cc < CPL; ++cc) v[i] = fma(ar[i][cc], xr[cc], v[i]);
         }
         if constexpr (RPW > 0) warp_reduce_scatter<RPW>(v, lane);
         const int k = warp + 16 * rs_row<RPW>(lane);
@@ -513,7 +557,11 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       if (tid < R * G2) {
         const int row = tid % R, grp = tid / R;
         double v = 0.0;
-        for (int qq = grp; qq < NQ; qq += G2) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
+        if ((NQ - grp + G2 - 1) / G2 <= 16) {
+          v = ll_gather_sum<16>(gll + (long long)(r0 + row) * 2, (long long)s * 2, grp, G2, NQ, tag, p.err);
+        } else {
+          for (int qq = grp; qq < NQ; qq += G2) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
+        }
         red_sm[grp * R + row] = v;
       }
     } else if (R > T2) {
@@ -558,10 +606,11 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
     // ---- row 4: my slice of y = M r (tq threads per row); all-gather (LL over DSMEM)
-    if (R > 0) {
+    if (R > 0 && warp < NW2 - 1) {  // the last warp runs the window logic meanwhile
+      constexpr int TY = T2 - 32;
       int tq = 1;
-      while (tq < 32 && tq * 2 * R <= T2) tq *= 2;
-      const int rows_per_pass = T2 / tq;
+      while (tq < 32 && tq * 2 * R <= TY) tq *= 2;
+      const int rows_per_pass = TY / tq;
       const int sub = tid & (tq - 1);
       for (int rp = 0; rp < R; rp += rows_per_pass) {
         const int row = rp + tid / tq;
