@@ -557,8 +557,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       if (tid < R * G2) {
         const int row = tid % R, grp = tid / R;
         double v = 0.0;
-        if ((NQ - grp + G2 - 1) / G2 <= 16) {
-          v = ll_gather_sum<16>(gll + (long long)(r0 + row) * 2, (long long)s * 2, grp, G2, NQ, tag, p.err);
+        if ((NQ - grp + G2 - 1) / G2 <= 4) {
+          v = ll_gather_sum<4>(gll + (long long)(r0 + row) * 2, (long long)s * 2, grp, G2, NQ, tag, p.err);
         } else {
           for (int qq = grp; qq < NQ; qq += G2) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
         }
