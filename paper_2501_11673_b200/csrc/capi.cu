@@ -701,10 +701,10 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     long long pr[16];
     CK(cudaMemcpy(pr, ctx->d_prof, sizeof pr, cudaMemcpyDeviceToHost));
     CK(cudaMemset(ctx->d_prof, 0, sizeof pr));
-    const char* names[13] = {"wait", "pf_rest", "rows3_Ax", "clpart", "xcluster_wait", "r_gather", "y",
-                             "window", "-", "pf_tma", "pf_cpasync", "w", "mom"};
+    const char* names[16] = {"top", "-", "P1", "clpart", "gather_sync", "r_wait", "y_wait", "P4b", "-", "-", "-",
+                             "P4a", "-", "y_comp", "gather_poll", "r_comb"};
     fprintf(stderr, "[kpp phase cycles/iter, CTA 0]");
-    for (int i = 0; i < 13; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
+    for (int i = 0; i < 16; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
     fprintf(stderr, "\n");
   }
   if (fin.stopped == 2) return fail(ctx, KPP_EDIVERGED, "non-finite block residual at iteration %lld", fin.t_done - 1);

@@ -165,11 +165,14 @@ __device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned 
                "r"(rbar)
                : "memory");
 }
+// Wait for bytes delivered by peers' st.async.  CTA-scope acquire is enough: the data are in this
+// CTA's shared memory and complete_tx makes them visible with the phase; a cluster-scope acquire
+// would also invalidate L1 (CCTL.IVALL) on every wait.
 __device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "WAITC_%=:\n"
-      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -564,6 +567,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         }
         red_sm[grp * R + row] = v;
       }
+      PHASE_MARK(14);  // this thread's polls done
     } else if (R > T2) {
       for (int row = tid; row < R; row += T2) {
         double v = 0.0;
@@ -586,6 +590,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       v -= bSc[r0 + row];
       for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_r, cc));
     }
+    PHASE_MARK(15);  // r slice combined and sent
     mbar_wait_cluster(bars + 3, it & 1u);  // r complete (every rank's slice)
     PHASE_MARK(5);
     TRACE(5);
@@ -626,6 +631,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
             st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_y, cc));
       }
     }
+    PHASE_MARK(13);  // y slice computed and sent
     mbar_wait_cluster(bars + 4, it & 1u);  // y complete
     PHASE_MARK(6);
     TRACE(6);
