@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     PHASE_MARK(3);
     TRACE(3);
     // ---- r slice: every (row, cluster-group) polls at once; fixed-order combine over the groups
-    const int G2 = (R > 0 && R <= T2) ? T2 / R : 1;
+    const int G2 = (R > 0 && R <= T2) ? min(16, T2 / R) : 1;
     if (R > 0 && R <= T2) {
       if (tid < R * G2) {
         const int row = tid % R, grp = tid / R;
@@ -582,8 +582,14 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     for (int row = tid; row < R; row += T2) {
       double v;
       if (R <= T2) {
-        v = 0.0;
-        for (int grp = 0; grp < G2; ++grp) v += red_sm[grp * R + row];
+        double g[16];  // G2 <= 16 partial sums: all loads at once, fixed pairwise tree
+#pragma unroll
+        for (int i = 0; i < 16; ++i) g[i] = (i < G2) ? red_sm[i * R + row] : 0.0;
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+          for (int i = 0; i < h; ++i) g[i] += g[i + h];
+        v = g[0];
       } else {
         v = red_sm[row];
       }
@@ -610,25 +616,41 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       }
     }
     tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
-    // ---- row 4: my slice of y = M r (tq threads per row); all-gather (LL over DSMEM)
-    if (R > 0 && warp < NW2 - 1) {  // the last warp runs the window logic meanwhile
-      constexpr int TY = T2 - 32;
-      int tq = 1;
-      while (tq < 32 && tq * 2 * R <= TY) tq *= 2;
-      const int rows_per_pass = TY / tq;
-      const int sub = tid & (tq - 1);
-      for (int rp = 0; rp < R; rp += rows_per_pass) {
-        const int row = rp + tid / tq;
-        double v = 0.0;
-        if (row < R && !p.dbg_skip) {
-          const double* Mrow = p.m_in_smem ? Msl + (long long)row * s
-                                           : p.M_pool + (long long)p.bid[t - p.t0] * ss + (long long)(r0 + row) * s;
-          for (int l = sub; l < s; l += tq) v = fma(Mrow[l], r_sm[l], v);
+    // ---- row 4: my slice of y = M r; warps 0..14 take groups of RY rows (lanes over columns,
+    //      conflict-free shared-memory reads, butterfly reduce-scatter); lanes of each group then
+    //      send the row to peer (lane & 7) by st.async.  The last warp runs the window logic.
+    if (R > 0 && warp < NW2 - 1) {
+      constexpr int RY = 4;
+      const int ngroups = (R + RY - 1) / RY;
+      const double* Mg = p.M_pool + (long long)p.bid[t - p.t0] * ss + (long long)r0 * s;
+      for (int gi = warp; gi < ngroups; gi += NW2 - 1) {
+        const int rb = gi * RY;
+        double v[RY] = {0.0, 0.0, 0.0, 0.0};
+        if (!p.dbg_skip) {
+          if (p.m_in_smem) {
+#pragma unroll 4
+            for (int l = lane; l < s; l += 32) {
+              const double rl = r_sm[l];
+#pragma unroll
+              for (int i = 0; i < RY; ++i)
+                if (rb + i < R) v[i] = fma(Msl[(long long)(rb + i) * s + l], rl, v[i]);
+            }
+          } else {
+#pragma unroll 4
+            for (int l = lane; l < s; l += 32) {
+              const double rl = r_sm[l];
+#pragma unroll
+              for (int i = 0; i < RY; ++i)
+                if (rb + i < R) v[i] = fma(__ldg(Mg + (long long)(rb + i) * s + l), rl, v[i]);
+            }
+          }
         }
-        for (int o = tq >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (row < R)
-          for (int cc = sub; cc < C; cc += tq)
-            st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_y, cc));
+        warp_reduce_scatter<RY>(v, lane);
+        const int row = rb + rs_row<RY>(lane);
+        const int cc = lane & 7;  // lanes of a row group share the value; lane & 7 picks the peer
+        if (row < R && cc < C) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v[0], mapa_u32(lb_y, cc));
+        if (row < R && C > 8)
+          for (int c2 = cc + 8; c2 < C; c2 += 8) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, c2), v[0], mapa_u32(lb_y, c2));
       }
     }
     PHASE_MARK(13);  // y slice computed and sent
