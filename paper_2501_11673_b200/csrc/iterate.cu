@@ -363,45 +363,6 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
 
   const unsigned la_rp = smem_u32(rp_sm), la_r = smem_u32(r_sm), la_y = smem_u32(y_sm);
   const unsigned lb_rp = smem_u32(bars + 2), lb_r = smem_u32(bars + 3), lb_y = smem_u32(bars + 4);
-  // ---- per-thread constants of the iteration loop (hoisted: no divisions inside the loop)
-  const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL && !p.dbg_skip;
-  unsigned amask = 0;  // bit i*CPL+cc: element (row warp + 16 i, column lane + 32 cc) exists
-#pragma unroll
-  for (int i = 0; i < (RPW > 0 ? RPW : 1); ++i)
-#pragma unroll
-    for (int cc = 0; cc < (CPL > 0 ? CPL : 1); ++cc)
-      if (warp + 16 * i < s && lane + 32 * cc < w) amask |= 1u << (i * (CPL > 0 ? CPL : 1) + cc);
-  const int a_off0 = warp * p.sw + lane;
-  const int a_step = 16 * p.sw;
-  // A_S x partial of this lane after the reduce-scatter: row p1_k goes to its owner by st.async
-  const int p1_k = warp + 16 * rs_row<(RPW > 0 ? RPW : 1)>(lane);
-  const bool p1_send = regpath && (lane & (32 / (RPW > 0 ? RPW : 1) - 1)) == 0 && p1_k < s;
-  unsigned p1_ra = 0, p1_rb = 0;
-  if (p1_send) {
-    const int owner = p1_k / sl;
-    p1_ra = mapa_u32(la_rp + (unsigned)(c * sl + p1_k - owner * sl) * 8u, owner);
-    p1_rb = mapa_u32(lb_rp, owner);
-  }
-  // cross-cluster gather: (row, group) of this thread
-  const int G2 = (R > 0 && R <= T2) ? min(16, T2 / R) : 1;
-  const bool g_on = R > 0 && R <= T2 && tid < R * G2;
-  const int g_row = g_on ? tid % R : 0, g_grp = g_on ? tid / R : 0;
-  const bool g_fast = g_on && (NQ - g_grp + G2 - 1) / G2 <= 4;
-  // prefetch issue (TMA gather4 ops spread over the non-owner warps)
-  const int pf_stride = (pf_n / nops) >= 1 ? pf_n / nops : 1;
-  const bool pf_tma_thread = pf_tid >= 0 && (pf_tid % pf_stride) == 0;
-  const int pf_j0 = pf_tid >= 0 ? pf_tid / pf_stride : 0;
-  const int pf_jstep = pf_n / pf_stride;
-  // remote (cluster) addresses of r, y buffers and barriers, per peer
-  __shared__ unsigned peer_r[16], peer_rb[16], peer_y[16], peer_yb[16];
-  if (tid < C) {
-    peer_r[tid] = mapa_u32(la_r, tid);
-    peer_rb[tid] = mapa_u32(lb_r, tid);
-    peer_y[tid] = mapa_u32(la_y, tid);
-    peer_yb[tid] = mapa_u32(lb_y, tid);
-  }
-  __syncthreads();
-
   const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   long long prof_acc[16] = {};
   long long prof_last = prof_on ? clock64() : 0;
@@ -425,13 +386,16 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     // register tile of the slab (rows wi + 16 i, columns lane + 32 c): loaded as soon as the slab
     // has landed, before the barrier (it does not depend on x)
+    const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL && !p.dbg_skip;
     double ar[RPW > 0 ? RPW : 1][CPL > 0 ? CPL : 1];
     if (regpath) {
 #pragma unroll
-      for (int i = 0; i < RPW; ++i)
+      for (int i = 0; i < RPW; ++i) {
+        const int k = warp + 16 * i;
+        const double* arow = Ac + (long long)k * p.sw;
 #pragma unroll
-        for (int cc = 0; cc < CPL; ++cc)
-          ar[i][cc] = (amask >> (i * CPL + cc) & 1u) ? Ac[a_off0 + i * a_step + 32 * cc] : 0.0;
+        for (int cc = 0; cc < CPL; ++cc) ar[i][cc] = (k < s && lane + 32 * cc < w) ? arow[lane + 32 * cc] : 0.0;
+      }
     }
     cp_async_wait_all();
     if (tid == 0) {
@@ -461,7 +425,11 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
           for (int cc = 0; cc < CPL; ++cc) v[i] = fma(ar[i][cc], xr[cc], v[i]);
         }
         if constexpr (RPW > 0) warp_reduce_scatter<RPW>(v, lane);
-        if (p1_send) st_async_f64(p1_ra, v[0], p1_rb);
+        const int k = warp + 16 * rs_row<RPW>(lane);
+        if ((lane & (32 / (RPW > 0 ? RPW : 1) - 1)) == 0 && k < s) {
+          const int owner = k / sl;
+          st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), v[0], mapa_u32(lb_rp, owner));
+        }
       } else {
         const int tpr = p.tpr;
         const int rows_per_pass = T2 / tpr;
@@ -541,8 +509,9 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         double* adst = Abuf + (buf ^ 1) * absz;
         if (p.resident) {
           if (bulk && tm) {
-            if (pf_tma_thread)
-              for (int j = pf_j0; j < nops; j += pf_jstep) {
+            const int stride = pf_n / nops >= 1 ? pf_n / nops : 1;
+            if (pf_tid % stride == 0)
+              for (int j = pf_tid / stride; j < nops; j += pf_n / stride) {
                 const int k = 4 * j;
                 fence_proxy_async();
                 tma_gather4(adst + (long long)k * p.sw, tm, (int)c0, S1[k], S1[min(k + 1, s - 1)],
@@ -586,15 +555,17 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     PHASE_MARK(3);
     TRACE(3);
     // ---- r slice: every (row, cluster-group) polls at once; fixed-order combine over the groups
+    const int G2 = (R > 0 && R <= T2) ? min(16, T2 / R) : 1;
     if (R > 0 && R <= T2) {
-      if (g_on) {
+      if (tid < R * G2) {
+        const int row = tid % R, grp = tid / R;
         double v = 0.0;
-        if (g_fast) {
-          v = ll_gather_sum<4>(gll + (long long)(r0 + g_row) * 2, (long long)s * 2, g_grp, G2, NQ, tag, p.err);
+        if ((NQ - grp + G2 - 1) / G2 <= 4) {
+          v = ll_gather_sum<4>(gll + (long long)(r0 + row) * 2, (long long)s * 2, grp, G2, NQ, tag, p.err);
         } else {
-          for (int qq = g_grp; qq < NQ; qq += G2) v += ll_wait_global(gll + ((long long)qq * s + r0 + g_row) * 2, tag, p.err);
+          for (int qq = grp; qq < NQ; qq += G2) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
         }
-        red_sm[g_grp * R + g_row] = v;
+        red_sm[grp * R + row] = v;
       }
       PHASE_MARK(14);  // this thread's polls done
     } else if (R > T2) {
@@ -623,7 +594,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         v = red_sm[row];
       }
       v -= bSc[r0 + row];
-      for (int cc = 0; cc < C; ++cc) st_async_f64(peer_r[cc] + (unsigned)(r0 + row) * 8u, v, peer_rb[cc]);
+      for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_r, cc));
     }
     PHASE_MARK(15);  // r slice combined and sent
     mbar_wait_cluster(bars + 3, it & 1u);  // r complete (every rank's slice)
@@ -677,9 +648,9 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         warp_reduce_scatter<RY>(v, lane);
         const int row = rb + rs_row<RY>(lane);
         const int cc = lane & 7;  // lanes of a row group share the value; lane & 7 picks the peer
-        if (row < R && cc < C) st_async_f64(peer_y[cc] + (unsigned)(r0 + row) * 8u, v[0], peer_yb[cc]);
+        if (row < R && cc < C) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v[0], mapa_u32(lb_y, cc));
         if (row < R && C > 8)
-          for (int c2 = cc + 8; c2 < C; c2 += 8) st_async_f64(peer_y[c2] + (unsigned)(r0 + row) * 8u, v[0], peer_yb[c2]);
+          for (int c2 = cc + 8; c2 < C; c2 += 8) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, c2), v[0], mapa_u32(lb_y, c2));
       }
     }
     PHASE_MARK(13);  // y slice computed and sent
