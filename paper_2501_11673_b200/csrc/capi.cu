@@ -489,7 +489,7 @@ kpp_status setup_common(kpp_ctx* ctx) {
   CKS(plan_persistent(ctx));
   const long long part_need = std::max<long long>((long long)ctx->grid * ctx->s, 2LL * ctx->num_sms * ctx->s);
   CKS(dalloc(ctx, &ctx->part, (size_t)part_need));
-  ctx->ll_bytes = (size_t)2 * ctx->num_sms * ctx->s * 2 * sizeof(unsigned long long);
+  ctx->ll_bytes = ((size_t)2 * ctx->num_sms * ctx->s * 2 + 4 * (size_t)ctx->s) * sizeof(unsigned long long);
   CKS(dalloc(ctx, &ctx->d_ll, ctx->ll_bytes / sizeof(unsigned long long)));
   CKS(dalloc(ctx, &ctx->d_err, 1));
   CK(cudaMemset(ctx->d_err, 0, sizeof(int)));
@@ -616,6 +616,9 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       p.ll = ctx->d_ll; p.err = ctx->d_err; p.st = ctx->dstate;
       p.hist_res = ctx->hist_res; p.hist_rho = ctx->hist_rho; p.hist_cap = ctx->hist_capd;
       CK(cudaMemsetAsync(ctx->d_ll, 0, ctx->ll_bytes, st));
+      // blocks that stream from HBM (c4/c5 sizes): y once per GPU, gathered through L2
+      p.ygl = p.resident ? 0 : 1;
+      p.yll = ctx->d_ll + ctx->ll_bytes / sizeof(unsigned long long) - 4LL * ctx->s;
       p.dbg_skip = getenv("KPP_DBG_SKIP") ? 1 : 0;
       if (getenv("KPP_TRACE")) {
         static long long* dtr = nullptr;

@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       // this iteration's DSMEM exchanges (phase `it` of bars[2..4])
       if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
       mbar_expect_tx(bars + 3, (unsigned)s * 8u);
-      mbar_expect_tx(bars + 4, (unsigned)s * 8u);
+      if (!p.ygl) mbar_expect_tx(bars + 4, (unsigned)s * 8u);
     }
     __syncthreads();
     PHASE_MARK(0);
@@ -449,36 +449,49 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         }
       }
     } else {
+      // streaming: a warp takes 2 rows at a time; each lane keeps 4 x 2 sixteen-byte loads in
+      // flight (64 KB per SM) so HBM stays saturated
       const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
-      for (int kbase = warp * 4; kbase < s; kbase += NW2 * 4) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        const double* rows[4];
+      constexpr int UR = 2, UQ = 4;
+      for (int kbase = warp * UR; kbase < s; kbase += NW2 * UR) {
+        double acc[UR] = {0.0, 0.0};
+        const double* rows[UR];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) rows[u] = p.A + (long long)Sc[min(kbase + u, s - 1)] * p.lda + c0;
+        for (int u = 0; u < UR; ++u) rows[u] = p.A + (long long)Sc[min(kbase + u, s - 1)] * p.lda + c0;
         if (vec) {
           const int w2 = w >> 1;
-          for (int j2 = lane; j2 < w2; j2 += 32) {
-            const double2 xv = *reinterpret_cast<const double2*>(x_sm + 2 * j2);
+          const double2* x2 = reinterpret_cast<const double2*>(x_sm);
+          for (int jb = lane; jb < w2; jb += 32 * UQ) {
+            double2 a[UR][UQ], xv[UQ];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const double2 a = __ldcs(reinterpret_cast<const double2*>(rows[u]) + j2);
-              acc[u] = fma(a.x, xv.x, acc[u]);
-              acc[u] = fma(a.y, xv.y, acc[u]);
+            for (int q = 0; q < UQ; ++q) {
+              const int j2 = jb + 32 * q;
+              xv[q] = j2 < w2 ? x2[j2] : make_double2(0.0, 0.0);
+#pragma unroll
+              for (int u = 0; u < UR; ++u)
+                a[u][q] = j2 < w2 ? __ldcs(reinterpret_cast<const double2*>(rows[u]) + j2) : make_double2(0.0, 0.0);
             }
+#pragma unroll
+            for (int q = 0; q < UQ; ++q)
+#pragma unroll
+              for (int u = 0; u < UR; ++u) {
+                acc[u] = fma(a[u][q].x, xv[q].x, acc[u]);
+                acc[u] = fma(a[u][q].y, xv[q].y, acc[u]);
+              }
           }
           if ((w & 1) && lane == 0) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] = fma(__ldcs(rows[u] + w - 1), x_sm[w - 1], acc[u]);
+            for (int u = 0; u < UR; ++u) acc[u] = fma(__ldcs(rows[u] + w - 1), x_sm[w - 1], acc[u]);
           }
         } else {
           for (int j = lane; j < w; j += 32) {
             const double xv = x_sm[j];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] = fma(__ldcs(rows[u] + j), xv, acc[u]);
+            for (int u = 0; u < UR; ++u) acc[u] = fma(__ldcs(rows[u] + j), xv, acc[u]);
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < UR; ++u) {
           const double v = warp_sum(acc[u]);
           const int k = kbase + u;
           if (lane == 0 && k < s) {
@@ -616,45 +629,68 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       }
     }
     tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
+    if (p.ygl) {
+      // ---- row 4, large blocks: y rows [yg0, yg1) of this CTA (every M element read once per
+      //      iteration on the whole GPU), published to L2 as LL words; all CTAs gather y below
+      const int yg0 = (int)((long long)blockIdx.x * s / gridDim.x);
+      const int yg1 = (int)((long long)(blockIdx.x + 1) * s / gridDim.x);
+      if (warp < NW2 - 1) {
+        const double* Mb = p.M_pool + (long long)p.bid[t - p.t0] * ss;
+        for (int k = yg0 + warp; k < yg1; k += NW2 - 1) {
+          double v = 0.0;
+          const double* Mrow = Mb + (long long)k * s;
+#pragma unroll 4
+          for (int l = lane; l < s; l += 32) v = fma(__ldg(Mrow + l), r_sm[l], v);
+          v = warp_sum(v);
+          if (lane == 0) ll_store_global(p.yll + ((long long)par * s + k) * 2, v, tag);
+        }
+      }
+    } else {
     // ---- row 4: my slice of y = M r; warps 0..14 take groups of RY rows (lanes over columns,
-    //      conflict-free shared-memory reads, butterfly reduce-scatter); lanes of each group then
-    //      send the row to peer (lane & 7) by st.async.  The last warp runs the window logic.
-    if (R > 0 && warp < NW2 - 1) {
-      constexpr int RY = 4;
-      const int ngroups = (R + RY - 1) / RY;
-      const double* Mg = p.M_pool + (long long)p.bid[t - p.t0] * ss + (long long)r0 * s;
-      for (int gi = warp; gi < ngroups; gi += NW2 - 1) {
-        const int rb = gi * RY;
-        double v[RY] = {0.0, 0.0, 0.0, 0.0};
-        if (!p.dbg_skip) {
-          if (p.m_in_smem) {
+      //      conflict-free shared-memory reads, butterfly reduce-scatter); lanes of each group then
+      //      send the row to peer (lane & 7) by st.async.  The last warp runs the window logic.
+      if (R > 0 && warp < NW2 - 1) {
+        constexpr int RY = 4;
+        const int ngroups = (R + RY - 1) / RY;
+        const double* Mg = p.M_pool + (long long)p.bid[t - p.t0] * ss + (long long)r0 * s;
+        for (int gi = warp; gi < ngroups; gi += NW2 - 1) {
+          const int rb = gi * RY;
+          double v[RY] = {0.0, 0.0, 0.0, 0.0};
+          if (!p.dbg_skip) {
+            if (p.m_in_smem) {
 #pragma unroll 4
-            for (int l = lane; l < s; l += 32) {
-              const double rl = r_sm[l];
+              for (int l = lane; l < s; l += 32) {
+                const double rl = r_sm[l];
 #pragma unroll
-              for (int i = 0; i < RY; ++i)
-                if (rb + i < R) v[i] = fma(Msl[(long long)(rb + i) * s + l], rl, v[i]);
-            }
-          } else {
+                for (int i = 0; i < RY; ++i)
+                  if (rb + i < R) v[i] = fma(Msl[(long long)(rb + i) * s + l], rl, v[i]);
+              }
+            } else {
 #pragma unroll 4
-            for (int l = lane; l < s; l += 32) {
-              const double rl = r_sm[l];
+              for (int l = lane; l < s; l += 32) {
+                const double rl = r_sm[l];
 #pragma unroll
-              for (int i = 0; i < RY; ++i)
-                if (rb + i < R) v[i] = fma(__ldg(Mg + (long long)(rb + i) * s + l), rl, v[i]);
+                for (int i = 0; i < RY; ++i)
+                  if (rb + i < R) v[i] = fma(__ldg(Mg + (long long)(rb + i) * s + l), rl, v[i]);
+              }
             }
           }
+          warp_reduce_scatter<RY>(v, lane);
+          const int row = rb + rs_row<RY>(lane);
+          const int cc = lane & 7;  // lanes of a row group share the value; lane & 7 picks the peer
+          if (row < R && cc < C) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v[0], mapa_u32(lb_y, cc));
+          if (row < R && C > 8)
+            for (int c2 = cc + 8; c2 < C; c2 += 8) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, c2), v[0], mapa_u32(lb_y, c2));
         }
-        warp_reduce_scatter<RY>(v, lane);
-        const int row = rb + rs_row<RY>(lane);
-        const int cc = lane & 7;  // lanes of a row group share the value; lane & 7 picks the peer
-        if (row < R && cc < C) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v[0], mapa_u32(lb_y, cc));
-        if (row < R && C > 8)
-          for (int c2 = cc + 8; c2 < C; c2 += 8) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, c2), v[0], mapa_u32(lb_y, c2));
       }
     }
     PHASE_MARK(13);  // y slice computed and sent
-    mbar_wait_cluster(bars + 4, it & 1u);  // y complete
+    if (p.ygl) {
+      for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_global(p.yll + ((long long)par * s + l) * 2, tag, p.err);
+      __syncthreads();
+    } else {
+      mbar_wait_cluster(bars + 4, it & 1u);  // y complete
+    }
     PHASE_MARK(6);
     TRACE(6);
 
@@ -699,12 +735,35 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
             w_sm[jj] = v;
           }
         } else {
-          for (int jj = tid; jj < w; jj += T2) {
-            double a = 0.0;
-            const double* col = p.A + c0 + jj;
+          const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
+          if (vec) {
+            // second pass: a thread owns a column pair, 8 sixteen-byte row loads in flight
+            for (int j2 = tid; 2 * j2 < w; j2 += T2) {
+              double ax = 0.0, ay = 0.0;
+              const double* col = p.A + c0 + 2 * j2;
+              const bool pair = 2 * j2 + 1 < w;
 #pragma unroll 8
-            for (int k = 0; k < s; ++k) a = fma(__ldcg(col + (long long)Sc[k] * p.lda), y_sm[k], a);
-            w_sm[jj] = a;
+              for (int k = 0; k < s; ++k) {
+                const double yk = y_sm[k];
+                if (pair) {
+                  const double2 a = __ldcs(reinterpret_cast<const double2*>(col + (long long)Sc[k] * p.lda));
+                  ax = fma(a.x, yk, ax);
+                  ay = fma(a.y, yk, ay);
+                } else {
+                  ax = fma(__ldcs(col + (long long)Sc[k] * p.lda), yk, ax);
+                }
+              }
+              w_sm[2 * j2] = ax;
+              if (pair) w_sm[2 * j2 + 1] = ay;
+            }
+          } else {
+            for (int jj = tid; jj < w; jj += T2) {
+              double a = 0.0;
+              const double* col = p.A + c0 + jj;
+#pragma unroll 8
+              for (int k = 0; k < s; ++k) a = fma(__ldcs(col + (long long)Sc[k] * p.lda), y_sm[k], a);
+              w_sm[jj] = a;
+            }
           }
         }
       } else {

@@ -95,6 +95,8 @@ struct alignas(64) IterParams {
   int adaptive;          // 0: rho fixed
   int writer;            // this rank writes the history
   unsigned long long* ll; // [2][clusters][s][2] tagged cluster partials (zeroed before launch)
+  unsigned long long* yll; // [2][s][2] tagged y (global-y mode; zeroed before launch)
+  int ygl;               // 1: y computed once on the GPU (CTA-owned rows) and gathered from L2
   int* err;              // set if a spin-wait times out
   DevState* st;
   double* hist_res;      // [hist_cap]
