@@ -395,36 +395,53 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
     if (ctx->cluster_opt && C != ctx->cluster_opt) continue;
     int G = ctx->num_sms / C * C;
     if (G <= 0) continue;
-    Cand best{0, 0, {}, 0};
-    for (int variant = 0; variant < 4 && best.G == 0; ++variant) {
-      const bool res = ctx->resident_opt && variant < 2;
-      const bool msm = (variant % 2) == 0;
+    // variants in order of preference: resident slab with M rows double-/single-buffered in
+    // shared memory, resident without M, streaming with M, streaming
+    const int res_list[6] = {1, 1, 1, 0, 0, 0};
+    const int msm_list[6] = {1, 2, 0, 1, 2, 0};
+    for (int variant = 0; variant < 6; ++variant) {
+      const bool res = res_list[variant] && ctx->resident_opt;
+      if (res_list[variant] && !ctx->resident_opt) continue;
       int g = G;
       for (int rep = 0; rep < 4 && g > 0; ++rep) {
-        IterParams p = plan_params(ctx, g, res, msm);
+        IterParams p = plan_params(ctx, g, res, msm_list[variant] != 0);
+        p.m_in_smem = msm_list[variant];
         if (res && !p.resident) break;
         const size_t smem = iterate_smem_bytes(p, C);
         if ((long long)smem > maxsm) break;
         const int nq = iterate_max_clusters(p, C, smem);
         if (nq <= 0) break;
         if (nq * C >= g) {
-          best = {C, g, p, smem};
+          cands.push_back({C, g, p, smem});
           break;
         }
         g = nq * C;
       }
     }
-    if (best.G > 0) cands.push_back(best);
   }
   if (cands.empty()) return fail(ctx, KPP_ECUDA, "no feasible launch plan for the persistent kernel");
+  // Pick by the measured behaviour on B200: resident slabs want the M
+  // rows in shared memory and clusters of 4 (8, 2, 16 next); streaming blocks want every SM
+  // (HBM bandwidth) and clusters of 2.  Candidates losing more than 15% of the SMs are skipped.
   int gmax = 0;
   for (auto& c : cands) gmax = std::max(gmax, c.G);
-  // prefer resident plans, then the largest cluster within 5% of the best SM count
+  auto score = [&](const Cand& c) {
+    double sc = (double)c.G;
+    if (c.p.resident) {
+      sc *= c.p.m_in_smem ? 1.0 : 0.35;
+      const double cw = c.C == 4 ? 1.0 : c.C == 8 ? 0.9 : c.C == 2 ? 0.8 : c.C == 16 ? 0.8 : 0.3;
+      sc *= cw;
+    } else {
+      sc *= 0.6;  // a resident plan, when feasible, always wins
+      const double cw = c.C == 2 ? 1.0 : c.C == 4 ? 0.97 : c.C == 8 ? 0.9 : c.C == 16 ? 0.85 : 0.5;
+      sc *= cw;
+    }
+    if (c.G * 100 < gmax * 85) sc *= 0.5;
+    return sc;
+  };
   const Cand* pick = nullptr;
-  for (int pass = 0; pass < 2 && !pick; ++pass)
-    for (auto& c : cands)
-      if ((pass == 1 || c.p.resident || !ctx->resident_opt) && c.G * 20 >= gmax * 19) { pick = &c; break; }
-  if (!pick) pick = &cands.front();
+  for (auto& c : cands)
+    if (!pick || score(c) > score(*pick)) pick = &c;
   ctx->pC = pick->C;
   ctx->pgrid = pick->G;
   ctx->pplan = pick->p;

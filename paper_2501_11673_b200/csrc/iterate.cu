@@ -323,10 +323,12 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   const CUtensorMap* tm = p.tma ? &p.tmA : nullptr;
   const long long ss = (long long)s * s;
   const bool stageM = p.m_in_smem && R > 0;
+  const bool m2 = p.m_in_smem == 2;  // single buffer: M rows of t+1 are loaded once y(t) is complete
   const int nops = (s + 3) >> 2;
   // bytes landing on bars[buf] per iteration: the slab (resident) + this rank's M rows (staged)
   const unsigned slab_bytes = p.resident ? (tm ? (unsigned)nops * 4u * (unsigned)p.sw * 8u : (unsigned)s * (unsigned)w * 8u) : 0u;
   const unsigned m_bytes = stageM ? (unsigned)(R * s) * 8u : 0u;
+  const unsigned m_bytes_slab = m2 ? 0u : m_bytes;  // part of the per-buffer barrier's byte count
   // warps that issue the prefetch (the others do the slice-owner work in the same window)
   const int own_warps = (R + 31) / 32;
   const int pf_tid = tid - 32 * own_warps;
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     st = *p.st;
     stop_sh = 0;
     tmod_sh = p.t0 % (2 * p.zeta);
-    for (int i = 0; i < 5; ++i) mbar_init(bars + i, 1);
+    for (int i = 0; i < 6; ++i) mbar_init(bars + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int j = tid; j < w; j += T2) {
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     const int32_t* Sc = S_sh + (it % 3) * sp;
     const double* bSc = bS_sh + (it % 3) * sp;
     const double* Ac = Abuf + buf * absz;
-    const double* Msl = Mbuf + buf * mslz;
+    const double* Msl = Mbuf + (m2 ? 0 : buf * mslz);
     const bool pf = t + 1 < p.t1;
     // ---- top: this iteration's slab and M rows have landed; this thread's cp.async loads
     //      (S, b_S) of the previous iteration have landed; arm the barrier of the next buffer
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     cp_async_wait_all();
     if (tid == 0) {
-      if (pf && bulk) mbar_expect_tx(bars + (buf ^ 1), slab_bytes + m_bytes);
+      if (pf && bulk) mbar_expect_tx(bars + (buf ^ 1), slab_bytes + m_bytes_slab);
       // this iteration's DSMEM exchanges (phase `it` of bars[2..4])
       if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
       mbar_expect_tx(bars + 3, (unsigned)s * 8u);
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
             }
           }
         }
-        if (stageM) {
+        if (stageM && !m2) {
           const double* msrc = p.M_pool + qb1 * ss + (long long)r0 * s;
           double* mdst = Mbuf + (buf ^ 1) * mslz;
           if (bulk) {
@@ -629,6 +631,11 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       }
     }
     tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
+    if (m2 && stageM && it > 0) {  // M rows of block t, loaded after y(t-1) completed
+      if (bulk) mbar_wait(bars + 5, (it - 1) & 1u);
+      else if (warp == 0) cp_async_wait_all();
+      if (!bulk) __syncwarp();
+    }
     if (p.ygl) {
       // ---- row 4, large blocks: y rows [yg0, yg1) of this CTA (every M element read once per
       //      iteration on the whole GPU), published to L2 as LL words; all CTAs gather y below
@@ -690,6 +697,21 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       __syncthreads();
     } else {
       mbar_wait_cluster(bars + 4, it & 1u);  // y complete
+    }
+    // single-buffered M rows: every reader of Msl in this CTA has sent its y rows (they all
+    // arrived), so the rows of block t+1 can be brought in now
+    if (m2 && stageM && pf && tid == 0) {
+      const double* msrc = p.M_pool + qb1 * ss + (long long)r0 * s;
+      fence_proxy_async();
+      if (bulk) {
+        mbar_expect_tx(bars + 5, m_bytes);
+        bulk_g2s(Mbuf, msrc, m_bytes, bars + 5);
+      }
+    }
+    if (m2 && stageM && pf && !bulk && warp == 0) {
+      const double* msrc = p.M_pool + qb1 * ss + (long long)r0 * s;
+      for (int e = lane; e < R * s; e += 32) cp_async8(Mbuf + e, msrc + e);
+      cp_async_commit();
     }
     PHASE_MARK(6);
     TRACE(6);
@@ -794,6 +816,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   // drain copies still in flight after an early stop (their barriers must complete before exit)
   if (bulk && t < p.t1) {
     if (it & 1) mbar_wait(bars + 0, phA0); else mbar_wait(bars + 1, phA1);
+    if (m2 && stageM) mbar_wait(bars + 5, it & 1u);
   }
   cp_async_wait_all();
   __syncthreads();
@@ -827,7 +850,7 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   bytes += 3LL * sp * 4;                // S (triple-buffered)
   bytes = (bytes + 127) & ~127LL;
   if (p.resident) bytes += 2LL * ((s + 3) & ~3LL) * p.sw * 8;
-  if (p.m_in_smem) bytes += 2LL * ((sl * s + 15) & ~15LL) * 8;
+  if (p.m_in_smem) bytes += (p.m_in_smem == 2 ? 1LL : 2LL) * ((sl * s + 15) & ~15LL) * 8;
   return (size_t)bytes + 128;
 }
 
@@ -848,6 +871,7 @@ static KernelFn pick_kernel(const IterParams& p) {
       if (rpw <= 2) return iterate_kernel<2, 2>;
       if (rpw == 4) return iterate_kernel<4, 2>;
       if (rpw == 8) return iterate_kernel<8, 2>;
+      if (rpw == 16) return iterate_kernel<16, 2>;
     }
   }
   return iterate_kernel<0, 0>;
