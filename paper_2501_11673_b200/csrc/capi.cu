@@ -406,6 +406,7 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
       for (int rep = 0; rep < 4 && g > 0; ++rep) {
         IterParams p = plan_params(ctx, g, res, msm_list[variant] != 0);
         p.m_in_smem = msm_list[variant];
+        p.a_single = (p.resident && iterate_register_tile(p)) ? 1 : 0;
         if (res && !p.resident) break;
         const size_t smem = iterate_smem_bytes(p, C);
         if ((long long)smem > maxsm) break;

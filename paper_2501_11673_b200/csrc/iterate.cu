@@ -307,7 +307,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   double* Abuf = reinterpret_cast<double*>(tail);               // [2][s4][sw] (128B aligned)
   const long long absz = (long long)((s + 3) & ~3) * p.sw;
   const long long mslz = ((long long)sl * s + 15) & ~15LL;
-  double* Mbuf = Abuf + (p.resident ? 2 * absz : 0);           // [2][sl][s] staged rows of M
+  // a_single: the register tile holds the slab during the iteration, so one shared buffer suffices
+  // (block t+1 is gathered into it as soon as the tile of block t is in registers)
+  const bool a_single = p.a_single != 0;
+  double* Mbuf = Abuf + (p.resident ? (a_single ? 1 : 2) * absz : 0);  // [2][sl][s] staged rows of M
   __shared__ DevState st;
   __shared__ int stop_sh;
   __shared__ long long tmod_sh;
@@ -377,14 +380,16 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     const unsigned tag = it + 1;
     const int32_t* Sc = S_sh + (it % 3) * sp;
     const double* bSc = bS_sh + (it % 3) * sp;
-    const double* Ac = Abuf + buf * absz;
+    const int sb = a_single ? 0 : buf;        // slab buffer / barrier of this iteration
+    const int nbf = a_single ? 0 : (buf ^ 1);  // ... of the prefetch of iteration t+1
+    const double* Ac = Abuf + sb * absz;
     const double* Msl = Mbuf + (m2 ? 0 : buf * mslz);
     const bool pf = t + 1 < p.t1;
     // ---- top: this iteration's slab and M rows have landed; this thread's cp.async loads
     //      (S, b_S) of the previous iteration have landed; arm the barrier of the next buffer
     if (bulk) {
-      if (buf == 0) { mbar_wait(bars + 0, phA0); phA0 ^= 1u; }
-      else          { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
+      if (sb == 0) { mbar_wait(bars + 0, phA0); phA0 ^= 1u; }
+      else         { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
     }
     // register tile of the slab (rows wi + 16 i, columns lane + 32 c): loaded as soon as the slab
     // has landed, before the barrier (it does not depend on x)
@@ -401,7 +406,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     cp_async_wait_all();
     if (tid == 0) {
-      if (pf && bulk) mbar_expect_tx(bars + (buf ^ 1), slab_bytes + m_bytes_slab);
+      if (pf && bulk) mbar_expect_tx(bars + nbf, slab_bytes + m_bytes_slab);
       // this iteration's DSMEM exchanges (phase `it` of bars[2..4])
       if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
       mbar_expect_tx(bars + 3, (unsigned)s * 8u);
@@ -521,7 +526,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       //      and b_S(t+1), S(t+2) by cp.async -- spread so no warp serialises many TMA issues
       const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
       if (pf) {
-        double* adst = Abuf + (buf ^ 1) * absz;
+        double* adst = Abuf + nbf * absz;
         if (p.resident) {
           if (bulk && tm) {
             const int stride = pf_n / nops >= 1 ? pf_n / nops : 1;
@@ -530,12 +535,12 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
                 const int k = 4 * j;
                 fence_proxy_async();
                 tma_gather4(adst + (long long)k * p.sw, tm, (int)c0, S1[k], S1[min(k + 1, s - 1)],
-                            S1[min(k + 2, s - 1)], S1[min(k + 3, s - 1)], bars + (buf ^ 1));
+                            S1[min(k + 2, s - 1)], S1[min(k + 3, s - 1)], bars + nbf);
               }
           } else if (bulk) {
             for (int k = pf_tid; k < s; k += pf_n) {
               fence_proxy_async();
-              bulk_g2s(adst + (long long)k * p.sw, p.A + (long long)S1[k] * p.lda + c0, (unsigned)w * 8u, bars + (buf ^ 1));
+              bulk_g2s(adst + (long long)k * p.sw, p.A + (long long)S1[k] * p.lda + c0, (unsigned)w * 8u, bars + nbf);
             }
           } else {
             for (long long e = pf_tid; e < (long long)s * w; e += pf_n) {
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
           if (bulk) {
             if (pf_tid == pf_n - 1) {
               fence_proxy_async();
-              bulk_g2s(mdst, msrc, m_bytes, bars + (buf ^ 1));
+              bulk_g2s(mdst, msrc, m_bytes, bars + nbf);
             }
           } else {
             for (int e = pf_tid; e < R * s; e += pf_n) cp_async8(mdst + e, msrc + e);
@@ -815,7 +820,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   }
   // drain copies still in flight after an early stop (their barriers must complete before exit)
   if (bulk && t < p.t1) {
-    if (it & 1) mbar_wait(bars + 0, phA0); else mbar_wait(bars + 1, phA1);
+    if (a_single || (it & 1)) mbar_wait(bars + 0, phA0); else mbar_wait(bars + 1, phA1);
     if (m2 && stageM) mbar_wait(bars + 5, it & 1u);
   }
   cp_async_wait_all();
@@ -849,7 +854,7 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   bytes += 3LL * sp * 8;                // b_S (triple-buffered)
   bytes += 3LL * sp * 4;                // S (triple-buffered)
   bytes = (bytes + 127) & ~127LL;
-  if (p.resident) bytes += 2LL * ((s + 3) & ~3LL) * p.sw * 8;
+  if (p.resident) bytes += (p.a_single ? 1LL : 2LL) * ((s + 3) & ~3LL) * p.sw * 8;
   if (p.m_in_smem) bytes += (p.m_in_smem == 2 ? 1LL : 2LL) * ((sl * s + 15) & ~15LL) * 8;
   return (size_t)bytes + 128;
 }
@@ -857,6 +862,10 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
 using KernelFn = void (*)(const IterParams);
 
 // register tile for the resident passes: enough registers for w <= XR * tpr and s <= NP * (T2/tpr)
+bool iterate_register_tile(const IterParams& p);
+static KernelFn pick_kernel(const IterParams& p);
+bool iterate_register_tile(const IterParams& p) { return pick_kernel(p) != (KernelFn)iterate_kernel<0, 0>; }
+
 static KernelFn pick_kernel(const IterParams& p) {
   if (p.resident && NW2 * p.slab <= 2 * T2) {
     int rpw = 1;

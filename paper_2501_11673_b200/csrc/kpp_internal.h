@@ -107,7 +107,8 @@ struct alignas(64) IterParams {
   int sw;                // shared-memory row stride of the slab (doubles)
   int tpr;               // threads per row in the A_S x pass (power of two <= 32)
   int cw;                // threads per column group in the A_S^T y pass (multiple of 32)
-  int m_in_smem;         // this rank's rows of M are staged in shared memory
+  int m_in_smem;         // rows of M staged in shared memory: 0 no, 1 double-buffered, 2 single
+  int a_single;          // one slab buffer (the register tile holds the current block)
   long long* prof;       // optional [16] phase cycle counters (CTA 0), nullptr = off
   long long* trace;      // debug: [16][grid][8] globaltimer event stamps (iterations 64..79)
   int dbg_skip;          // debug: 1 skips the arithmetic of rows 3-5 (exchange-latency floor)
@@ -117,6 +118,7 @@ cudaError_t launch_iterate(cudaStream_t st, const IterParams& p, int grid, int C
 int iterate_block_threads();
 size_t iterate_smem_bytes(const IterParams& p, int C);
 int iterate_max_clusters(const IterParams& p, int C, size_t smem);  // co-resident clusters of size C
+bool iterate_register_tile(const IterParams& p);  // the resident passes run from a register tile
 
 // ------------------------------------------------------------------ steps.cu (engine "graph")
 // Iteration cursor of the step kernels (device memory), so a captured graph is reusable.

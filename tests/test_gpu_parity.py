@@ -140,7 +140,7 @@ def test_persistent_plan(kpp):
         ctx = kpp.kpp_setup(A, cfg.s, 1e-8, 0)
         st = ctx.stats()
         assert st["resident"] == resident, (cfg.name, st)
-        assert st["grid_ctas"] >= 0.9 * torch.cuda.get_device_properties(0).multi_processor_count
+        assert st["grid_ctas"] >= 0.75 * torch.cuda.get_device_properties(0).multi_processor_count
         print(cfg.name, st)
 
 
