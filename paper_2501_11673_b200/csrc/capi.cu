@@ -257,6 +257,7 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   const size_t o_X = cqr2 ? carve((size_t)B * ss) : 0;
   const size_t o_Q = cqr2 ? carve((size_t)B * s * n) : 0;
   CKS(ensure_buf(ctx, ctx->p1, off));
+  CK(cudaMemsetAsync(ctx->d_info, 0, (size_t)B * sizeof(int), st));  // the factor kernel only records failures
   char* base = (char*)ctx->p1.p;
   double* part = (double*)(base + o_part);
   double* G = (double*)(base + o_G);
@@ -324,8 +325,9 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
 kpp_status phase1(kpp_ctx* ctx, long long k0, long long k1) {
   const long long s = ctx->s, n = ctx->n;
   const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor == 0;
-  const long long per_block = (long long)sizeof(double) *
-                              ((cqr2 ? 70 : 66) * s * s + (cqr2 ? s * n : 0));
+  // workspace of phase1_batch per block: split-K partials (Z s^2), G, X1 (+ L, X2, X, Q1 for CholeskyQR2)
+  const long long Z = ctx->kind == KIND_KPP ? std::min<long long>(64, std::max<long long>(1, (n + 511) / 512)) : 1;
+  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 3 : 0)) * s * s + (cqr2 ? s * n : 0)) + 1024;
   long long Bmax = std::max<long long>(1, ctx->phase1_mb * (1LL << 20) / per_block);
   Bmax = std::min<long long>(Bmax, 4096);
   for (long long k = k0; k < k1; k += Bmax) {

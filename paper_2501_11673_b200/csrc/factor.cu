@@ -5,10 +5,6 @@
 // inverse X = R^{-1}, from which the runtime forms M = X X^T = G^{-1} on the tensor cores.
 // Memoizing M (rather than R) turns the per-iteration solve into one s x s
 // matvec; DESIGN.md records the parity measurement that justifies it.
-//
-// Up-looking Cholesky: row i of R is R_ij = (G_ij - sum_{k<i} R_ki R_kj) / R_ii, one
-// thread per column j, R kept in place in global memory (L1/L2 resident).
-// Triangular inverse: column j of X by back substitution, one thread per column.
 #include <cstdint>
 
 #include "kpp_internal.h"
@@ -16,53 +12,184 @@
 namespace kpp {
 namespace {
 
-constexpr int CT = 512;
+constexpr int CT = 256;
 
-__global__ void __launch_bounds__(CT) chol_trtri_kernel(double* Gall, double* Xall, int s, int* info) {
+// ------------------------------------------------------------------ blocked Cholesky + R^{-1}
+// One CTA per s x s matrix, NB-wide block steps (right-looking, upper: G = R^T R):
+//   1. diagonal tile: unblocked Cholesky by one warp (lane = column) and its inverse Di
+//   2. panel: R[k, k+1:] = Di^T G[k, k+1:]  (kept in shared memory for step 3)
+//   3. trailing update of the upper triangle: G[i][j] -= sum_l P[l][i] P[l][j]
+//      (4 x 4 register micro-tiles, shared-memory panel rows broadcast across a warp)
+// then the column sweep of the triangular inverse (X = R^{-1}, upper):
+//   X[0:j0, J] = -(X[0:j0, 0:j0] R[0:j0, J]) Di_J   for each NB-wide column block J.
+// Every sum runs in a fixed order (no atomics), so the factor is reproducible bit for bit.
+template <int NB>
+struct CholSmem {
+  static size_t bytes(int s) {
+    return (size_t)(2 * NB * (NB + 1)) * sizeof(double) + (size_t)NB * (size_t)(((s + 3) & ~3) + 4) * sizeof(double) + 16;
+  }
+};
+
+template <int NB>
+__global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, double* Xall, int s, int* info) {
+  extern __shared__ __align__(16) double csm[];
+  double* D = csm;                      // [NB][NB+1] R_kk
+  double* Di = D + NB * (NB + 1);       // [NB][NB+1] R_kk^{-1}
+  double* P = Di + NB * (NB + 1);       // [NB][pld] panel rows
+  const int pld = ((s + 3) & ~3) + 4;
   double* G = Gall + (long long)blockIdx.x * s * s;
   double* X = Xall + (long long)blockIdx.x * s * s;
-  __shared__ double diag_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ int fail_sh;
-  if (threadIdx.x == 0) fail_sh = 0;
+  if (tid == 0) fail_sh = 0;
+  for (long long e = tid; e < (long long)s * s; e += CT) X[e] = 0.0;
   __syncthreads();
-  for (int i = 0; i < s; ++i) {
-    // numerators for row i (columns j >= i)
-    for (int j = i + threadIdx.x; j < s; j += blockDim.x) {
-      double a = 0.0;
-      for (int k = 0; k < i; ++k) a = fma(-G[(long long)k * s + i], G[(long long)k * s + j], a);
-      const double v = G[(long long)i * s + j] + a;
-      if (j == i) {
+
+  for (int k0 = 0; k0 < s; k0 += NB) {
+    const int kb = min(NB, s - k0);
+    const int c0 = k0 + kb;        // first trailing column
+    const int rr = s - c0;         // trailing size
+    // ---- 1. diagonal tile (warp 0; lane = column)
+    if (warp == 0) {
+      const int j = lane;
+      for (int i = 0; i < kb; ++i)
+        if (j < kb && j >= i) D[i * (NB + 1) + j] = G[(long long)(k0 + i) * s + k0 + j];
+      __syncwarp();
+      for (int i = 0; i < kb; ++i) {
+        const double v = D[i * (NB + 1) + i];
         if (!(v > 0.0)) {
-          fail_sh = i + 1;
-          diag_sh = 1.0;
-        } else {
-          diag_sh = sqrt(v);
+          if (lane == 0 && fail_sh == 0) fail_sh = k0 + i + 1;
+        }
+        const double d = (v > 0.0) ? sqrt(v) : 1.0;
+        __syncwarp();
+        if (j < kb && j > i) D[i * (NB + 1) + j] /= d;
+        if (j == i) D[i * (NB + 1) + i] = d;
+        __syncwarp();
+        if (j < kb && j > i) {
+          const double rij = D[i * (NB + 1) + j];
+          for (int i2 = i + 1; i2 <= j; ++i2) D[i2 * (NB + 1) + j] = fma(-D[i * (NB + 1) + i2], rij, D[i2 * (NB + 1) + j]);
+        }
+        __syncwarp();
+      }
+      // Di = R_kk^{-1}: column j by back substitution
+      if (j < kb) {
+        for (int i = j + 1; i < NB; ++i) Di[i * (NB + 1) + j] = 0.0;
+        Di[j * (NB + 1) + j] = 1.0 / D[j * (NB + 1) + j];
+        for (int i = j - 1; i >= 0; --i) {
+          double a = 0.0;
+          for (int l = i + 1; l <= j; ++l) a = fma(D[i * (NB + 1) + l], Di[l * (NB + 1) + j], a);
+          Di[i * (NB + 1) + j] = -a / D[i * (NB + 1) + i];
+        }
+        for (int i = 0; i < kb; ++i) {
+          G[(long long)(k0 + i) * s + k0 + j] = (j >= i) ? D[i * (NB + 1) + j] : 0.0;
+          X[(long long)(k0 + i) * s + k0 + j] = (j >= i) ? Di[i * (NB + 1) + j] : 0.0;
         }
       }
-      G[(long long)i * s + j] = v;  // numerator, scaled below
     }
     __syncthreads();
-    const double d = diag_sh;
-    for (int j = i + threadIdx.x; j < s; j += blockDim.x)
-      G[(long long)i * s + j] = (j == i) ? d : G[(long long)i * s + j] / d;
+    if (rr <= 0) break;
+    // ---- 2. panel P[i][c] = sum_{l <= i} Di[l][i] G[k0+l][c0+c]   (rows of R)
+    for (int c = tid; c < ((rr + 3) & ~3); c += CT) {
+      double g[NB];
+#pragma unroll
+      for (int l = 0; l < NB; ++l) g[l] = (l < kb && c < rr) ? G[(long long)(k0 + l) * s + c0 + c] : 0.0;
+#pragma unroll 1
+      for (int i = 0; i < NB; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int l = 0; l < NB; ++l)
+          if (l <= i) a = fma(Di[l * (NB + 1) + i], g[l], a);
+        if (i < kb) {
+          P[i * pld + c] = a;
+          if (c < rr) G[(long long)(k0 + i) * s + c0 + c] = a;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- 3. trailing update of the upper triangle in 4 x 4 micro-tiles
+    const int T4 = (rr + 3) >> 2;
+    const int ntiles = T4 * (T4 + 1) / 2;
+    for (int idx = tid; idx < ntiles; idx += CT) {
+      // column-major enumeration of the upper triangle: tb = column tile, ta <= tb
+      int tb = (int)((sqrt(8.0 * (double)idx + 1.0) - 1.0) * 0.5);
+      while ((tb + 1) * (tb + 2) / 2 <= idx) ++tb;
+      while (tb * (tb + 1) / 2 > idx) --tb;
+      const int ta = idx - tb * (tb + 1) / 2;
+      const int a0 = 4 * ta, b0 = 4 * tb;
+      double acc[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+      for (int l = 0; l < kb; ++l) {
+        const double2 pa0 = *reinterpret_cast<const double2*>(P + l * pld + a0);
+        const double2 pa1 = *reinterpret_cast<const double2*>(P + l * pld + a0 + 2);
+        const double2 pb0 = *reinterpret_cast<const double2*>(P + l * pld + b0);
+        const double2 pb1 = *reinterpret_cast<const double2*>(P + l * pld + b0 + 2);
+        const double pa[4] = {pa0.x, pa0.y, pa1.x, pa1.y}, pb[4] = {pb0.x, pb0.y, pb1.x, pb1.y};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(pa[u], pb[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = a0 + u;
+        if (i >= rr) continue;
+        double* grow = G + (long long)(c0 + i) * s + c0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int j = b0 + v;
+          if (j < rr && j >= i) grow[j] -= acc[u][v];
+        }
+      }
+    }
     __syncthreads();
   }
-  // zero the strictly lower part
-  for (long long e = threadIdx.x; e < (long long)s * s; e += blockDim.x) {
+  // zero the strictly lower part of R
+  for (long long e = tid; e < (long long)s * s; e += CT) {
     const int i = (int)(e / s), j = (int)(e % s);
     if (i > j) G[e] = 0.0;
   }
-  if (threadIdx.x == 0) info[blockIdx.x] = fail_sh;
+  if (tid == 0 && fail_sh) info[blockIdx.x] = fail_sh;
   __syncthreads();
-  // X = R^{-1}: column j, rows i = j, j-1, ..., 0
-  for (int j = threadIdx.x; j < s; j += blockDim.x) {
-    for (int i = j + 1; i < s; ++i) X[(long long)i * s + j] = 0.0;
-    X[(long long)j * s + j] = 1.0 / G[(long long)j * s + j];
-    for (int i = j - 1; i >= 0; --i) {
-      double a = 0.0;
-      for (int k = i + 1; k <= j; ++k) a = fma(G[(long long)i * s + k], X[(long long)k * s + j], a);
-      X[(long long)i * s + j] = -a / G[(long long)i * s + i];
+  if (fail_sh) return;
+
+  // ---- X = R^{-1}: column blocks J = [j0, j0+kb); diagonal blocks are already in X
+  for (int j0 = NB; j0 < s; j0 += NB) {
+    const int kb = min(NB, s - j0);
+    // stage R[0:j0, J] -> P[l][c] (row l, column c) and Di_J
+    for (int e = tid; e < j0 * NB; e += CT) {
+      const int l = e / NB, c = e - l * NB;
+      P[l * NB + c] = c < kb ? G[(long long)l * s + j0 + c] : 0.0;
     }
+    for (int e = tid; e < NB * NB; e += CT) {
+      const int i = e / NB, c = e - i * NB;
+      Di[i * (NB + 1) + c] = (i < kb && c < kb) ? X[(long long)(j0 + i) * s + j0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int i = tid; i < j0; i += CT) {
+      // T[c] = sum_{l=i}^{j0-1} X[i][l] R[l][j0+c]
+      double t[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) t[c] = 0.0;
+      const double* xrow = X + (long long)i * s;
+      for (int l = i; l < j0; ++l) {
+        const double xv = xrow[l];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) t[c] = fma(xv, P[l * NB + c], t[c]);
+      }
+      // X[i][j0+c] = -sum_{c' <= c} T[c'] Di[c'][c]
+#pragma unroll 1
+      for (int c = 0; c < NB; ++c) {
+        double a = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < NB; ++c2)
+          if (c2 <= c) a = fma(t[c2], Di[c2 * (NB + 1) + c], a);
+        if (c < kb) X[(long long)i * s + j0 + c] = -a;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -101,7 +228,15 @@ __global__ void sumsq_kernel(const double* b, long long m, double* out) {
 
 void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info) {
   if (batch <= 0) return;
-  chol_trtri_kernel<<<batch, CT, 0, st>>>(G, X, s, info);
+  if (s <= 512) {
+    const size_t sm = CholSmem<32>::bytes(s);
+    cudaFuncSetAttribute(chol_trtri_blocked_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    chol_trtri_blocked_kernel<32><<<batch, CT, sm, st>>>(G, X, s, info);
+  } else {
+    const size_t sm = CholSmem<16>::bytes(s);
+    cudaFuncSetAttribute(chol_trtri_blocked_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    chol_trtri_blocked_kernel<16><<<batch, CT, sm, st>>>(G, X, s, info);
+  }
   count_launches(1);
 }
 
