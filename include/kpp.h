@@ -75,8 +75,12 @@ typedef enum {
                              fits; 0: always stream A_S from HBM/L2 */
   KPP_OPT_ENGINE = 9,     /* 0 (default on one GPU): persistent cluster kernel; 1: replayed CUDA
                              graph of step kernels (the multi-GPU engine, NCCL between steps) */
-  KPP_OPT_CLUSTER = 10    /* 0 (default): choose the thread-block cluster size automatically;
+  KPP_OPT_CLUSTER = 10,   /* 0 (default): choose the thread-block cluster size automatically;
                              1, 2, 4, 8 or 16: force it (the grid shrinks to co-resident clusters) */
+  KPP_OPT_YGL = 11        /* where the persistent kernel computes y = M r: -1 (default) automatic;
+                             2: in every CTA from a full copy of M staged in shared memory;
+                             1: once per GPU (rows of M spread over all CTAs), gathered through L2;
+                             0: once per thread-block cluster (DSMEM all-gather of y) */
 } kpp_option;
 
 /* ---- setup ------------------------------------------------------------------ */
@@ -145,6 +149,7 @@ typedef struct {
   int32_t cluster;       /* thread-block cluster size of the persistent kernel */
   int32_t m_in_smem;     /* 1 if each CTA stages its rows of M in shared memory */
   int32_t tma;           /* 1 if resident slabs are gathered by TMA (tile::gather4) */
+  int32_t ygl;           /* where y = M r is computed (KPP_OPT_YGL values 0, 1, 2) */
 } kpp_stats;
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */

@@ -58,7 +58,7 @@ struct kpp_ctx {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   // options
-  int accel = 1, memo = 1, factor = 0, resident_opt = 1, engine = 0, cluster_opt = 0;
+  int accel = 1, memo = 1, factor = 0, resident_opt = 1, engine = 0, cluster_opt = 0, ygl_opt = -1;
   double eta_opt = -1.0, rho_fixed = -1.0;
   long long window = 8192, phase1_mb = 4096;
   cudaStream_t stream = nullptr;
@@ -296,7 +296,7 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
       double* X = (double*)(base + o_X);
       double* Q = (double*)(base + o_Q);
       Operand x1t{X1, s, ss, nullptr, 0, 1}, as{ctx->A, ctx->lda, 0, S, s, 0};
-      launch_dgemm(st, B, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0);  // Q1 = X1^T A_S
+      launch_dgemm(st, B, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);  // Q1 = X1^T A_S (X1^T lower)
       Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
       const int z2 = launch_dgemm(st, B, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
       Operand x1n{X1, s, ss, nullptr, 0, 0};
@@ -397,17 +397,23 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
     if (ctx->cluster_opt && C != ctx->cluster_opt) continue;
     int G = ctx->num_sms / C * C;
     if (G <= 0) continue;
-    // variants in order of preference: resident slab with M rows double-/single-buffered in
-    // shared memory, resident without M, streaming with M, streaming
-    const int res_list[6] = {1, 1, 1, 0, 0, 0};
-    const int msm_list[6] = {1, 2, 0, 1, 2, 0};
-    for (int variant = 0; variant < 6; ++variant) {
-      const bool res = res_list[variant] && ctx->resident_opt;
-      if (res_list[variant] && !ctx->resident_opt) continue;
+    // variants: (resident slab, M rows staged per CTA, where y = M r is computed)
+    //   ygl 2: every CTA holds the whole M(t) in shared memory and computes y locally
+    //   ygl 0: each cluster computes y from its CTAs' rows of M (DSMEM all-gather of y)
+    //   ygl 1: y computed once per GPU (a few rows per CTA) and gathered through L2
+    struct V { int res, msm, ygl; };
+    const V vlist[] = {{1, 0, 2}, {1, 1, 0}, {1, 2, 0}, {1, 0, 1}, {1, 0, 0},
+                       {0, 0, 1}, {0, 1, 0}, {0, 2, 0}, {0, 0, 0}};
+    for (const V& v : vlist) {
+      if (ctx->ygl_opt >= 0 && v.ygl != ctx->ygl_opt) continue;
+      if (v.res && !ctx->resident_opt) continue;
+      if (v.ygl == 2 && (ctx->s & 1)) continue;  // one bulk copy of s*s doubles: a multiple of 16 bytes
+      const bool res = v.res != 0;
       int g = G;
       for (int rep = 0; rep < 4 && g > 0; ++rep) {
-        IterParams p = plan_params(ctx, g, res, msm_list[variant] != 0);
-        p.m_in_smem = msm_list[variant];
+        IterParams p = plan_params(ctx, g, res, v.msm != 0);
+        p.m_in_smem = v.msm;
+        p.ygl = v.ygl;
         p.a_single = (p.resident && iterate_register_tile(p)) ? 1 : 0;
         if (res && !p.resident) break;
         const size_t smem = iterate_smem_bytes(p, C);
@@ -431,11 +437,15 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
   auto score = [&](const Cand& c) {
     double sc = (double)c.G;
     if (c.p.resident) {
-      sc *= c.p.m_in_smem ? 1.0 : 0.35;
+      // measured: c2 ygl0+M rows double-buffered 7.9 us/it, ygl2 8.65,
+      // ygl1 9.1; c3 (M rows only single-buffered) ygl1 9.7, ygl0 12.7
+      if (c.p.ygl == 0) sc *= c.p.m_in_smem == 1 ? 1.0 : c.p.m_in_smem == 2 ? 0.85 : 0.35;
+      else if (c.p.ygl == 1) sc *= 0.97;
+      else sc *= 0.9;
       const double cw = c.C == 4 ? 1.0 : c.C == 8 ? 0.9 : c.C == 2 ? 0.8 : c.C == 16 ? 0.8 : 0.3;
       sc *= cw;
     } else {
-      sc *= 0.6;  // a resident plan, when feasible, always wins
+      sc *= c.p.ygl == 1 ? 0.6 : 0.5;  // a resident plan, when feasible, always wins
       const double cw = c.C == 2 ? 1.0 : c.C == 4 ? 0.97 : c.C == 8 ? 0.9 : c.C == 16 ? 0.85 : 0.5;
       sc *= cw;
     }
@@ -478,6 +488,7 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
   ctx->stats.grid_ctas = pick->G;
   ctx->stats.cluster = pick->C;
   ctx->stats.m_in_smem = pick->p.m_in_smem;
+  ctx->stats.ygl = pick->p.ygl;
   return KPP_OK;
 }
 
@@ -637,7 +648,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       p.hist_res = ctx->hist_res; p.hist_rho = ctx->hist_rho; p.hist_cap = ctx->hist_capd;
       CK(cudaMemsetAsync(ctx->d_ll, 0, ctx->ll_bytes, st));
       // blocks that stream from HBM (c4/c5 sizes): y once per GPU, gathered through L2
-      p.ygl = p.resident ? 0 : 1;
+      // p.ygl comes from the launch plan
       p.yll = ctx->d_ll + ctx->ll_bytes / sizeof(unsigned long long) - 4LL * ctx->s;
       p.dbg_skip = getenv("KPP_DBG_SKIP") ? 1 : 0;
       if (getenv("KPP_TRACE")) {
@@ -900,6 +911,10 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
     case KPP_OPT_CLUSTER:
       if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8 && v != 16) return KPP_EINVAL;
       ctx->cluster_opt = (int)v;
+      return plan_persistent(ctx);
+    case KPP_OPT_YGL:
+      if (v != -1.0 && v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;
+      ctx->ygl_opt = (int)v;
       return plan_persistent(ctx);
     case KPP_OPT_ENGINE:
       if (v != 0.0 && v != 1.0) return KPP_EINVAL;

@@ -7,6 +7,7 @@
 // mma tiles, double-buffered shared-memory stages.  Split-K across gridDim.z; partial
 // products are reduced in a fixed order by splitk_reduce (deterministic, no atomics).
 #include <cstdint>
+#include <cstdlib>
 
 #include "kpp_internal.h"
 
@@ -127,6 +128,140 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(int M, int N, int K, int
   }
 }
 
+// ------------------------------------------------------------------ pipelined DMMA GEMM
+// 128 x 64 output tile, K step 16, 3-stage cp.async (16-byte, zero-filling) pipeline, 8 warps of
+// 32 x 32 (4 x 4 m8n8k4 DMMA tiles: 8 fragment loads per 16 MMAs).  Each operand keeps its memory
+// orientation in shared memory ([outer][k] when k is contiguous in memory, [k][outer] otherwise),
+// padded so that the fragment loads of a half-warp hit distinct banks.  Requires 16-byte aligned
+// rows (even ld and batch strides, aligned base pointers); launch_dgemm falls back otherwise.
+constexpr int B2M = 128, B2N = 64, B2K = 16, B2S = 3, B2T = 256;
+constexpr int KC_LD = B2K + 4;      // [outer][k] row stride (doubles)
+constexpr int AM_LD = B2M + 4;      // [k][outer] row stride of A
+constexpr int BN_LD = B2N + 4;      // [k][outer] row stride of B
+constexpr int A_STAGE = (B2M * KC_LD > B2K * AM_LD) ? B2M * KC_LD : B2K * AM_LD;  // doubles
+constexpr int B_STAGE = (B2N * KC_LD > B2K * BN_LD) ? B2N * KC_LD : B2K * BN_LD;
+constexpr size_t B2_SMEM = (size_t)B2S * (A_STAGE + B_STAGE) * sizeof(double);
+
+__device__ __forceinline__ void cp_async16z(double* dst, const double* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
+// Stage one OUTER x 16 operand tile.  KC: memory rows are `outer` (k contiguous) -> sm[outer][k];
+// otherwise memory rows are k (outer contiguous) -> sm[k][outer].
+template <bool KC, int OUTER, int LDO>
+__device__ __forceinline__ void stage_tile(double* sm, const double* base, long long ld, const int32_t* idx,
+                                           int outer0, int outer_lim, int k0, int k_lim) {
+  constexpr int CH = KC ? OUTER * (B2K / 2) : B2K * (OUTER / 2);  // 16-byte chunks
+#pragma unroll
+  for (int c = threadIdx.x; c < CH; c += B2T) {
+    if (KC) {
+      const int o = c / (B2K / 2), kc = (c % (B2K / 2)) * 2;
+      const int go = outer0 + o, gk = k0 + kc;
+      int valid = (go < outer_lim) ? min(2, max(0, k_lim - gk)) : 0;
+      const double* src = valid ? base + (long long)(idx ? idx[go] : go) * ld + gk : base;
+      cp_async16z(sm + o * KC_LD + kc, src, valid * 8);
+    } else {
+      const int kk = c / (OUTER / 2), oc = (c % (OUTER / 2)) * 2;
+      const int gk = k0 + kk, go = outer0 + oc;
+      int valid = (gk < k_lim) ? min(2, max(0, outer_lim - go)) : 0;
+      const double* src = valid ? base + (long long)(idx ? idx[gk] : gk) * ld + go : base;
+      cp_async16z(sm + kk * LDO + oc, src, valid * 8);
+    }
+  }
+}
+
+template <bool AT, bool BT, bool ALOWER>
+__global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int Z, int kchunk, Operand a,
+                                                        Operand b, double* C, long long ldc, long long c_bstride,
+                                                        int upper_only) {
+  extern __shared__ __align__(16) double g2sm[];
+  const int tn = blockIdx.x, tm = blockIdx.y;
+  if (upper_only && tm * B2M >= (tn + 1) * B2N) return;  // tile entirely below the diagonal
+  const int bz = blockIdx.z;
+  const int batch = bz / Z, z = bz % Z;
+  const int kbeg = z * kchunk;
+  int kend = min(K, kbeg + kchunk);
+  if (ALOWER) kend = min(kend, (tm + 1) * B2M);  // A(i,k) = 0 for k > i
+  double* As = g2sm;
+  double* Bs = g2sm + B2S * A_STAGE;
+  const double* abase = a.ptr + (long long)batch * a.bstride;
+  const double* bbase = b.ptr + (long long)batch * b.bstride;
+  const int32_t* aidx = a.idx ? a.idx + (long long)batch * a.idx_bstride : nullptr;
+  const int32_t* bidx = b.idx ? b.idx + (long long)batch * b.idx_bstride : nullptr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int fr = lane >> 2, fc = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nk = kend > kbeg ? (kend - kbeg + B2K - 1) / B2K : 0;
+  const int wrow0 = tm * B2M + wm * 32, wcol0 = tn * B2N + wn * 32;
+  const bool wskip = upper_only && wrow0 >= wcol0 + 32;
+  const int wrow_end = wrow0 + 32;
+  // A logical (i,k): !AT -> memory row i (k contiguous); B logical (k,j): BT -> memory row j
+#pragma unroll
+  for (int st = 0; st < B2S - 1; ++st) {
+    if (st < nk) {
+      stage_tile<!AT, B2M, AM_LD>(As + st * A_STAGE, abase, a.ld, aidx, tm * B2M, M, kbeg + st * B2K, kend);
+      stage_tile<BT, B2N, BN_LD>(Bs + st * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, kbeg + st * B2K, kend);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(B2S - 2) : "memory");
+    __syncthreads();
+    {
+      const int ln = kt + B2S - 1;
+      if (ln < nk) {
+        const int sl = ln % B2S;
+        stage_tile<!AT, B2M, AM_LD>(As + sl * A_STAGE, abase, a.ld, aidx, tm * B2M, M, kbeg + ln * B2K, kend);
+        stage_tile<BT, B2N, BN_LD>(Bs + sl * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, kbeg + ln * B2K, kend);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    const double* Ast = As + (kt % B2S) * A_STAGE;
+    const double* Bst = Bs + (kt % B2S) * B_STAGE;
+    if (wskip) continue;  // this warp's 32 x 32 tile lies below the diagonal (Gram, upper only)
+    // logical A lower triangular: k-steps past this warp's last row contribute nothing
+    if (ALOWER && kbeg + kt * B2K >= wrow_end) continue;
+#pragma unroll
+    for (int kk = 0; kk < B2K; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm * 32 + i * 8 + fr;
+        af[i] = !AT ? Ast[m * KC_LD + kk + fc] : Ast[(kk + fc) * AM_LD + m];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int nn = wn * 32 + j * 8 + fr;
+        bf[j] = BT ? Bst[nn * KC_LD + kk + fc] : Bst[(kk + fc) * BN_LD + nn];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  double* Cb = C + (long long)bz * c_bstride;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gi = tm * B2M + wm * 32 + i * 8 + fr;
+    if (gi >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gj = tn * B2N + wn * 32 + j * 8 + fc * 2;
+      if (gj < N) Cb[(long long)gi * ldc + gj] = acc[i][j][0];
+      if (gj + 1 < N) Cb[(long long)gi * ldc + gj + 1] = acc[i][j][1];
+    }
+  }
+}
+
 __global__ void splitk_reduce_kernel(int M, int N, int Z, const double* part, long long p_bstride,
                                      double diag_add, const double* add, double add_scale,
                                      long long add_bstride, double* out, long long o_bstride,
@@ -149,14 +284,39 @@ __global__ void splitk_reduce_kernel(int M, int N, int Z, const double* part, lo
 
 }  // namespace
 
+static bool aligned16(const Operand& o) {
+  return (reinterpret_cast<uintptr_t>(o.ptr) & 15) == 0 && (o.ld & 1) == 0 && (o.bstride & 1) == 0;
+}
+
+template <bool AT, bool BT, bool AL>
+static void launch2(cudaStream_t st, dim3 grid, int M, int N, int K, int Z, int kchunk, const Operand& a,
+                    const Operand& b, double* C, long long ldc, long long c_bstride, int upper_only) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dgemm2_kernel<AT, BT, AL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)B2_SMEM);
+    attr = true;
+  }
+  dgemm2_kernel<AT, BT, AL><<<grid, B2T, B2_SMEM, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
+}
+
 int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand& a, const Operand& b,
-                 double* C, long long ldc, long long c_bstride, int Z, int upper_only) {
+                 double* C, long long ldc, long long c_bstride, int Z, int upper_only, int a_lower) {
   if (batch <= 0 || M <= 0 || N <= 0) return Z;
   if (Z < 1) Z = 1;
   int kchunk = (K + Z - 1) / Z;
   kchunk = ((kchunk + BK - 1) / BK) * BK;
   Z = (K + kchunk - 1) / kchunk;
   if (Z < 1) Z = 1;
+  count_launches(1);
+  if (aligned16(a) && aligned16(b) && !getenv("KPP_GEMM_V1")) {
+    dim3 grid((N + B2N - 1) / B2N, (M + B2M - 1) / B2M, batch * Z);
+    const bool al = a_lower != 0;
+    if (!a.trans && !b.trans) { if (al) launch2<false, false, true>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); else launch2<false, false, false>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); }
+    else if (!a.trans && b.trans) { if (al) launch2<false, true, true>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); else launch2<false, true, false>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); }
+    else if (a.trans && !b.trans) { if (al) launch2<true, false, true>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); else launch2<true, false, false>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); }
+    else { if (al) launch2<true, true, true>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); else launch2<true, true, false>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); }
+    return Z;
+  }
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch * Z);
   if (!a.trans && !b.trans)
     dgemm_kernel<false, false><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
@@ -166,7 +326,6 @@ int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand&
     dgemm_kernel<true, false><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
   else
     dgemm_kernel<true, true><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
-  count_launches(1);
   return Z;
 }
 

@@ -363,6 +363,12 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   if (warp == 0)  // block t0: slab + M rows on bars[0]
     issue_loads(bulk, tm, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, p.resident,
                 stageM ? p.M_pool + (long long)p.bid[0] * ss + (long long)r0 * s : nullptr, R * s, Mbuf, bars + 0);
+  const bool ylocal = p.ygl == 2;  // every CTA computes y = M r from its own copy of M(t)
+  const unsigned mfull_bytes = (unsigned)ss * 8u;
+  if (ylocal && tid == 0) {
+    mbar_expect_tx(bars + 5, mfull_bytes);
+    bulk_g2s(Mbuf, p.M_pool + (long long)p.bid[0] * ss, mfull_bytes, bars + 5);
+  }
   cluster.sync();  // every peer's LL buffers are zeroed before any DSMEM store
   long long tmod = tmod_sh;
 
@@ -563,6 +569,15 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         }
         double* b1 = bS_sh + ((it + 1) % 3) * sp;
         for (int i = pf_tid; i < s; i += pf_n) cp_async8(b1 + i, p.b + S1[i]);
+        if (p.ygl == 1 && pf_tid == 0) {
+          // rows [yg0, yg1) of M(t+1) into L2 ahead of the y pass of the next iteration
+          const int yg0 = (int)((long long)blockIdx.x * s / gridDim.x);
+          const int yg1 = (int)((long long)(blockIdx.x + 1) * s / gridDim.x);
+          const double* src = p.M_pool + qb1 * ss + (long long)yg0 * s;
+          const unsigned bytes = (unsigned)(yg1 - yg0) * (unsigned)s * 8u;
+          if (bytes > 0 && (s & 1) == 0 && (reinterpret_cast<uintptr_t>(p.M_pool) & 15) == 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+        }
       }
       if (t + 2 < p.t1) {
         int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
@@ -641,7 +656,24 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       else if (warp == 0) cp_async_wait_all();
       if (!bulk) __syncwarp();
     }
-    if (p.ygl) {
+    if (ylocal) {
+      // ---- row 4: y = M r in this CTA from its staged copy of M(t) (no exchange of y)
+      mbar_wait(bars + 5, it & 1u);
+      for (int k = warp; k < s; k += NW2) {
+        const double* Mr = Mbuf + (long long)k * s;
+        double v = 0.0;
+#pragma unroll 4
+        for (int l = lane; l < s; l += 32) v = fma(Mr[l], r_sm[l], v);
+        v = warp_sum(v);
+        if (lane == 0) y_sm[k] = v;
+      }
+      __syncthreads();
+      if (pf && tid == 0) {  // every read of M(t) is done: bring in M(t+1)
+        fence_proxy_async();
+        mbar_expect_tx(bars + 5, mfull_bytes);
+        bulk_g2s(Mbuf, p.M_pool + qb1 * ss, mfull_bytes, bars + 5);
+      }
+    } else if (p.ygl) {
       // ---- row 4, large blocks: y rows [yg0, yg1) of this CTA (every M element read once per
       //      iteration on the whole GPU), published to L2 as LL words; all CTAs gather y below
       const int yg0 = (int)((long long)blockIdx.x * s / gridDim.x);
@@ -697,10 +729,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       }
     }
     PHASE_MARK(13);  // y slice computed and sent
-    if (p.ygl) {
+    if (p.ygl == 1) {
       for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_global(p.yll + ((long long)par * s + l) * 2, tag, p.err);
       __syncthreads();
-    } else {
+    } else if (!p.ygl) {
       mbar_wait_cluster(bars + 4, it & 1u);  // y complete
     }
     // single-buffered M rows: every reader of Msl in this CTA has sent its y rows (they all
@@ -823,6 +855,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     if (a_single || (it & 1)) mbar_wait(bars + 0, phA0); else mbar_wait(bars + 1, phA1);
     if (m2 && stageM) mbar_wait(bars + 5, it & 1u);
   }
+  if (ylocal && t < p.t1) mbar_wait(bars + 5, (it + 1) & 1u);  // M(t+1) copy in flight
   cp_async_wait_all();
   __syncthreads();
   for (int j = tid; j < w; j += T2) {
@@ -856,6 +889,7 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   bytes = (bytes + 127) & ~127LL;
   if (p.resident) bytes += (p.a_single ? 1LL : 2LL) * ((s + 3) & ~3LL) * p.sw * 8;
   if (p.m_in_smem) bytes += (p.m_in_smem == 2 ? 1LL : 2LL) * ((sl * s + 15) & ~15LL) * 8;
+  if (p.ygl == 2) bytes += ((s * s + 15) & ~15LL) * 8;  // full copy of M(t)
   return (size_t)bytes + 128;
 }
 

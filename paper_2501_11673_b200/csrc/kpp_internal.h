@@ -50,9 +50,10 @@ struct Operand {
   int trans;
 };
 // Returns the effective split count Z (K chunks are rounded to the K step).
+// a_lower: the logical A is lower triangular (A(i,k) = 0 for k > i): K is cut per row tile.
 int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand& a,
                  const Operand& b, double* C, long long ldc, long long c_bstride, int Z,
-                 int upper_only);
+                 int upper_only, int a_lower = 0);
 // out[b] = sum_z part[b*Z+z] (+ diag_add on the diagonal) (+ add_scale * add[b]);
 // with upper_only, element (i,j), i>j, is taken from (j,i).
 void launch_splitk_reduce(cudaStream_t st, int batch, int M, int N, int Z, const double* part,

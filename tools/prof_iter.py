@@ -15,12 +15,14 @@ ap.add_argument("--iters", type=int, default=1024)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--cluster", type=int, default=0)
+ap.add_argument("--ygl", type=int, default=-1)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 A, b, _ = synth.make_problem(cfg, device="cuda")
 ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A, cfg.s, cfg.lam, 0)
 ctx.set_option(kpp.OPT_ENGINE, a.engine)
 ctx.set_option(kpp.OPT_CLUSTER, a.cluster)
+ctx.set_option(kpp.OPT_YGL, a.ygl)
 ctx.set_option(kpp.OPT_WINDOW, a.iters)
 ctx.prepare(a.iters)
 for _ in range(a.reps):
@@ -28,4 +30,4 @@ for _ in range(a.reps):
     r = ctx.solve(b, max_iters=a.iters)
     st = ctx.stats()
     print(f"{a.config}: {a.iters} iters phase2 {st['phase2_ms']:.3f} ms -> {st['phase2_ms'] * 1e3 / a.iters:.2f} us/iter; "
-          f"plan grid={st['grid_ctas']} C={st['cluster']} resident={st['resident']} msm={st['m_in_smem']} tma={st['tma']}")
+          f"plan grid={st['grid_ctas']} C={st['cluster']} resident={st['resident']} msm={st['m_in_smem']} tma={st['tma']} ygl={st['ygl']}")
