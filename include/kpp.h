@@ -78,9 +78,10 @@ typedef enum {
   KPP_OPT_CLUSTER = 10,   /* 0 (default): choose the thread-block cluster size automatically;
                              1, 2, 4, 8 or 16: force it (the grid shrinks to co-resident clusters) */
   KPP_OPT_YGL = 11        /* where the persistent kernel computes y = M r: -1 (default) automatic;
-                             2: in every CTA from a full copy of M staged in shared memory;
+                             0: once per thread-block cluster from the CTAs' staged rows of M
+                                (DSMEM all-gather of y);
                              1: once per GPU (rows of M spread over all CTAs), gathered through L2;
-                             0: once per thread-block cluster (DSMEM all-gather of y) */
+                             4: per cluster as the sum of the CTAs' partials M[slice,:]^T r_slice */
 } kpp_option;
 
 /* ---- setup ------------------------------------------------------------------ */
@@ -149,7 +150,7 @@ typedef struct {
   int32_t cluster;       /* thread-block cluster size of the persistent kernel */
   int32_t m_in_smem;     /* 1 if each CTA stages its rows of M in shared memory */
   int32_t tma;           /* 1 if resident slabs are gathered by TMA (tile::gather4) */
-  int32_t ygl;           /* where y = M r is computed (KPP_OPT_YGL values 0, 1, 2) */
+  int32_t ygl;           /* where y = M r is computed (KPP_OPT_YGL values 0, 1, 4) */
 } kpp_stats;
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */

@@ -26,7 +26,7 @@ OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENOTPD, EDIVERGED, EMAXITER = range(8)
 OPT_ACCEL, OPT_MEMO, OPT_ETA, OPT_RHO_FIXED, OPT_FACTOR, OPT_WINDOW, OPT_PHASE1_MB, OPT_RESIDENT = range(1, 9)
 OPT_ENGINE = 9  # 0: persistent kernel (1 GPU default); 1: graph of step kernels (+NCCL)
 OPT_CLUSTER = 10  # 0: automatic; 1/2/4/8/16: forced thread-block cluster size
-OPT_YGL = 11  # -1: automatic; 2: y = M r in every CTA; 1: once per GPU (L2 gather); 0: per cluster
+OPT_YGL = 11  # -1: automatic; 0: y = M r per cluster; 1: once per GPU (L2 gather); 4: per cluster from partials
 
 LIB_PATH = _build.LIB
 _lib = None

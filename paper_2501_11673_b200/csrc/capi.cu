@@ -384,6 +384,7 @@ IterParams plan_params(const kpp_ctx* ctx, int G, bool resident, bool m_in_smem)
   p.cw = (int)((slab + 31) / 32 * 32);
   p.resident = resident && slab <= iterate_block_threads();
   p.m_in_smem = m_in_smem;
+  p.cd = ctx->kind == KIND_CDPP;
   return p;
 }
 
@@ -398,16 +399,17 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
     int G = ctx->num_sms / C * C;
     if (G <= 0) continue;
     // variants: (resident slab, M rows staged per CTA, where y = M r is computed)
-    //   ygl 2: every CTA holds the whole M(t) in shared memory and computes y locally
     //   ygl 0: each cluster computes y from its CTAs' rows of M (DSMEM all-gather of y)
     //   ygl 1: y computed once per GPU (a few rows per CTA) and gathered through L2
+    //   ygl 4: like 0, but y = sum over the cluster of M[slice,:]^T r_slice (no all-gather of r)
+    // (a full copy of M per CTA -- y with no exchange at all -- was measured slower: every CTA
+    //  re-reads the same 128 KB from L2 per iteration)
     struct V { int res, msm, ygl; };
-    const V vlist[] = {{1, 0, 2}, {1, 1, 0}, {1, 2, 0}, {1, 0, 1}, {1, 0, 0},
+    const V vlist[] = {{1, 1, 4}, {1, 2, 4}, {1, 1, 0}, {1, 2, 0}, {1, 0, 1}, {1, 0, 0},
                        {0, 0, 1}, {0, 1, 0}, {0, 2, 0}, {0, 0, 0}};
     for (const V& v : vlist) {
       if (ctx->ygl_opt >= 0 && v.ygl != ctx->ygl_opt) continue;
       if (v.res && !ctx->resident_opt) continue;
-      if (v.ygl == 2 && (ctx->s & 1)) continue;  // one bulk copy of s*s doubles: a multiple of 16 bytes
       const bool res = v.res != 0;
       int g = G;
       for (int rep = 0; rep < 4 && g > 0; ++rep) {
@@ -439,8 +441,11 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
     if (c.p.resident) {
       // measured: c2 ygl0+M rows double-buffered 7.9 us/it, ygl2 8.65,
       // ygl1 9.1; c3 (M rows only single-buffered) ygl1 9.7, ygl0 12.7
-      if (c.p.ygl == 0) sc *= c.p.m_in_smem == 1 ? 1.0 : c.p.m_in_smem == 2 ? 0.85 : 0.35;
-      else if (c.p.ygl == 1) sc *= 0.97;
+      // after per-mode specialisation: c2 ygl0/msm1 5.6 us/it (ygl4 6.3, ygl1 8.4);
+      // c3 ygl0/msm2 7.8 (ygl4 8.3, ygl1 9.4)
+      if (c.p.ygl == 0) sc *= c.p.m_in_smem == 1 ? 1.0 : c.p.m_in_smem == 2 ? 0.95 : 0.35;
+      else if (c.p.ygl == 4) sc *= c.p.m_in_smem == 1 ? 0.9 : 0.88;
+      else if (c.p.ygl == 1) sc *= 0.8;
       else sc *= 0.9;
       const double cw = c.C == 4 ? 1.0 : c.C == 8 ? 0.9 : c.C == 2 ? 0.8 : c.C == 16 ? 0.8 : 0.3;
       sc *= cw;
@@ -913,7 +918,7 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
       ctx->cluster_opt = (int)v;
       return plan_persistent(ctx);
     case KPP_OPT_YGL:
-      if (v != -1.0 && v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;
+      if (v != -1.0 && v != 0.0 && v != 1.0 && v != 4.0) return KPP_EINVAL;
       ctx->ygl_opt = (int)v;
       return plan_persistent(ctx);
     case KPP_OPT_ENGINE:

@@ -1,876 +1,13 @@
-// iterate.cu -- Phase 2: the per-iteration memoized block update.
-//
-// For each iteration t of a window (Alg 5 l.9-18 P:1346-1357 / Alg 3 l.10-20 P:755-766):
-//   r   = A_S x - b_S                                        (row 3)
-//   y   = M r,  M = (A_S A_S^T + lam I)^{-1}  memoized (K++)  / (A_SS + lam I)^{-1} (CD++)  (row 4)
-//   w   = A_S^T y (K++, Eq (bk))  |  I_S^T y (CD++, Alg 3 l.11)            (row 5)
-//   m   = (1-rho)/(1+rho) (m - w);  x = x - w + eta m        (row 6, Eq (momentum))
-//   E0/E1 window sums; checkpoint every 2 zeta: stop test, adaptive rho   (row 8)
-//
-// Engine "persistent": one launch per window, one CTA per SM, thread-block clusters of C CTAs.
-//  * CTA g owns the column slab [g*slab, (g+1)*slab) of A, x and m; x and m stay in shared
-//    memory for the whole launch.
-//  * Resident mode (the s x slab block fits on chip): the block schedule is data independent,
-//    so while iteration t runs, the TMA engine (cp.async.bulk, one bulk copy per row segment,
-//    completion on an mbarrier) brings the slab of block t+1 into the other half of a
-//    double buffer, and the M rows this CTA needs for t+1 into a staging buffer.  Both
-//    passes (A_S x and A_S^T y) read shared memory and A_S crosses HBM once per iteration.
-//    Streaming mode (c4/c5-sized blocks): both passes stream 16-byte loads from HBM/L2.
-//  * The one all-reduce of the iteration (the s-vector A_S x) is a barrier-free dataflow
-//    exchange.  Inside a cluster values move by st.async (DSMEM stores that complete bytes on
-//    the receiver's mbarrier, so the receiver sleeps on its barrier instead of polling);
-//    across clusters through L2 as two 8-byte words, each carrying 32 data bits and a 32-bit
-//    iteration tag (the "LL" protocol of NCCL): an 8-byte store is single-copy atomic, so a
-//    consumer that sees the current tag has the data -- no flag round trip.
-//      partials --st.async--> slice owner in the cluster (rank c owns rows slice c)
-//      cluster partial of the slice --L2 (LL)--> the slice owners of every cluster
-//      r slice (fixed-order sum, - b_S) --st.async--> every CTA of the cluster
-//      y slice = M[slice] r --st.async--> every CTA of the cluster
-//    Every CTA then holds identical r and y, so the scalar window logic is replicated
-//    bit-for-bit and nobody broadcasts a decision.  No floating-point atomics anywhere.
-#include <cooperative_groups.h>
-
-#include <cmath>
+// iterate.cu -- host side of the persistent Phase-2 kernel (iterate_kernel.cuh): shared-memory
+// budget, choice of the compile-time instantiation, launch with thread-block clusters.
 #include <cstdint>
 
 #include "kpp_internal.h"
-#include "window.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace kpp {
 namespace {
-
 constexpr int T2 = 512;
 constexpr int NW2 = T2 / 32;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// ------------------------------------------------------------------ LL words
-// value v with tag g -> two words (g << 32 | lo32(v)), (g << 32 | hi32(v))
-__device__ __forceinline__ void ll_store_global(unsigned long long* dst, double v, unsigned tag) {
-  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
-  const unsigned long long t = (unsigned long long)tag << 32;
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(dst), "l"(t | (u & 0xffffffffull)),
-               "l"(t | (u >> 32))
-               : "memory");
-}
-__device__ __noinline__ void spin_fail(int* err) {
-  atomicExch(err, 1);
-  __trap();
-}
-__device__ __forceinline__ double ll_wait_global(const unsigned long long* src, unsigned tag, int* err) {
-  unsigned long long a, b;
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(src) : "memory");
-  if ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
-    const unsigned long long t0 = globaltimer();
-    unsigned n = 0;
-    while ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
-      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(src) : "memory");
-      if ((++n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) spin_fail(err);
-    }
-  }
-  return __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
-}
-
-// Sum of LL values at src[q * stride] for q = q0, q0 + dq, ... < nq (fixed order), with every
-// load of the thread in flight at once: one L2 round trip once the data is there.
-template <int KQ>
-__device__ __forceinline__ double ll_gather_sum(const unsigned long long* src, long long stride, int q0, int dq, int nq,
-                                                unsigned tag, int* err) {
-  unsigned long long a[KQ], b[KQ];
-  int cnt = 0;
-#pragma unroll
-  for (int i = 0; i < KQ; ++i) {
-    const int qq = q0 + i * dq;
-    if (qq < nq) {
-      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a[i]), "=l"(b[i]) : "l"(src + qq * stride) : "memory");
-      cnt = i + 1;
-    } else {
-      a[i] = b[i] = (unsigned long long)tag << 32;
-    }
-  }
-  const unsigned long long t0 = globaltimer();
-  unsigned n = 0;
-  for (;;) {
-    bool all = true;
-#pragma unroll
-    for (int i = 0; i < KQ; ++i) {
-      if ((unsigned)(a[i] >> 32) != tag || (unsigned)(b[i] >> 32) != tag) {
-        all = false;
-        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a[i]), "=l"(b[i]) : "l"(src + (q0 + i * dq) * stride) : "memory");
-      }
-    }
-    if (all) break;
-    if ((++n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) spin_fail(err);
-  }
-  double v = 0.0;
-#pragma unroll
-  for (int i = 0; i < KQ; ++i)
-    if (i < cnt) v += __longlong_as_double((long long)((a[i] & 0xffffffffull) | (b[i] << 32)));
-  return v;
-}
-
-// ------------------------------------------------------------------ TMA bulk copies + mbarriers
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// TMA gather4: 4 rows (r0..r3) x box columns starting at column c0 -> dst (dense rows)
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int c0, int r0, int r1, int r2, int r3,
-                                            unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
-      : "memory");
-}
-// DSMEM: remote shared::cluster address of a local shared variable in CTA `rank`
-__device__ __forceinline__ unsigned mapa_u32(unsigned la, int rank) {
-  unsigned ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(rank));
-  return ra;
-}
-// asynchronous remote store that completes `8` transaction bytes on the remote mbarrier
-__device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(raddr), "d"(v),
-               "r"(rbar)
-               : "memory");
-}
-// Wait for bytes delivered by peers' st.async.  CTA-scope acquire is enough: the data are in this
-// CTA's shared memory and complete_tx makes them visible with the phase; a cluster-scope acquire
-// would also invalidate L1 (CCTL.IVALL) on every wait.
-__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAITC_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-
-// cp.async fallback (rows that are not 16-byte aligned)
-__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-// Warp 0: load s row segments of the slab (and optionally `mcount` doubles of M rows).
-// bulk: TMA bulk copies completing on `bar` (lane 0 registers the byte count first);
-// otherwise 8-byte cp.async (waited with cp.async.wait_group by warp 0).
-__device__ __forceinline__ void issue_loads(bool bulk, const CUtensorMap* tm, const double* A, long long lda,
-                                            const int32_t* S, int s, long long c0, int w, double* adst, int sw,
-                                            bool slab, const double* msrc, int mcount, double* mdst,
-                                            unsigned long long* bar) {
-  const int lane = threadIdx.x & 31;
-  if (bulk) {
-    const int nops = (s + 3) >> 2;  // gather4 ops (TMA path)
-    unsigned bytes = 0;
-    if (slab && w > 0) bytes += tm ? (unsigned)nops * 4u * (unsigned)sw * 8u : (unsigned)s * (unsigned)w * 8u;
-    if (msrc && mcount > 0) bytes += (unsigned)mcount * 8u;
-    if (lane == 0) mbar_expect_tx(bar, bytes);
-    __syncwarp();
-    if (slab && w > 0) {
-      if (tm) {
-        for (int j = lane; j < nops; j += 32) {
-          const int k = 4 * j;
-          tma_gather4(adst + (long long)k * sw, tm, (int)c0, S[k], S[min(k + 1, s - 1)], S[min(k + 2, s - 1)],
-                      S[min(k + 3, s - 1)], bar);
-        }
-      } else {
-        for (int k = lane; k < s; k += 32)
-          bulk_g2s(adst + (long long)k * sw, A + (long long)S[k] * lda + c0, (unsigned)w * 8u, bar);
-      }
-    }
-    if (msrc && mcount > 0 && lane == 0) bulk_g2s(mdst, msrc, (unsigned)mcount * 8u, bar);
-  } else {
-    if (slab)
-      for (int k = 0; k < s; ++k) {
-        const double* src = A + (long long)S[k] * lda + c0;
-        double* d = adst + (long long)k * sw;
-        for (int j = lane; j < w; j += 32) cp_async8(d + j, src + j);
-      }
-    if (msrc)
-      for (int e = lane; e < mcount; e += 32) cp_async8(mdst + e, msrc + e);
-    cp_async_commit();
-  }
-}
-
-#define TRACE(e)                                                                              \
-  do {                                                                                        \
-    if (p.trace && tid == 0 && it >= 64 && it < 64 + 16)                                      \
-      p.trace[(((long long)(it - 64) * gridDim.x) + blockIdx.x) * 8 + (e)] = (long long)globaltimer(); \
-  } while (0)
-
-#define PHASE_MARK(i)                   \
-  do {                                  \
-    if (prof_on) {                      \
-      const long long now_ = clock64(); \
-      prof_acc[i] += now_ - prof_last;  \
-      prof_last = now_;                 \
-    }                                   \
-  } while (0)
-
-// Butterfly reduce-scatter of RPW per-lane values over the 32 lanes of a warp: afterwards
-// v[0] of lane l is the full warp sum of value index rs_row<RPW>(l) (fixed order: deterministic).
-template <int RPW>
-__device__ __forceinline__ void warp_reduce_scatter(double (&v)[RPW], int lane) {
-  int o = 16;
-#pragma unroll
-  for (int cnt = RPW; cnt > 1; cnt >>= 1, o >>= 1) {
-    const int half = cnt >> 1;
-    const bool upper = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const double send = upper ? v[i] : v[i + half];
-      const double keep = upper ? v[i + half] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-  for (; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
-}
-template <int RPW>
-__device__ __forceinline__ int rs_row(int lane) {
-  int r = 0, o = 16;
-#pragma unroll
-  for (int cnt = RPW; cnt > 1; cnt >>= 1, o >>= 1)
-    if (lane & o) r += cnt >> 1;
-  return r;
-}
-
-// Register tile of the resident A_S x / A_S^T y passes: warp wi holds rows wi + 16 i (i < RPW),
-// lane l holds columns l + 32 c (c < CPL).  RPW = 0: shared-memory path.
-template <int RPW, int CPL>
-__global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ IterParams p) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int s = p.s;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = (int)cluster.num_blocks();
-  const int c = (int)cluster.block_rank();
-  const int q = blockIdx.x / C;    // cluster index
-  const int NQ = gridDim.x / C;    // clusters
-  const int sl = (s + C - 1) / C;  // rank cc owns rows [cc*sl, min(s, cc*sl + sl))
-  const int r0 = min(s, c * sl), r1 = min(s, r0 + sl);
-  const int R = r1 - r0;
-
-  // ---- shared memory carve-up (must match iterate_smem_bytes) ----
-  const int sp = (s + 1) & ~1;
-  // mbarriers: [0],[1] slab buffers (TMA); [2] partials of my slice arrived; [3] r arrived;
-  // [4] y arrived (the DSMEM exchanges are st.async stores completing bytes on these)
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);
-  double* rp_sm = reinterpret_cast<double*>(bars + 8);  // [C][sl] partials of my slice, from each rank
-  double* x_sm = rp_sm + ((C * sl + 1) & ~1);
-  double* m_sm = x_sm + p.slab;
-  double* w_sm = m_sm + p.slab;
-  double* r_sm = w_sm + p.slab;
-  double* y_sm = r_sm + sp;
-  double* red_sm = y_sm + sp;                                   // [2*T2] reduction scratch
-  double* bS_sh = red_sm + 2 * T2;                              // [3][sp] b_S of blocks t, t+1, t+2
-  int32_t* S_sh = reinterpret_cast<int32_t*>(bS_sh + 3 * sp);   // [3][sp]
-  unsigned char* tail = reinterpret_cast<unsigned char*>(S_sh + 3 * sp);
-  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 127) & ~uintptr_t(127));
-  double* Abuf = reinterpret_cast<double*>(tail);               // [2][s4][sw] (128B aligned)
-  const long long absz = (long long)((s + 3) & ~3) * p.sw;
-  const long long mslz = ((long long)sl * s + 15) & ~15LL;
-  // a_single: the register tile holds the slab during the iteration, so one shared buffer suffices
-  // (block t+1 is gathered into it as soon as the tile of block t is in registers)
-  const bool a_single = p.a_single != 0;
-  double* Mbuf = Abuf + (p.resident ? (a_single ? 1 : 2) * absz : 0);  // [2][sl][s] staged rows of M
-  __shared__ DevState st;
-  __shared__ int stop_sh;
-  __shared__ long long tmod_sh;
-
-  const long long c0 = (long long)blockIdx.x * p.slab;
-  const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
-  const int w = (int)(c1 > c0 ? c1 - c0 : 0);
-  // TMA eligibility: 16-byte aligned row segments of a multiple of 16 bytes, aligned M slices
-  const bool bulkA = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((w & 1) == 0) && ((p.sw & 1) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
-  const bool bulkM = ((s & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.M_pool) & 15) == 0);
-  const bool bulk = (!p.resident || bulkA || p.tma) && (!p.m_in_smem || bulkM);
-  const CUtensorMap* tm = p.tma ? &p.tmA : nullptr;
-  const long long ss = (long long)s * s;
-  const bool stageM = p.m_in_smem && R > 0;
-  const bool m2 = p.m_in_smem == 2;  // single buffer: M rows of t+1 are loaded once y(t) is complete
-  const int nops = (s + 3) >> 2;
-  // bytes landing on bars[buf] per iteration: the slab (resident) + this rank's M rows (staged)
-  const unsigned slab_bytes = p.resident ? (tm ? (unsigned)nops * 4u * (unsigned)p.sw * 8u : (unsigned)s * (unsigned)w * 8u) : 0u;
-  const unsigned m_bytes = stageM ? (unsigned)(R * s) * 8u : 0u;
-  const unsigned m_bytes_slab = m2 ? 0u : m_bytes;  // part of the per-buffer barrier's byte count
-  // warps that issue the prefetch (the others do the slice-owner work in the same window)
-  const int own_warps = (R + 31) / 32;
-  const int pf_tid = tid - 32 * own_warps;
-  const int pf_n = T2 - 32 * own_warps;
-
-  if (tid == 0) {
-    st = *p.st;
-    stop_sh = 0;
-    tmod_sh = p.t0 % (2 * p.zeta);
-    for (int i = 0; i < 6; ++i) mbar_init(bars + i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  for (int j = tid; j < w; j += T2) {
-    x_sm[j] = p.x[c0 + j];
-    m_sm[j] = p.mom[c0 + j];
-  }
-  for (int i = tid; i < s; i += T2) {
-    const int32_t v = p.S_pool[(long long)p.bid[0] * s + i];
-    S_sh[i] = v;
-    bS_sh[i] = p.b[v];
-  }
-  if (p.t0 + 1 < p.t1)
-    for (int i = tid; i < s; i += T2) S_sh[sp + i] = p.S_pool[(long long)p.bid[1] * s + i];
-  // block ids of t+1 and t+2 in registers (each loaded an iteration before it is needed)
-  long long qb1 = (p.t0 + 1 < p.t1) ? p.bid[1] : 0;
-  long long qb2 = (p.t0 + 2 < p.t1) ? p.bid[2] : 0;
-  long long qb3 = 0;
-  __syncthreads();
-  if (warp == 0)  // block t0: slab + M rows on bars[0]
-    issue_loads(bulk, tm, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, p.resident,
-                stageM ? p.M_pool + (long long)p.bid[0] * ss + (long long)r0 * s : nullptr, R * s, Mbuf, bars + 0);
-  const bool ylocal = p.ygl == 2;  // every CTA computes y = M r from its own copy of M(t)
-  const unsigned mfull_bytes = (unsigned)ss * 8u;
-  if (ylocal && tid == 0) {
-    mbar_expect_tx(bars + 5, mfull_bytes);
-    bulk_g2s(Mbuf, p.M_pool + (long long)p.bid[0] * ss, mfull_bytes, bars + 5);
-  }
-  cluster.sync();  // every peer's LL buffers are zeroed before any DSMEM store
-  long long tmod = tmod_sh;
-
-  const unsigned la_rp = smem_u32(rp_sm), la_r = smem_u32(r_sm), la_y = smem_u32(y_sm);
-  const unsigned lb_rp = smem_u32(bars + 2), lb_r = smem_u32(bars + 3), lb_y = smem_u32(bars + 4);
-  const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-  long long prof_acc[16] = {};
-  long long prof_last = prof_on ? clock64() : 0;
-  long long t = p.t0;
-  unsigned it = 0;
-  unsigned phA0 = 0, phA1 = 0;  // mbarrier parities of bars[0], bars[1]
-  for (; t < p.t1; ++t, ++it) {
-    const int buf = it & 1;
-    const int par = it & 1;
-    const unsigned tag = it + 1;
-    const int32_t* Sc = S_sh + (it % 3) * sp;
-    const double* bSc = bS_sh + (it % 3) * sp;
-    const int sb = a_single ? 0 : buf;        // slab buffer / barrier of this iteration
-    const int nbf = a_single ? 0 : (buf ^ 1);  // ... of the prefetch of iteration t+1
-    const double* Ac = Abuf + sb * absz;
-    const double* Msl = Mbuf + (m2 ? 0 : buf * mslz);
-    const bool pf = t + 1 < p.t1;
-    // ---- top: this iteration's slab and M rows have landed; this thread's cp.async loads
-    //      (S, b_S) of the previous iteration have landed; arm the barrier of the next buffer
-    if (bulk) {
-      if (sb == 0) { mbar_wait(bars + 0, phA0); phA0 ^= 1u; }
-      else         { mbar_wait(bars + 1, phA1); phA1 ^= 1u; }
-    }
-    // register tile of the slab (rows wi + 16 i, columns lane + 32 c): loaded as soon as the slab
-    // has landed, before the barrier (it does not depend on x)
-    const bool regpath = RPW > 0 && p.resident && s <= 16 * RPW && w <= 32 * CPL && !p.dbg_skip;
-    double ar[RPW > 0 ? RPW : 1][CPL > 0 ? CPL : 1];
-    if (regpath) {
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const int k = warp + 16 * i;
-        const double* arow = Ac + (long long)k * p.sw;
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) ar[i][cc] = (k < s && lane + 32 * cc < w) ? arow[lane + 32 * cc] : 0.0;
-      }
-    }
-    cp_async_wait_all();
-    if (tid == 0) {
-      if (pf && bulk) mbar_expect_tx(bars + nbf, slab_bytes + m_bytes_slab);
-      // this iteration's DSMEM exchanges (phase `it` of bars[2..4])
-      if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
-      mbar_expect_tx(bars + 3, (unsigned)s * 8u);
-      if (!p.ygl) mbar_expect_tx(bars + 4, (unsigned)s * 8u);
-    }
-    __syncthreads();
-    PHASE_MARK(0);
-    TRACE(0);
-    const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
-
-    // ---- row 3: partial block residual over the slab; each value goes (LL) to its slice owner
-    if (p.resident) {
-      if (regpath) {
-        // register tile: rows wi + 16 i, columns lane + 32 c, kept until the A_S^T y pass
-        double xr[CPL > 0 ? CPL : 1];
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) xr[cc] = (lane + 32 * cc < w) ? x_sm[lane + 32 * cc] : 0.0;
-        double v[RPW > 0 ? RPW : 1];
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-          v[i] = 0.0;
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) v[i] = fma(ar[i][cc], xr[cc], v[i]);
-        }
-        if constexpr (RPW > 0) warp_reduce_scatter<RPW>(v, lane);
-        const int k = warp + 16 * rs_row<RPW>(lane);
-        if ((lane & (32 / (RPW > 0 ? RPW : 1) - 1)) == 0 && k < s) {
-          const int owner = k / sl;
-          st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), v[0], mapa_u32(lb_rp, owner));
-        }
-      } else {
-        const int tpr = p.tpr;
-        const int rows_per_pass = T2 / tpr;
-        const int sub = tid & (tpr - 1);
-        for (int kp = 0; kp < s; kp += rows_per_pass) {
-          const int k = kp + tid / tpr;
-          double acc = 0.0;
-          if (k < s && !p.dbg_skip) {
-            const double* arow = Ac + (long long)k * p.sw;
-            for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
-          }
-          for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-          if (k < s && sub == 0) {
-            const int owner = k / sl;
-            st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), acc, mapa_u32(lb_rp, owner));
-          }
-        }
-      }
-    } else {
-      // streaming: a warp takes 2 rows at a time; each lane keeps 4 x 2 sixteen-byte loads in
-      // flight (64 KB per SM) so HBM stays saturated
-      const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
-      constexpr int UR = 2, UQ = 4;
-      for (int kbase = warp * UR; kbase < s; kbase += NW2 * UR) {
-        double acc[UR] = {0.0, 0.0};
-        const double* rows[UR];
-#pragma unroll
-        for (int u = 0; u < UR; ++u) rows[u] = p.A + (long long)Sc[min(kbase + u, s - 1)] * p.lda + c0;
-        if (vec) {
-          const int w2 = w >> 1;
-          const double2* x2 = reinterpret_cast<const double2*>(x_sm);
-          for (int jb = lane; jb < w2; jb += 32 * UQ) {
-            double2 a[UR][UQ], xv[UQ];
-#pragma unroll
-            for (int q = 0; q < UQ; ++q) {
-              const int j2 = jb + 32 * q;
-              xv[q] = j2 < w2 ? x2[j2] : make_double2(0.0, 0.0);
-#pragma unroll
-              for (int u = 0; u < UR; ++u)
-                a[u][q] = j2 < w2 ? __ldcs(reinterpret_cast<const double2*>(rows[u]) + j2) : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int q = 0; q < UQ; ++q)
-#pragma unroll
-              for (int u = 0; u < UR; ++u) {
-                acc[u] = fma(a[u][q].x, xv[q].x, acc[u]);
-                acc[u] = fma(a[u][q].y, xv[q].y, acc[u]);
-              }
-          }
-          if ((w & 1) && lane == 0) {
-#pragma unroll
-            for (int u = 0; u < UR; ++u) acc[u] = fma(__ldcs(rows[u] + w - 1), x_sm[w - 1], acc[u]);
-          }
-        } else {
-          for (int j = lane; j < w; j += 32) {
-            const double xv = x_sm[j];
-#pragma unroll
-            for (int u = 0; u < UR; ++u) acc[u] = fma(__ldcs(rows[u] + j), xv, acc[u]);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < UR; ++u) {
-          const double v = warp_sum(acc[u]);
-          const int k = kbase + u;
-          if (lane == 0 && k < s) {
-            const int owner = k / sl;
-            st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), v, mapa_u32(lb_rp, owner));
-          }
-        }
-      }
-    }
-    PHASE_MARK(2);
-    TRACE(1);
-
-    unsigned long long* gll = p.ll + (long long)par * NQ * s * 2;
-    if (pf_tid < 0) {
-      // ---- slice owner warps: cluster partial of my slice -> L2 (LL) for every cluster's owner
-      if (R > 0) mbar_wait_cluster(bars + 2, it & 1u);
-      TRACE(2);
-      for (int row = tid; row < R; row += 32 * own_warps) {
-        double v = 0.0;
-        for (int cc = 0; cc < C; ++cc) v += rp_sm[cc * sl + row];
-        ll_store_global(gll + ((long long)q * s + r0 + row) * 2, v, tag);
-      }
-    } else {
-      // ---- the other warps: prefetch block t+1 (slab by TMA gather4, M rows by one bulk copy)
-      //      and b_S(t+1), S(t+2) by cp.async -- spread so no warp serialises many TMA issues
-      const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
-      if (pf) {
-        double* adst = Abuf + nbf * absz;
-        if (p.resident) {
-          if (bulk && tm) {
-            const int stride = pf_n / nops >= 1 ? pf_n / nops : 1;
-            if (pf_tid % stride == 0)
-              for (int j = pf_tid / stride; j < nops; j += pf_n / stride) {
-                const int k = 4 * j;
-                fence_proxy_async();
-                tma_gather4(adst + (long long)k * p.sw, tm, (int)c0, S1[k], S1[min(k + 1, s - 1)],
-                            S1[min(k + 2, s - 1)], S1[min(k + 3, s - 1)], bars + nbf);
-              }
-          } else if (bulk) {
-            for (int k = pf_tid; k < s; k += pf_n) {
-              fence_proxy_async();
-              bulk_g2s(adst + (long long)k * p.sw, p.A + (long long)S1[k] * p.lda + c0, (unsigned)w * 8u, bars + nbf);
-            }
-          } else {
-            for (long long e = pf_tid; e < (long long)s * w; e += pf_n) {
-              const int k = (int)(e / w), j = (int)(e - (long long)k * w);
-              cp_async8(adst + (long long)k * p.sw + j, p.A + (long long)S1[k] * p.lda + c0 + j);
-            }
-          }
-        }
-        if (stageM && !m2) {
-          const double* msrc = p.M_pool + qb1 * ss + (long long)r0 * s;
-          double* mdst = Mbuf + (buf ^ 1) * mslz;
-          if (bulk) {
-            if (pf_tid == pf_n - 1) {
-              fence_proxy_async();
-              bulk_g2s(mdst, msrc, m_bytes, bars + nbf);
-            }
-          } else {
-            for (int e = pf_tid; e < R * s; e += pf_n) cp_async8(mdst + e, msrc + e);
-          }
-        }
-        double* b1 = bS_sh + ((it + 1) % 3) * sp;
-        for (int i = pf_tid; i < s; i += pf_n) cp_async8(b1 + i, p.b + S1[i]);
-        if (p.ygl == 1 && pf_tid == 0) {
-          // rows [yg0, yg1) of M(t+1) into L2 ahead of the y pass of the next iteration
-          const int yg0 = (int)((long long)blockIdx.x * s / gridDim.x);
-          const int yg1 = (int)((long long)(blockIdx.x + 1) * s / gridDim.x);
-          const double* src = p.M_pool + qb1 * ss + (long long)yg0 * s;
-          const unsigned bytes = (unsigned)(yg1 - yg0) * (unsigned)s * 8u;
-          if (bytes > 0 && (s & 1) == 0 && (reinterpret_cast<uintptr_t>(p.M_pool) & 15) == 0)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-        }
-      }
-      if (t + 2 < p.t1) {
-        int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
-        const int32_t* src = p.S_pool + qb2 * s;
-        for (int i = pf_tid; i < s; i += pf_n) cp_async4(S2 + i, src + i);
-      }
-      cp_async_commit();
-    }
-    if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
-    PHASE_MARK(3);
-    TRACE(3);
-    // ---- r slice: every (row, cluster-group) polls at once; fixed-order combine over the groups
-    const int G2 = (R > 0 && R <= T2) ? min(16, T2 / R) : 1;
-    if (R > 0 && R <= T2) {
-      if (tid < R * G2) {
-        const int row = tid % R, grp = tid / R;
-        double v = 0.0;
-        if ((NQ - grp + G2 - 1) / G2 <= 4) {
-          v = ll_gather_sum<4>(gll + (long long)(r0 + row) * 2, (long long)s * 2, grp, G2, NQ, tag, p.err);
-        } else {
-          for (int qq = grp; qq < NQ; qq += G2) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
-        }
-        red_sm[grp * R + row] = v;
-      }
-      PHASE_MARK(14);  // this thread's polls done
-    } else if (R > T2) {
-      for (int row = tid; row < R; row += T2) {
-        double v = 0.0;
-        for (int qq = 0; qq < NQ; ++qq) v += ll_wait_global(gll + ((long long)qq * s + r0 + row) * 2, tag, p.err);
-        red_sm[row] = v;  // R <= 2 * T2
-      }
-    }
-    __syncthreads();
-    PHASE_MARK(4);
-    TRACE(4);
-    // ---- r = A_S x - b_S for my slice; all-gather to the cluster (LL over DSMEM)
-    for (int row = tid; row < R; row += T2) {
-      double v;
-      if (R <= T2) {
-        double g[16];  // G2 <= 16 partial sums: all loads at once, fixed pairwise tree
-#pragma unroll
-        for (int i = 0; i < 16; ++i) g[i] = (i < G2) ? red_sm[i * R + row] : 0.0;
-#pragma unroll
-        for (int h = 8; h >= 1; h >>= 1)
-#pragma unroll
-          for (int i = 0; i < h; ++i) g[i] += g[i + h];
-        v = g[0];
-      } else {
-        v = red_sm[row];
-      }
-      v -= bSc[r0 + row];
-      for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_r, cc));
-    }
-    PHASE_MARK(15);  // r slice combined and sent
-    mbar_wait_cluster(bars + 3, it & 1u);  // r complete (every rank's slice)
-    PHASE_MARK(5);
-    TRACE(5);
-    // ---- row 8 (off the critical path of the others): ||r||^2 in a fixed order (identical in
-    //      every CTA) and the replicated window logic; rho for t+1 is read after the next barrier
-    if (warp == NW2 - 1) {
-      double e = 0.0;
-      for (int i = lane; i < s; i += 32) e = fma(r_sm[i], r_sm[i], e);
-      e = warp_sum(e);
-      if (lane == 0) {
-        const int res = window_step_dev(st, tmod, e, p.zeta, p.tol2bb, p.bb, p.adaptive,
-                                        blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
-        if (res) {
-          st.stopped = res;
-          stop_sh = 1;
-        }
-      }
-    }
-    tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
-    if (m2 && stageM && it > 0) {  // M rows of block t, loaded after y(t-1) completed
-      if (bulk) mbar_wait(bars + 5, (it - 1) & 1u);
-      else if (warp == 0) cp_async_wait_all();
-      if (!bulk) __syncwarp();
-    }
-    if (ylocal) {
-      // ---- row 4: y = M r in this CTA from its staged copy of M(t) (no exchange of y)
-      mbar_wait(bars + 5, it & 1u);
-      for (int k = warp; k < s; k += NW2) {
-        const double* Mr = Mbuf + (long long)k * s;
-        double v = 0.0;
-#pragma unroll 4
-        for (int l = lane; l < s; l += 32) v = fma(Mr[l], r_sm[l], v);
-        v = warp_sum(v);
-        if (lane == 0) y_sm[k] = v;
-      }
-      __syncthreads();
-      if (pf && tid == 0) {  // every read of M(t) is done: bring in M(t+1)
-        fence_proxy_async();
-        mbar_expect_tx(bars + 5, mfull_bytes);
-        bulk_g2s(Mbuf, p.M_pool + qb1 * ss, mfull_bytes, bars + 5);
-      }
-    } else if (p.ygl) {
-      // ---- row 4, large blocks: y rows [yg0, yg1) of this CTA (every M element read once per
-      //      iteration on the whole GPU), published to L2 as LL words; all CTAs gather y below
-      const int yg0 = (int)((long long)blockIdx.x * s / gridDim.x);
-      const int yg1 = (int)((long long)(blockIdx.x + 1) * s / gridDim.x);
-      if (warp < NW2 - 1) {
-        const double* Mb = p.M_pool + (long long)p.bid[t - p.t0] * ss;
-        for (int k = yg0 + warp; k < yg1; k += NW2 - 1) {
-          double v = 0.0;
-          const double* Mrow = Mb + (long long)k * s;
-#pragma unroll 4
-          for (int l = lane; l < s; l += 32) v = fma(__ldg(Mrow + l), r_sm[l], v);
-          v = warp_sum(v);
-          if (lane == 0) ll_store_global(p.yll + ((long long)par * s + k) * 2, v, tag);
-        }
-      }
-    } else {
-    // ---- row 4: my slice of y = M r; warps 0..14 take groups of RY rows (lanes over columns,
-      //      conflict-free shared-memory reads, butterfly reduce-scatter); lanes of each group then
-      //      send the row to peer (lane & 7) by st.async.  The last warp runs the window logic.
-      if (R > 0 && warp < NW2 - 1) {
-        constexpr int RY = 4;
-        const int ngroups = (R + RY - 1) / RY;
-        const double* Mg = p.M_pool + (long long)p.bid[t - p.t0] * ss + (long long)r0 * s;
-        for (int gi = warp; gi < ngroups; gi += NW2 - 1) {
-          const int rb = gi * RY;
-          double v[RY] = {0.0, 0.0, 0.0, 0.0};
-          if (!p.dbg_skip) {
-            if (p.m_in_smem) {
-#pragma unroll 4
-              for (int l = lane; l < s; l += 32) {
-                const double rl = r_sm[l];
-#pragma unroll
-                for (int i = 0; i < RY; ++i)
-                  if (rb + i < R) v[i] = fma(Msl[(long long)(rb + i) * s + l], rl, v[i]);
-              }
-            } else {
-#pragma unroll 4
-              for (int l = lane; l < s; l += 32) {
-                const double rl = r_sm[l];
-#pragma unroll
-                for (int i = 0; i < RY; ++i)
-                  if (rb + i < R) v[i] = fma(__ldg(Mg + (long long)(rb + i) * s + l), rl, v[i]);
-              }
-            }
-          }
-          warp_reduce_scatter<RY>(v, lane);
-          const int row = rb + rs_row<RY>(lane);
-          const int cc = lane & 7;  // lanes of a row group share the value; lane & 7 picks the peer
-          if (row < R && cc < C) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v[0], mapa_u32(lb_y, cc));
-          if (row < R && C > 8)
-            for (int c2 = cc + 8; c2 < C; c2 += 8) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, c2), v[0], mapa_u32(lb_y, c2));
-        }
-      }
-    }
-    PHASE_MARK(13);  // y slice computed and sent
-    if (p.ygl == 1) {
-      for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_global(p.yll + ((long long)par * s + l) * 2, tag, p.err);
-      __syncthreads();
-    } else if (!p.ygl) {
-      mbar_wait_cluster(bars + 4, it & 1u);  // y complete
-    }
-    // single-buffered M rows: every reader of Msl in this CTA has sent its y rows (they all
-    // arrived), so the rows of block t+1 can be brought in now
-    if (m2 && stageM && pf && tid == 0) {
-      const double* msrc = p.M_pool + qb1 * ss + (long long)r0 * s;
-      fence_proxy_async();
-      if (bulk) {
-        mbar_expect_tx(bars + 5, m_bytes);
-        bulk_g2s(Mbuf, msrc, m_bytes, bars + 5);
-      }
-    }
-    if (m2 && stageM && pf && !bulk && warp == 0) {
-      const double* msrc = p.M_pool + qb1 * ss + (long long)r0 * s;
-      for (int e = lane; e < R * s; e += 32) cp_async8(Mbuf + e, msrc + e);
-      cp_async_commit();
-    }
-    PHASE_MARK(6);
-    TRACE(6);
-
-    // ---- rows 5-6: w on the slab, momentum, x (the next iteration's first barrier orders
-    //      these shared-memory updates before its A_S x pass)
-    const double cm = (1.0 - rho) / (1.0 + rho);
-    if (!p.cd && regpath) {
-      // w_j = sum_k A[k][j] y_k: the warp's rows from registers, then a fixed-order sum over warps
-#pragma unroll
-      for (int cc = 0; cc < CPL; ++cc) {
-        double a = 0.0;
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-          const int k = warp + 16 * i;
-          if (k < s) a = fma(ar[i][cc], y_sm[k], a);
-        }
-        if (lane + 32 * cc < w) red_sm[warp * p.slab + lane + 32 * cc] = a;
-      }
-      __syncthreads();
-      PHASE_MARK(11);
-      for (int jj = tid; jj < w; jj += T2) {
-        double wv = 0.0;
-        for (int ww = 0; ww < NW2; ++ww) wv += red_sm[ww * p.slab + jj];
-        const double mm = cm * (m_sm[jj] - wv);
-        m_sm[jj] = mm;
-        x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
-      }
-    } else {
-      if (!p.cd) {
-        if (p.resident) {
-          const int cw = p.cw, ng = T2 / cw, rg = (s + ng - 1) / ng;
-          const int g = tid / cw, j = tid - g * cw;
-          const int ka = min(s, g * rg), kz = min(s, ka + rg);
-          double a = 0.0;
-          if (j < w)
-            for (int k = ka; k < kz; ++k) a = fma(Ac[(long long)k * p.sw + j], y_sm[k], a);
-          red_sm[g * cw + j] = a;
-          __syncthreads();
-          for (int jj = tid; jj < w; jj += T2) {
-            double v = 0.0;
-            for (int gg = 0; gg < ng; ++gg) v += red_sm[gg * cw + jj];
-            w_sm[jj] = v;
-          }
-        } else {
-          const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
-          if (vec) {
-            // second pass: a thread owns a column pair, 8 sixteen-byte row loads in flight
-            for (int j2 = tid; 2 * j2 < w; j2 += T2) {
-              double ax = 0.0, ay = 0.0;
-              const double* col = p.A + c0 + 2 * j2;
-              const bool pair = 2 * j2 + 1 < w;
-#pragma unroll 8
-              for (int k = 0; k < s; ++k) {
-                const double yk = y_sm[k];
-                if (pair) {
-                  const double2 a = __ldcs(reinterpret_cast<const double2*>(col + (long long)Sc[k] * p.lda));
-                  ax = fma(a.x, yk, ax);
-                  ay = fma(a.y, yk, ay);
-                } else {
-                  ax = fma(__ldcs(col + (long long)Sc[k] * p.lda), yk, ax);
-                }
-              }
-              w_sm[2 * j2] = ax;
-              if (pair) w_sm[2 * j2 + 1] = ay;
-            }
-          } else {
-            for (int jj = tid; jj < w; jj += T2) {
-              double a = 0.0;
-              const double* col = p.A + c0 + jj;
-#pragma unroll 8
-              for (int k = 0; k < s; ++k) a = fma(__ldcs(col + (long long)Sc[k] * p.lda), y_sm[k], a);
-              w_sm[jj] = a;
-            }
-          }
-        }
-      } else {
-        for (int jj = tid; jj < w; jj += T2) w_sm[jj] = 0.0;
-        __syncthreads();
-        for (int k = tid; k < s; k += T2) {
-          const long long gj = (long long)Sc[k] - p.col_base;
-          if (gj >= c0 && gj < c1) w_sm[gj - c0] = y_sm[k];
-        }
-      }
-      __syncthreads();
-      for (int jj = tid; jj < w; jj += T2) {
-        const double wv = w_sm[jj];
-        const double mm = cm * (m_sm[jj] - wv);
-        m_sm[jj] = mm;
-        x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
-      }
-    }
-    PHASE_MARK(7);
-    TRACE(7);
-    qb1 = qb2;
-    qb2 = qb3;
-    if (stop_sh) {  // written before the y barrier of this iteration: every thread sees it
-      ++t;
-      break;
-    }
-  }
-  // drain copies still in flight after an early stop (their barriers must complete before exit)
-  if (bulk && t < p.t1) {
-    if (a_single || (it & 1)) mbar_wait(bars + 0, phA0); else mbar_wait(bars + 1, phA1);
-    if (m2 && stageM) mbar_wait(bars + 5, it & 1u);
-  }
-  if (ylocal && t < p.t1) mbar_wait(bars + 5, (it + 1) & 1u);  // M(t+1) copy in flight
-  cp_async_wait_all();
-  __syncthreads();
-  for (int j = tid; j < w; j += T2) {
-    p.x[c0 + j] = x_sm[j];
-    p.mom[c0 + j] = m_sm[j];
-  }
-  if (blockIdx.x == 0 && tid == 0) {
-    st.t_done = t;
-    *p.st = st;
-  }
-  if (prof_on)
-    for (int i = 0; i < 16; ++i) p.prof[i] += prof_acc[i];
-  cluster.sync();  // keep shared memory alive until every peer is done with DSMEM
-}
-
 }  // namespace
 
 int iterate_block_threads() { return T2; }
@@ -889,38 +26,47 @@ size_t iterate_smem_bytes(const IterParams& p, int C) {
   bytes = (bytes + 127) & ~127LL;
   if (p.resident) bytes += (p.a_single ? 1LL : 2LL) * ((s + 3) & ~3LL) * p.sw * 8;
   if (p.m_in_smem) bytes += (p.m_in_smem == 2 ? 1LL : 2LL) * ((sl * s + 15) & ~15LL) * 8;
-  if (p.ygl == 2) bytes += ((s * s + 15) & ~15LL) * 8;  // full copy of M(t)
+  if (p.ygl == 4) bytes += ((C * (s + 1) + 1) & ~1LL) * 8;      // partial y vectors
   return (size_t)bytes + 128;
 }
 
 using KernelFn = void (*)(const IterParams);
 
-// register tile for the resident passes: enough registers for w <= XR * tpr and s <= NP * (T2/tpr)
-bool iterate_register_tile(const IterParams& p);
-static KernelFn pick_kernel(const IterParams& p);
-bool iterate_register_tile(const IterParams& p) { return pick_kernel(p) != (KernelFn)iterate_kernel<0, 0>; }
+// instantiations (one translation unit per y placement, compiled in parallel)
+KernelFn iterate_pick_reg_y0(int rpw, int cpl);
+KernelFn iterate_pick_reg_y1(int rpw, int cpl);
+KernelFn iterate_pick_reg_y4(int rpw, int cpl);
+KernelFn iterate_pick_generic(int resident, int yg, int cd);
+
+static bool reg_shape(const IterParams& p, int* rpw_out, int* cpl_out) {
+  if (!p.resident || p.cd || NW2 * p.slab > 2 * T2) return false;
+  int rpw = 2;
+  while (16 * rpw < p.s) rpw *= 2;
+  const int cpl = (p.slab + 31) / 32;
+  if (rpw > 16 || cpl > 2) return false;
+  *rpw_out = rpw;
+  *cpl_out = cpl;
+  return true;
+}
 
 static KernelFn pick_kernel(const IterParams& p) {
-  if (p.resident && NW2 * p.slab <= 2 * T2) {
-    int rpw = 1;
-    while (16 * rpw < p.s) rpw *= 2;
-    const int cpl = (p.slab + 31) / 32;
-    if (cpl == 1) {
-      if (rpw <= 2) return iterate_kernel<2, 1>;
-      if (rpw == 4) return iterate_kernel<4, 1>;
-      if (rpw == 8) return iterate_kernel<8, 1>;
-      if (rpw == 16) return iterate_kernel<16, 1>;
-    } else if (cpl == 2) {
-      if (rpw <= 2) return iterate_kernel<2, 2>;
-      if (rpw == 4) return iterate_kernel<4, 2>;
-      if (rpw == 8) return iterate_kernel<8, 2>;
-      if (rpw == 16) return iterate_kernel<16, 2>;
-    }
+  int rpw = 0, cpl = 0;
+  if (reg_shape(p, &rpw, &cpl)) {
+    KernelFn f = p.ygl == 0 ? iterate_pick_reg_y0(rpw, cpl) : p.ygl == 1 ? iterate_pick_reg_y1(rpw, cpl)
+               : p.ygl == 4 ? iterate_pick_reg_y4(rpw, cpl) : nullptr;
+    if (f) return f;
   }
-  return iterate_kernel<0, 0>;
+  return iterate_pick_generic(p.resident, p.ygl, p.cd);
+}
+
+// the resident passes run from a register tile (one slab buffer suffices)
+bool iterate_register_tile(const IterParams& p) {
+  int rpw = 0, cpl = 0;
+  return reg_shape(p, &rpw, &cpl);
 }
 
 static void set_attrs(KernelFn fn, size_t smem, int C) {
+  if (!fn) return;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (C > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }

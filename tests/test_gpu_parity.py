@@ -300,3 +300,31 @@ def test_cdpp_identity_and_scalar(kpp, ora):
     ctx.set_option(kpp.OPT_ACCEL, 0)
     res = ctx.solve(torch.from_numpy(b).to(DEV), torch.from_numpy(x0).to(DEV), max_iters=30)
     assert rel(res.x.cpu().numpy(), ref.x) <= 1e-12
+
+
+PLAN_CASES = [(cfg, y, C) for cfg in (synth.twin("c2", 2048, 2048, 128, k=64), synth.twin("c3", 1000, 778, 50, k=8))
+              for y in (0, 1, 4) for C in (0, 2, 8)]
+
+
+@pytest.mark.parametrize("cfg,ygl,cluster", PLAN_CASES,
+                         ids=[f"{c.name}-ygl{y}-C{cc}" for c, y, cc in PLAN_CASES])
+def test_launch_plans_parity(kpp, ora, cfg, ygl, cluster):
+    """Every placement of y = M r (per cluster / once per GPU / per cluster from partial sums) and
+    several cluster sizes give the oracle's iterates."""
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+    try:
+        ctx.set_option(kpp.OPT_CLUSTER, cluster)
+        ctx.set_option(kpp.OPT_YGL, ygl)
+    except kpp.KppError:
+        pytest.skip("no feasible plan for this combination")
+    st = ctx.stats()
+    assert st["ygl"] == ygl
+    ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=300, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=300)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    # early stop inside a window (drains in-flight copies) and a second, warm solve
+    res2 = ctx.solve(b.to(DEV), max_iters=300, tol=0.5)
+    assert res2.iters < 300
+    res3 = ctx.solve(b.to(DEV), max_iters=300)
+    assert np.array_equal(res3.x.cpu().numpy(), res.x.cpu().numpy())

@@ -1,5 +1,3 @@
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c5.csv python tools/prof_iter.py --config c5 --iters 1024 --reps 1 > gpurun_out/ncu_launch5.log 2>&1
-KPP_PHASE_PROFILE=1 timeout 300 python tools/prof_iter.py --config c5 --iters 512 --reps 2 > gpurun_out/exp.log 2>&1
-KPP_DBG_SKIP=1 timeout 300 python tools/prof_iter.py --config c5 --iters 512 --reps 2 >> gpurun_out/exp.log 2>&1
-for C in 1 4 8; do timeout 300 python tools/prof_iter.py --config c5 --iters 512 --reps 1 --cluster $C >> gpurun_out/exp.log 2>&1; done
-KPP_PHASE_PROFILE=1 timeout 300 python tools/prof_iter.py --config c4 --iters 256 --reps 2 >> gpurun_out/exp.log 2>&1
+for y in 0 4; do timeout 120 python tools/prof_iter.py --config c3 --iters 4096 --reps 2 --ygl $y; echo "rc=$?"; done > gpurun_out/exp.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/exp.log; tail -3 gpurun_out/pytest_gpu.log >> gpurun_out/exp.log
+for c in c2 c3; do timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_$c.json 2>gpurun_out/bench_$c.err; done
