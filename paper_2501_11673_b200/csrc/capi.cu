@@ -256,12 +256,15 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   const size_t o_X2 = cqr2 ? carve((size_t)B * ss) : 0;
   const size_t o_X = cqr2 ? carve((size_t)B * ss) : 0;
   const size_t o_Q = cqr2 ? carve((size_t)B * s * n) : 0;
+  const size_t wsb = chol_inv_workspace(s);
+  const size_t o_W = wsb ? carve((size_t)B * wsb / sizeof(double)) : 0;
   CKS(ensure_buf(ctx, ctx->p1, off));
   CK(cudaMemsetAsync(ctx->d_info, 0, (size_t)B * sizeof(int), st));  // the factor kernel only records failures
   char* base = (char*)ctx->p1.p;
   double* part = (double*)(base + o_part);
   double* G = (double*)(base + o_G);
   double* X1 = (double*)(base + o_X1);
+  double* W = wsb ? (double*)(base + o_W) : nullptr;
 
   if (ctx->kind == KIND_CDPP) {
     // G = A_SS + lam I (Alg 3 l.8); multi-GPU: disjoint column supports summed exactly
@@ -271,9 +274,9 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
       CKS(allreduce(ctx, G, (size_t)B * ss));
       launch_add_diag(st, B, G, s, ctx->lam);
     }
-    launch_chol_trtri(st, B, G, X1, s, ctx->d_info);
+    launch_chol_trtri(st, B, G, X1, s, ctx->d_info, W);
     Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
-    launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0);  // M = X X^T
+    launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);  // M = X X^T (X upper)
   } else {
     // G1 = A_S A_S^T (+ lam I): NT GEMM with row gathers on both operands, split-K
     Operand a{ctx->A, ctx->lda, 0, S, s, 0}, b{ctx->A, ctx->lda, 0, S, s, 1};
@@ -284,10 +287,10 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
       CKS(allreduce(ctx, G, (size_t)B * ss));
       launch_add_diag(st, B, G, s, ctx->lam);
     }
-    launch_chol_trtri(st, B, G, X1, s, ctx->d_info);  // R1, X1 = R1^{-1}
+    launch_chol_trtri(st, B, G, X1, s, ctx->d_info, W);  // R1, X1 = R1^{-1}
     if (!cqr2) {
       Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
-      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0);
+      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);
     } else {
       // shifted CholeskyQR2 of A_aug = [A_S, sqrt(lam) I]:
       //   Q1 = R1^{-T} A_aug,  G2 = Q1 Q1^T = X1^T A_S A_S^T X1 + lam X1^T X1  (Q1 formed explicitly)
@@ -300,15 +303,15 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
       Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
       const int z2 = launch_dgemm(st, B, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
       Operand x1n{X1, s, ss, nullptr, 0, 0};
-      launch_dgemm(st, B, s, s, s, x1t, x1n, L, s, ss, 1, 0);  // X1^T X1
+      launch_dgemm(st, B, s, s, s, x1t, x1n, L, s, ss, 1, 0, 1);  // X1^T X1 (X1^T lower)
       const double lscale = (dist && ctx->rank != 0) ? 0.0 : ctx->lam;
       launch_splitk_reduce(st, B, s, s, z2, part, ss, 0.0, L, lscale, ss, G, ss, 1);
       if (dist) CKS(allreduce(ctx, G, (size_t)B * ss));
-      launch_chol_trtri(st, B, G, X2, s, ctx->d_info + 0);  // R2, X2 = R2^{-1}
+      launch_chol_trtri(st, B, G, X2, s, ctx->d_info + 0, W);  // R2, X2 = R2^{-1}
       Operand x1a{X1, s, ss, nullptr, 0, 0}, x2b{X2, s, ss, nullptr, 0, 0};
-      launch_dgemm(st, B, s, s, s, x1a, x2b, X, s, ss, 1, 0);  // X = R^{-1} = X1 X2
+      launch_dgemm(st, B, s, s, s, x1a, x2b, X, s, ss, 1, 0, 2);  // X = R^{-1} = X1 X2 (upper)
       Operand xa{X, s, ss, nullptr, 0, 0}, xb{X, s, ss, nullptr, 0, 1};
-      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0);  // M = X X^T
+      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);  // M = X X^T
     }
   }
   CK(cudaGetLastError());
@@ -327,7 +330,8 @@ kpp_status phase1(kpp_ctx* ctx, long long k0, long long k1) {
   const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor == 0;
   // workspace of phase1_batch per block: split-K partials (Z s^2), G, X1 (+ L, X2, X, Q1 for CholeskyQR2)
   const long long Z = ctx->kind == KIND_KPP ? std::min<long long>(64, std::max<long long>(1, (n + 511) / 512)) : 1;
-  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 3 : 0)) * s * s + (cqr2 ? s * n : 0)) + 1024;
+  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 3 : 0)) * s * s + (cqr2 ? s * n : 0)) +
+                              (long long)chol_inv_workspace((int)s) + 2048;
   long long Bmax = std::max<long long>(1, ctx->phase1_mb * (1LL << 20) / per_block);
   Bmax = std::min<long long>(Bmax, 4096);
   for (long long k = k0; k < k1; k += Bmax) {

@@ -30,19 +30,23 @@ struct CholSmem {
   }
 };
 
+// Views: matrix b is G = Gall + b*gstride with element (i,j) at G[i*ldg + j] (likewise X), so the
+// kernel also factors a diagonal tile of a larger matrix in place (blocked driver below).
 template <int NB>
-__global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, double* Xall, int s, int* info) {
+__global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, long long ldg, long long gstride,
+                                                                double* Xall, long long ldx, long long xstride,
+                                                                int s, int* info, int info_base) {
   extern __shared__ __align__(16) double csm[];
   double* D = csm;                      // [NB][NB+1] R_kk
   double* Di = D + NB * (NB + 1);       // [NB][NB+1] R_kk^{-1}
   double* P = Di + NB * (NB + 1);       // [NB][pld] panel rows
   const int pld = ((s + 3) & ~3) + 4;
-  double* G = Gall + (long long)blockIdx.x * s * s;
-  double* X = Xall + (long long)blockIdx.x * s * s;
+  double* G = Gall + (long long)blockIdx.x * gstride;
+  double* X = Xall + (long long)blockIdx.x * xstride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ int fail_sh;
   if (tid == 0) fail_sh = 0;
-  for (long long e = tid; e < (long long)s * s; e += CT) X[e] = 0.0;
+  for (long long e = tid; e < (long long)s * s; e += CT) X[(e / s) * ldx + e % s] = 0.0;
   __syncthreads();
 
   for (int k0 = 0; k0 < s; k0 += NB) {
@@ -53,7 +57,7 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
     if (warp == 0) {
       const int j = lane;
       for (int i = 0; i < kb; ++i)
-        if (j < kb && j >= i) D[i * (NB + 1) + j] = G[(long long)(k0 + i) * s + k0 + j];
+        if (j < kb && j >= i) D[i * (NB + 1) + j] = G[(long long)(k0 + i) * ldg + k0 + j];
       __syncwarp();
       for (int i = 0; i < kb; ++i) {
         const double v = D[i * (NB + 1) + i];
@@ -81,8 +85,8 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
           Di[i * (NB + 1) + j] = -a / D[i * (NB + 1) + i];
         }
         for (int i = 0; i < kb; ++i) {
-          G[(long long)(k0 + i) * s + k0 + j] = (j >= i) ? D[i * (NB + 1) + j] : 0.0;
-          X[(long long)(k0 + i) * s + k0 + j] = (j >= i) ? Di[i * (NB + 1) + j] : 0.0;
+          G[(long long)(k0 + i) * ldg + k0 + j] = (j >= i) ? D[i * (NB + 1) + j] : 0.0;
+          X[(long long)(k0 + i) * ldx + k0 + j] = (j >= i) ? Di[i * (NB + 1) + j] : 0.0;
         }
       }
     }
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
     for (int c = tid; c < ((rr + 3) & ~3); c += CT) {
       double g[NB];
 #pragma unroll
-      for (int l = 0; l < NB; ++l) g[l] = (l < kb && c < rr) ? G[(long long)(k0 + l) * s + c0 + c] : 0.0;
+      for (int l = 0; l < NB; ++l) g[l] = (l < kb && c < rr) ? G[(long long)(k0 + l) * ldg + c0 + c] : 0.0;
 #pragma unroll 1
       for (int i = 0; i < NB; ++i) {
         double a = 0.0;
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
           if (l <= i) a = fma(Di[l * (NB + 1) + i], g[l], a);
         if (i < kb) {
           P[i * pld + c] = a;
-          if (c < rr) G[(long long)(k0 + i) * s + c0 + c] = a;
+          if (c < rr) G[(long long)(k0 + i) * ldg + c0 + c] = a;
         }
       }
     }
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
       for (int u = 0; u < 4; ++u) {
         const int i = a0 + u;
         if (i >= rr) continue;
-        double* grow = G + (long long)(c0 + i) * s + c0;
+        double* grow = G + (long long)(c0 + i) * ldg + c0;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int j = b0 + v;
@@ -149,9 +153,9 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
   // zero the strictly lower part of R
   for (long long e = tid; e < (long long)s * s; e += CT) {
     const int i = (int)(e / s), j = (int)(e % s);
-    if (i > j) G[e] = 0.0;
+    if (i > j) G[(long long)i * ldg + j] = 0.0;
   }
-  if (tid == 0 && fail_sh) info[blockIdx.x] = fail_sh;
+  if (tid == 0 && fail_sh) info[blockIdx.x] = info_base + fail_sh;
   __syncthreads();
   if (fail_sh) return;
 
@@ -161,11 +165,11 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
     // stage R[0:j0, J] -> P[l][c] (row l, column c) and Di_J
     for (int e = tid; e < j0 * NB; e += CT) {
       const int l = e / NB, c = e - l * NB;
-      P[l * NB + c] = c < kb ? G[(long long)l * s + j0 + c] : 0.0;
+      P[l * NB + c] = c < kb ? G[(long long)l * ldg + j0 + c] : 0.0;
     }
     for (int e = tid; e < NB * NB; e += CT) {
       const int i = e / NB, c = e - i * NB;
-      Di[i * (NB + 1) + c] = (i < kb && c < kb) ? X[(long long)(j0 + i) * s + j0 + c] : 0.0;
+      Di[i * (NB + 1) + c] = (i < kb && c < kb) ? X[(long long)(j0 + i) * ldx + j0 + c] : 0.0;
     }
     __syncthreads();
     for (int i = tid; i < j0; i += CT) {
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
       double t[NB];
 #pragma unroll
       for (int c = 0; c < NB; ++c) t[c] = 0.0;
-      const double* xrow = X + (long long)i * s;
+      const double* xrow = X + (long long)i * ldx;
       for (int l = i; l < j0; ++l) {
         const double xv = xrow[l];
 #pragma unroll
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(CT) chol_trtri_blocked_kernel(double* Gall, do
 #pragma unroll
         for (int c2 = 0; c2 < NB; ++c2)
           if (c2 <= c) a = fma(t[c2], Di[c2 * (NB + 1) + c], a);
-        if (c < kb) X[(long long)i * s + j0 + c] = -a;
+        if (c < kb) X[(long long)i * ldx + j0 + c] = -a;
       }
     }
     __syncthreads();
@@ -226,18 +230,61 @@ __global__ void sumsq_kernel(const double* b, long long m, double* out) {
 
 }  // namespace
 
-void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info) {
-  if (batch <= 0) return;
+static void chol_tile(cudaStream_t st, int batch, double* G, long long ldg, long long gstride, double* X,
+                      long long ldx, long long xstride, int s, int* info, int info_base) {
   if (s <= 512) {
     const size_t sm = CholSmem<32>::bytes(s);
     cudaFuncSetAttribute(chol_trtri_blocked_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    chol_trtri_blocked_kernel<32><<<batch, CT, sm, st>>>(G, X, s, info);
+    chol_trtri_blocked_kernel<32><<<batch, CT, sm, st>>>(G, ldg, gstride, X, ldx, xstride, s, info, info_base);
   } else {
     const size_t sm = CholSmem<16>::bytes(s);
     cudaFuncSetAttribute(chol_trtri_blocked_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    chol_trtri_blocked_kernel<16><<<batch, CT, sm, st>>>(G, X, s, info);
+    chol_trtri_blocked_kernel<16><<<batch, CT, sm, st>>>(G, ldg, gstride, X, ldx, xstride, s, info, info_base);
   }
   count_launches(1);
+}
+
+size_t chol_inv_workspace(int s) {
+  // the batched (DMMA) route needs the off-diagonal blocks of R and one s x 64 panel per matrix
+  return (s >= 128 && (s & 1) == 0) ? ((size_t)s * s + (size_t)s * 64) * sizeof(double) : 0;
+}
+
+void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info, double* ws) {
+  if (batch <= 0) return;
+  const long long ss = (long long)s * s;
+  if (!ws || chol_inv_workspace(s) == 0) {
+    chol_tile(st, batch, G, s, ss, X, s, ss, s, info, 0);  // one CTA per matrix
+    return;
+  }
+  // Blocked, batched over all matrices: per 64-wide step k
+  //   diag:     R_kk, X_kk = R_kk^{-1}                    (chol_tile on the diagonal tile, in place)
+  //   panel:    R[k, k+1:] = X_kk^T G[k, k+1:]             (DMMA, X_kk^T lower triangular)
+  //   trailing: G[k+1:, k+1:] -= R[k, k+1:]^T R[k, k+1:]   (DMMA, upper triangle only)
+  // then X = R^{-1} by column blocks: X[0:j, J] = -(X[0:j, 0:j] R[0:j, J]) X_JJ.
+  constexpr int NB = 64;
+  double* R = ws;                  // [batch][s][s]: off-diagonal blocks of R
+  double* T = ws + (long long)batch * ss;  // [batch][s][64]
+  cudaMemsetAsync(X, 0, (size_t)batch * ss * sizeof(double), st);
+  for (int k0 = 0; k0 < s; k0 += NB) {
+    const int kb = s - k0 < NB ? s - k0 : NB;
+    const long long dk = (long long)k0 * (s + 1);
+    chol_tile(st, batch, G + dk, s, ss, X + dk, s, ss, kb, info, k0);
+    const int c0 = k0 + kb, tr = s - c0;
+    if (tr <= 0) break;
+    Operand xkk{X + dk, s, ss, nullptr, 0, 1};                        // logical (i,k) = X[k][i]
+    Operand gp{G + (long long)k0 * s + c0, s, ss, nullptr, 0, 0};
+    launch_dgemm(st, batch, kb, tr, kb, xkk, gp, R + (long long)k0 * s + c0, s, ss, 1, 0, 1);
+    Operand rpt{R + (long long)k0 * s + c0, s, ss, nullptr, 0, 1};    // logical (i,k) = R[k0+k][c0+i]
+    Operand rp{R + (long long)k0 * s + c0, s, ss, nullptr, 0, 0};
+    launch_dgemm(st, batch, tr, tr, kb, rpt, rp, G + (long long)c0 * (s + 1), s, ss, 1, 1, 0, -1.0, 1);
+  }
+  for (int j0 = NB; j0 < s; j0 += NB) {
+    const int kb = s - j0 < NB ? s - j0 : NB;
+    Operand xa{X, s, ss, nullptr, 0, 0}, rj{R + j0, s, ss, nullptr, 0, 0};
+    launch_dgemm(st, batch, j0, kb, j0, xa, rj, T, NB, (long long)s * NB, 1, 0, 2);      // T = X00 R0J
+    Operand ta{T, NB, (long long)s * NB, nullptr, 0, 0}, xjj{X + (long long)j0 * (s + 1), s, ss, nullptr, 0, 0};
+    launch_dgemm(st, batch, j0, kb, kb, ta, xjj, X + j0, s, ss, 1, 0, 0, -1.0, 0);       // X0J = -T XJJ
+  }
 }
 
 void launch_gather_principal(cudaStream_t st, int batch, const double* A, long long lda,

@@ -62,7 +62,7 @@ template <bool AT, bool BT>
 __global__ void __launch_bounds__(THREADS) dgemm_kernel(int M, int N, int K, int Z, int kchunk,
                                                         Operand a, Operand b, double* C,
                                                         long long ldc, long long c_bstride,
-                                                        int upper_only) {
+                                                        int upper_only, double alpha, int beta1) {
   const int tn = blockIdx.x, tm = blockIdx.y;
   if (upper_only && tm > tn) return;
   const int bz = blockIdx.z;
@@ -122,8 +122,9 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(int M, int N, int K, int
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int gj = tn * BN + wn * 16 + j * 8 + fc * 2;
-      if (gj < N) Cb[(long long)gi * ldc + gj] = acc[i][j][0];
-      if (gj + 1 < N) Cb[(long long)gi * ldc + gj + 1] = acc[i][j][1];
+      double* cp = Cb + (long long)gi * ldc + gj;
+      if (gj < N) cp[0] = beta1 ? cp[0] + alpha * acc[i][j][0] : alpha * acc[i][j][0];
+      if (gj + 1 < N) cp[1] = beta1 ? cp[1] + alpha * acc[i][j][1] : alpha * acc[i][j][1];
     }
   }
 }
@@ -172,18 +173,24 @@ __device__ __forceinline__ void stage_tile(double* sm, const double* base, long 
   }
 }
 
-template <bool AT, bool BT, bool ALOWER>
+// ATRI: 0 general A; 1 logical A lower triangular (A(i,k) = 0 for k > i); 2 upper (A(i,k) = 0 for
+// k < i) -- the K range of each row tile / warp is clipped (the stored zeros are skipped, not
+// assumed).  Epilogue: C = alpha * A B (+ C when beta1).
+template <bool AT, bool BT, int ATRI>
 __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int Z, int kchunk, Operand a,
                                                         Operand b, double* C, long long ldc, long long c_bstride,
-                                                        int upper_only) {
+                                                        int upper_only, double alpha, int beta1) {
+  constexpr bool ALOWER = ATRI == 1;
   extern __shared__ __align__(16) double g2sm[];
   const int tn = blockIdx.x, tm = blockIdx.y;
   if (upper_only && tm * B2M >= (tn + 1) * B2N) return;  // tile entirely below the diagonal
   const int bz = blockIdx.z;
   const int batch = bz / Z, z = bz % Z;
   const int kbeg = z * kchunk;
+  int kbeg_t = kbeg;
   int kend = min(K, kbeg + kchunk);
   if (ALOWER) kend = min(kend, (tm + 1) * B2M);  // A(i,k) = 0 for k > i
+  if (ATRI == 2) kbeg_t = max(kbeg, (tm * B2M) / B2K * B2K);  // A(i,k) = 0 for k < i
   double* As = g2sm;
   double* Bs = g2sm + B2S * A_STAGE;
   const double* abase = a.ptr + (long long)batch * a.bstride;
@@ -198,7 +205,7 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int nk = kend > kbeg ? (kend - kbeg + B2K - 1) / B2K : 0;
+  const int nk = kend > kbeg_t ? (kend - kbeg_t + B2K - 1) / B2K : 0;
   const int wrow0 = tm * B2M + wm * 32, wcol0 = tn * B2N + wn * 32;
   const bool wskip = upper_only && wrow0 >= wcol0 + 32;
   const int wrow_end = wrow0 + 32;
@@ -206,8 +213,8 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
 #pragma unroll
   for (int st = 0; st < B2S - 1; ++st) {
     if (st < nk) {
-      stage_tile<!AT, B2M, AM_LD>(As + st * A_STAGE, abase, a.ld, aidx, tm * B2M, M, kbeg + st * B2K, kend);
-      stage_tile<BT, B2N, BN_LD>(Bs + st * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, kbeg + st * B2K, kend);
+      stage_tile<!AT, B2M, AM_LD>(As + st * A_STAGE, abase, a.ld, aidx, tm * B2M, M, kbeg_t + st * B2K, kend);
+      stage_tile<BT, B2N, BN_LD>(Bs + st * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, kbeg_t + st * B2K, kend);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
@@ -218,8 +225,8 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
       const int ln = kt + B2S - 1;
       if (ln < nk) {
         const int sl = ln % B2S;
-        stage_tile<!AT, B2M, AM_LD>(As + sl * A_STAGE, abase, a.ld, aidx, tm * B2M, M, kbeg + ln * B2K, kend);
-        stage_tile<BT, B2N, BN_LD>(Bs + sl * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, kbeg + ln * B2K, kend);
+        stage_tile<!AT, B2M, AM_LD>(As + sl * A_STAGE, abase, a.ld, aidx, tm * B2M, M, kbeg_t + ln * B2K, kend);
+        stage_tile<BT, B2N, BN_LD>(Bs + sl * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, kbeg_t + ln * B2K, kend);
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
@@ -227,7 +234,8 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
     const double* Bst = Bs + (kt % B2S) * B_STAGE;
     if (wskip) continue;  // this warp's 32 x 32 tile lies below the diagonal (Gram, upper only)
     // logical A lower triangular: k-steps past this warp's last row contribute nothing
-    if (ALOWER && kbeg + kt * B2K >= wrow_end) continue;
+    if (ALOWER && kbeg_t + kt * B2K >= wrow_end) continue;
+    if (ATRI == 2 && kbeg_t + kt * B2K + B2K <= wrow0) continue;  // whole k-step left of this warp's rows
 #pragma unroll
     for (int kk = 0; kk < B2K; kk += 4) {
       double af[4], bf[4];
@@ -256,8 +264,9 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int gj = tn * B2N + wn * 32 + j * 8 + fc * 2;
-      if (gj < N) Cb[(long long)gi * ldc + gj] = acc[i][j][0];
-      if (gj + 1 < N) Cb[(long long)gi * ldc + gj + 1] = acc[i][j][1];
+      double* cp = Cb + (long long)gi * ldc + gj;
+      if (gj < N) cp[0] = beta1 ? cp[0] + alpha * acc[i][j][0] : alpha * acc[i][j][0];
+      if (gj + 1 < N) cp[1] = beta1 ? cp[1] + alpha * acc[i][j][1] : alpha * acc[i][j][1];
     }
   }
 }
@@ -288,19 +297,31 @@ static bool aligned16(const Operand& o) {
   return (reinterpret_cast<uintptr_t>(o.ptr) & 15) == 0 && (o.ld & 1) == 0 && (o.bstride & 1) == 0;
 }
 
-template <bool AT, bool BT, bool AL>
+template <bool AT, bool BT, int TRI>
 static void launch2(cudaStream_t st, dim3 grid, int M, int N, int K, int Z, int kchunk, const Operand& a,
-                    const Operand& b, double* C, long long ldc, long long c_bstride, int upper_only) {
+                    const Operand& b, double* C, long long ldc, long long c_bstride, int upper_only, double alpha,
+                    int beta1) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dgemm2_kernel<AT, BT, AL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)B2_SMEM);
+    cudaFuncSetAttribute(dgemm2_kernel<AT, BT, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)B2_SMEM);
     attr = true;
   }
-  dgemm2_kernel<AT, BT, AL><<<grid, B2T, B2_SMEM, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
+  dgemm2_kernel<AT, BT, TRI><<<grid, B2T, B2_SMEM, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only,
+                                                         alpha, beta1);
+}
+
+template <bool AT, bool BT>
+static void launch2t(int tri, cudaStream_t st, dim3 grid, int M, int N, int K, int Z, int kchunk, const Operand& a,
+                     const Operand& b, double* C, long long ldc, long long c_bstride, int upper_only, double alpha,
+                     int beta1) {
+  if (tri == 1) launch2<AT, BT, 1>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
+  else if (tri == 2) launch2<AT, BT, 2>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
+  else launch2<AT, BT, 0>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
 }
 
 int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand& a, const Operand& b,
-                 double* C, long long ldc, long long c_bstride, int Z, int upper_only, int a_lower) {
+                 double* C, long long ldc, long long c_bstride, int Z, int upper_only, int a_tri, double alpha,
+                 int beta1) {
   if (batch <= 0 || M <= 0 || N <= 0) return Z;
   if (Z < 1) Z = 1;
   int kchunk = (K + Z - 1) / Z;
@@ -310,22 +331,21 @@ int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand&
   count_launches(1);
   if (aligned16(a) && aligned16(b) && !getenv("KPP_GEMM_V1")) {
     dim3 grid((N + B2N - 1) / B2N, (M + B2M - 1) / B2M, batch * Z);
-    const bool al = a_lower != 0;
-    if (!a.trans && !b.trans) { if (al) launch2<false, false, true>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); else launch2<false, false, false>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); }
-    else if (!a.trans && b.trans) { if (al) launch2<false, true, true>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); else launch2<false, true, false>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); }
-    else if (a.trans && !b.trans) { if (al) launch2<true, false, true>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); else launch2<true, false, false>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); }
-    else { if (al) launch2<true, true, true>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); else launch2<true, true, false>(st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only); }
+    if (!a.trans && !b.trans) launch2t<false, false>(a_tri, st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
+    else if (!a.trans && b.trans) launch2t<false, true>(a_tri, st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
+    else if (a.trans && !b.trans) launch2t<true, false>(a_tri, st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
+    else launch2t<true, true>(a_tri, st, grid, M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
     return Z;
   }
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch * Z);
   if (!a.trans && !b.trans)
-    dgemm_kernel<false, false><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
+    dgemm_kernel<false, false><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
   else if (!a.trans && b.trans)
-    dgemm_kernel<false, true><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
+    dgemm_kernel<false, true><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
   else if (a.trans && !b.trans)
-    dgemm_kernel<true, false><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
+    dgemm_kernel<true, false><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
   else
-    dgemm_kernel<true, true><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only);
+    dgemm_kernel<true, true><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
   return Z;
 }
 

@@ -50,10 +50,11 @@ struct Operand {
   int trans;
 };
 // Returns the effective split count Z (K chunks are rounded to the K step).
-// a_lower: the logical A is lower triangular (A(i,k) = 0 for k > i): K is cut per row tile.
+// a_tri: 1 the logical A is lower triangular (A(i,k) = 0 for k > i), 2 upper (A(i,k) = 0 for
+// k < i): the K range is clipped per row tile.  C = alpha * A B (+ C when beta1; Z must be 1).
 int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand& a,
                  const Operand& b, double* C, long long ldc, long long c_bstride, int Z,
-                 int upper_only, int a_lower = 0);
+                 int upper_only, int a_tri = 0, double alpha = 1.0, int beta1 = 0);
 // out[b] = sum_z part[b*Z+z] (+ diag_add on the diagonal) (+ add_scale * add[b]);
 // with upper_only, element (i,j), i>j, is taken from (j,i).
 void launch_splitk_reduce(cudaStream_t st, int batch, int M, int N, int Z, const double* part,
@@ -71,7 +72,9 @@ void launch_gather_principal(cudaStream_t st, int batch, const double* A, long l
 void launch_add_diag(cudaStream_t st, int batch, double* G, int s, double lam);
 // In place: G[b] -> R[b] upper with R^T R = G (lower part zeroed); X[b] = R^{-1}.
 // info[b] = 0 on success, 1 + pivot index on a non-positive pivot.
-void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info);
+// ws: workspace of chol_inv_workspace(s) bytes per matrix (nullptr: one CTA per matrix).
+void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info, double* ws);
+size_t chol_inv_workspace(int s);
 
 // ------------------------------------------------------------------ iterate.cu
 struct alignas(64) IterParams {
