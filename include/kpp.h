@@ -77,11 +77,15 @@ typedef enum {
                              graph of step kernels (the multi-GPU engine, NCCL between steps) */
   KPP_OPT_CLUSTER = 10,   /* 0 (default): choose the thread-block cluster size automatically;
                              1, 2, 4, 8 or 16: force it (the grid shrinks to co-resident clusters) */
-  KPP_OPT_YGL = 11        /* where the persistent kernel computes y = M r: -1 (default) automatic;
+  KPP_OPT_YGL = 11,       /* where the persistent kernel computes y = M r: -1 (default) automatic;
                              0: once per thread-block cluster from the CTAs' staged rows of M
                                 (DSMEM all-gather of y);
                              1: once per GPU (rows of M spread over all CTAs), gathered through L2;
                              4: per cluster as the sum of the CTAs' partials M[slice,:]^T r_slice */
+  KPP_OPT_REASSOC = 12,   /* CD++ only.  1 (default): blocks that stream from HBM use the kernel that
+                             re-associates r_{t+1} = A_{S'} (x_t + eta c m_t) - (1 + eta c) A[S', S] y_t
+                             - b_{S'} (exact in real arithmetic, from Alg 3 l.11-13 P:756-759) so the
+                             dense pass of t+1 overlaps the exchange of t; 0: off; 2: always */
 } kpp_option;
 
 /* ---- setup ------------------------------------------------------------------ */
@@ -151,6 +155,7 @@ typedef struct {
   int32_t m_in_smem;     /* 1 if each CTA stages its rows of M in shared memory */
   int32_t tma;           /* 1 if resident slabs are gathered by TMA (tile::gather4) */
   int32_t ygl;           /* where y = M r is computed (KPP_OPT_YGL values 0, 1, 4) */
+  int32_t reassoc;       /* 1 if the CD++ re-associated streaming kernel runs (KPP_OPT_REASSOC) */
 } kpp_stats;
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */

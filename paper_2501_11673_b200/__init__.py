@@ -19,13 +19,14 @@ __all__ = [
     "KppError", "Ctx", "SolveResult", "kpp_setup", "cdpp_setup", "kpp_solve", "cdpp_solve",
     "kpp_destroy", "kpp_get_unique_id", "kpp_setup_dist", "cdpp_setup_dist", "load_library",
     "OPT_ACCEL", "OPT_MEMO", "OPT_ETA", "OPT_RHO_FIXED", "OPT_FACTOR", "OPT_WINDOW",
-    "OPT_PHASE1_MB", "OPT_RESIDENT", "OPT_ENGINE", "OPT_CLUSTER", "OPT_YGL",
+    "OPT_PHASE1_MB", "OPT_RESIDENT", "OPT_ENGINE", "OPT_CLUSTER", "OPT_YGL", "OPT_REASSOC",
 ]
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENOTPD, EDIVERGED, EMAXITER = range(8)
 OPT_ACCEL, OPT_MEMO, OPT_ETA, OPT_RHO_FIXED, OPT_FACTOR, OPT_WINDOW, OPT_PHASE1_MB, OPT_RESIDENT = range(1, 9)
 OPT_ENGINE = 9  # 0: persistent kernel (1 GPU default); 1: graph of step kernels (+NCCL)
 OPT_CLUSTER = 10  # 0: automatic; 1/2/4/8/16: forced thread-block cluster size
+OPT_REASSOC = 12  # CD++: 1 re-associated streaming kernel when blocks stream (default), 0 off, 2 always
 OPT_YGL = 11  # -1: automatic; 0: y = M r per cluster; 1: once per GPU (L2 gather); 4: per cluster from partials
 
 LIB_PATH = _build.LIB
@@ -44,7 +45,7 @@ class _Stats(ctypes.Structure):
                 ("n_fresh_last", ctypes.c_int64), ("iter_launches", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("grid_ctas", ctypes.c_int32),
                 ("resident", ctypes.c_int32), ("cluster", ctypes.c_int32), ("m_in_smem", ctypes.c_int32),
-                ("tma", ctypes.c_int32), ("ygl", ctypes.c_int32)]
+                ("tma", ctypes.c_int32), ("ygl", ctypes.c_int32), ("reassoc", ctypes.c_int32)]
 
 
 def load_library():

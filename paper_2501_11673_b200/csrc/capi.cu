@@ -58,7 +58,7 @@ struct kpp_ctx {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   // options
-  int accel = 1, memo = 1, factor = 0, resident_opt = 1, engine = 0, cluster_opt = 0, ygl_opt = -1;
+  int accel = 1, memo = 1, factor = 0, resident_opt = 1, engine = 0, cluster_opt = 0, ygl_opt = -1, reassoc = 1;
   double eta_opt = -1.0, rho_fixed = -1.0;
   long long window = 8192, phase1_mb = 4096;
   cudaStream_t stream = nullptr;
@@ -89,6 +89,10 @@ struct kpp_ctx {
   int pC = 1, pgrid = 0;                 // persistent kernel: cluster size, grid
   IterParams pplan{};
   size_t psmem = 0;
+  // CD++ streaming kernel with the re-associated residual
+  int cs_ok = 0, cs_C = 0, cs_grid = 0;
+  IterParams cs_plan{};
+  size_t cs_smem = 0;
   unsigned long long* d_ll = nullptr;
   size_t ll_bytes = 0;
   int* d_err = nullptr;
@@ -501,6 +505,48 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
   return KPP_OK;
 }
 
+// Launch plan of the CD++ re-associated streaming kernel (cdpp_stream.cu): clusters of 4 (then 2,
+// 8), as many co-resident clusters as fit.
+kpp_status plan_cdpp_stream(kpp_ctx* ctx) {
+  ctx->cs_ok = 0;
+  if (ctx->kind != KIND_CDPP) return KPP_OK;
+  int maxsm = 0;
+  CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  double best = -1.0;
+  const int sizes[] = {4, 2, 8};
+  for (int C : sizes) {
+    if (ctx->cluster_opt && C != ctx->cluster_opt) continue;
+    int g = ctx->num_sms / C * C;
+    for (int rep = 0; rep < 4 && g > 0; ++rep) {
+      IterParams p = plan_params(ctx, g, false, false);
+      p.ygl = 1;
+      const size_t smem = cdpp_stream_smem_bytes(p, C);
+      if ((long long)smem > maxsm) break;
+      const int nq = cdpp_stream_max_clusters(p, C, smem);
+      if (nq <= 0) break;
+      if (nq * C >= g) {
+        const double sc = g * (C == 4 ? 1.0 : C == 2 ? 0.9 : 0.85);
+        if (sc > best) {
+          best = sc;
+          ctx->cs_ok = 1;
+          ctx->cs_C = C;
+          ctx->cs_grid = g;
+          ctx->cs_plan = p;
+          ctx->cs_smem = smem;
+        }
+        break;
+      }
+      g = nq * C;
+    }
+  }
+  return KPP_OK;
+}
+
+bool use_cdpp_stream(const kpp_ctx* ctx) {
+  return ctx->kind == KIND_CDPP && ctx->cs_ok && ctx->engine == 0 && ctx->nranks == 1 &&
+         (ctx->reassoc == 2 || (ctx->reassoc == 1 && !ctx->pplan.resident));
+}
+
 kpp_status setup_common(kpp_ctx* ctx) {
   CK(cudaGetDevice(&ctx->device));
   CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -527,6 +573,7 @@ kpp_status setup_common(kpp_ctx* ctx) {
   slab = std::max<long long>(4, (slab + 3) / 4 * 4);
   ctx->slab = (int)slab;
   CKS(plan_persistent(ctx));
+  CKS(plan_cdpp_stream(ctx));
   const long long part_need = std::max<long long>((long long)ctx->grid * ctx->s, 2LL * ctx->num_sms * ctx->s);
   CKS(dalloc(ctx, &ctx->part, (size_t)part_need));
   ctx->ll_bytes = ((size_t)2 * ctx->num_sms * ctx->s * 2 + 4 * (size_t)ctx->s) * sizeof(unsigned long long);
@@ -674,7 +721,19 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
         }
         p.prof = ctx->d_prof;
       }
-      CK(launch_iterate(st, p, ctx->pgrid, ctx->pC, ctx->psmem));
+      if (use_cdpp_stream(ctx)) {
+        IterParams q = ctx->cs_plan;
+        q.A = p.A; q.lda = p.lda; q.m = p.m; q.n = p.n; q.s = p.s; q.cd = 1; q.col_base = p.col_base;
+        q.b = p.b; q.tol2bb = p.tol2bb; q.bb = p.bb; q.S_pool = p.S_pool; q.M_pool = p.M_pool; q.bid = p.bid;
+        q.t0 = p.t0; q.t1 = p.t1; q.x = p.x; q.mom = p.mom; q.eta = p.eta; q.zeta = p.zeta;
+        q.adaptive = p.adaptive; q.writer = p.writer; q.ll = p.ll; q.err = p.err; q.st = p.st;
+        q.hist_res = p.hist_res; q.hist_rho = p.hist_rho; q.hist_cap = p.hist_cap;
+        q.ygl = 1; q.yll = ctx->d_ll + ctx->ll_bytes / sizeof(unsigned long long) - 4LL * ctx->s;
+        q.prof = p.prof;
+        CK(launch_cdpp_stream(st, q, ctx->cs_grid, ctx->cs_C, ctx->cs_smem));
+      } else {
+        CK(launch_iterate(st, p, ctx->pgrid, ctx->pC, ctx->psmem));
+      }
       ctx->stats.iter_launches += 1;
     } else {
       StepParams sp{};
@@ -744,8 +803,11 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     long long pr[16];
     CK(cudaMemcpy(pr, ctx->d_prof, sizeof pr, cudaMemcpyDeviceToHost));
     CK(cudaMemset(ctx->d_prof, 0, sizeof pr));
-    const char* names[16] = {"top", "-", "P1", "clpart", "gather_sync", "r_wait", "y_wait", "P4b", "-", "-", "-",
-                             "P4a", "-", "y_comp", "gather_poll", "r_comb"};
+    const char* names_it[16] = {"top", "-", "P1", "clpart", "gather_sync", "r_wait", "y_wait", "P4b", "-", "-", "-",
+                                "P4a", "-", "y_comp", "gather_poll", "r_comb"};
+    const char* names_cs[16] = {"t0:A", "t0:stream", "-", "-", "-", "-", "t0:barrier", "-",
+                                "ch:A", "-", "ch:gather", "ch:r_wait", "ch:y_rows", "ch:y_gather", "ch:barrier", "-"};
+    const char* const* names = use_cdpp_stream(ctx) ? names_cs : names_it;
     fprintf(stderr, "[kpp phase cycles/iter, CTA 0]");
     for (int i = 0; i < 16; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
     fprintf(stderr, "\n");
@@ -920,7 +982,13 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
     case KPP_OPT_CLUSTER:
       if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8 && v != 16) return KPP_EINVAL;
       ctx->cluster_opt = (int)v;
+      CKS(plan_cdpp_stream(ctx));
       return plan_persistent(ctx);
+    case KPP_OPT_REASSOC:
+      if (v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;
+      ctx->reassoc = (int)v;
+      ctx->stats.reassoc = use_cdpp_stream(ctx) ? 1 : 0;
+      return KPP_OK;
     case KPP_OPT_YGL:
       if (v != -1.0 && v != 0.0 && v != 1.0 && v != 4.0) return KPP_EINVAL;
       ctx->ygl_opt = (int)v;
@@ -986,6 +1054,13 @@ kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out) {
   if (!ctx || !out) return KPP_EINVAL;
   *out = ctx->stats;
   out->n_blocks = ctx->nb_ready;
+  out->reassoc = use_cdpp_stream(ctx) ? 1 : 0;
+  if (out->reassoc) {
+    out->grid_ctas = ctx->cs_grid;
+    out->cluster = ctx->cs_C;
+    out->resident = 0;
+    out->ygl = 1;
+  }
   return KPP_OK;
 }
 

@@ -124,6 +124,12 @@ size_t iterate_smem_bytes(const IterParams& p, int C);
 int iterate_max_clusters(const IterParams& p, int C, size_t smem);  // co-resident clusters of size C
 bool iterate_register_tile(const IterParams& p);  // the resident passes run from a register tile
 
+// ------------------------------------------------------------------ cdpp_stream.cu
+// CD++ streaming kernel with the re-associated residual
+size_t cdpp_stream_smem_bytes(const IterParams& p, int C);
+cudaError_t launch_cdpp_stream(cudaStream_t st, const IterParams& p, int grid, int C, size_t smem);
+int cdpp_stream_max_clusters(const IterParams& p, int C, size_t smem);
+
 // ------------------------------------------------------------------ steps.cu (engine "graph")
 // Iteration cursor of the step kernels (device memory), so a captured graph is reusable.
 struct DevStep {

@@ -328,3 +328,37 @@ def test_launch_plans_parity(kpp, ora, cfg, ygl, cluster):
     assert res2.iters < 300
     res3 = ctx.solve(b.to(DEV), max_iters=300)
     assert np.array_equal(res3.x.cpu().numpy(), res.x.cpu().numpy())
+
+
+REASSOC_CASES = [synth.twin("c5", 2048, 2048, 512, k=100), synth.twin("c5", 1001, 1001, 77, k=16),
+                 synth.twin("c5", 4096, 4096, 256, k=50)]
+
+
+@pytest.mark.parametrize("cfg", REASSOC_CASES, ids=[c.name for c in REASSOC_CASES])
+@pytest.mark.parametrize("cluster", [0, 2, 8])
+def test_cdpp_reassociated_parity(kpp, ora, cfg, cluster):
+    """CD++ with the re-associated residual (the c5 streaming kernel), forced on
+    small systems: iterates within 1e-10 of the oracle, early stop, x0, warm second solve."""
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.cdpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+    ctx.set_option(kpp.OPT_CLUSTER, cluster)
+    ctx.set_option(kpp.OPT_REASSOC, 2)
+    assert ctx.stats()["reassoc"] == 1
+    ref = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=300, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=300)
+    assert res.iters == 300
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    # windows of 7 iterations: the pipeline restarts at every launch
+    ctx.set_option(kpp.OPT_WINDOW, 7)
+    res_w = ctx.solve(b.to(DEV), max_iters=300)
+    assert rel(res_w.x.cpu().numpy(), ref.x) <= 1e-10
+    # stop at the oracle's iteration
+    ref2 = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=3000, tol=0.05, threads=8)
+    res2 = ctx.solve(b.to(DEV), max_iters=3000, tol=0.05)
+    assert res2.iters == ref2.iters
+    assert rel(res2.x.cpu().numpy(), ref2.x) <= 1e-10
+    x0 = np.random.default_rng(1).standard_normal(A.shape[1])
+    ref3 = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=100, x0=x0, threads=8)
+    res3 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=100)
+    assert rel(res3.x.cpu().numpy(), ref3.x) <= 1e-10

@@ -16,6 +16,7 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--cluster", type=int, default=0)
 ap.add_argument("--ygl", type=int, default=-1)
+ap.add_argument("--reassoc", type=int, default=1)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 A, b, _ = synth.make_problem(cfg, device="cuda")
@@ -23,6 +24,8 @@ ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A, cfg.s, cfg.la
 ctx.set_option(kpp.OPT_ENGINE, a.engine)
 ctx.set_option(kpp.OPT_CLUSTER, a.cluster)
 ctx.set_option(kpp.OPT_YGL, a.ygl)
+if cfg.kind == 'cdpp':
+    ctx.set_option(kpp.OPT_REASSOC, a.reassoc)
 ctx.set_option(kpp.OPT_WINDOW, a.iters)
 ctx.prepare(a.iters)
 for _ in range(a.reps):
@@ -30,4 +33,4 @@ for _ in range(a.reps):
     r = ctx.solve(b, max_iters=a.iters)
     st = ctx.stats()
     print(f"{a.config}: {a.iters} iters phase2 {st['phase2_ms']:.3f} ms -> {st['phase2_ms'] * 1e3 / a.iters:.2f} us/iter; "
-          f"plan grid={st['grid_ctas']} C={st['cluster']} resident={st['resident']} msm={st['m_in_smem']} tma={st['tma']} ygl={st['ygl']}")
+          f"plan grid={st['grid_ctas']} C={st['cluster']} resident={st['resident']} msm={st['m_in_smem']} tma={st['tma']} ygl={st['ygl']} reassoc={st['reassoc']}")
