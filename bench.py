@@ -347,6 +347,7 @@ def main():
         "hbm_gbs_alg_warm": (bpi * iters / (warm["phase2_ms"] / 1e3) / 1e9) if warm["phase2_ms"] > 0 else None,
         "time_to_tol": ttt,
         "n_blocks_per_step": warm["n_blocks"],
+        "n_refined_per_step": st.get("n_refined", 0) // max(1, args.steps),
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -67,8 +67,10 @@ typedef enum {
   KPP_OPT_MEMO = 2,       /* 1 (default): online memoization; 0: a fresh block every iteration */
   KPP_OPT_ETA = 3,        /* < 0 (default): s/(2n); otherwise the momentum step eta */
   KPP_OPT_RHO_FIXED = 4,  /* < 0 (default): adaptive rho; >= 0: fixed rho, never updated */
-  KPP_OPT_FACTOR = 5,     /* K++ factor route: 0 (default) shifted CholeskyQR2 of [A_S, sqrt(lam) I];
-                             1 literal Gram + Cholesky -- same R in exact arithmetic */
+  KPP_OPT_FACTOR = 5,     /* K++ factor route (same R in exact arithmetic): 2 (default) Gram + Cholesky,
+                             then a second (shifted CholeskyQR2) pass only for blocks whose power-
+                             iteration estimate of u*kappa(A_S)^2 exceeds 1e-11; 0 shifted CholeskyQR2
+                             of [A_S, sqrt(lam) I] for every block; 1 literal Gram + Cholesky */
   KPP_OPT_WINDOW = 6,     /* iterations per device window (default 8192; rounded to >= 1) */
   KPP_OPT_PHASE1_MB = 7,  /* device workspace budget for a Phase-1 batch, MiB (default 4096) */
   KPP_OPT_RESIDENT = 8,   /* 1 (default): keep the block slab on chip across both passes when it
@@ -156,6 +158,7 @@ typedef struct {
   int32_t tma;           /* 1 if resident slabs are gathered by TMA (tile::gather4) */
   int32_t ygl;           /* where y = M r is computed (KPP_OPT_YGL values 0, 1, 4) */
   int32_t reassoc;       /* 1 if the CD++ re-associated streaming kernel runs (KPP_OPT_REASSOC) */
+  int64_t n_refined;     /* blocks that received the second CholeskyQR pass (since reset) */
 } kpp_stats;
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */

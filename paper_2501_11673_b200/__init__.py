@@ -45,7 +45,8 @@ class _Stats(ctypes.Structure):
                 ("n_fresh_last", ctypes.c_int64), ("iter_launches", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("grid_ctas", ctypes.c_int32),
                 ("resident", ctypes.c_int32), ("cluster", ctypes.c_int32), ("m_in_smem", ctypes.c_int32),
-                ("tma", ctypes.c_int32), ("ygl", ctypes.c_int32), ("reassoc", ctypes.c_int32)]
+                ("tma", ctypes.c_int32), ("ygl", ctypes.c_int32), ("reassoc", ctypes.c_int32),
+                ("n_refined", ctypes.c_int64)]
 
 
 def load_library():

@@ -58,7 +58,7 @@ struct kpp_ctx {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   // options
-  int accel = 1, memo = 1, factor = 0, resident_opt = 1, engine = 0, cluster_opt = 0, ygl_opt = -1, reassoc = 1;
+  int accel = 1, memo = 1, factor = 2, resident_opt = 1, engine = 0, cluster_opt = 0, ygl_opt = -1, reassoc = 1;
   double eta_opt = -1.0, rho_fixed = -1.0;
   long long window = 8192, phase1_mb = 4096;
   cudaStream_t stream = nullptr;
@@ -227,7 +227,44 @@ kpp_status allreduce(kpp_ctx* ctx, double* buf, size_t count) {
 
 // ------------------------------------------------------------------ Phase 1
 // Factor blocks [k0, k1) (their index sets are in S_pool) into M_pool.
+// optional per-step timing of Phase 1 (KPP_P1_PROFILE=1): CUDA events between the steps
+struct P1Prof {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> name;
+  void mark(const char* n) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    name.push_back(n);
+  }
+  void report() {
+    if (!on || ev.size() < 2) return;
+    cudaEventSynchronize(ev.back());
+    static std::vector<std::pair<std::string, double>> acc;
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      bool found = false;
+      for (auto& a : acc)
+        if (a.first == name[i]) { a.second += ms; found = true; }
+      if (!found) acc.push_back({name[i], ms});
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    fprintf(stderr, "[kpp phase1 ms, cumulative]");
+    for (auto& a : acc) fprintf(stderr, " %s=%.2f", a.first.c_str(), a.second);
+    fprintf(stderr, "\n");
+  }
+};
+
 kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
+  P1Prof pp;
+  pp.on = getenv("KPP_P1_PROFILE") != nullptr;
+  pp.st = ctx->stream;
+  pp.mark("start");
   const int s = ctx->s;
   const long long ss = (long long)s * s;
   const long long n = ctx->n;
@@ -246,7 +283,11 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   (void)tiles_up;
   int Z = 1;
   if (ctx->kind == KIND_KPP) Z = (int)std::min<long long>(64, std::max<long long>(1, (n + 511) / 512));
-  const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor == 0;
+  // factor 0: shifted CholeskyQR2 for every block; 2 (default): the second CholeskyQR pass only for
+  // blocks whose estimated u * kappa(A_S)^2 exceeds 1e-11;
+  // 1: the literal Gram + Cholesky for every block
+  const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor != 1;
+  const bool adaptive = ctx->kind == KIND_KPP && ctx->factor == 2;
   size_t off = 0;
   auto carve = [&](size_t count) {
     size_t o = off;
@@ -262,6 +303,10 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   const size_t o_Q = cqr2 ? carve((size_t)B * s * n) : 0;
   const size_t wsb = chol_inv_workspace(s);
   const size_t o_W = wsb ? carve((size_t)B * wsb / sizeof(double)) : 0;
+  const size_t o_X1c = adaptive ? carve((size_t)B * ss) : 0;         // refined sub-batch: X1, S, M
+  const size_t o_Mc = adaptive ? carve((size_t)B * ss) : 0;
+  const size_t o_Sc = adaptive ? carve(((size_t)B * s + 1) / 2) : 0;
+  const size_t o_lam = adaptive ? carve(3 * (size_t)B + 4) : 0;      // lamG, lamM, list, count
   CKS(ensure_buf(ctx, ctx->p1, off));
   CK(cudaMemsetAsync(ctx->d_info, 0, (size_t)B * sizeof(int), st));  // the factor kernel only records failures
   char* base = (char*)ctx->p1.p;
@@ -285,39 +330,80 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
     // G1 = A_S A_S^T (+ lam I): NT GEMM with row gathers on both operands, split-K
     Operand a{ctx->A, ctx->lda, 0, S, s, 0}, b{ctx->A, ctx->lda, 0, S, s, 1};
     const int z1 = launch_dgemm(st, B, s, s, (int)n, a, b, part, s, ss, Z, 1);
+    pp.mark("gram1");
     const bool dist = ctx->nranks > 1;
     launch_splitk_reduce(st, B, s, s, z1, part, ss, dist ? 0.0 : ctx->lam, nullptr, 0.0, 0, G, ss, 1);
+    pp.mark("reduce");
     if (dist) {
       CKS(allreduce(ctx, G, (size_t)B * ss));
       launch_add_diag(st, B, G, s, ctx->lam);
     }
+    double* lamG = adaptive ? (double*)(base + o_lam) : nullptr;
+    double* lamM = adaptive ? lamG + B : nullptr;
+    int* list = adaptive ? (int*)(lamM + B) : nullptr;
+    int* d_cnt = adaptive ? list + B : nullptr;
+    if (adaptive) launch_lmax(st, B, G, s, 0, 12, lamG);  // lambda_max(A_S A_S^T + lam I)
     launch_chol_trtri(st, B, G, X1, s, ctx->d_info, W);  // R1, X1 = R1^{-1}
-    if (!cqr2) {
+    pp.mark("chol");
+    if (!cqr2 || adaptive) {
       Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
-      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);
-    } else {
+      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);  // M = X1 X1^T
+    }
+    int nref = cqr2 ? B : 0;
+    const int32_t* Sr = S;
+    double* X1r = X1;
+    double* Mr = Mout;
+    if (adaptive) {
+      // kappa(A_aug)^2 = lambda_max(G) * lambda_max(G^{-1}) ~ lamG * lamM (power iteration = lower
+      // bounds; x4 safety): refine when u * 4 * lamG * lamM > 1e-11
+      const double thresh = 1e-11 / (4.0 * 0x1p-53);
+      launch_lmax(st, B, X1, s, 1, 12, lamM, lamG, thresh);
+      launch_refine_select(st, B, lamG, lamM, thresh, list, d_cnt);
+      CK(cudaMemcpyAsync(&nref, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      pp.mark("estimate");
+      ctx->stats.n_refined += nref;
+      if (nref > 0 && nref < B) {  // gather the blocks to refine into a contiguous sub-batch
+        int32_t* Sc = (int32_t*)(base + o_Sc);
+        double* X1c = (double*)(base + o_X1c);
+        launch_batch_move(st, nref, S, Sc, list, (long long)s * sizeof(int32_t), 0);
+        launch_batch_move(st, nref, X1, X1c, list, ss * (long long)sizeof(double), 0);
+        Sr = Sc;
+        X1r = X1c;
+        Mr = (double*)(base + o_Mc);
+      }
+    }
+    if (nref > 0) {
       // shifted CholeskyQR2 of A_aug = [A_S, sqrt(lam) I]:
       //   Q1 = R1^{-T} A_aug,  G2 = Q1 Q1^T = X1^T A_S A_S^T X1 + lam X1^T X1  (Q1 formed explicitly)
+      const int Bn = nref;
       double* L = (double*)(base + o_L);
       double* X2 = (double*)(base + o_X2);
       double* X = (double*)(base + o_X);
       double* Q = (double*)(base + o_Q);
-      Operand x1t{X1, s, ss, nullptr, 0, 1}, as{ctx->A, ctx->lda, 0, S, s, 0};
-      launch_dgemm(st, B, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);  // Q1 = X1^T A_S (X1^T lower)
+      Operand x1t{X1r, s, ss, nullptr, 0, 1}, as{ctx->A, ctx->lda, 0, Sr, s, 0};
+      launch_dgemm(st, Bn, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);  // Q1 = X1^T A_S (X1^T lower)
+      pp.mark("Q1");
       Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
-      const int z2 = launch_dgemm(st, B, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
-      Operand x1n{X1, s, ss, nullptr, 0, 0};
-      launch_dgemm(st, B, s, s, s, x1t, x1n, L, s, ss, 1, 0, 1);  // X1^T X1 (X1^T lower)
+      const int z2 = launch_dgemm(st, Bn, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
+      pp.mark("gram2");
+      Operand x1n{X1r, s, ss, nullptr, 0, 0};
+      launch_dgemm(st, Bn, s, s, s, x1t, x1n, L, s, ss, 1, 0, 1);  // X1^T X1 (X1^T lower)
       const double lscale = (dist && ctx->rank != 0) ? 0.0 : ctx->lam;
-      launch_splitk_reduce(st, B, s, s, z2, part, ss, 0.0, L, lscale, ss, G, ss, 1);
-      if (dist) CKS(allreduce(ctx, G, (size_t)B * ss));
-      launch_chol_trtri(st, B, G, X2, s, ctx->d_info + 0, W);  // R2, X2 = R2^{-1}
-      Operand x1a{X1, s, ss, nullptr, 0, 0}, x2b{X2, s, ss, nullptr, 0, 0};
-      launch_dgemm(st, B, s, s, s, x1a, x2b, X, s, ss, 1, 0, 2);  // X = R^{-1} = X1 X2 (upper)
+      launch_splitk_reduce(st, Bn, s, s, z2, part, ss, 0.0, L, lscale, ss, G, ss, 1);
+      pp.mark("reduce");
+      if (dist) CKS(allreduce(ctx, G, (size_t)Bn * ss));
+      launch_chol_trtri(st, Bn, G, X2, s, ctx->d_info + 0, W);  // R2, X2 = R2^{-1}
+      pp.mark("chol");
+      Operand x1a{X1r, s, ss, nullptr, 0, 0}, x2b{X2, s, ss, nullptr, 0, 0};
+      launch_dgemm(st, Bn, s, s, s, x1a, x2b, X, s, ss, 1, 0, 2);  // X = R^{-1} = X1 X2 (upper)
       Operand xa{X, s, ss, nullptr, 0, 0}, xb{X, s, ss, nullptr, 0, 1};
-      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);  // M = X X^T
+      launch_dgemm(st, Bn, s, s, s, xa, xb, Mr, s, ss, 1, 0, 2);  // M = X X^T
+      if (Mr != Mout) launch_batch_move(st, Bn, Mr, Mout, list, ss * (long long)sizeof(double), 1);
+      pp.mark("small");
     }
   }
+  pp.report();
   CK(cudaGetLastError());
   std::vector<int> info((size_t)B);
   CK(cudaMemcpyAsync(info.data(), ctx->d_info, (size_t)B * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -334,7 +420,7 @@ kpp_status phase1(kpp_ctx* ctx, long long k0, long long k1) {
   const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor == 0;
   // workspace of phase1_batch per block: split-K partials (Z s^2), G, X1 (+ L, X2, X, Q1 for CholeskyQR2)
   const long long Z = ctx->kind == KIND_KPP ? std::min<long long>(64, std::max<long long>(1, (n + 511) / 512)) : 1;
-  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 3 : 0)) * s * s + (cqr2 ? s * n : 0)) +
+  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 5 : 0)) * s * s + (cqr2 ? s * n + s : 0)) +
                               (long long)chol_inv_workspace((int)s) + 2048;
   long long Bmax = std::max<long long>(1, ctx->phase1_mb * (1LL << 20) / per_block);
   Bmax = std::min<long long>(Bmax, 4096);
@@ -964,7 +1050,7 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
       ctx->rho_fixed = v;
       break;
     case KPP_OPT_FACTOR:
-      if (v != 0.0 && v != 1.0) return KPP_EINVAL;
+      if (v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;
       if ((int)v != ctx->factor) ctx->nb_ready = 0;  // recompute factors
       ctx->factor = (int)v;
       break;
@@ -1067,6 +1153,7 @@ kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out) {
 kpp_status kpp_reset_stats(kpp_ctx* ctx) {
   if (!ctx) return KPP_EINVAL;
   ctx->stats.phase1_ms = ctx->stats.phase2_ms = ctx->stats.iter_kernel_ms = 0.0;
+  ctx->stats.n_refined = 0;
   return KPP_OK;
 }
 

@@ -14,6 +14,12 @@ namespace {
 
 constexpr int CT = 256;
 
+__device__ __forceinline__ double warp_sum_f(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // ------------------------------------------------------------------ blocked Cholesky + R^{-1}
 // One CTA per s x s matrix, NB-wide block steps (right-looking, upper: G = R^T R):
 //   1. diagonal tile: unblocked Cholesky by one warp (lane = column) and its inverse Di
@@ -228,6 +234,99 @@ __global__ void sumsq_kernel(const double* b, long long m, double* out) {
   if (threadIdx.x == 0) *out = sh[0];
 }
 
+// ------------------------------------------------------------------ adaptive CholeskyQR2
+// lam_out[b] ~ lambda_max of (mode 0) the symmetric G[b] or (mode 1) X[b] X[b]^T with X upper:
+// power iteration from the all-ones vector (deterministic), `iters` steps; ||A v|| with ||v|| = 1
+// is a lower bound of lambda_max.
+// (early exit: once lam > stop[b] / other[b] the refinement decision is already made; the power
+// estimate of a PSD operator never decreases)
+template <int MODE>
+__global__ void __launch_bounds__(256) lmax_kernel(const double* Aall, int s, int iters, double* lam_out,
+                                                   const double* other, double stop) {
+  extern __shared__ double lsm[];
+  double* v = lsm;
+  double* u = lsm + s;
+  double* wv = lsm + 2 * s;
+  __shared__ double nrm_sh;
+  const double* A = Aall + (long long)blockIdx.x * s * s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < s; i += 256) v[i] = 1.0 / sqrt((double)s);
+  __syncthreads();
+  double lam = 0.0;
+  for (int itn = 0; itn < iters; ++itn) {
+    const double* src = v;
+    if (MODE == 1) {
+      for (int j = tid; j < s; j += 256) {  // u = X^T v (X upper: rows i <= j)
+        double a = 0.0;
+        for (int i = 0; i <= j; ++i) a = fma(A[(long long)i * s + j], v[i], a);
+        u[j] = a;
+      }
+      __syncthreads();
+      src = u;
+    }
+    for (int i = warp; i < s; i += 8) {  // w = A src (MODE 0) or X u (MODE 1, columns j >= i)
+      double a = 0.0;
+      for (int j = (MODE == 1 ? i : 0) + lane; j < s; j += 32) a = fma(A[(long long)i * s + j], src[j], a);
+      a = warp_sum_f(a);
+      if (lane == 0) wv[i] = a;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double q = 0.0;
+      for (int i = lane; i < s; i += 32) q = fma(wv[i], wv[i], q);
+      q = warp_sum_f(q);
+      if (lane == 0) nrm_sh = sqrt(q);
+    }
+    __syncthreads();
+    lam = nrm_sh;
+    if (other && lam * other[blockIdx.x] > stop) break;  // uniform across the CTA
+    const double inv = lam > 0.0 ? 1.0 / lam : 0.0;
+    for (int i = tid; i < s; i += 256) v[i] = wv[i] * inv;
+    __syncthreads();
+  }
+  if (tid == 0) lam_out[blockIdx.x] = lam;
+}
+
+// list[0..cnt) = blocks whose estimated u * kappa(A_S)^2 = u * lamG * lamM (x safety) exceeds tau
+__global__ void __launch_bounds__(1024) refine_select_kernel(int B, const double* lamG, const double* lamM,
+                                                             double thresh, int* list, int* cnt) {
+  __shared__ int base_sh;
+  if (threadIdx.x == 0) base_sh = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < B; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    const bool need = b < B && !(lamG[b] * lamM[b] <= thresh);  // NaN -> refine
+    const unsigned bal = __ballot_sync(0xffffffffu, need);
+    __shared__ int wcount[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int off = base_sh;
+    for (int w2 = 0; w2 < warp; ++w2) off += wcount[w2];
+    if (need) list[off + __popc(bal & ((1u << lane) - 1u))] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w2 = 0; w2 < 32; ++w2) tot += wcount[w2];
+      base_sh += tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *cnt = base_sh;
+}
+
+// dst[i] = src[list[i]] (gather, dir 0) or dst[list[i]] = src[i] (scatter, dir 1); `count` doubles or
+// ints (elem 8 or 4 bytes) per matrix
+__global__ void batch_move_kernel(const char* src, char* dst, const int* list, long long bytes, int dir) {
+  const int i = blockIdx.x;
+  const long long so = (dir == 0 ? (long long)list[i] : (long long)i) * bytes;
+  const long long d0 = (dir == 0 ? (long long)i : (long long)list[i]) * bytes;
+  for (long long e = threadIdx.x * 8LL; e < bytes; e += blockDim.x * 8LL) {
+    if (e + 8 <= bytes) *reinterpret_cast<unsigned long long*>(dst + d0 + e) = *reinterpret_cast<const unsigned long long*>(src + so + e);
+    else for (long long k = e; k < bytes; ++k) dst[d0 + k] = src[so + k];
+  }
+}
+
 }  // namespace
 
 static void chol_tile(cudaStream_t st, int batch, double* G, long long ldg, long long gstride, double* X,
@@ -307,4 +406,31 @@ void launch_sumsq(cudaStream_t st, const double* b, long long m, double* out) {
   count_launches(1);
 }
 
+}  // namespace kpp
+
+namespace kpp {
+void launch_lmax(cudaStream_t st, int batch, const double* A, int s, int mode, int iters, double* lam,
+                 const double* other, double stop) {
+  if (batch <= 0) return;
+  const size_t sm = 3 * (size_t)s * sizeof(double);
+  if (mode == 0) {
+    cudaFuncSetAttribute(lmax_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    lmax_kernel<0><<<batch, 256, sm, st>>>(A, s, iters, lam, other, stop);
+  } else {
+    cudaFuncSetAttribute(lmax_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    lmax_kernel<1><<<batch, 256, sm, st>>>(A, s, iters, lam, other, stop);
+  }
+  count_launches(1);
+}
+void launch_refine_select(cudaStream_t st, int batch, const double* lamG, const double* lamM, double thresh,
+                          int* list, int* cnt) {
+  refine_select_kernel<<<1, 1024, 0, st>>>(batch, lamG, lamM, thresh, list, cnt);
+  count_launches(1);
+}
+void launch_batch_move(cudaStream_t st, int count, const void* src, void* dst, const int* list, long long bytes,
+                       int scatter) {
+  if (count <= 0) return;
+  batch_move_kernel<<<count, 256, 0, st>>>((const char*)src, (char*)dst, list, bytes, scatter);
+  count_launches(1);
+}
 }  // namespace kpp

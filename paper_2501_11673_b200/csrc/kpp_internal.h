@@ -75,6 +75,17 @@ void launch_add_diag(cudaStream_t st, int batch, double* G, int s, double lam);
 // ws: workspace of chol_inv_workspace(s) bytes per matrix (nullptr: one CTA per matrix).
 void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info, double* ws);
 size_t chol_inv_workspace(int s);
+// lam[b] = power-iteration estimate (lower bound) of lambda_max of A[b] (mode 0, symmetric) or of
+// A[b] A[b]^T with A[b] upper triangular (mode 1)
+// (other != nullptr: stop as soon as lam * other[b] > stop)
+void launch_lmax(cudaStream_t st, int batch, const double* A, int s, int mode, int iters, double* lam,
+                 const double* other = nullptr, double stop = 0.0);
+// list[0..*cnt) = blocks b with lamG[b] * lamM[b] > thresh (or NaN), ascending
+void launch_refine_select(cudaStream_t st, int batch, const double* lamG, const double* lamM, double thresh,
+                          int* list, int* cnt);
+// gather (scatter = 0: dst[i] = src[list[i]]) or scatter (dst[list[i]] = src[i]) of `bytes` per item
+void launch_batch_move(cudaStream_t st, int count, const void* src, void* dst, const int* list, long long bytes,
+                       int scatter);
 
 // ------------------------------------------------------------------ iterate.cu
 struct alignas(64) IterParams {

@@ -94,7 +94,7 @@ torch::Tensor run(torch::Tensor c, torch::Tensor key) {
 
 
 # ----------------------------------------------------------------- Phase-1 operator
-@pytest.mark.parametrize("factor", [0, 1])
+@pytest.mark.parametrize("factor", [0, 1, 2])
 def test_factor_operator(kpp, ora, factor):
     """M_k = (A_S A_S^T + lam I)^{-1} from the GPU against the oracle's Householder R
     (M = R^{-1} R^{-T}); error bound ~ u kappa(G)."""
@@ -362,3 +362,28 @@ def test_cdpp_reassociated_parity(kpp, ora, cfg, cluster):
     ref3 = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=100, x0=x0, threads=8)
     res3 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=100)
     assert rel(res3.x.cpu().numpy(), ref3.x) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg,expect", [(synth.twin("c2", 2048, 2048, 128, k=64), "some"),
+                                        (synth.twin("c3", 8192, 512, 256), "all")],
+                         ids=["c2twin", "c3twin"])
+def test_adaptive_refinement(kpp, ora, cfg, expect):
+    """Default factor route: Gram + Cholesky, second CholeskyQR pass only for ill-conditioned blocks
+    (estimated u kappa(A_S)^2 > 1e-11).  Iterates within 1e-10 of the oracle either way; the spiked
+    over-determined twin (kappa ~ 3e3) refines every block."""
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+    ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=200, threads=8)
+    ctx.reset_stats()
+    res = ctx.solve(b.to(DEV), max_iters=200)
+    st = ctx.stats()
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    if expect == "all":
+        assert st["n_refined"] == st["n_fresh_last"] > 0
+    else:
+        assert 0 <= st["n_refined"] <= st["n_fresh_last"]
+    # the refined blocks' operators equal the always-CholeskyQR2 route closely
+    ctx2 = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+    ctx2.set_option(kpp.OPT_FACTOR, 0)
+    res2 = ctx2.solve(b.to(DEV), max_iters=200)
+    assert rel(res.x.cpu().numpy(), res2.x.cpu().numpy()) <= 1e-10
