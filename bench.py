@@ -45,8 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=list(synth.CONFIGS))
     ap.add_argument("--iters", type=int, default=0, help="block iterations per step (0: config default)")
-    ap.add_argument("--ttt", action="store_true", help="also measure time to the 1e-8 tolerance")
-    ap.add_argument("--ttt-cap", type=int, default=2_000_000)
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-8 measurement")
+    ap.add_argument("--ttt-cap", type=int, default=4_000_000, help="iteration cap of the time-to-tolerance solve")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=-1)
@@ -289,7 +289,7 @@ def main():
            "d2h_bytes_per_step": 8 * n_local}
 
     ttt = None
-    if args.ttt:
+    if not args.no_ttt:
         ctx.clear_cache()
         ctx.reset_stats()
         torch.cuda.synchronize()
@@ -317,11 +317,17 @@ def main():
     hbm_peak = hbm_peak or 6650.0
     bpi = bytes_per_iter(cfg, n_local)
     achieved = bpi * total_iters / (p2max / 1e3) / 1e9 if p2max > 0 else None
+    # per launch: one persistent launch per window of min(iters, window) iterations
+    iters_per_launch = min(iters, 8192)
     tr = ncu_traffic(cfg.name)
-    roof = {"bound": "hbm", "kernel": "iterate_kernel (persistent Phase 2)", "achieved": achieved,
-            "peak": hbm_peak, "unit": "GB/s", "frac": (achieved / hbm_peak) if achieved else None,
-            "traffic": tr, "peak_source": peak_note,
-            "bytes_per_iter": bpi, "iter_kernel_share": p2max / ms if ms > 0 else None}
+    roof = {"bound": "hbm", "kernel": "Phase-2 persistent kernel (iterate_kernel / cdpp_stream_kernel)",
+            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": (achieved / hbm_peak) if achieved else None,
+            "traffic": tr * iters_per_launch if tr else None,
+            "traffic_note": "ncu dram read+write bytes per launch (per-iteration bytes from profiles/ncu_summary.json x iterations per launch)",
+            "algorithmic_bytes_per_launch": bpi * iters_per_launch, "iters_per_launch": iters_per_launch,
+            "peak_source": peak_note, "bytes_per_iter": bpi,
+            "iter_kernel_share": p2max / ms if ms > 0 else None}
     cpu = None
     if not args.no_cpu and not dist:
         cpu = cpu_oracle_sample(cfg, A_keep.cpu().numpy(), b.cpu().numpy(), args.cpu_seconds)
