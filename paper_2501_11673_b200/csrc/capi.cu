@@ -491,6 +491,7 @@ kpp_status plan_persistent(kpp_ctx* ctx) {
   for (int C : sizes) {
     if (ctx->cluster_opt && C != ctx->cluster_opt) continue;
     int G = ctx->num_sms / C * C;
+    if (getenv("KPP_MAX_GRID")) G = std::min(G, atoi(getenv("KPP_MAX_GRID")) / C * C);  // experiments
     if (G <= 0) continue;
     // variants: (resident slab, M rows staged per CTA, where y = M r is computed)
     //   ygl 0: each cluster computes y from its CTAs' rows of M (DSMEM all-gather of y)

@@ -387,3 +387,25 @@ def test_adaptive_refinement(kpp, ora, cfg, expect):
     ctx2.set_option(kpp.OPT_FACTOR, 0)
     res2 = ctx2.solve(b.to(DEV), max_iters=200)
     assert rel(res.x.cpu().numpy(), res2.x.cpu().numpy()) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg", [synth.twin("c3", 4096, 512, 64, k=16), synth.twin("c5", 1024, 1024, 128, k=25)],
+                         ids=["kpp", "cdpp"])
+def test_dist_path_single_rank(kpp, ora, cfg):
+    """The column-sharded entry points (kpp_setup_dist / cdpp_setup_dist) with a one-rank NCCL
+    communicator: graph engine with the per-iteration allreduce and the per-fresh-block Gram /
+    principal-block allreduce inside, against the oracle."""
+    A, b, _ = synth.make_problem(cfg)
+    uid = kpp.kpp_get_unique_id()
+    n = A.shape[1]
+    if cfg.kind == "cdpp":
+        ctx = kpp.cdpp_setup_dist(A.to(DEV), n, 0, n, cfg.s, cfg.lam, 0, uid, 0, 1)
+        ref = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=300, threads=8)
+    else:
+        ctx = kpp.kpp_setup_dist(A.to(DEV), A.shape[0], n, 0, n, cfg.s, cfg.lam, 0, uid, 0, 1)
+        ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=300, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=300)
+    assert res.iters == 300
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    ctx.destroy()
