@@ -319,13 +319,16 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
     // G = A_SS + lam I (Alg 3 l.8); multi-GPU: disjoint column supports summed exactly
     launch_gather_principal(st, B, ctx->A, ctx->lda, S, s, ctx->nranks > 1 ? 0.0 : ctx->lam,
                             ctx->col_begin, ctx->col_end, G);
+    pp.mark("gather");
     if (ctx->nranks > 1) {
       CKS(allreduce(ctx, G, (size_t)B * ss));
       launch_add_diag(st, B, G, s, ctx->lam);
     }
     launch_chol_trtri(st, B, G, X1, s, ctx->d_info, W);
+    pp.mark("chol");
     Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
     launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);  // M = X X^T (X upper)
+    pp.mark("M");
   } else {
     // G1 = A_S A_S^T (+ lam I): NT GEMM with row gathers on both operands, split-K
     Operand a{ctx->A, ctx->lda, 0, S, s, 0}, b{ctx->A, ctx->lda, 0, S, s, 1};

@@ -6,6 +6,8 @@
 // Memoizing M (rather than R) turns the per-iteration solve into one s x s
 // matvec; DESIGN.md records the parity measurement that justifies it.
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kpp_internal.h"
 
@@ -207,12 +209,24 @@ __global__ void gather_principal_kernel(const double* A, long long lda, const in
                                         double lam, long long cb, long long ce, double* Gall) {
   const int32_t* S = Sall + (long long)blockIdx.y * s;
   double* G = Gall + (long long)blockIdx.y * s * s;
-  const int k = blockIdx.x;  // row of the block
+  // 4 rows per CTA (128 threads each), 4 independent gathered loads in flight per thread
+  const int k = blockIdx.x * 4 + (threadIdx.x >> 7);
+  if (k >= s) return;
   const double* row = A + (long long)S[k] * lda;
-  for (int l = threadIdx.x; l < s; l += blockDim.x) {
-    const long long c = S[l];
-    const double v = (c >= cb && c < ce) ? row[c - cb] : 0.0;
-    G[(long long)k * s + l] = v + ((k == l) ? lam : 0.0);
+  const int t = threadIdx.x & 127;
+  for (int l0 = t; l0 < s; l0 += 512) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int l = l0 + 128 * u;
+      const long long c = l < s ? (long long)S[l] : -1;
+      v[u] = (l < s && c >= cb && c < ce) ? __ldg(row + (c - cb)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int l = l0 + 128 * u;
+      if (l < s) G[(long long)k * s + l] = v[u] + ((k == l) ? lam : 0.0);
+    }
   }
 }
 
@@ -232,6 +246,83 @@ __global__ void sumsq_kernel(const double* b, long long m, double* out) {
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = sh[0];
+}
+
+// ------------------------------------------------------------------ 64 x 64 diagonal tile
+// One CTA (256 threads) per tile of size kb <= 64 (views with leading dimensions): right-looking
+// Cholesky with one barrier per pivot (row i of R kept apart from the working copy so the trailing
+// update of step i and the scaling of row i need no second barrier), then X = R^{-1} by rows from
+// the bottom (4 threads per column, shuffle-reduced dots).  In place: G <- R (lower part zeroed).
+__global__ void __launch_bounds__(256) chol_diag_kernel(double* Gall, long long ldg, long long gstride, double* Xall,
+                                                        long long ldx, long long xstride, int kb, int* info,
+                                                        int info_base) {
+  extern __shared__ double dsm[];
+  double (*a)[65] = reinterpret_cast<double (*)[65]>(dsm);             // working copy
+  double (*rx)[65] = reinterpret_cast<double (*)[65]>(dsm + 64 * 65);  // R, then X row by row
+  double* rrow = dsm + 2 * 64 * 65;
+  __shared__ int fail_sh;
+  double* G = Gall + (long long)blockIdx.x * gstride;
+  double* X = Xall + (long long)blockIdx.x * xstride;
+  const int tid = threadIdx.x;
+  if (tid == 0) fail_sh = 0;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int i = e >> 6, j = e & 63;
+    a[i][j] = (i < kb && j < kb && j >= i) ? G[(long long)i * ldg + j] : 0.0;
+    rx[i][j] = 0.0;
+  }
+  __syncthreads();
+  const int q = tid & 63, p0 = tid >> 6;  // column q, rows p0, p0 + 4, ...
+  for (int i = 0; i < kb; ++i) {
+    const double v = a[i][i];
+    const bool ok = v > 0.0;
+    if (!ok && tid == 0 && fail_sh == 0) fail_sh = i + 1;
+    const double d = ok ? sqrt(v) : 1.0;
+    const double dinv = 1.0 / d;
+    // row i of R: R[i][j] = a[i][j] / d
+    if (tid < kb && tid >= i) rx[i][tid] = (tid == i) ? d : a[i][tid] * dinv;
+    // trailing update with the scaled row: a[p][q] -= R[i][p] R[i][q], i < p <= q
+    if (q > i && q < kb) {
+      const double riq = a[i][q] * dinv;
+      // 4 rows per round, loads first (row i is read-only in this step)
+      for (int pp = i + 1 + p0; pp <= q; pp += 16) {
+        double ri[4], aq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = pp + 4 * u;
+          ri[u] = r <= q ? a[i][r] : 0.0;
+          aq[u] = r <= q ? a[r][q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = pp + 4 * u;
+          if (r <= q) a[r][q] = fma(-(ri[u] * dinv), riq, aq[u]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // X = R^{-1}, rows from the bottom: X[i][j] = (delta_ij - sum_{l=i+1..j} R[i][l] X[l][j]) / R[i][i]
+  const int lane = tid & 31;
+  const int col = tid >> 2, sub = tid & 3;  // 4 threads per column
+  for (int i = kb - 1; i >= 0; --i) {
+    if (tid < kb) rrow[tid] = rx[i][tid];
+    __syncthreads();
+    double acc = 0.0;
+    if (col < kb && col > i)
+      for (int l = i + 1 + sub; l <= col; l += 4) acc = fma(rrow[l], rx[l][col], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    (void)lane;
+    const double rinv = 1.0 / rrow[i];
+    if (sub == 0 && col < kb && col >= i) rx[i][col] = (col == i) ? rinv : -acc * rinv;
+    __syncthreads();
+  }
+  // only X_kk is needed by the blocked driver (R_kk itself is never read again)
+  for (int e = tid; e < kb * kb; e += 256) {
+    const int i = e / kb, j = e - i * kb;
+    X[(long long)i * ldx + j] = (j >= i) ? rx[i][j] : 0.0;
+  }
+  if (tid == 0 && fail_sh) info[blockIdx.x] = info_base + fail_sh;
 }
 
 // ------------------------------------------------------------------ adaptive CholeskyQR2
@@ -360,23 +451,51 @@ void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, 
   //   panel:    R[k, k+1:] = X_kk^T G[k, k+1:]             (DMMA, X_kk^T lower triangular)
   //   trailing: G[k+1:, k+1:] -= R[k, k+1:]^T R[k, k+1:]   (DMMA, upper triangle only)
   // then X = R^{-1} by column blocks: X[0:j, J] = -(X[0:j, 0:j] R[0:j, J]) X_JJ.
-  constexpr int NB = 64;
+  constexpr int NB = 64;  // (128-wide steps measured slower: the diagonal tiles dominate)
+  constexpr size_t kDiagSmem = (2 * 64 * 65 + 64) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem);
+    attr = true;
+  }
+  static const bool prof = getenv("KPP_P1_PROFILE") != nullptr;
+  cudaEvent_t ev[5];
+  if (prof) for (auto& e : ev) { cudaEventCreate(&e); }
+  if (prof) cudaEventRecord(ev[0], st);
   double* R = ws;                  // [batch][s][s]: off-diagonal blocks of R
-  double* T = ws + (long long)batch * ss;  // [batch][s][64]
+  double* T = ws + (long long)batch * ss;  // [batch][s][NB]
   cudaMemsetAsync(X, 0, (size_t)batch * ss * sizeof(double), st);
   for (int k0 = 0; k0 < s; k0 += NB) {
     const int kb = s - k0 < NB ? s - k0 : NB;
     const long long dk = (long long)k0 * (s + 1);
-    chol_tile(st, batch, G + dk, s, ss, X + dk, s, ss, kb, info, k0);
+    cudaEvent_t e0, e1, e2, e3;
+    if (prof) { cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3); cudaEventRecord(e0, st); }
+    chol_diag_kernel<<<batch, 256, kDiagSmem, st>>>(G + dk, s, ss, X + dk, s, ss, kb, info, k0);
+    count_launches(1);
+    if (prof) cudaEventRecord(e1, st);
     const int c0 = k0 + kb, tr = s - c0;
-    if (tr <= 0) break;
+    if (tr <= 0) {
+      if (prof) { cudaEventSynchronize(e1); float a; cudaEventElapsedTime(&a, e0, e1); fprintf(stderr, "  step %d: diag %.3f\n", k0, a); }
+      break;
+    }
     Operand xkk{X + dk, s, ss, nullptr, 0, 1};                        // logical (i,k) = X[k][i]
     Operand gp{G + (long long)k0 * s + c0, s, ss, nullptr, 0, 0};
     launch_dgemm(st, batch, kb, tr, kb, xkk, gp, R + (long long)k0 * s + c0, s, ss, 1, 0, 1);
     Operand rpt{R + (long long)k0 * s + c0, s, ss, nullptr, 0, 1};    // logical (i,k) = R[k0+k][c0+i]
     Operand rp{R + (long long)k0 * s + c0, s, ss, nullptr, 0, 0};
+    if (prof) cudaEventRecord(e2, st);
     launch_dgemm(st, batch, tr, tr, kb, rpt, rp, G + (long long)c0 * (s + 1), s, ss, 1, 1, 0, -1.0, 1);
+    if (prof) {
+      cudaEventRecord(e3, st);
+      cudaEventSynchronize(e3);
+      float a, b, c;
+      cudaEventElapsedTime(&a, e0, e1);
+      cudaEventElapsedTime(&b, e1, e2);
+      cudaEventElapsedTime(&c, e2, e3);
+      fprintf(stderr, "  step %d: diag %.3f panel %.3f trailing %.3f\n", k0, a, b, c);
+    }
   }
+  if (prof) cudaEventRecord(ev[1], st);
   for (int j0 = NB; j0 < s; j0 += NB) {
     const int kb = s - j0 < NB ? s - j0 : NB;
     Operand xa{X, s, ss, nullptr, 0, 0}, rj{R + j0, s, ss, nullptr, 0, 0};
@@ -384,14 +503,23 @@ void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, 
     Operand ta{T, NB, (long long)s * NB, nullptr, 0, 0}, xjj{X + (long long)j0 * (s + 1), s, ss, nullptr, 0, 0};
     launch_dgemm(st, batch, j0, kb, kb, ta, xjj, X + j0, s, ss, 1, 0, 0, -1.0, 0);       // X0J = -T XJJ
   }
+  if (prof) {
+    cudaEventRecord(ev[2], st);
+    cudaEventSynchronize(ev[2]);
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    fprintf(stderr, "[kpp blocked chol] batch %d s %d: cholesky %.3f ms, inverse %.3f ms\n", batch, s, a, b);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
 }
 
 void launch_gather_principal(cudaStream_t st, int batch, const double* A, long long lda,
                              const int32_t* S, int s, double lam, long long col_begin,
                              long long col_end, double* G) {
   if (batch <= 0) return;
-  dim3 grid(s, batch);
-  gather_principal_kernel<<<grid, 128, 0, st>>>(A, lda, S, s, lam, col_begin, col_end, G);
+  dim3 grid((s + 3) / 4, batch);
+  gather_principal_kernel<<<grid, 512, 0, st>>>(A, lda, S, s, lam, col_begin, col_end, G);
   count_launches(1);
 }
 
