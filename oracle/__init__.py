@@ -69,6 +69,13 @@ def lib():
         L.ora_cdpp_run.argtypes = [P, i64, i64, P, P, i32, f64, u64, i64, f64,
                                    ctypes.POINTER(_Opts), P, P, P, i64, P, P, P]
         L.ora_rho_update.argtypes = [i64, f64, f64, f64, i64, P, P]
+        L.ora_next_pow2.argtypes = [i64]
+        L.ora_next_pow2.restype = i64
+        L.ora_rht_signs.argtypes = [u64, i64, P]
+        L.ora_fht.argtypes = [P, i64]
+        L.ora_rht_rows.argtypes = [P, i64, i64, i64, P, u64, P, P]
+        L.ora_rht_sym.argtypes = [P, i64, i64, P, u64, P, P]
+        L.ora_rht_vec.argtypes = [P, i64, i64, u64, i32, P]
         _lib = L
     return _lib
 
@@ -191,3 +198,67 @@ def cdpp_run(A, b, s, lam=1e-8, seed=0, max_iters=100, tol=0.0, x0=None, accel=T
     """CD++ (Alg 3 without SymFHT) -- see kpp_oracle.h."""
     return _run(True, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed,
                 HOUSEHOLDER, reverse, threads, hist_cap)
+
+
+# ---------------------------------------------------------------- RHT (SURVEY 8(f) NEXT-1)
+def next_pow2(n: int) -> int:
+    return int(lib().ora_next_pow2(n))
+
+
+def rht_signs(seed: int, n: int) -> np.ndarray:
+    d = np.zeros(n, dtype=np.int8)
+    lib().ora_rht_signs(seed, n, _p(d))
+    return d
+
+
+def fht(v) -> np.ndarray:
+    w = _f64(v).copy()
+    lib().ora_fht(_p(w), w.shape[0])
+    return w
+
+
+def rht_rows(A, b, seed: int):
+    """K++ preprocessing: (H D [A; 0], H D [b; 0]) with m2 = next power of 2 rows."""
+    A = _f64(A)
+    m, n = A.shape
+    m2 = next_pow2(m)
+    At = np.zeros((m2, n))
+    bt = np.zeros(m2)
+    lib().ora_rht_rows(_p(A), m, n, n, _p(_f64(b)), seed, _p(At), _p(bt))
+    return At, bt
+
+
+def rht_sym(A, b, seed: int):
+    """CD++ preprocessing: (H D A_pad D H, H D [b; 0])."""
+    A = _f64(A)
+    n = A.shape[0]
+    n2 = next_pow2(n)
+    At = np.zeros((n2, n2))
+    bt = np.zeros(n2)
+    lib().ora_rht_sym(_p(A), n, n, _p(_f64(b)), seed, _p(At), _p(bt))
+    return At, bt
+
+
+def rht_vec(v, n: int, n2: int, seed: int, forward: bool) -> np.ndarray:
+    """forward: H D [v; 0] (n2 values); backward: (D H v)[:n] (Alg 3 l.16)."""
+    v = _f64(v)
+    out = np.zeros(n2 if forward else n)
+    lib().ora_rht_vec(_p(v), n, n2, seed, int(forward), _p(out))
+    return out
+
+
+def kpp_run_rht(A, b, s, seed=0, **kw) -> Result:
+    """Alg 5 with its preprocessing lines 2-3: solve H D A x = H D b (same x)."""
+    At, bt = rht_rows(A, b, seed)
+    return kpp_run(At, bt, s, seed=seed, **kw)
+
+
+def cdpp_run_rht(A, b, s, seed=0, x0=None, **kw) -> Result:
+    """Alg 3 with lines 2-3 and the back-rotation of line 16: x = D H xt."""
+    n = A.shape[0]
+    n2 = next_pow2(n)
+    At, bt = rht_sym(A, b, seed)
+    xt0 = None if x0 is None else rht_vec(x0, n, n2, seed, True)
+    r = cdpp_run(At, bt, s, seed=seed, x0=xt0, **kw)
+    r.x = rht_vec(r.x, n, n2, seed, False)
+    return r

@@ -370,6 +370,40 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
   return status;
 }
 
+// ---------------------------------------------------------------- RHT
+// Def 1.1: Q = H D, D = diag(d)/sqrt(m2), d_i Rademacher.  Sign stream (binding
+// convention, reading R3): word (i mod 4) of philox((lo32(i/4), hi32(i/4), 3, 0), key),
+// d_i = -1 if its lowest bit is set, else +1.
+int rht_sign(uint64_t seed, int64_t i) {
+  uint32_t key[2];
+  seed_key(seed, key);
+  const uint64_t c = (uint64_t)i >> 2;
+  uint32_t ctr[4] = {(uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 3u, 0u};
+  uint32_t w[4];
+  philox(ctr, key, w);
+  return (w[i & 3] & 1u) ? -1 : 1;
+}
+
+int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// H_n v in place for the n = 2^k values v[0], v[stride], ...: Sylvester's recursion
+// H_{2h} = [[H_h, H_h], [H_h, -H_h]] (Def E.1 convention; Alg 4 P:1230-1243 prints the second
+// half with the opposite sign, SPEC S:189/S:204 -- we follow the definition), one butterfly
+// (a, b) -> (a + b, a - b) per pair, half-sizes h = 1, 2, 4, ...
+void fht(double* v, int64_t n, int64_t stride) {
+  for (int64_t h = 1; h < n; h <<= 1)
+    for (int64_t i0 = 0; i0 < n; i0 += 2 * h)
+      for (int64_t i = i0; i < i0 + h; ++i) {
+        const double a = v[i * stride], b = v[(i + h) * stride];
+        v[i * stride] = a + b;
+        v[(i + h) * stride] = a - b;
+      }
+}
+
 }  // namespace
 
 extern "C" {
@@ -436,6 +470,68 @@ int ora_cdpp_run(const double* A, int64_t n, int64_t lda, const double* b, const
 void ora_rho_update(int64_t i, double rhat_prev, double E0, double E1, int64_t zeta, double* rhat_out,
                     double* rho_out) {
   rho_update(i, rhat_prev, E0, E1, zeta, rhat_out, rho_out);
+}
+
+int64_t ora_next_pow2(int64_t n) { return next_pow2(n); }
+
+void ora_rht_signs(uint64_t seed, int64_t n, int8_t* d) {
+  for (int64_t i = 0; i < n; ++i) d[i] = (int8_t)rht_sign(seed, i);
+}
+
+void ora_fht(double* v, int64_t n) { fht(v, n, 1); }
+
+// K++ preprocessing (Alg 5 l.2-3): At = H D [A; 0] (m2 x n, row-major, ld n),
+// bt = H D [b; 0] (m2); m2 = next power of 2 >= m, D = diag(d)/sqrt(m2).
+void ora_rht_rows(const double* A, int64_t m, int64_t n, int64_t lda, const double* b, uint64_t seed,
+                  double* At, double* bt) {
+  const int64_t m2 = next_pow2(m);
+  const double sc = 1.0 / std::sqrt((double)m2);
+  for (int64_t i = 0; i < m2; ++i) {
+    const double di = i < m ? rht_sign(seed, i) * sc : 0.0;
+    for (int64_t j = 0; j < n; ++j) At[i * n + j] = i < m ? di * A[i * lda + j] : 0.0;
+    if (bt) bt[i] = i < m ? di * b[i] : 0.0;
+  }
+  for (int64_t j = 0; j < n; ++j) fht(At + j, m2, n);
+  if (bt) fht(bt, m2, 1);
+}
+
+// CD++ preprocessing (Alg 3 l.2-3): At = H D A_pad D H (n2 x n2), bt = H D [b; 0],
+// with A_pad = [[A, 0], [0, I]] (reading R4: the padded diagonal is 1 so A_pad stays PD where A
+// is, and the padded coordinates of the solution are 0).  H D A D H is formed as two one-sided
+// transforms (the result SymFHT, Alg 2, computes with fewer operations).
+void ora_rht_sym(const double* A, int64_t n, int64_t lda, const double* b, uint64_t seed, double* At,
+                 double* bt) {
+  const int64_t n2 = next_pow2(n);
+  const double sc = 1.0 / std::sqrt((double)n2);
+  std::vector<double> d((size_t)n2);
+  for (int64_t i = 0; i < n2; ++i) d[(size_t)i] = rht_sign(seed, i) * sc;
+  for (int64_t i = 0; i < n2; ++i)
+    for (int64_t j = 0; j < n2; ++j) {
+      const double a = (i < n && j < n) ? A[i * lda + j] : (i == j ? 1.0 : 0.0);
+      At[i * n2 + j] = d[(size_t)i] * a * d[(size_t)j];
+    }
+  for (int64_t j = 0; j < n2; ++j) fht(At + j, n2, n2);   // H (D A D): mix rows
+  for (int64_t i = 0; i < n2; ++i) fht(At + i * n2, n2, 1);  // (...) H: mix columns
+  if (bt) {
+    for (int64_t i = 0; i < n2; ++i) bt[i] = i < n ? d[(size_t)i] * b[i] : 0.0;
+    fht(bt, n2, 1);
+  }
+}
+
+// CD++ back-rotation (Alg 3 l.16): x = D H xt, first n of n2 entries.  Also the forward
+// map of an initial iterate: xt = Q x = H D x (fwd = 1).
+void ora_rht_vec(const double* v, int64_t n, int64_t n2, uint64_t seed, int32_t fwd, double* out) {
+  const double sc = 1.0 / std::sqrt((double)n2);
+  std::vector<double> w((size_t)n2);
+  if (fwd) {
+    for (int64_t i = 0; i < n2; ++i) w[(size_t)i] = i < n ? rht_sign(seed, i) * sc * v[i] : 0.0;
+    fht(w.data(), n2, 1);
+    for (int64_t i = 0; i < n2; ++i) out[i] = w[(size_t)i];
+  } else {
+    for (int64_t i = 0; i < n2; ++i) w[(size_t)i] = v[i];
+    fht(w.data(), n2, 1);
+    for (int64_t i = 0; i < n; ++i) out[i] = rht_sign(seed, i) * sc * w[(size_t)i];
+  }
 }
 
 }  // extern "C"

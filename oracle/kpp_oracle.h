@@ -27,6 +27,9 @@
  *                       worked example (SPEC), A=I one-step solve.
  *   ora_cdpp_run        pinned: CD++ <-> K++ reduction z_t = Phi^T x_t,
  *                       scalar coordinate-descent step, A=I.
+ *   ora_fht / ora_rht_*  pinned: H_2 and e_1 examples, H^2 = n I, dense
+ *                       Sylvester H_8, isometry Q^T Q = I, spectrum of Q A Q^T, [[1,2],[2,3]]
+ *                       -> [[8,-2],[-2,0]], solution invariance of the transformed system.
  *   adaptive-rho trajectory / stop iteration on the BASELINE configs:
  *                       "parity unpinned" (no closed form, no published values).
  */
@@ -99,6 +102,18 @@ int ora_cdpp_run(const double* A, int64_t n, int64_t lda, const double* b, const
    writes the new r_hat and rho. */
 void ora_rho_update(int64_t i, double rhat_prev, double E0, double E1, int64_t zeta,
                     double* rhat_out, double* rho_out);
+
+/* ---- RHT preprocessing (Def 1.1, Alg 4 P:1230-1243,
+   Alg 5 l.2-3 P:1337-1338, Alg 3 l.2-3 and l.16 P:745-746).  Sign stream: reading R3;
+   padding: zero rows (K++), unit diagonal (CD++, reading R4). */
+int64_t ora_next_pow2(int64_t n);
+void ora_rht_signs(uint64_t seed, int64_t n, int8_t* d);
+void ora_fht(double* v, int64_t n); /* in place, n a power of 2, Sylvester order */
+void ora_rht_rows(const double* A, int64_t m, int64_t n, int64_t lda, const double* b, uint64_t seed,
+                  double* At, double* bt);
+void ora_rht_sym(const double* A, int64_t n, int64_t lda, const double* b, uint64_t seed, double* At,
+                 double* bt);
+void ora_rht_vec(const double* v, int64_t n, int64_t n2, uint64_t seed, int32_t fwd, double* out);
 
 #ifdef __cplusplus
 }

@@ -420,3 +420,110 @@ def test_cdpp_converges_psd(ora):
     res = ora.cdpp_run(A, b, 64, max_iters=20000, tol=1e-8)
     assert res.status == ora.OK
     assert np.linalg.norm(A @ res.x - b) / np.linalg.norm(b) < 1e-7
+
+
+# ----------------------------------------------------------------- RHT
+def _sylvester(n):
+    H = np.array([[1.0]])
+    while H.shape[0] < n:
+        H = np.block([[H, H], [H, -H]])
+    return H
+
+
+def test_fht_examples(ora):
+    """(1,2) -> (3,-1); e_1 (n=4) -> (1,1,1,1); H^2 = n I."""
+    assert np.array_equal(ora.fht([1.0, 2.0]), [3.0, -1.0])
+    assert np.array_equal(ora.fht([1.0, 0.0, 0.0, 0.0]), [1.0, 1.0, 1.0, 1.0])
+    v = np.random.default_rng(0).standard_normal(64)
+    assert np.allclose(ora.fht(ora.fht(v)), 64 * v, rtol=0, atol=1e-12 * 64 * np.abs(v).max())
+
+
+@pytest.mark.parametrize("n", [2, 8, 32, 256])
+def test_fht_matches_dense_sylvester(ora, n):
+    """Def E.1: H_{2h} = [[H_h, H_h], [H_h, -H_h]] built densely, independent of the butterflies."""
+    H = _sylvester(n)
+    X = np.random.default_rng(n).standard_normal((n, 3))
+    got = np.stack([ora.fht(X[:, j]) for j in range(3)], axis=1)
+    assert np.allclose(got, H @ X, rtol=0, atol=1e-12 * n)
+
+
+def test_rht_signs(ora):
+    d = ora.rht_signs(7, 4096)
+    assert set(np.unique(d)) == {-1, 1}
+    assert abs(int(d.sum())) < 4 * np.sqrt(4096)          # Rademacher balance
+    assert np.array_equal(d, ora.rht_signs(7, 4096))     # deterministic
+    assert not np.array_equal(d, ora.rht_signs(8, 4096))
+    # the convention: lowest bit of word (i mod 4) of philox((i/4, 0, 3, 0), key)
+    for i in (0, 1, 5, 4095):
+        w = ora.philox([i // 4, 0, 3, 0], [7, 0])
+        assert d[i] == (-1 if (w[i % 4] & 1) else 1)
+
+
+@pytest.mark.parametrize("m,n", [(64, 16), (100, 20), (37, 37)])
+def test_rht_rows_isometry_and_solution(ora, m, n):
+    """Q = H D with D = diag(d)/sqrt(m2): Q^T Q = I, so Q A has A's singular values and the
+    transformed system has A's solutions."""
+    rng = np.random.default_rng(m)
+    A = rng.standard_normal((m, n))
+    x = rng.standard_normal(n)
+    b = A @ x
+    At, bt = ora.rht_rows(A, b, 3)
+    m2 = ora.next_pow2(m)
+    assert At.shape == (m2, n)
+    H = _sylvester(m2)
+    D = np.diag(np.concatenate([ora.rht_signs(3, m).astype(float), np.zeros(m2 - m)])) / np.sqrt(m2)
+    Apad = np.vstack([A, np.zeros((m2 - m, n))])
+    assert np.allclose(At, H @ D @ Apad, rtol=0, atol=1e-13 * np.abs(A).max() * np.log2(m2) * 4)
+    assert np.allclose(np.linalg.svd(At, compute_uv=False), np.linalg.svd(A, compute_uv=False), rtol=1e-12)
+    xs = np.linalg.lstsq(At, bt, rcond=None)[0]
+    assert np.allclose(xs, x, rtol=0, atol=1e-10)
+
+
+@pytest.mark.parametrize("n", [16, 24])
+def test_rht_sym_conjugation(ora, n):
+    """Alg 3 l.3: H D A D H = Q A_pad Q^T is symmetric with the spectrum of A_pad (unit padded diagonal)."""
+    rng = np.random.default_rng(n)
+    G = rng.standard_normal((n, n))
+    A = G @ G.T + np.eye(n)
+    b = rng.standard_normal(n)
+    At, bt = ora.rht_sym(A, b, 5)
+    n2 = ora.next_pow2(n)
+    Apad = np.eye(n2)
+    Apad[:n, :n] = A
+    Q = _sylvester(n2) @ np.diag(np.concatenate([ora.rht_signs(5, n2).astype(float)])) / np.sqrt(n2)
+    assert np.allclose(At, Q @ Apad @ Q.T, rtol=0, atol=1e-12 * np.abs(A).max())
+    assert np.allclose(At, At.T, rtol=0, atol=1e-12 * np.abs(A).max())
+    assert np.allclose(np.linalg.eigvalsh(At), np.linalg.eigvalsh(Apad), rtol=1e-11)
+    # back-rotation (Alg 3 l.16): x = D H xt solves A x = b when xt solves the transformed system
+    xt = np.linalg.solve(At, bt)
+    x = ora.rht_vec(xt, n, n2, 5, False)
+    assert np.allclose(A @ x, b, rtol=0, atol=1e-9 * np.abs(b).max())
+    # forward then backward is the identity (Q^T Q = I)
+    v = rng.standard_normal(n)
+    assert np.allclose(ora.rht_vec(ora.rht_vec(v, n, n2, 5, True), n, n2, 5, False), v, rtol=0, atol=1e-13)
+
+
+def test_spec_symfht_2x2(ora):
+    """H [[1,2],[2,3]] H = [[8,-2],[-2,0]] (the unscaled two-sided transform)."""
+    A = np.array([[1.0, 2.0], [2.0, 3.0]])
+    HA = np.stack([ora.fht(A[:, j]) for j in range(2)], axis=1)
+    HAH = np.stack([ora.fht(HA[i, :]) for i in range(2)], axis=0)
+    assert np.array_equal(HAH, [[8.0, -2.0], [-2.0, 0.0]])
+
+
+def test_kpp_rht_converges(ora):
+    """Alg 5 with preprocessing (l.2-3): still converges to the solution of the original system."""
+    cfg = synth.twin("c3", 1000, 100, 25, k=6)   # over-determined consistent; m padded to 1024
+    A, b, xs = synth.make_problem(cfg)
+    r = ora.kpp_run_rht(A.numpy(), b.numpy(), 25, seed=0, max_iters=20000, tol=1e-10)
+    assert r.status == ora.OK
+    assert np.linalg.norm(r.x - xs.numpy()) / np.linalg.norm(xs.numpy()) < 1e-7
+
+
+def test_cdpp_rht_converges(ora):
+    """Alg 3 with SymFHT preprocessing and the back-rotation (l.2-3, l.16), ragged n (padding)."""
+    cfg = synth.twin("c5", 200, 200, 32, k=10)
+    A, b, _ = synth.make_problem(cfg)
+    An, bn = A.numpy(), b.numpy()
+    r = ora.cdpp_run_rht(An, bn, 32, seed=1, max_iters=20000, tol=1e-11)
+    assert np.linalg.norm(An @ r.x - bn) / np.linalg.norm(bn) < 1e-8
