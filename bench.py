@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=-1)
+    ap.add_argument("--rht", action="store_true", help="randomized Hadamard preprocessing (SURVEY 8(f) NEXT-1)")
     return ap.parse_args()
 
 
@@ -226,6 +227,10 @@ def main():
     ctx.set_stream(stream)
     if args.engine >= 0:
         ctx.set_option(kpp.OPT_ENGINE, args.engine)
+    rht_ms = None
+    if args.rht:
+        ctx.enable_rht()  # one-time transform of A (not part of a step: the paper's Alg 5/3 line 2-3)
+        rht_ms = ctx.stats()["rht_ms"]
     x_out = torch.empty(n_local, dtype=torch.float64, device=dev)
 
     def step():
@@ -354,6 +359,7 @@ def main():
         "time_to_tol": ttt,
         "n_blocks_per_step": warm["n_blocks"],
         "n_refined_per_step": st.get("n_refined", 0) // max(1, args.steps),
+        "rht_preprocess_ms": rht_ms,
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -159,6 +159,7 @@ typedef struct {
   int32_t ygl;           /* where y = M r is computed (KPP_OPT_YGL values 0, 1, 4) */
   int32_t reassoc;       /* 1 if the CD++ re-associated streaming kernel runs (KPP_OPT_REASSOC) */
   int64_t n_refined;     /* blocks that received the second CholeskyQR pass (since reset) */
+  double rht_ms;         /* device time of the randomized Hadamard preprocessing (kpp_enable_rht) */
 } kpp_stats;
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */
@@ -177,6 +178,20 @@ kpp_status kpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t m, int64_
 kpp_status cdpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t n, int64_t col_begin,
                            int64_t col_end, int64_t lda, int32_t block_size, double lambda,
                            uint64_t seed, const uint8_t id[128], int32_t rank, int32_t nranks);
+
+/* ---- randomized Hadamard preprocessing ----------------- */
+/* Def 1.1: Q = H D, H the Sylvester-order Hadamard matrix, D = diag(d)/sqrt(m2) with
+   Rademacher d (Philox-4x32-10 stream 3 of the context's seed).  K++ (Alg 5 l.2-3):
+   the context solves (Q A) x = Q b, A zero-padded to m2 = next power of 2 >= m rows (x unchanged).
+   CD++ (Alg 3 l.2-3 and l.16): it solves (Q A_pad Q^T) x~ = Q b with
+   A_pad = [[A, 0], [0, I]] of size n2 and returns x = (Q^T x~)[0:n]; x0 is mapped by Q.
+   The transformed matrix is computed once, here, into a buffer the context owns (m2 x n or
+   n2 x n2 doubles; A is no longer read); the memo cache is dropped.  Later kpp_solve calls take
+   and return the caller's sizes (b: m values, x0 / x_out: n).  Single-GPU contexts only
+   (KPP_EINVAL on a column-sharded context).  Idempotent. */
+kpp_status kpp_enable_rht(kpp_ctx* ctx);
+/* The transformed matrix (HOST, m2 x n or n2 x n2 row-major); requires kpp_enable_rht. */
+kpp_status kpp_get_rht_matrix(kpp_ctx* ctx, double* out);
 
 /* Library version string. */
 const char* kpp_version(void);

@@ -46,7 +46,7 @@ class _Stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64), ("grid_ctas", ctypes.c_int32),
                 ("resident", ctypes.c_int32), ("cluster", ctypes.c_int32), ("m_in_smem", ctypes.c_int32),
                 ("tma", ctypes.c_int32), ("ygl", ctypes.c_int32), ("reassoc", ctypes.c_int32),
-                ("n_refined", ctypes.c_int64)]
+                ("n_refined", ctypes.c_int64), ("rht_ms", ctypes.c_double)]
 
 
 def load_library():
@@ -81,6 +81,8 @@ def load_library():
         "kpp_setup_dist": ([PP, P, i64, i64, i64, i64, i64, i32, f64, u64, P, i32, i32], i32),
         "cdpp_setup_dist": ([PP, P, i64, i64, i64, i64, i32, f64, u64, P, i32, i32], i32),
         "kpp_version": ([], ctypes.c_char_p),
+        "kpp_enable_rht": ([P], i32),
+        "kpp_get_rht_matrix": ([P, P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -190,6 +192,21 @@ class Ctx:
 
     def reset_stats(self):
         _check(load_library().kpp_reset_stats(self.handle), self.handle)
+
+    def enable_rht(self):
+        """Randomized Hadamard preprocessing (kpp_enable_rht): later solves run on Q A (K++) or
+        Q A Q^T (CD++) with the caller's b / x sizes unchanged."""
+        _check(load_library().kpp_enable_rht(self.handle), self.handle)
+        self._rht_dims = self._rht_shape()
+
+    def _rht_shape(self):
+        p2 = lambda v: 1 << max(0, (v - 1).bit_length())
+        return (p2(self.m), self.n) if self.kind == "kpp" else (p2(self.n), p2(self.n))
+
+    def rht_matrix(self) -> torch.Tensor:
+        out = torch.zeros(*self._rht_shape(), dtype=torch.float64)
+        _check(load_library().kpp_get_rht_matrix(self.handle, _ptr(out)), self.handle)
+        return out
 
     def destroy(self):
         if self._h:

@@ -89,6 +89,12 @@ struct kpp_ctx {
   int pC = 1, pgrid = 0;                 // persistent kernel: cluster size, grid
   IterParams pplan{};
   size_t psmem = 0;
+  // randomized Hadamard preprocessing (kpp_enable_rht): the context solves the transformed system
+  int rht = 0;
+  long long m_user = 0, n_user = 0;   // the caller's dimensions (== m, n without RHT)
+  double* rht_A = nullptr;            // owned transformed matrix
+  double* rht_d = nullptr;            // D's diagonal d_i / sqrt(m2)
+  double* rht_v = nullptr;            // vector workspace (m2 or n2)
   // CD++ streaming kernel with the re-associated residual
   int cs_ok = 0, cs_C = 0, cs_grid = 0;
   IterParams cs_plan{};
@@ -670,8 +676,8 @@ kpp_status setup_common(kpp_ctx* ctx) {
   CKS(dalloc(ctx, &ctx->d_ll, ctx->ll_bytes / sizeof(unsigned long long)));
   CKS(dalloc(ctx, &ctx->d_err, 1));
   CK(cudaMemset(ctx->d_err, 0, sizeof(int)));
-  CK(cudaEventCreate(&ctx->ev0));
-  CK(cudaEventCreate(&ctx->ev1));
+  if (!ctx->ev0) CK(cudaEventCreate(&ctx->ev0));
+  if (!ctx->ev1) CK(cudaEventCreate(&ctx->ev1));
   ctx->stats.grid_ctas = ctx->pgrid;
   return KPP_OK;
 }
@@ -732,6 +738,8 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     return KPP_EINVAL;
   cudaStream_t st = ctx->stream;
   const long long m = ctx->m, n = ctx->n;
+  const long long mu = ctx->rht ? ctx->m_user : m;  // the caller's b has mu values
+  const long long nu = ctx->rht ? ctx->n_user : n;  // ... and x0 / x_out nu
   ctx->stats.n_fresh_last = 0;
   ctx->stats.iter_launches = 0;
   ctx->stats.kernel_launches = 0;
@@ -740,11 +748,23 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   // inputs: b (m, replicated), x0 (n local)
   const double* b_dev = b;
   if (!is_device_ptr(b)) {
-    CK(cudaMemcpyAsync(ctx->bstage, b, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->bstage, b, (size_t)mu * sizeof(double), cudaMemcpyHostToDevice, st));
+    b_dev = ctx->bstage;
+  }
+  if (ctx->rht) {
+    // b~ = H D [b; 0] (Alg 5 l.3 / Alg 3 l.3) into rht_v, then used as the system's b
+    launch_fht_rows(st, b_dev, 1, mu, 1, ctx->rht_v, 1, m, 1, ctx->rht_d, nullptr, 0);
+    CK(cudaMemcpyAsync(ctx->bstage, ctx->rht_v, (size_t)m * sizeof(double), cudaMemcpyDeviceToDevice, st));
     b_dev = ctx->bstage;
   }
   if (x0) {
-    CK(cudaMemcpyAsync(ctx->x, x0, (size_t)n * sizeof(double), cudaMemcpyDefault, st));
+    if (ctx->rht && ctx->kind == KIND_CDPP) {
+      // x~0 = Q x0 = H D [x0; 0]
+      CK(cudaMemcpyAsync(ctx->rht_v, x0, (size_t)nu * sizeof(double), cudaMemcpyDefault, st));
+      launch_fht_rows(st, ctx->rht_v, 1, nu, 1, ctx->x, 1, n, 1, ctx->rht_d, nullptr, 0);
+    } else {
+      CK(cudaMemcpyAsync(ctx->x, x0, (size_t)n * sizeof(double), cudaMemcpyDefault, st));
+    }
   } else {
     CK(cudaMemsetAsync(ctx->x, 0, (size_t)n * sizeof(double), st));
   }
@@ -868,7 +888,14 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   ctx->stats.iter_kernel_ms += p2ms;
   ctx->stats.n_blocks = ctx->nb_ready;
   // outputs
-  CK(cudaMemcpyAsync(x_out, ctx->x, (size_t)n * sizeof(double), cudaMemcpyDefault, st));
+  if (ctx->rht && ctx->kind == KIND_CDPP) {
+    // back-rotation (Alg 3 l.16): x = D H x~, the first n of n2 entries
+    launch_fht_rows(st, ctx->x, 1, n, 1, ctx->rht_v, 1, n, 1, nullptr, nullptr, 0);
+    launch_scale(st, ctx->rht_v, ctx->rht_d, nu, ctx->rht_v);
+    CK(cudaMemcpyAsync(x_out, ctx->rht_v, (size_t)nu * sizeof(double), cudaMemcpyDefault, st));
+  } else {
+    CK(cudaMemcpyAsync(x_out, ctx->x, (size_t)n * sizeof(double), cudaMemcpyDefault, st));
+  }
   const long long nh = fin.nh;
   const long long keep = std::min(nh, ctx->hist_capd);
   ctx->rho_hist.assign((size_t)keep, 0.0);
@@ -1022,7 +1049,7 @@ void kpp_destroy(kpp_ctx* ctx) {
   if (!ctx) return;
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  void* ptrs[] = {ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
+  void* ptrs[] = {ctx->rht_A, ctx->rht_d, ctx->rht_v, ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
                   ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->d_info};
   for (void* p : ptrs)
@@ -1137,6 +1164,68 @@ kpp_status kpp_get_rho_history(kpp_ctx* ctx, double* rho_hist, int64_t cap, int6
   const long long k = (long long)ctx->rho_hist.size();
   if (n) *n = k;
   if (rho_hist && cap > 0) memcpy(rho_hist, ctx->rho_hist.data(), (size_t)std::min<long long>(k, cap) * sizeof(double));
+  return KPP_OK;
+}
+
+kpp_status kpp_enable_rht(kpp_ctx* ctx) {
+  if (!ctx || ctx->nranks > 1) return KPP_EINVAL;
+  if (ctx->rht) return KPP_OK;
+  cudaStream_t st = ctx->stream;
+  auto np2 = [](long long v) { long long p = 1; while (p < v) p <<= 1; return p; };
+  ctx->m_user = ctx->m;
+  ctx->n_user = ctx->n;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  if (ctx->kind == KIND_KPP) {
+    // A~ = H D [A; 0]: m2 x n, rows mixed (Alg 5 l.2-3)
+    const long long m2 = np2(ctx->m), n = ctx->n;
+    CKS(dalloc(ctx, &ctx->rht_d, (size_t)m2));
+    CKS(dalloc(ctx, &ctx->rht_v, (size_t)m2));
+    CKS(dalloc(ctx, &ctx->rht_A, (size_t)(m2 * n)));
+    launch_rht_signs(st, ctx->seed, ctx->m, m2, ctx->rht_d);
+    launch_fht_rows(st, ctx->A, ctx->lda, ctx->m, n, ctx->rht_A, n, m2, n, ctx->rht_d, nullptr, 0);
+    ctx->m = m2;
+    ctx->lda = n;
+  } else {
+    // A~ = H D A_pad D H (Alg 3 l.2-3): row pass, transpose, row pass (both factors symmetric)
+    const long long n = ctx->n, n2 = np2(n);
+    CKS(dalloc(ctx, &ctx->rht_d, (size_t)n2));
+    CKS(dalloc(ctx, &ctx->rht_v, (size_t)n2));
+    CKS(dalloc(ctx, &ctx->rht_A, (size_t)(n2 * n2)));
+    double* tmp = nullptr;
+    CK(cudaMalloc((void**)&tmp, (size_t)(n2 * n2) * sizeof(double)));
+    launch_rht_signs(st, ctx->seed, n2, n2, ctx->rht_d);
+    launch_fht_rows(st, ctx->A, ctx->lda, n, n, tmp, n2, n2, n2, ctx->rht_d, ctx->rht_d, 1);
+    launch_transpose(st, tmp, ctx->rht_A, n2);
+    launch_fht_rows(st, ctx->rht_A, n2, n2, n2, ctx->rht_A, n2, n2, n2, nullptr, nullptr, 0);
+    CK(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+    ctx->m = ctx->n = ctx->n_global = ctx->col_end = n2;
+    ctx->lda = n2;
+  }
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CK(cudaGetLastError());
+  ctx->stats.rht_ms = ms;
+  ctx->A = ctx->rht_A;
+  ctx->rht = 1;
+  ctx->nb_gen = ctx->nb_ready = 0;  // a different matrix: drop the memo cache
+  if (ctx->gexec) {
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  return setup_common(ctx);  // derived constants, work vectors and launch plans for the new sizes
+}
+
+kpp_status kpp_get_rht_matrix(kpp_ctx* ctx, double* out) {
+  if (!ctx || !out || !ctx->rht) return KPP_EINVAL;
+  CK(cudaMemcpy(out, ctx->rht_A, (size_t)(ctx->m * ctx->n) * sizeof(double), cudaMemcpyDeviceToHost));
   return KPP_OK;
 }
 

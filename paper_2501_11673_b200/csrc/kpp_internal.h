@@ -141,6 +141,17 @@ size_t cdpp_stream_smem_bytes(const IterParams& p, int C);
 cudaError_t launch_cdpp_stream(cudaStream_t st, const IterParams& p, int grid, int C, size_t smem);
 int cdpp_stream_max_clusters(const IterParams& p, int C, size_t smem);
 
+// ------------------------------------------------------------------ rht.cu (NEXT-1 preprocessing)
+// dvec[i] = d_i / sqrt(m2) for i < m (Rademacher signs of the Philox stream 3), 0 beyond
+void launch_rht_signs(cudaStream_t st, uint64_t seed, long long m, long long m2, double* dvec);
+// dst (m2 x n, ld ldd) = H_m2 (diag(rowscale) src [diag(colscale)]) along rows; src is m_src x n_src
+// (ld lds), zero beyond (or rowscale_i colscale_i on the padded diagonal when pad_diag)
+void launch_fht_rows(cudaStream_t st, const double* src, long long lds, long long m_src, long long n_src,
+                     double* dst, long long ldd, long long m2, long long n, const double* rowscale,
+                     const double* colscale, int pad_diag);
+void launch_transpose(cudaStream_t st, const double* src, double* dst, long long n);
+void launch_scale(cudaStream_t st, const double* v, const double* dvec, long long n, double* out);
+
 // ------------------------------------------------------------------ steps.cu (engine "graph")
 // Iteration cursor of the step kernels (device memory), so a captured graph is reusable.
 struct DevStep {

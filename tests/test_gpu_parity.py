@@ -409,3 +409,47 @@ def test_dist_path_single_rank(kpp, ora, cfg):
     assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
     assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
     ctx.destroy()
+
+
+# ----------------------------------------------------------------- RHT preprocessing (NEXT-1)
+RHT_CASES = [synth.twin("c3", 1024, 128, 32, k=8), synth.twin("c3", 1000, 100, 25, k=6),
+             synth.twin("c5", 512, 512, 64, k=16), synth.twin("c5", 300, 300, 37, k=10)]
+
+
+@pytest.mark.parametrize("cfg", RHT_CASES, ids=[c.name for c in RHT_CASES])
+def test_rht_transform_parity(kpp, ora, cfg):
+    """The transformed matrix (H D A or H D A_pad D H) element by element against the oracle."""
+    A, b, _ = synth.make_problem(cfg)
+    if cfg.kind == "cdpp":
+        ctx = kpp.cdpp_setup(A.to(DEV), cfg.s, cfg.lam, 11)
+        ref, _ = ora.rht_sym(A.numpy(), b.numpy(), 11)
+    else:
+        ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 11)
+        ref, _ = ora.rht_rows(A.numpy(), b.numpy(), 11)
+    ctx.enable_rht()
+    got = ctx.rht_matrix().numpy()
+    assert got.shape == ref.shape
+    assert np.allclose(got, ref, rtol=0, atol=1e-13 * np.abs(ref).max() * np.log2(ref.shape[0]))
+
+
+@pytest.mark.parametrize("cfg", RHT_CASES, ids=[c.name for c in RHT_CASES])
+def test_rht_solve_parity(kpp, ora, cfg):
+    """Alg 5 / Alg 3 with their preprocessing lines (and CD++'s back-rotation): GPU vs oracle."""
+    A, b, _ = synth.make_problem(cfg)
+    T = 300
+    if cfg.kind == "cdpp":
+        ctx = kpp.cdpp_setup(A.to(DEV), cfg.s, cfg.lam, 4)
+        ref = ora.cdpp_run_rht(A.numpy(), b.numpy(), cfg.s, seed=4, lam=cfg.lam, max_iters=T, threads=8)
+    else:
+        ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 4)
+        ref = ora.kpp_run_rht(A.numpy(), b.numpy(), cfg.s, seed=4, lam=cfg.lam, max_iters=T, threads=8)
+    ctx.enable_rht()
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    assert res.x.shape[0] == A.shape[1]
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    if cfg.kind == "cdpp":  # x0 goes through Q
+        x0 = np.random.default_rng(2).standard_normal(A.shape[1])
+        ref0 = ora.cdpp_run_rht(A.numpy(), b.numpy(), cfg.s, seed=4, lam=cfg.lam, max_iters=50, x0=x0, threads=8)
+        res0 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=50)
+        assert rel(res0.x.cpu().numpy(), ref0.x) <= 1e-10

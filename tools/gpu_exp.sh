@@ -1,3 +1,2 @@
-KPP_P1_PROFILE=1 timeout 300 python tools/prof_iter.py --config c5 --iters 256 --reps 1 > gpurun_out/exp.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q -k "factor or twin or cdpp or dist or adaptive" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/exp.log; tail -2 gpurun_out/pytest_gpu.log >> gpurun_out/exp.log
-for c in c5 c2; do timeout 600 python bench.py --config $c --steps 3 --warmup 2 --no-cpu --no-ttt > gpurun_out/bench_$c.json 2>gpurun_out/bench_$c.err; done
+for c in c3 c4 c5; do timeout 600 python tools/prof_iter.py --config $c --iters 512 --reps 1 --rht; done > gpurun_out/exp.log 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:fht_rows_pass -c 2 -f -o gpurun_out/fht_c3 python tools/prof_iter.py --config c3 --iters 16 --reps 1 --rht > gpurun_out/ncu_fht.log 2>&1

@@ -17,6 +17,7 @@ ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--cluster", type=int, default=0)
 ap.add_argument("--ygl", type=int, default=-1)
 ap.add_argument("--reassoc", type=int, default=1)
+ap.add_argument("--rht", action="store_true")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 A, b, _ = synth.make_problem(cfg, device="cuda")
@@ -26,6 +27,12 @@ ctx.set_option(kpp.OPT_CLUSTER, a.cluster)
 ctx.set_option(kpp.OPT_YGL, a.ygl)
 if cfg.kind == 'cdpp':
     ctx.set_option(kpp.OPT_REASSOC, a.reassoc)
+if a.rht:
+    ctx.enable_rht()
+    torch.cuda.synchronize()
+    st0 = ctx.stats()
+    mb = A.numel() * 8 / 1e6
+    print(f"{a.config}: RHT preprocessing {st0['rht_ms']:.2f} ms  (matrix {mb:.0f} MB)", flush=True)
 ctx.set_option(kpp.OPT_WINDOW, a.iters)
 ctx.prepare(a.iters)
 for _ in range(a.reps):
