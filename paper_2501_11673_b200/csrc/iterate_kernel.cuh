@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   const unsigned m_bytes = stageM ? (unsigned)(R * s) * 8u : 0u;
   const unsigned m_bytes_slab = m2 ? 0u : m_bytes;  // part of the per-buffer barrier's byte count
   // warps that issue the prefetch (the others do the slice-owner work in the same window)
-  const int own_warps = (R + 31) / 32;
+  // (at most half the warps: the others must remain to issue the prefetch of block t+1)
+  const int own_warps = min((R + 31) / 32, NW2 / 2);
   const int pf_tid = tid - 32 * own_warps;
   const int pf_n = T2 - 32 * own_warps;
 

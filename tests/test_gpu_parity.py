@@ -453,3 +453,23 @@ def test_rht_solve_parity(kpp, ora, cfg):
         ref0 = ora.cdpp_run_rht(A.numpy(), b.numpy(), cfg.s, seed=4, lam=cfg.lam, max_iters=50, x0=x0, threads=8)
         res0 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=50)
         assert rel(res0.x.cpu().numpy(), ref0.x) <= 1e-10
+
+
+MAX_CASES = [synth.twin("c3", 2048, 1100, 1024, k=8), synth.twin("c4", 1030, 3000, 1023, k=8),
+             synth.twin("c5", 1100, 1100, 1024, k=16), synth.twin("c5", 1100, 1100, 1023, k=16)]
+
+
+@pytest.mark.parametrize("cfg", MAX_CASES, ids=[c.name for c in MAX_CASES])
+def test_max_block_size(kpp, ora, cfg):
+    """The largest block the ABI accepts (s = 1024) and an odd neighbour (1023): blocked and one-CTA
+    factorisations, slices of a whole CTA's row range in the exchange."""
+    A, b, _ = synth.make_problem(cfg)
+    T = 40
+    if cfg.kind == "cdpp":
+        ctx = kpp.cdpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+        ref = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8)
+    else:
+        ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+        ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
