@@ -72,14 +72,20 @@ __host__ __device__ inline Smem cs_layout(int s, int slab, int C) {
 // Stream rows of A[S, c0:c0+w] against zv (warps 0..NSW-1): out[k] = sum_j A[S_k, c0+j] zv[j]
 // (fixed order: lane-strided 16-byte chunks, then a butterfly); columns with cmap[j] >= 0 are
 // copied to stash[k][cmap[j]].
-template <int NSW>
+// Row pairs are taken dynamically from *ctr (shared memory), so warps that join late (the chain
+// warps, once the chain of the slot is done) take a share; each row's dot product is computed by
+// one warp in a fixed order, so the result does not depend on which warp takes it.
 __device__ __forceinline__ void stream_pass(const IterParams& p, const int32_t* S, long long c0, int w,
                                             const double* zv, double* out, const int* cmap, double* stash,
-                                            bool vec) {
+                                            bool vec, int* ctr) {
   const int s = p.s;
-  const int lane = threadIdx.x & 31, swarp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   constexpr int UR = 2, UQ = 8;  // a whole 444-column row segment per round: 16 loads in flight per lane
-  for (int kbase = swarp * UR; kbase < s; kbase += NSW * UR) {
+  for (;;) {
+    int kbase = 0;
+    if (lane == 0) kbase = atomicAdd(ctr, UR);
+    kbase = __shfl_sync(0xffffffffu, kbase, 0);
+    if (kbase >= s) break;
     double acc[UR] = {0.0, 0.0};
     const double* rows[UR];
 #pragma unroll
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   int* lkb = I + L.lk;
   int32_t* S_sh = I + L.S;
   __shared__ DevState st;
-  __shared__ int stop_sh, nl_sh[3];
+  __shared__ int stop_sh, nl_sh[3], row_ctr;
   __shared__ long long tmod_sh;
 
   const long long c0 = (long long)blockIdx.x * p.slab;
@@ -275,9 +281,10 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
     const int n = build_list(S_sh, s, gc0, gc1, ljb, lkb, cmap[0], lane);
     if (lane == 0) nl_sh[0] = n;
   }
+  if (tid == 0) row_ctr = 0;
   cluster.sync();
   // prologue: D_{t0} = A_{S_{t0}} x_{t0} (no correction: nothing was applied before t0 here)
-  if (warp < NSW) stream_pass<NSW>(p, S_sh, c0, w, x_sm, dbuf[0], nullptr, stash[0], vec);
+  stream_pass(p, S_sh, c0, w, x_sm, dbuf[0], nullptr, stash[0], vec, &row_ctr);
   __syncthreads();
 
   const unsigned la_rp = smem_u32(rp_sm), la_r = smem_u32(r_sm);
@@ -318,6 +325,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
     if (tid == 0) {
       if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
       mbar_expect_tx(bars + 3, (unsigned)s * 8u);
+      row_ctr = 0;  // read only after the phase-A barrier
     }
     // ---- phase A (all threads)
     // A1: x_t, m_t from w_{t-1} = I_{S_{t-1}}^T y_{t-1} (cmap[prv] holds S_{t-1}'s positions), z_t
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
 
     if (warp < NSW) {
       // ---- B (streaming warps): D_{t+1} = A[S_{t+1}, slab] z_t, stash A[S_{t+1}, S_t in slab]
-      if (pf) stream_pass<NSW>(p, Sn, c0, w, z_sm, dbuf[prv], cmap[cur], stash[prv], vec);
+      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf[prv], cmap[cur], stash[prv], vec, &row_ctr);
       CS_MARK(1);  // stream (thread 0)
     } else {
       // ---- B (chain threads): exchange, window logic and projection of iteration t
@@ -433,6 +441,8 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
       // y_t from every CTA's rows
       ll_gather_vec<4>(y_sm, p.yll + (long long)(it & 1) * s * 2, s, tag, p.err, ct, NCH);
       CS_MARK(5);  // y gathered
+      // the chain of t is done: help stream D_{t+1}
+      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf[prv], cmap[cur], stash[prv], vec, &row_ctr);
     }
     __syncthreads();
     CS_MARK(6);  // end-of-slot barrier wait
