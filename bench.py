@@ -159,6 +159,15 @@ def cpu_oracle_sample(cfg, A_host, b_host, seconds):
                       f"factors included), {threads} OpenMP threads over independent outputs, {dt:.1f} s"}
 
 
+def workload_config(cfg, iters, world, dist):
+    """The `config` object of the JSON line (shared by both arms)."""
+    return {"workload": f"{cfg.name}: {'CD++' if cfg.kind == 'cdpp' else 'Kaczmarz++'} "
+                        f"m={cfg.m} n={cfg.n} s={cfg.s} lam={cfg.lam:g}",
+            "iters_per_step": iters, "step": "cold solve (memo cache cleared)",
+            "parallelism": f"column-sharded x{world}" if dist else "1 GPU",
+            "l2": f"inputs larger than L2 (A = {cfg.m * cfg.n * 8 / 2**20:.0f} MiB)"}
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -166,19 +175,22 @@ def run_reference(args, cfg):
     A, b, _ = synth.make_problem(cfg, seed=0, device="cuda" if torch.cuda.is_available() else "cpu")
     A_host, b_host = A.cpu().numpy(), b.cpu().numpy()
     del A, b
-    per_step = []
+    per_step, step_ms = [], []
     cb = None
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         r = cpu_oracle_sample(cfg, A_host, b_host, args.cpu_seconds / max(1, args.steps))
         if i >= args.warmup:
             per_step.append(r["value"])
+            step_ms.append((time.perf_counter() - t0) * 1e3)
             cb = r
     v = float(np.median(per_step))
     cb["value"] = v
+    iters = args.iters or DEFAULT_ITERS[cfg.name]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(step_ms)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": cfg.name},
+            "data": "synthetic", "config": workload_config(cfg, iters, 1, False),
             "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -342,11 +354,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {'CD++' if cfg.kind == 'cdpp' else 'Kaczmarz++'} "
-                               f"m={cfg.m} n={cfg.n} s={cfg.s} lam={cfg.lam:g}",
-                   "iters_per_step": iters, "step": "cold solve (memo cache cleared)",
-                   "parallelism": f"column-sharded x{world}" if dist else "1 GPU",
-                   "l2": f"inputs larger than L2 (A = {cfg.m * cfg.n * 8 / 2**20:.0f} MiB)"},
+        "config": workload_config(cfg, iters, world, dist),
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
