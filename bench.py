@@ -137,6 +137,20 @@ def ncu_traffic(cfg_name):
         return None
 
 
+FP64_DGEMM_TFLOPS = 35.47  # measured: torch.matmul fp64 8192^3, best of 10 (profiles/r01/fp64_peak.txt)
+
+
+def phase1_flops(cfg, n_blocks, n_refined):
+    """Algorithmic flops of Phase 1: per fresh block Gram s(s+1)n (K++) plus
+    Cholesky, triangular inverse and M = X X^T (s^3/3 each); per refined block (second CholeskyQR
+    pass) Q1 = X1^T A_S (s^2 n, X1 triangular), Gram s(s+1)n and the s x s products (~5 s^3/3)."""
+    s, n = cfg.s, cfg.n
+    small = s ** 3
+    if cfg.kind == "cdpp":
+        return n_blocks * small
+    return n_blocks * (s * (s + 1) * n + small) + n_refined * (s * s * n + s * (s + 1) * n + 5 * small / 3)
+
+
 def cpu_oracle_sample(cfg, A_host, b_host, seconds):
     """Time the oracle, as it stands, on the host cores: iterations 0..T-1 of the same cold
     solve, T grown until the call takes about `seconds`."""
@@ -367,6 +381,13 @@ def main():
         "time_to_tol": ttt,
         "n_blocks_per_step": warm["n_blocks"],
         "n_refined_per_step": st.get("n_refined", 0) // max(1, args.steps),
+        "phase1_fp64": (lambda fl, ms1: {"gflop_per_step": fl / 1e9,
+                                          "tflops": fl / (ms1 / 1e3) / 1e12 if ms1 > 0 else None,
+                                          "peak_tflops": FP64_DGEMM_TFLOPS,
+                                          "frac": fl / (ms1 / 1e3) / 1e12 / FP64_DGEMM_TFLOPS if ms1 > 0 else None,
+                                          "peak_source": "measured fp64 DGEMM (cuBLAS, DMMA 8x8x4)"})(
+            phase1_flops(cfg, warm["n_blocks"], st.get("n_refined", 0) // max(1, args.steps)),
+            st["phase1_ms"] / args.steps),
         "rht_preprocess_ms": rht_ms,
     }
     print(json.dumps(line), flush=True)
