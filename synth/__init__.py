@@ -136,3 +136,31 @@ def make_vector(n: int, seed: int, device="cpu"):
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     return torch.randn((n,), generator=g, dtype=torch.float64, device=device)
+
+
+# ---------------------------------------------------------------- bell-spectrum systems (NEXT-3)
+def bell_profile(k: int, effective_rank: int, tail_strength: float = 0.01) -> torch.Tensor:
+    """Singular value profile of the paper's synthetic low-rank matrices (App F):
+    sigma_i = (1 - ts) exp(-(i/er)^2) + ts exp(-0.1 i/er), i = 0, 1, ...  The paper prints the tail
+    as ts*exp(i/er) (growing); we take the decaying form of the cited generator."""
+    i = torch.arange(k, dtype=torch.float64)
+    return (1.0 - tail_strength) * torch.exp(-(i / effective_rank) ** 2) + tail_strength * torch.exp(-0.1 * i / effective_rank)
+
+
+@torch.no_grad()
+def make_bell_psd(n: int = 4096, effective_rank: int = 25, tail_strength: float = 0.01, phi: float = 1e-3,
+                  seed: int = 0, device="cpu"):
+    """CD++ test system of App F: A = Phi Phi^T + phi I with Phi = U diag(sigma) V^T,
+    U, V Haar-random orthogonal (QR of Gaussians, signs fixed by diag(R)), so A = U diag(sigma^2) U^T
+    + phi I; b ~ N(0, I).  Symmetrised bitwise.  Returns (A, b)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    G = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
+    Q, R = torch.linalg.qr(G)
+    Q = Q * torch.sign(torch.diagonal(R))
+    sig = bell_profile(n, effective_rank, tail_strength).to(device)
+    A = (Q * sig ** 2) @ Q.T
+    A = 0.5 * (A + A.T)
+    A.diagonal().add_(phi)
+    b = torch.randn((n,), generator=g, dtype=torch.float64, device=device)
+    return A, b

@@ -11,6 +11,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 import synth
 
@@ -527,3 +528,17 @@ def test_cdpp_rht_converges(ora):
     An, bn = A.numpy(), b.numpy()
     r = ora.cdpp_run_rht(An, bn, 32, seed=1, max_iters=20000, tol=1e-11)
     assert np.linalg.norm(An @ r.x - bn) / np.linalg.norm(bn) < 1e-8
+
+
+def test_bell_spectrum_generator():
+    """NEXT-3 workload: sigma_0 = 1 at er=25, ts=0.01 (SPEC S:229 example); A = Phi Phi^T + phi I has
+    eigenvalues sigma_i^2 + phi; bitwise symmetric."""
+    prof = synth.bell_profile(64, 25, 0.01)
+    assert abs(float(prof[0]) - 1.0) < 1e-15
+    assert bool(torch.all(prof[1:] < prof[:-1]))
+    A, b = synth.make_bell_psd(64, 8, seed=3)
+    A = A.numpy()
+    assert np.array_equal(A, A.T)
+    ev = np.sort(np.linalg.eigvalsh(A))[::-1]
+    want = np.sort(synth.bell_profile(64, 8).numpy() ** 2 + 1e-3)[::-1]
+    assert np.allclose(ev, want, rtol=0, atol=1e-12)
