@@ -40,7 +40,8 @@ class _Opts(ctypes.Structure):
     _fields_ = [("accel", ctypes.c_int32), ("memo", ctypes.c_int32),
                 ("eta_override", ctypes.c_double), ("rho_fixed", ctypes.c_double),
                 ("factor", ctypes.c_int32), ("reverse", ctypes.c_int32),
-                ("threads", ctypes.c_int32)]
+                ("threads", ctypes.c_int32), ("proj", ctypes.c_int32), ("tmax", ctypes.c_int32),
+                ("tau", ctypes.c_int32)]
 
 
 _lib = None
@@ -69,6 +70,9 @@ def lib():
         L.ora_cdpp_run.argtypes = [P, i64, i64, P, P, i32, f64, u64, i64, f64,
                                    ctypes.POINTER(_Opts), P, P, P, i64, P, P, P]
         L.ora_rho_update.argtypes = [i64, f64, f64, f64, i64, P, P]
+        L.ora_srht.argtypes = [u64, i64, i32, P, P]
+        L.ora_sketch_factor.argtypes = [P, i64, i64, P, i32, f64, u64, i32, P]
+        L.ora_lsqr_proj.argtypes = [P, i64, i64, P, i32, f64, P, P, i32, P]
         L.ora_next_pow2.argtypes = [i64]
         L.ora_next_pow2.restype = i64
         L.ora_rht_signs.argtypes = [u64, i64, P]
@@ -157,7 +161,7 @@ class Result:
 
 
 def _run(cd, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed, factor,
-         reverse, threads, hist_cap):
+         reverse, threads, hist_cap, proj=0, tmax=8, tau=0):
     A = _f64(A)
     b = _f64(b)
     n = A.shape[1]
@@ -172,7 +176,7 @@ def _run(cd, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed
     nh, it, nf = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     o = _Opts(int(accel), int(memo), -1.0 if eta is None else float(eta),
               -1.0 if rho_fixed is None else float(rho_fixed), int(factor), int(reverse),
-              int(threads))
+              int(threads), int(proj), int(tmax), int(tau))
     if cd:
         rc = lib().ora_cdpp_run(_p(A), n, n, _p(b), x0p, s, lam, seed, max_iters, tol,
                                 ctypes.byref(o), _p(x), _p(hr), _p(hp), hist_cap,
@@ -187,10 +191,11 @@ def _run(cd, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed
 
 def kpp_run(A, b, s, lam=1e-8, seed=0, max_iters=100, tol=0.0, x0=None, accel=True, memo=True,
             eta=None, rho_fixed=None, factor=HOUSEHOLDER, reverse=False, threads=1,
-            hist_cap=1 << 16) -> Result:
-    """Kaczmarz++ (Alg 5 with exact projections) -- see kpp_oracle.h."""
+            hist_cap=1 << 16, proj=0, tmax=8, tau=0) -> Result:
+    """Kaczmarz++ (Alg 5; proj=0 exact projections (K++(Cholesky)), proj=1 sketch + LSQR, Alg 6)
+    -- see kpp_oracle.h."""
     return _run(False, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed,
-                factor, reverse, threads, hist_cap)
+                factor, reverse, threads, hist_cap, proj, tmax, tau)
 
 
 def cdpp_run(A, b, s, lam=1e-8, seed=0, max_iters=100, tol=0.0, x0=None, accel=True, memo=True,
@@ -262,3 +267,32 @@ def cdpp_run_rht(A, b, s, seed=0, x0=None, **kw) -> Result:
     r = cdpp_run(At, bt, s, seed=seed, x0=xt0, **kw)
     r.x = rht_vec(r.x, n, n2, seed, False)
     return r
+
+
+# ---------------------------------------------------------------- sketch + LSQR (NEXT-2)
+def srht(seed: int, n: int, tau: int):
+    n2 = next_pow2(n)
+    d = np.zeros(n2)
+    T = np.zeros(tau, dtype=np.int32)
+    lib().ora_srht(seed, n, tau, _p(d), _p(T))
+    return d, T
+
+
+def sketch_factor(A, S, lam, seed, tau):
+    A = _f64(A)
+    S = np.ascontiguousarray(S, dtype=np.int32)
+    s = S.shape[0]
+    R = np.zeros((s, s))
+    rc = lib().ora_sketch_factor(_p(A), A.shape[1], A.shape[1], _p(S), s, lam, seed, tau, _p(R))
+    if rc != OK:
+        raise RuntimeError(f"sketch factor failed: {rc}")
+    return R
+
+
+def lsqr_proj(A, S, lam, R, r, tmax):
+    A = _f64(A)
+    S = np.ascontiguousarray(S, dtype=np.int32)
+    w = np.zeros(A.shape[1])
+    lib().ora_lsqr_proj(_p(A), A.shape[1], A.shape[1], _p(S), S.shape[0], lam, _p(_f64(R)), _p(_f64(r)),
+                        tmax, _p(w))
+    return w

@@ -247,12 +247,182 @@ struct Block {
   std::vector<double> R;
 };
 
+// ---------------------------------------------------------------- sketch + LSQR (NEXT-2)
+int64_t next_pow2_(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+void fht_inplace(double* v, int64_t n) {  // Sylvester order, half-sizes 1, 2, 4, ... (Def E.1)
+  for (int64_t h = 1; h < n; h <<= 1)
+    for (int64_t i0 = 0; i0 < n; i0 += 2 * h)
+      for (int64_t i = i0; i < i0 + h; ++i) {
+        const double a = v[i], b = v[i + h];
+        v[i] = a + b;
+        v[i + h] = a - b;
+      }
+}
+
+// SRHT parameters (reading R5): d_j = +-1 (stream 4: word (j mod 4) of counter (lo32(j/4),
+// hi32(j/4), 4, 0), lowest bit), T = sorted first tau entries of a partial Fisher-Yates shuffle of
+// [0, n2) drawing word (i mod 4) of counter (i/4, 0, 5, 0).
+void srht_params(uint64_t seed, int64_t n2, int32_t tau, std::vector<double>& d, std::vector<int32_t>& T) {
+  uint32_t key[2];
+  seed_key(seed, key);
+  d.assign((size_t)n2, 0.0);
+  for (int64_t j = 0; j < n2; ++j) {
+    const uint64_t c = (uint64_t)j >> 2;
+    uint32_t ctr[4] = {(uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 4u, 0u}, w[4];
+    philox(ctr, key, w);
+    d[(size_t)j] = (w[j & 3] & 1u) ? -1.0 : 1.0;
+  }
+  std::vector<int32_t> perm((size_t)n2);
+  for (int64_t i = 0; i < n2; ++i) perm[(size_t)i] = (int32_t)i;
+  uint32_t w[4] = {0, 0, 0, 0};
+  for (int32_t i = 0; i < tau; ++i) {
+    if (i % 4 == 0) {
+      uint32_t ctr[4] = {(uint32_t)(i / 4), 0u, 5u, 0u};
+      philox(ctr, key, w);
+    }
+    const int64_t j = i + (int64_t)(((uint64_t)w[i % 4] * (uint64_t)(n2 - i)) >> 32);
+    std::swap(perm[(size_t)i], perm[(size_t)j]);
+  }
+  T.assign(perm.begin(), perm.begin() + tau);
+  std::sort(T.begin(), T.end());
+}
+
+// Alg 6 l.3-4: A_hat = A_S Pi^T, Pi = sqrt(n2/tau) I_T H diag(d)/sqrt(n2) = I_T H diag(d)/sqrt(tau);
+// R = chol(A_hat A_hat^T + lam I).
+int sketch_factor(const double* A, int64_t lda, int64_t n, const int32_t* S, int32_t s, double lam, uint64_t seed,
+                  int32_t tau, double* R) {
+  const int64_t n2 = next_pow2_(n);
+  std::vector<double> d;
+  std::vector<int32_t> T;
+  srht_params(seed, n2, tau, d, T);
+  std::vector<double> Ah((size_t)s * tau), v((size_t)n2);
+  const double sc = 1.0 / std::sqrt((double)tau);
+  for (int32_t k = 0; k < s; ++k) {
+    for (int64_t j = 0; j < n2; ++j) v[(size_t)j] = j < n ? d[(size_t)j] * A[(size_t)S[k] * lda + j] : 0.0;
+    fht_inplace(v.data(), n2);
+    for (int32_t q = 0; q < tau; ++q) Ah[(size_t)k * tau + q] = sc * v[(size_t)T[(size_t)q]];
+  }
+  std::vector<double> G((size_t)s * s);
+  for (int32_t k = 0; k < s; ++k)
+    for (int32_t l = 0; l < s; ++l) {
+      double a = 0.0;
+      for (int32_t q = 0; q < tau; ++q) a += Ah[(size_t)k * tau + q] * Ah[(size_t)l * tau + q];
+      G[(size_t)k * s + l] = a + ((k == l) ? lam : 0.0);
+    }
+  return cholesky_upper(G, s, false, R);
+}
+
+// z = R^{-T} v (forward substitution), z = R^{-1} v (back substitution); R upper s x s
+void solve_rt(const double* R, int32_t s, const double* v, double* z) {
+  for (int32_t k = 0; k < s; ++k) {
+    double a = v[k];
+    for (int32_t l = 0; l < k; ++l) a -= R[(size_t)l * s + k] * z[l];
+    z[k] = a / R[(size_t)k * s + k];
+  }
+}
+void solve_r(const double* R, int32_t s, const double* v, double* z) {
+  for (int32_t k = s - 1; k >= 0; --k) {
+    double a = v[k];
+    for (int32_t l = k + 1; l < s; ++l) a -= R[(size_t)k * s + l] * z[l];
+    z[k] = a / R[(size_t)k * s + k];
+  }
+}
+
+// Alg 6 l.6-8: LSQR (Paige & Saunders 1982, Algorithm LSQR) on M z = R^{-T} r with
+// M = R^{-T} [A_S, sqrt(lam) I] (implicit), z0 = 0, exactly tmax steps; returns w = z[0:n].
+// Degenerate steps (a zero beta or alpha) leave the normalised vector at 0.
+void lsqr_proj(const double* A, int64_t lda, int64_t n, const int32_t* S, int32_t s, double lam, const double* R,
+               const double* r, int32_t tmax, double* wout) {
+  const double sl = std::sqrt(lam);
+  std::vector<double> u((size_t)s), t1((size_t)s), t2((size_t)s), vn((size_t)n), vs((size_t)s),
+      xn((size_t)n, 0.0), xs((size_t)s, 0.0), wn((size_t)n), ws((size_t)s);
+  // [on; os] = M^T uu = [A_S^T R^{-1} uu; sqrt(lam) R^{-1} uu]
+  auto matvec_t = [&](const std::vector<double>& uu, std::vector<double>& on, std::vector<double>& os) {
+    solve_r(R, s, uu.data(), t1.data());
+    for (int64_t j = 0; j < n; ++j) {
+      double acc = 0.0;
+      for (int32_t k = 0; k < s; ++k) acc += A[(size_t)S[k] * lda + j] * t1[(size_t)k];
+      on[(size_t)j] = acc;
+    }
+    for (int32_t k = 0; k < s; ++k) os[(size_t)k] = sl * t1[(size_t)k];
+  };
+  // out = M [zn; zs] = R^{-T} (A_S zn + sqrt(lam) zs)
+  auto matvec = [&](const std::vector<double>& zn, const std::vector<double>& zs, std::vector<double>& out) {
+    for (int32_t k = 0; k < s; ++k) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < n; ++j) acc += A[(size_t)S[k] * lda + j] * zn[(size_t)j];
+      t2[(size_t)k] = acc + sl * zs[(size_t)k];
+    }
+    solve_rt(R, s, t2.data(), out.data());
+  };
+  auto nrm = [](const std::vector<double>& a, const std::vector<double>* b2) {
+    double q = 0.0;
+    for (double v : a) q += v * v;
+    if (b2)
+      for (double v : *b2) q += v * v;
+    return std::sqrt(q);
+  };
+  auto scale = [](std::vector<double>& a, double d) {
+    for (double& v : a) v = d > 0.0 ? v / d : 0.0;
+  };
+  // beta_1 u_1 = b,  alpha_1 v_1 = M^T u_1,  w_1 = v_1,  phibar_1 = beta_1,  rhobar_1 = alpha_1
+  std::vector<double> rr(r, r + s);
+  solve_rt(R, s, rr.data(), u.data());
+  double beta = nrm(u, nullptr);
+  scale(u, beta);
+  matvec_t(u, vn, vs);
+  double alpha = nrm(vn, &vs);
+  scale(vn, alpha);
+  scale(vs, alpha);
+  wn = vn;
+  ws = vs;
+  double phibar = beta, rhobar = alpha;
+  std::vector<double> mv((size_t)s), qn((size_t)n), qs((size_t)s);
+  for (int32_t it = 0; it < tmax; ++it) {
+    // beta u = M v - alpha u
+    matvec(vn, vs, mv);
+    for (int32_t k = 0; k < s; ++k) u[(size_t)k] = mv[(size_t)k] - alpha * u[(size_t)k];
+    beta = nrm(u, nullptr);
+    scale(u, beta);
+    // alpha v = M^T u - beta v
+    matvec_t(u, qn, qs);
+    for (int64_t j = 0; j < n; ++j) vn[(size_t)j] = qn[(size_t)j] - beta * vn[(size_t)j];
+    for (int32_t k = 0; k < s; ++k) vs[(size_t)k] = qs[(size_t)k] - beta * vs[(size_t)k];
+    alpha = nrm(vn, &vs);
+    scale(vn, alpha);
+    scale(vs, alpha);
+    // plane rotation
+    const double rho = std::sqrt(rhobar * rhobar + beta * beta);
+    const double c = rho > 0.0 ? rhobar / rho : 1.0, sn = rho > 0.0 ? beta / rho : 0.0;
+    const double theta = sn * alpha;
+    rhobar = -c * alpha;
+    const double phi = c * phibar;
+    phibar = sn * phibar;
+    // x = x + (phi/rho) w;  w = v - (theta/rho) w
+    const double f1 = rho > 0.0 ? phi / rho : 0.0, f2 = rho > 0.0 ? theta / rho : 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      xn[(size_t)j] += f1 * wn[(size_t)j];
+      wn[(size_t)j] = vn[(size_t)j] - f2 * wn[(size_t)j];
+    }
+    for (int32_t k = 0; k < s; ++k) {
+      xs[(size_t)k] += f1 * ws[(size_t)k];
+      ws[(size_t)k] = vs[(size_t)k] - f2 * ws[(size_t)k];
+    }
+  }
+  for (int64_t j = 0; j < n; ++j) wout[j] = xn[(size_t)j];
+}
+
 // The shared outer loop of Alg 5 / Alg 3 (lines 5-18).  `cd` selects CD++.
 int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
         const double* x0, int32_t s, double lam, uint64_t seed, int64_t max_iters, double tol,
         const ora_opts* opt_in, double* x_out, double* hist_res, double* hist_rho,
         int64_t hist_cap, int64_t* n_hist, int64_t* iters_out, int64_t* nfresh_out) {
-  ora_opts opt = {1, 1, -1.0, -1.0, ORA_FACTOR_HOUSEHOLDER, 0, 1};
+  ora_opts opt = {1, 1, -1.0, -1.0, ORA_FACTOR_HOUSEHOLDER, 0, 1, 0, 8, 0};
   if (opt_in) opt = *opt_in;
   const int64_t pop = cd ? n : m;  // sampling population: rows (K++) or coordinates (CD++)
   if (s < 1 || s > pop || lam < 0.0 || tol < 0.0 || max_iters < 0 || lda < n) return ORA_EINVAL;
@@ -288,8 +458,12 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
       nbk.R.resize((size_t)s * s);
       fresh_block(seed, pop, s, opt.memo ? nfresh : t, nbk.S.data());
       int rc;
+      const bool lsqr = !cd && opt.proj == 1;
+      const int32_t tau = opt.tau > 0 ? opt.tau : 2 * s;
       if (cd)
         rc = cdpp_factor(A, lda, nbk.S.data(), s, lam, par, nbk.R.data());
+      else if (lsqr)
+        rc = sketch_factor(A, lda, n, nbk.S.data(), s, lam, seed, tau, nbk.R.data());  // Alg 6 l.2-5
       else if (opt.factor == ORA_FACTOR_GRAM)
         rc = gram_factor(A, lda, n, nbk.S.data(), s, lam, par, nbk.R.data());
       else
@@ -319,9 +493,16 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
       r[(size_t)k] = a - b[S[k]];
     }
     // line 10 / 11: y = (A_S A_S^T + lam I)^{-1} r (K++) or (A_SS + lam I)^{-1} r (CD++)
-    chol_solve(blk->R.data(), s, r.data(), par.rev, y.data());
+    if (!cd && opt.proj == 1) {
+      // Alg 5 l.10 with Proj = Alg 6: w_t from tmax LSQR steps on the preconditioned system
+      lsqr_proj(A, lda, n, S, s, lam, blk->R.data(), r.data(), opt.tmax, w.data());
+    } else {
+      chol_solve(blk->R.data(), s, r.data(), par.rev, y.data());
+    }
     // w_t = A_S^T y (K++, Eq (bk)) or I_S^T y (CD++, Alg 3 l.11)
-    if (cd) {
+    if (!cd && opt.proj == 1) {
+      // w already holds the LSQR solution
+    } else if (cd) {
       std::fill(w.begin(), w.end(), 0.0);
       for (int32_t k = 0; k < s; ++k) w[(size_t)S[k]] = y[(size_t)k];
     } else {
@@ -473,6 +654,24 @@ void ora_rho_update(int64_t i, double rhat_prev, double E0, double E1, int64_t z
 }
 
 int64_t ora_next_pow2(int64_t n) { return next_pow2(n); }
+
+void ora_srht(uint64_t seed, int64_t n, int32_t tau, double* d_out, int32_t* T_out) {
+  std::vector<double> d;
+  std::vector<int32_t> T;
+  srht_params(seed, next_pow2_(n), tau, d, T);
+  for (size_t i = 0; i < d.size(); ++i) d_out[i] = d[i];
+  for (size_t i = 0; i < T.size(); ++i) T_out[i] = T[i];
+}
+
+int ora_sketch_factor(const double* A, int64_t lda, int64_t n, const int32_t* S, int32_t s, double lam,
+                      uint64_t seed, int32_t tau, double* R) {
+  return sketch_factor(A, lda, n, S, s, lam, seed, tau, R);
+}
+
+void ora_lsqr_proj(const double* A, int64_t lda, int64_t n, const int32_t* S, int32_t s, double lam,
+                   const double* R, const double* r, int32_t tmax, double* w) {
+  lsqr_proj(A, lda, n, S, s, lam, R, r, tmax, w);
+}
 
 void ora_rht_signs(uint64_t seed, int64_t n, int8_t* d) {
   for (int64_t i = 0; i < n; ++i) d[i] = (int8_t)rht_sign(seed, i);

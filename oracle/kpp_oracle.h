@@ -52,6 +52,10 @@ typedef struct {
   int32_t factor;      /* ORA_FACTOR_*; K++ only (CD++ always chol(A_SS + lam I)) */
   int32_t reverse;     /* 1: every sum runs in reverse order (noise-floor experiments) */
   int32_t threads;     /* OpenMP threads over independent outputs (<=1: sequential) */
+  int32_t proj;        /* K++ projection: 0 exact factor (K++(Cholesky)); 1 sketch-and-
+                          precondition LSQR (Alg 6) */
+  int32_t tmax;        /* LSQR iterations t_max (default 8) */
+  int32_t tau;         /* sketch size tau (<= 0: 2 s) */
 } ora_opts;
 
 /* Philox-4x32-10 (Salmon et al., SC'11): out = philox(ctr, key). */
@@ -102,6 +106,17 @@ int ora_cdpp_run(const double* A, int64_t n, int64_t lda, const double* b, const
    writes the new r_hat and rho. */
 void ora_rho_update(int64_t i, double rhat_prev, double E0, double E1, int64_t zeta,
                     double* rhat_out, double* rho_out);
+
+/* ---- sketch-and-precondition projection (NEXT-2; Alg 6, Lemma l:inner P:491-493).
+   SRHT Pi = sqrt(n2/tau) I_T H D over the column space (n padded to n2; reading R5): D from the
+   sign stream 4, T = tau indices of [0, n2) by a partial Fisher-Yates on stream 5, sorted.
+   A_hat = A_S Pi^T (s x tau); R = chol(A_hat A_hat^T + lam I). */
+void ora_srht(uint64_t seed, int64_t n, int32_t tau, double* d_out /* n2 */, int32_t* T_out /* tau */);
+int ora_sketch_factor(const double* A, int64_t lda, int64_t n, const int32_t* S, int32_t s, double lam,
+                      uint64_t seed, int32_t tau, double* R);
+/* w = first n entries of LSQR(R^{-T}[A_S, sqrt(lam) I], R^{-T} r, tmax) from zero (Paige-Saunders) */
+void ora_lsqr_proj(const double* A, int64_t lda, int64_t n, const int32_t* S, int32_t s, double lam,
+                   const double* R, const double* r, int32_t tmax, double* w);
 
 /* ---- RHT preprocessing (Def 1.1, Alg 4 P:1230-1243,
    Alg 5 l.2-3 P:1337-1338, Alg 3 l.2-3 and l.16 P:745-746).  Sign stream: reading R3;

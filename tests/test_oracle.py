@@ -542,3 +542,65 @@ def test_bell_spectrum_generator():
     ev = np.sort(np.linalg.eigvalsh(A))[::-1]
     want = np.sort(synth.bell_profile(64, 8).numpy() ** 2 + 1e-3)[::-1]
     assert np.allclose(ev, want, rtol=0, atol=1e-12)
+
+
+# ----------------------------------------------------------------- sketch + LSQR (NEXT-2)
+def test_srht_full_sketch_is_orthogonal(ora):
+    """tau = n2 (T = every index): Pi = H D/sqrt(n2) is orthogonal, so A_hat A_hat^T = A_S A_S^T."""
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((40, 64))
+    S = np.arange(0, 40, 4, dtype=np.int32)
+    R = ora.sketch_factor(A, S, 1e-8, 3, 64)
+    G = A[S] @ A[S].T + 1e-8 * np.eye(len(S))
+    assert np.allclose(R.T @ R, G, rtol=0, atol=1e-12 * np.abs(G).max())
+    d, T = ora.srht(3, 64, 64)
+    assert np.array_equal(T, np.arange(64)) and set(np.unique(d)) <= {-1.0, 1.0}
+
+
+def test_srht_subspace_embedding(ora):
+    """Lemma l:inner: the preconditioned system is well conditioned; for a Gaussian A_S
+    (d_lambda = s) the singular values of the subsampled orthogonal sketch concentrate in
+    [1 - sqrt(s/tau), 1 + sqrt(s/tau)] (Marchenko-Pastur), i.e. kappa ~ 5.8 at tau = 2s, 2.4 at 4s."""
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((256, 1000))
+    s = 32
+    S = np.sort(rng.choice(256, s, replace=False)).astype(np.int32)
+    lam = 1e-8
+    for tau in (2 * s, 4 * s):
+        R = ora.sketch_factor(A, S, lam, 5, tau)
+        Maug = np.linalg.solve(R.T, np.hstack([A[S], np.sqrt(lam) * np.eye(s)]))
+        sv = np.linalg.svd(Maug, compute_uv=False)
+        q = np.sqrt(s / tau)
+        assert sv[0] / sv[-1] < 1.5 * (1 + q) / (1 - q)
+
+
+def test_lsqr_converges_to_exact_projection(ora):
+    """Alg 6 with many LSQR steps = the exact regularised projection A_S^T (A_S A_S^T + lam I)^{-1} r;
+    8 steps are already close for tau = 2s."""
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((300, 500))
+    s = 40
+    S = np.sort(rng.choice(300, s, replace=False)).astype(np.int32)
+    lam = 1e-6
+    r = rng.standard_normal(s)
+    w_exact = A[S].T @ np.linalg.solve(A[S] @ A[S].T + lam * np.eye(s), r)
+    R = ora.sketch_factor(A, S, lam, 7, 2 * s)
+    w40 = ora.lsqr_proj(A, S, lam, R, r, 40)
+    assert np.linalg.norm(w40 - w_exact) / np.linalg.norm(w_exact) < 1e-10
+    # 8 steps at kappa ~ 5.8 (flat Gaussian spectrum, d_lambda = s): error ~ ((k-1)/(k+1))^8 ~ 6e-2
+    errs = [np.linalg.norm(ora.lsqr_proj(A, S, lam, R, r, t) - w_exact) / np.linalg.norm(w_exact)
+            for t in (2, 4, 8, 16)]
+    assert all(b2 < a2 for a2, b2 in zip(errs, errs[1:])) and errs[2] < 6e-2
+
+
+def test_kpp_lsqr_matches_exact_with_many_steps(ora):
+    """Alg 5 + Alg 6 with t_max large reproduces K++(Cholesky); with t_max = 8 it still converges."""
+    cfg = synth.twin("c3", 1024, 128, 32, k=8)
+    A, b, xs = synth.make_problem(cfg)
+    An, bn = A.numpy(), b.numpy()
+    ex = ora.kpp_run(An, bn, 32, seed=0, max_iters=150, rho_fixed=0.2)
+    ls = ora.kpp_run(An, bn, 32, seed=0, max_iters=150, rho_fixed=0.2, proj=1, tmax=60)
+    assert np.linalg.norm(ls.x - ex.x) / np.linalg.norm(ex.x) < 1e-9
+    l8 = ora.kpp_run(An, bn, 32, seed=0, max_iters=6000, proj=1, tmax=8, tol=1e-8)
+    assert l8.status == ora.OK
+    assert np.linalg.norm(l8.x - xs.numpy()) / np.linalg.norm(xs.numpy()) < 1e-6
