@@ -84,6 +84,13 @@ typedef enum {
                                 (DSMEM all-gather of y);
                              1: once per GPU (rows of M spread over all CTAs), gathered through L2;
                              4: per cluster as the sum of the CTAs' partials M[slice,:]^T r_slice */
+  KPP_OPT_PROJ = 13,      /* K++ projection (single-GPU contexts): 0 (default) the exact memoized factor,
+                             "K++(Cholesky)" P:1319; 1 sketch-and-precondition LSQR, Alg 6
+                             (SRHT sketch of size tau, Cholesky preconditioner memoized as R^{-1},
+                             t_max LSQR steps per iteration from zero).  kpp_get_factor then returns
+                             R^{-1} of the sketch factor. */
+  KPP_OPT_TMAX = 14,      /* LSQR steps per iteration t_max (default 8) */
+  KPP_OPT_TAU = 15,       /* sketch size tau (default 0 = 2 s); before the first solve only */
   KPP_OPT_REASSOC = 12,   /* CD++ only.  1 (default): blocks that stream from HBM use the kernel that
                              re-associates r_{t+1} = A_{S'} (x_t + eta c m_t) - (1 + eta c) A[S', S] y_t
                              - b_{S'} (exact in real arithmetic, from Alg 3 l.11-13 P:756-759) so the

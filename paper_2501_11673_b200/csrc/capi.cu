@@ -89,6 +89,15 @@ struct kpp_ctx {
   int pC = 1, pgrid = 0;                 // persistent kernel: cluster size, grid
   IterParams pplan{};
   size_t psmem = 0;
+  // sketch-and-precondition projection (NEXT-2, KPP_OPT_PROJ = 1): Alg 6 instead of the exact factor
+  int proj = 0, tmax = 8, tau_opt = 0;
+  int lsqr_ready = 0;
+  long long lsqr_n2 = 0;
+  int lsqr_tau = 0;
+  double* srht_d = nullptr;
+  int32_t* srht_T = nullptr;
+  double* lsqr_buf = nullptr;     // n-parts of the LSQR vectors (3 n)
+  unsigned long long* lsqr_ll = nullptr;  // LL exchange words of the persistent LSQR kernel
   // randomized Hadamard preprocessing (kpp_enable_rht): the context solves the transformed system
   int rht = 0;
   long long m_user = 0, n_user = 0;   // the caller's dimensions (== m, n without RHT)
@@ -266,6 +275,8 @@ struct P1Prof {
   }
 };
 
+kpp_status lsqr_prepare(kpp_ctx* ctx);
+
 kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   P1Prof pp;
   pp.on = getenv("KPP_P1_PROFILE") != nullptr;
@@ -292,8 +303,8 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   // factor 0: shifted CholeskyQR2 for every block; 2 (default): the second CholeskyQR pass only for
   // blocks whose estimated u * kappa(A_S)^2 exceeds 1e-11;
   // 1: the literal Gram + Cholesky for every block
-  const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor != 1;
-  const bool adaptive = ctx->kind == KIND_KPP && ctx->factor == 2;
+  const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor != 1 && ctx->proj == 0;
+  const bool adaptive = ctx->kind == KIND_KPP && ctx->factor == 2 && ctx->proj == 0;
   size_t off = 0;
   auto carve = [&](size_t count) {
     size_t o = off;
@@ -313,6 +324,9 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   const size_t o_Mc = adaptive ? carve((size_t)B * ss) : 0;
   const size_t o_Sc = adaptive ? carve(((size_t)B * s + 1) / 2) : 0;
   const size_t o_lam = adaptive ? carve(3 * (size_t)B + 4) : 0;      // lamG, lamM, list, count
+  const bool skp = ctx->kind == KIND_KPP && ctx->proj == 1;
+  const size_t o_Y = skp ? carve((size_t)ctx->lsqr_n2 * B * s) : 0;    // sketch: n2 x (B s)
+  const size_t o_Ah = skp ? carve((size_t)B * ctx->lsqr_tau * s) : 0;
   CKS(ensure_buf(ctx, ctx->p1, off));
   CK(cudaMemsetAsync(ctx->d_info, 0, (size_t)B * sizeof(int), st));  // the factor kernel only records failures
   char* base = (char*)ctx->p1.p;
@@ -335,6 +349,21 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
     Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
     launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);  // M = X X^T (X upper)
     pp.mark("M");
+  } else if (ctx->proj == 1) {
+    // Alg 6 l.2-5: A_hat = A_S Pi^T (SRHT), R = chol(A_hat A_hat^T + lam I), memoized as X = R^{-1}
+    const long long n2 = ctx->lsqr_n2;
+    const int tau = ctx->lsqr_tau;
+    double* Y = (double*)(base + o_Y);
+    double* Ah = (double*)(base + o_Ah);
+    const long long ldy = (long long)B * s;
+    launch_sketch_gather_t(st, B, ctx->A, ctx->lda, n, S, s, Y, ldy);
+    launch_fht_rows(st, Y, ldy, n, ldy, Y, ldy, n2, ldy, ctx->srht_d, nullptr, 0);  // H diag(d) [A_S^T; 0]
+    launch_sketch_select(st, B, Y, ldy, ctx->srht_T, tau, s, 1.0 / std::sqrt((double)tau), Ah);
+    Operand aa{Ah, s, (long long)tau * s, nullptr, 0, 1}, ab{Ah, s, (long long)tau * s, nullptr, 0, 0};
+    launch_dgemm(st, B, s, s, tau, aa, ab, G, s, ss, 1, 0);  // A_hat A_hat^T
+    launch_add_diag(st, B, G, s, ctx->lam);
+    launch_chol_trtri(st, B, G, Mout, s, ctx->d_info, W);  // X = R^{-1} is the memoized operator
+    pp.mark("sketch");
   } else {
     // G1 = A_S A_S^T (+ lam I): NT GEMM with row gathers on both operands, split-K
     Operand a{ctx->A, ctx->lda, 0, S, s, 0}, b{ctx->A, ctx->lda, 0, S, s, 1};
@@ -425,11 +454,13 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
 }
 
 kpp_status phase1(kpp_ctx* ctx, long long k0, long long k1) {
+  if (ctx->kind == KIND_KPP && ctx->proj == 1) CKS(lsqr_prepare(ctx));
   const long long s = ctx->s, n = ctx->n;
-  const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor == 0;
+  const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor != 1 && ctx->proj == 0;
   // workspace of phase1_batch per block: split-K partials (Z s^2), G, X1 (+ L, X2, X, Q1 for CholeskyQR2)
   const long long Z = ctx->kind == KIND_KPP ? std::min<long long>(64, std::max<long long>(1, (n + 511) / 512)) : 1;
-  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 5 : 0)) * s * s + (cqr2 ? s * n + s : 0)) +
+  const long long skw = (ctx->kind == KIND_KPP && ctx->proj == 1) ? ctx->lsqr_n2 * s + (long long)ctx->lsqr_tau * s : 0;
+  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 5 : 0)) * s * s + (cqr2 ? s * n + s : 0) + skw) +
                               (long long)chol_inv_workspace((int)s) + 2048;
   long long Bmax = std::max<long long>(1, ctx->phase1_mb * (1LL << 20) / per_block);
   Bmax = std::min<long long>(Bmax, 4096);
@@ -731,6 +762,54 @@ kpp_status build_graph(kpp_ctx* ctx, const StepParams& sp, int U) {
   return KPP_OK;
 }
 
+// Sketch-and-precondition projection: SRHT parameters and the LSQR work vectors (once per context).
+kpp_status lsqr_prepare(kpp_ctx* ctx) {
+  if (ctx->lsqr_ready) return KPP_OK;
+  const long long n = ctx->n, s = ctx->s;
+  long long n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  ctx->lsqr_n2 = n2;
+  ctx->lsqr_tau = ctx->tau_opt > 0 ? ctx->tau_opt : (int)std::min<long long>(2 * s, n2);
+  CKS(dalloc(ctx, &ctx->srht_d, (size_t)n2));
+  CKS(dalloc(ctx, &ctx->srht_T, (size_t)ctx->lsqr_tau));
+  int32_t* perm = nullptr;
+  CK(cudaMalloc((void**)&perm, (size_t)n2 * sizeof(int32_t)));
+  launch_srht_setup(ctx->stream, ctx->seed, n2, ctx->lsqr_tau, ctx->srht_d, ctx->srht_T, perm);
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(perm);
+  // part [grid][s], npart [grid], 9 s-vectors, 3 n-vectors
+  CKS(dalloc(ctx, &ctx->lsqr_buf, (size_t)(3 * n)));
+  CK(cudaMalloc((void**)&ctx->lsqr_ll, lsqr_ll_words((int)s, ctx->grid) * sizeof(unsigned long long)));
+  ctx->lsqr_ready = 1;
+  return KPP_OK;
+}
+
+LsqrParams lsqr_params(kpp_ctx* ctx, const double* b_dev, double tol2bb, double bb, double eta) {
+  LsqrParams q{};
+  const long long n = ctx->n;
+  q.A = ctx->A; q.lda = ctx->lda; q.n = n; q.s = (int)ctx->s; q.grid = ctx->grid; q.slab = ctx->slab; q.tmax = ctx->tmax;
+  q.b = b_dev; q.S_pool = ctx->S_pool; q.X_pool = ctx->M_pool; q.bid = ctx->bid; q.lam_sqrt = std::sqrt(ctx->lam);
+  q.x = ctx->x; q.mom = ctx->mom; q.eta = eta; q.zeta = ctx->zeta; q.adaptive = ctx->rho_fixed < 0.0;
+  q.writer = ctx->rank == 0; q.tol2bb = tol2bb; q.bb = bb;
+  q.vn = ctx->lsqr_buf; q.wn = q.vn + n; q.xn = q.wn + n;
+  q.ll = ctx->lsqr_ll; q.err = ctx->d_err; q.st = ctx->dstate;
+  q.hist_res = ctx->hist_res; q.hist_rho = ctx->hist_rho; q.hist_cap = ctx->hist_capd;
+  // on-chip operands: the CTA's slab of A_S first (2 (t_max + 1) passes per iteration), then X
+  const size_t budget = 227 * 1024 - 4096;
+  const size_t fixed = lsqr_smem_bytes(q.s, 0, 0, 0);
+  const size_t as_b = (size_t)q.s * ctx->slab * sizeof(double), x_b = (size_t)q.s * q.s * sizeof(double);
+  const char* ea = getenv("KPP_LSQR_ASMEM");
+  const char* ex = getenv("KPP_LSQR_XSMEM");
+  q.sl = ctx->slab;
+  q.a_smem = (!ea || atoi(ea) != 0) && fixed + as_b <= budget;
+  q.x_smem = (!ex || atoi(ex) != 0) && q.s % 2 == 0 && fixed + (q.a_smem ? as_b : 0) + x_b <= budget;
+  ctx->stats.m_in_smem = q.x_smem;
+  ctx->stats.resident = q.a_smem;
+  ctx->stats.grid_ctas = q.grid;
+  ctx->stats.cluster = 1;
+  return q;
+}
+
 kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long max_iters, double tol,
                       double* x_out, double* res_hist, long long hist_cap, long long* n_hist,
                       long long* iters_out) {
@@ -788,7 +867,9 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   }
   const double eta = ctx->accel ? (ctx->eta_opt >= 0.0 ? ctx->eta_opt : (double)ctx->s / (2.0 * (double)ctx->n_global)) : 0.0;
   const long long W = std::max<long long>(1, ctx->window);
-  const bool use_graph = ctx->engine == 1 || ctx->nranks > 1;
+  const bool use_lsqr = ctx->kind == KIND_KPP && ctx->proj == 1;
+  const bool use_graph = !use_lsqr && (ctx->engine == 1 || ctx->nranks > 1);
+  if (use_lsqr) CKS(lsqr_prepare(ctx));
   float p1ms = 0.f, p2ms = 0.f;
   DevState fin = hs;
   for (long long t0 = 0; t0 < max_iters; t0 += W) {
@@ -801,7 +882,20 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     p1ms += ms;
     CK(cudaEventRecord(ctx->ev0, st));
-    if (!use_graph) {
+    if (use_lsqr) {
+      // K++ with Proj = Alg 6: one persistent cooperative launch per window
+      LsqrParams q = lsqr_params(ctx, b_dev, tol * tol * bb, bb, eta);
+      q.t0 = t0; q.t1 = t0 + cnt; q.t_base = t0;
+      if (getenv("KPP_PHASE_PROFILE")) {
+        if (!ctx->d_prof) {
+          CKS(dalloc(ctx, &ctx->d_prof, 16));
+          CK(cudaMemset(ctx->d_prof, 0, 16 * sizeof(long long)));
+        }
+        q.prof = ctx->d_prof;
+      }
+      CK(launch_lsqr_window(st, q));
+      ctx->stats.iter_launches += 1;
+    } else if (!use_graph) {
       IterParams p = ctx->pplan;  // carries the tensor map
       p.A = ctx->A; p.lda = ctx->lda; p.m = m; p.n = n; p.s = ctx->s;
       p.cd = ctx->kind == KIND_CDPP; p.col_base = ctx->col_begin;
@@ -924,7 +1018,9 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
                                 "P4a", "-", "y_comp", "gather_poll", "r_comb"};
     const char* names_cs[16] = {"t0:A", "t0:stream", "-", "-", "-", "-", "t0:barrier", "-",
                                 "ch:A", "-", "ch:gather", "ch:r_wait", "ch:y_rows", "ch:y_gather", "ch:barrier", "-"};
-    const char* const* names = use_cdpp_stream(ctx) ? names_cs : names_it;
+    const char* names_ls[16] = {"r0_pass", "r0_xchg", "r0_spart", "pass", "xchg", "rot", "spart", "update", "-", "-", "-", "-",
+                                "-", "-", "-", "-"};
+    const char* const* names = use_lsqr ? names_ls : use_cdpp_stream(ctx) ? names_cs : names_it;
     fprintf(stderr, "[kpp phase cycles/iter, CTA 0]");
     for (int i = 0; i < 16; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
     fprintf(stderr, "\n");
@@ -1049,7 +1145,7 @@ void kpp_destroy(kpp_ctx* ctx) {
   if (!ctx) return;
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  void* ptrs[] = {ctx->rht_A, ctx->rht_d, ctx->rht_v, ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
+  void* ptrs[] = {ctx->srht_d, ctx->srht_T, ctx->lsqr_buf, ctx->lsqr_ll, ctx->rht_A, ctx->rht_d, ctx->rht_v, ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
                   ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->d_info};
   for (void* p : ptrs)
@@ -1101,6 +1197,20 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
       ctx->cluster_opt = (int)v;
       CKS(plan_cdpp_stream(ctx));
       return plan_persistent(ctx);
+    case KPP_OPT_PROJ:
+      if (v != 0.0 && v != 1.0) return KPP_EINVAL;
+      if (ctx->kind != KIND_KPP || (v == 1.0 && ctx->nranks > 1)) return KPP_EINVAL;
+      if ((int)v != ctx->proj) ctx->nb_ready = 0;  // a different memoized operator
+      ctx->proj = (int)v;
+      return KPP_OK;
+    case KPP_OPT_TMAX:
+      if (v < 1 || v > 1000) return KPP_EINVAL;
+      ctx->tmax = (int)v;
+      return KPP_OK;
+    case KPP_OPT_TAU:
+      if (v < 0 || ctx->lsqr_ready) return KPP_EINVAL;  // fixed once the sketch exists
+      ctx->tau_opt = (int)v;
+      return KPP_OK;
     case KPP_OPT_REASSOC:
       if (v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;
       ctx->reassoc = (int)v;

@@ -190,6 +190,52 @@ void launch_step_solve(cudaStream_t st, const StepParams& p);    // y = M (rsum 
 void launch_step_update(cudaStream_t st, const StepParams& p);   // w, momentum, x
 void launch_step_window(cudaStream_t st, const StepParams& p);   // e, checkpoint, t_cur++
 
+// ------------------------------------------------------------------ lsqr.cu (NEXT-2: Alg 6)
+struct LsqrScal {
+  double alpha, beta, phibar, rhobar, f1, f2;
+};
+struct LsqrParams {
+  const double* A;
+  long long lda, n;
+  int s, grid, slab, tmax;
+  const double* b;
+  const int32_t* S_pool;
+  const double* X_pool;  // memoized R^{-1} of the sketch factor, s x s per block (upper)
+  const int32_t* bid;    // block id of iteration t at bid[t - t_base]
+  long long t0, t1, t_base;
+  double lam_sqrt;
+  double* x;
+  double* mom;
+  double eta;
+  long long zeta;
+  int adaptive, writer;
+  double tol2bb, bb;
+  double* vn;  // [n] n-parts of the LSQR vectors v, w and the iterate (slab-local)
+  double* wn;
+  double* xn;
+  unsigned long long* ll;  // LL exchange words (lsqr_ll_words)
+  int* err;
+  long long* prof;         // optional: ns per phase, accumulated by CTA 0 (KPP_PHASE_PROFILE)
+  int a_smem, sl;          // the A_S slab resident in shared memory (row stride sl), see lsqr_plan
+  int x_smem;              // X resident in shared memory
+  DevState* st;
+  double* hist_res;
+  double* hist_rho;
+  long long hist_cap;
+};
+// SRHT parameters: dsign[j] = +-1 (Philox stream 4), T = sorted tau draws of [0, n2) (stream 5)
+void launch_srht_setup(cudaStream_t st, uint64_t seed, long long n2, int tau, double* dsign, int32_t* T,
+                       int32_t* perm_ws);
+// Y[j][b s + k] = A[S_b[k]][j] (j < n), ldy = batch * s
+void launch_sketch_gather_t(cudaStream_t st, int batch, const double* A, long long lda, long long n,
+                            const int32_t* S, int s, double* Y, long long ldy);
+// Ah[b][q][k] = scale * Y[T_q][b s + k]
+void launch_sketch_select(cudaStream_t st, int batch, const double* Y, long long ldy, const int32_t* T, int tau,
+                          int s, double scale, double* Ah);
+size_t lsqr_ll_words(int s, int grid);
+size_t lsqr_smem_bytes(int s, int a_smem, int sl, int x_smem);
+cudaError_t launch_lsqr_window(cudaStream_t st, const LsqrParams& p);
+
 // sum of squares of b (single CTA, fixed order) -> *out
 void launch_sumsq(cudaStream_t st, const double* b, long long m, double* out);
 

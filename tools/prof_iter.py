@@ -18,6 +18,8 @@ ap.add_argument("--cluster", type=int, default=0)
 ap.add_argument("--ygl", type=int, default=-1)
 ap.add_argument("--reassoc", type=int, default=1)
 ap.add_argument("--rht", action="store_true")
+ap.add_argument("--proj", type=int, default=0)
+ap.add_argument("--tmax", type=int, default=8)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 A, b, _ = synth.make_problem(cfg, device="cuda")
@@ -27,6 +29,9 @@ ctx.set_option(kpp.OPT_CLUSTER, a.cluster)
 ctx.set_option(kpp.OPT_YGL, a.ygl)
 if cfg.kind == 'cdpp':
     ctx.set_option(kpp.OPT_REASSOC, a.reassoc)
+if a.proj:
+    ctx.set_option(kpp.OPT_PROJ, a.proj)
+    ctx.set_option(kpp.OPT_TMAX, a.tmax)
 if a.rht:
     ctx.enable_rht()
     torch.cuda.synchronize()
@@ -35,6 +40,8 @@ if a.rht:
     print(f"{a.config}: RHT preprocessing {st0['rht_ms']:.2f} ms  (matrix {mb:.0f} MB)", flush=True)
 ctx.set_option(kpp.OPT_WINDOW, a.iters)
 ctx.prepare(a.iters)
+st1 = ctx.stats()
+print(f"{a.config}: phase1 {st1['phase1_ms']:.2f} ms for {st1['n_blocks']} blocks", flush=True)
 for _ in range(a.reps):
     ctx.reset_stats()
     r = ctx.solve(b, max_iters=a.iters)
