@@ -796,11 +796,12 @@ LsqrParams lsqr_params(kpp_ctx* ctx, const double* b_dev, double tol2bb, double 
   q.hist_res = ctx->hist_res; q.hist_rho = ctx->hist_rho; q.hist_cap = ctx->hist_capd;
   // on-chip operands: the CTA's slab of A_S first (2 (t_max + 1) passes per iteration), then X
   const size_t budget = 227 * 1024 - 4096;
-  const size_t fixed = lsqr_smem_bytes(q.s, 0, 0, 0);
+  q.sl = ctx->slab;
+  q.v_smem = lsqr_smem_bytes(q.s, 0, q.sl, 0, 1) <= budget;
+  const size_t fixed = lsqr_smem_bytes(q.s, 0, q.sl, 0, q.v_smem);
   const size_t as_b = (size_t)q.s * ctx->slab * sizeof(double), x_b = (size_t)q.s * q.s * sizeof(double);
   const char* ea = getenv("KPP_LSQR_ASMEM");
   const char* ex = getenv("KPP_LSQR_XSMEM");
-  q.sl = ctx->slab;
   q.a_smem = (!ea || atoi(ea) != 0) && fixed + as_b <= budget;
   q.x_smem = (!ex || atoi(ex) != 0) && q.s % 2 == 0 && fixed + (q.a_smem ? as_b : 0) + x_b <= budget;
   ctx->stats.m_in_smem = q.x_smem;

@@ -218,6 +218,7 @@ struct LsqrParams {
   long long* prof;         // optional: ns per phase, accumulated by CTA 0 (KPP_PHASE_PROFILE)
   int a_smem, sl;          // the A_S slab resident in shared memory (row stride sl), see lsqr_plan
   int x_smem;              // X resident in shared memory
+  int v_smem;              // the slab parts of v, w and the LSQR iterate in shared memory
   DevState* st;
   double* hist_res;
   double* hist_rho;
@@ -233,7 +234,7 @@ void launch_sketch_gather_t(cudaStream_t st, int batch, const double* A, long lo
 void launch_sketch_select(cudaStream_t st, int batch, const double* Y, long long ldy, const int32_t* T, int tau,
                           int s, double scale, double* Ah);
 size_t lsqr_ll_words(int s, int grid);
-size_t lsqr_smem_bytes(int s, int a_smem, int sl, int x_smem);
+size_t lsqr_smem_bytes(int s, int a_smem, int sl, int x_smem, int v_smem);
 cudaError_t launch_lsqr_window(cudaStream_t st, const LsqrParams& p);
 
 // sum of squares of b (single CTA, fixed order) -> *out

@@ -30,17 +30,54 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// block-wide fixed-order sum (every thread gets the result)
-__device__ double block_sum(double v, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  v = wsum(v);
+// Sums of V values over the 32 lanes with V - 1 + log2(32 / V) shuffles (reduce-scatter butterflies,
+// then a plain butterfly): afterwards every lane l holds the total of value (l >> (5 - log2 V)),
+// returned.  Fixed order: the same in every warp and CTA.
+template <int V>
+__device__ __forceinline__ double warp_multi_sum(double (&a)[V]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = V / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? a[i] : a[i + h];
+      const double keep = up ? a[i + h] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  double v = a[0];
+#pragma unroll
+  for (int o = 16 / V; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int V>
+__device__ __forceinline__ int warp_multi_index() {
+  constexpr int SH = V == 1 ? 5 : V == 2 ? 4 : V == 4 ? 3 : V == 8 ? 2 : V == 16 ? 1 : 0;
+  return (threadIdx.x & 31) >> SH;
+}
+
+// block-wide fixed-order sums (every thread gets the results, one barrier): red holds 2 slots of
+// 2 x 32 doubles used alternately (slot toggled by the caller), so a slot is rewritten only after
+// every thread has passed the barrier of the call in between.
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* red, int& slot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  a = wsum(a);
+  b = wsum(b);
+  double* r = red + 64 * slot;
+  slot ^= 1;
+  if (lane == 0) {
+    r[warp] = a;
+    r[32 + warp] = b;
+  }
   __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int i = 0; i < nw; ++i) t += red[i];
-  __syncthreads();
-  return t;
+  a = wsum(lane < nw ? r[lane] : 0.0);
+  b = wsum(lane < nw ? r[32 + lane] : 0.0);
+}
+__device__ __forceinline__ double block_sum(double v, double* red, int& slot) {
+  double z = 0.0;
+  block_sum2(v, z, red, slot);
+  return v;
 }
 
 __device__ __forceinline__ void philox4(uint32_t c[4], uint32_t k0, uint32_t k1) {
@@ -232,12 +269,10 @@ __device__ __forceinline__ void slab_rowsums_x(const LsqrParams& p, const int32_
           acc[r] = fma(a, zj, acc[r]);
         }
     }
-#pragma unroll
-    for (int r = 0; r < RW; ++r) acc[r] = wsum(acc[r]);
-    if (lane == 0)
-#pragma unroll
-      for (int r = 0; r < RW; ++r)
-        if (k0 + r < s) ll_put(ll_part + 2LL * ((long long)blockIdx.x * (s + 1) + k0 + r), acc[r], tag);
+    const double tot = warp_multi_sum<RW>(acc);
+    const int r = warp_multi_index<RW>();
+    if ((lane & (32 / RW - 1)) == 0 && k0 + r < s)
+      ll_put(ll_part + 2LL * ((long long)blockIdx.x * (s + 1) + k0 + r), tot, tag);
   }
   if (threadIdx.x == 0) ll_put(ll_part + 2LL * ((long long)blockIdx.x * (s + 1) + s), 0.0, tag);
 }
@@ -249,16 +284,24 @@ struct SlabScal {
   double beta;    // beta_r of the C term (0 in round 1)
 };
 
+// The slab parts of the LSQR vectors: in shared memory when they fit (lsqr_plan), else global.
+struct SlabVec {
+  double* vn;  // indexed by the global column j
+  double* wn;
+  double* xn;
+};
+
 // Rounds >= 1: the fused slab pass.  Per tile of TW columns: (1) finish the previous v_n and the
 // deferred w/x updates, (2) v_n = A_S^T y - beta v (warps split rows, lanes columns), (3) the row
 // sums A_S v_n on the same tile (rows of warp w: k = w + NW i; per-lane partials kept in registers
 // across tiles when s <= NW * RA, else folded into shared memory per tile).  ASM: A_S from the
-// shared slab copy.
+// shared slab copy.  Also returns ||v_s||^2 of the (raw) s-part, reduced with the slab norm.
 template <bool ASM, bool REG>
-__device__ __forceinline__ void slab_fused(const LsqrParams& p, const int32_t* S_sh, const double* As,
-                                           const double* yv, const SlabScal& sc, long long c0, long long c1,
-                                           double (*part_sh)[TW], double* vt, double* pacc, double* red_sh,
-                                           unsigned long long* ll_part, unsigned tag) {
+__device__ __forceinline__ double slab_fused(const LsqrParams& p, const int32_t* S_sh, const double* As,
+                                             const double* yv, const double* vs, const SlabScal& sc, SlabVec sv,
+                                             long long c0, long long c1, double (*part_sh)[TW], double* vt,
+                                             double* pacc, double* red_sh, int& bs, unsigned long long* ll_part,
+                                             unsigned tag) {
   const int s = p.s, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double accA[RA];
 #pragma unroll
@@ -275,14 +318,14 @@ __device__ __forceinline__ void slab_fused(const LsqrParams& p, const int32_t* S
       const long long j = jb + tid;
       double v = 0.0;
       if (j < c1 && sc.ia != 0.0) {
-        v = p.vn[j] * sc.ia;
+        v = sv.vn[j] * sc.ia;
         if (sc.defer == 1) {
-          p.wn[j] = v;
-          p.xn[j] = 0.0;
+          sv.wn[j] = v;
+          sv.xn[j] = 0.0;
         } else if (sc.defer == 2) {
-          const double w = p.wn[j];
-          p.xn[j] = fma(sc.f1, w, p.xn[j]);
-          p.wn[j] = fma(-sc.f2, w, v);
+          const double w = sv.wn[j];
+          sv.xn[j] = fma(sc.f1, w, sv.xn[j]);
+          sv.wn[j] = fma(-sc.f2, w, v);
         }
       }
       vt[TW + tid] = v;
@@ -308,9 +351,14 @@ __device__ __forceinline__ void slab_fused(const LsqrParams& p, const int32_t* S
       const long long j = jb + tid;
       double a = 0.0;
       if (j < c1) {
-        for (int w = 0; w < NW; ++w) a += part_sh[w][tid];
-        a = fma(-sc.beta, vt[TW + tid], a);
-        p.vn[j] = a;
+        double h0 = 0.0, h1 = 0.0;  // two interleaved chains, fixed order
+#pragma unroll
+        for (int w = 0; w < NW; w += 2) {
+          h0 += part_sh[w][tid];
+          h1 += part_sh[w + 1][tid];
+        }
+        a = fma(-sc.beta, vt[TW + tid], h0 + h1);
+        sv.vn[j] = a;
         q2 = fma(a, a, q2);
       }
       vt[tid] = a;
@@ -346,18 +394,18 @@ __device__ __forceinline__ void slab_fused(const LsqrParams& p, const int32_t* S
   }
   const long long base = (long long)blockIdx.x * (s + 1);
   if (REG) {
-#pragma unroll
-    for (int i = 0; i < RA; ++i) {
-      const int k = warp + NW * i;
-      const double a = wsum(accA[i]);
-      if (lane == 0 && k < s) ll_put(ll_part + 2LL * (base + k), a, tag);
-    }
+    const double a = warp_multi_sum<RA>(accA);
+    const int k = warp + NW * warp_multi_index<RA>();
+    if ((lane & (32 / RA - 1)) == 0 && k < s) ll_put(ll_part + 2LL * (base + k), a, tag);
   } else {
     __syncthreads();
     for (int k = tid; k < s; k += NT) ll_put(ll_part + 2LL * (base + k), pacc[k], tag);
   }
-  q2 = block_sum(q2, red_sh);
+  double vq = 0.0;
+  for (int k = tid; k < s; k += NT) vq = fma(vs[k], vs[k], vq);
+  block_sum2(q2, vq, red_sh, bs);
   if (tid == 0) ll_put(ll_part + 2LL * (base + s), q2, tag);
+  return vq;
 }
 
 // Exchange of round `tag`: totals of the s + 1 words into out[0..s] (every CTA).
@@ -375,58 +423,69 @@ __device__ __forceinline__ void exchange(const LsqrParams& p, unsigned long long
 }
 
 // u = X^T vin (- alpha u when !init), beta = ||u||, u /= beta, y = X u, vs = sqrt(lam) y (- beta vs)
-// -- one CTA, X upper s x s (shared or global).  Returns beta.
-__device__ __forceinline__ double s_products(const LsqrParams& p, const double* X, const double* vin, double* u,
-                                             double* yv, double* vs, double* buf, double* red_sh, double alpha,
-                                             bool init) {
-  const int s = p.s, SP = (s + 31) & ~31, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int KTe = SP < NT ? SP : NT, P = NT / KTe, kk = tid % KTe, grp = tid / KTe;
-  for (int cb = 0; cb < SP; cb += KTe) {
-    const int k = cb + kk;
-    double acc = 0.0;
-    if (grp < P && k < s) {
-      const int iend = (k | 31) < s ? (k | 31) : s - 1;
-#pragma unroll 8
-      for (int i = grp; i <= iend; i += P) acc = fma(i <= k ? X[(long long)i * s + k] : 0.0, vin[i], acc);
-    }
-    buf[tid] = acc;
-    __syncthreads();
-    if (tid < KTe && cb + tid < s) {
-      double a = 0.0;
-      for (int gg = 0; gg < P; ++gg) a += buf[gg * KTe + tid];
-      u[cb + tid] = init ? a : fma(-alpha, u[cb + tid], a);
-    }
-    __syncthreads();
-  }
-  double uu = 0.0;
-  for (int k = tid; k < s; k += NT) uu = fma(u[k], u[k], uu);
-  const double beta = sqrt(block_sum(uu, red_sh));
-  const double ib = beta > 0.0 ? 1.0 / beta : 0.0;
-  for (int k = tid; k < s; k += NT) u[k] *= ib;
-  __syncthreads();
-  for (int r0 = warp * YR; r0 < s; r0 += NW * YR) {
-    double a[YR];
+// -- one CTA, X upper s x s (shared or global).  Load balance over the triangle: X^T vin pairs
+// column k with column SP-1-k (P row groups per pair), X u pairs row block b with block NB-1-b.
+// buf: 2 NT doubles.  Returns beta.
+__device__ __forceinline__ void xu_block(const LsqrParams& p, const double* X, const double* u, double ib, int r0,
+                                         double beta, bool init, double* yv, double* vs) {
+  const int s = p.s, lane = threadIdx.x & 31;
+  double a[YR];
 #pragma unroll
-    for (int r = 0; r < YR; ++r) a[r] = 0.0;
-    for (int l = (r0 & ~31) + lane; l < s; l += 32) {
-      const double ul = u[l];
-#pragma unroll
-      for (int r = 0; r < YR; ++r) {
-        const int row = r0 + r;
-        if (row < s && l >= row) a[r] = fma(X[(long long)row * s + l], ul, a[r]);
-      }
-    }
+  for (int r = 0; r < YR; ++r) a[r] = 0.0;
+  for (int l = (r0 & ~31) + lane; l < s; l += 32) {
+    const double ul = u[l] * ib;
 #pragma unroll
     for (int r = 0; r < YR; ++r) {
-      const double y = wsum(a[r]);
       const int row = r0 + r;
-      if (lane == 0 && row < s) {
-        yv[row] = y;
-        vs[row] = init ? p.lam_sqrt * y : fma(-beta, vs[row], p.lam_sqrt * y);
-      }
+      if (row < s && l >= row) a[r] = fma(X[(long long)row * s + l], ul, a[r]);
     }
   }
+  const double y = warp_multi_sum<YR>(a);
+  const int row = r0 + warp_multi_index<YR>();
+  if ((lane & (32 / YR - 1)) == 0 && row < s) {
+    yv[row] = y;
+    vs[row] = init ? p.lam_sqrt * y : fma(-beta, vs[row], p.lam_sqrt * y);
+  }
+}
+
+__device__ __forceinline__ double s_products(const LsqrParams& p, const double* X, const double* vin, double* u,
+                                             double* yv, double* vs, double* buf, double* red_sh, int& bs,
+                                             double alpha, bool init) {
+  const int s = p.s, SP = (s + 31) & ~31, tid = threadIdx.x, warp = tid >> 5;
+  const int NPR = SP / 2, P = NT / NPR, cp = tid % NPR, grp = tid / NPR;
+  if (grp < P) {
+    const int k1 = cp, k2 = SP - 1 - cp;
+    const bool v1 = k1 < s, v2 = k2 < s;
+    const int iend = v2 ? k2 : (v1 ? k1 : -1);
+    double a1 = 0.0, a2 = 0.0;
+#pragma unroll 8
+    for (int i = grp; i <= iend; i += P) {
+      const double vi = vin[i];
+      const double* xr = X + (long long)i * s;
+      if (i <= k1) a1 = fma(xr[k1], vi, a1);
+      if (v2) a2 = fma(xr[k2], vi, a2);
+    }
+    buf[grp * SP + k1] = a1;
+    buf[grp * SP + k2] = a2;
+  }
   __syncthreads();
+  double uu = 0.0;
+  for (int k = tid; k < s; k += NT) {
+    double a = 0.0;
+    for (int gg = 0; gg < P; ++gg) a += buf[gg * SP + k];
+    a = init ? a : fma(-alpha, u[k], a);
+    u[k] = a;
+    uu = fma(a, a, uu);
+  }
+  const double beta = sqrt(block_sum(uu, red_sh, bs));
+  const double ib = beta > 0.0 ? 1.0 / beta : 0.0;
+  const int NB = (s + YR - 1) / YR;
+  for (int bp = warp; bp < (NB + 1) / 2; bp += NW) {
+    xu_block(p, X, u, ib, bp * YR, beta, init, yv, vs);
+    if (NB - 1 - bp != bp) xu_block(p, X, u, ib, (NB - 1 - bp) * YR, beta, init, yv, vs);
+  }
+  __syncthreads();
+  for (int k = tid; k < s; k += NT) u[k] *= ib;  // read by the next product after its barriers
   return beta;
 }
 
@@ -434,7 +493,8 @@ template <bool REG>
 __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
   extern __shared__ double sm[];
   __shared__ DevState st_sh;
-  __shared__ double red_sh[32];
+  __shared__ double red_sh[128];
+  int bs = 0;  // block_sum slot
   const int s = p.s, SP = (s + 31) & ~31;
   double* tot = sm;        // exchange totals [s + 1]
   double* u = tot + SP + 32;
@@ -444,29 +504,42 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
   double* yv = xs + SP;
   double* vin = yv + SP;
   double* pacc = vin + SP;
-  double* buf = pacc + SP;
-  double(*part_sh)[TW] = reinterpret_cast<double(*)[TW]>(buf + NT);
-  double* vt = buf + NT + NW * TW;  // [2 TW]
-  int32_t* S_sh = reinterpret_cast<int32_t*>(vt + 2 * TW);
+  double* bS = pacc + SP;
+  double* buf = bS + SP;           // [2 NT]
+  double(*part_sh)[TW] = reinterpret_cast<double(*)[TW]>(buf + 2 * NT);
+  double* vt = buf + 2 * NT + NW * TW;  // [2 TW]
+  double* slv = vt + 2 * TW;        // [3 sl] when v_smem
+  int32_t* S_sh = reinterpret_cast<int32_t*>(slv + (p.v_smem ? 3LL * p.sl : 0));
   // on-chip operands (lsqr_plan): the CTA's slab of A_S (s x sl) and X (s x s), reused by all
   // t_max + 1 rounds of the iteration
-  double* As = vt + 2 * TW + SP / 2;
+  double* As = reinterpret_cast<double*>(S_sh) + SP / 2;
   double* Xs = As + (p.a_smem ? (long long)s * p.sl : 0);
-  const int tid = threadIdx.x, g = blockIdx.x, G = p.grid;
+  const int tid = threadIdx.x, g = blockIdx.x;
   unsigned long long* ll_part = p.ll;
-  unsigned long long* ll_red = p.ll + 2LL * G * (s + 1);
+  unsigned long long* ll_red = p.ll + 2LL * p.grid * (s + 1);
   const long long c0 = (long long)g * p.slab;
   const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
+  SlabVec sv;
+  if (p.v_smem) {
+    sv.vn = slv - c0;
+    sv.wn = slv + p.sl - c0;
+    sv.xn = slv + 2LL * p.sl - c0;
+  } else {
+    sv.vn = p.vn;
+    sv.wn = p.wn;
+    sv.xn = p.xn;
+  }
   if (tid == 0) st_sh = *p.st;
   __syncthreads();
   unsigned tag = 0;
   long long tm = p.t0 % (2 * p.zeta);
   const bool prof = p.prof != nullptr && g == 0 && tid == 0;
   long long tp = prof ? clock64() : 0;
+  long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   auto mark = [&](int i) {
     if (prof) {
       const long long now = clock64();
-      p.prof[i] += now - tp;
+      pr[i] += now - tp;
       tp = now;
     }
   };
@@ -480,7 +553,11 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     const double* X = p.x_smem ? Xs : Xg;
-    for (int i = tid; i < s; i += NT) S_sh[i] = p.S_pool[kb * s + i];
+    for (int i = tid; i < s; i += NT) {
+      const int32_t row = p.S_pool[kb * s + i];
+      S_sh[i] = row;
+      bS[i] = p.b[row];
+    }
     __syncthreads();
     // ---- round 0: r_t = A_S x_t - b_S, u_1 = R^{-T} r / beta_1, y_1 = R^{-1} u_1, v_s raw
     ++tag;
@@ -491,28 +568,28 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
     mark(1);
     double e = 0.0;
     for (int k = tid; k < s; k += NT) {
-      const double r = tot[k] - p.b[S_sh[k]];
+      const double r = tot[k] - bS[k];
       vin[k] = r;
       e = fma(r, r, e);
     }
-    e = block_sum(e, red_sh);
     if (p.x_smem) asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();
-    double beta = s_products(p, X, vin, u, yv, vs, buf, red_sh, 0.0, true);
+    e = block_sum(e, red_sh, bs);  // (its barrier also publishes vin and the copied X)
+    double beta = s_products(p, X, vin, u, yv, vs, buf, red_sh, bs, 0.0, true);
     mark(2);
     double phibar = beta, rhobar = 0.0, alpha = 0.0, f1 = 0.0, f2 = 0.0;
     SlabScal sc{0.0, 0, 0.0, 0.0, 0.0};
     for (int r = 1; r <= p.tmax; ++r) {
       ++tag;
-      if (p.a_smem) slab_fused<true, REG>(p, S_sh, As, yv, sc, c0, c1, part_sh, vt, pacc, red_sh, ll_part, tag);
-      else slab_fused<false, REG>(p, S_sh, As, yv, sc, c0, c1, part_sh, vt, pacc, red_sh, ll_part, tag);
+      const double vq = p.a_smem
+                            ? slab_fused<true, REG>(p, S_sh, As, yv, vs, sc, sv, c0, c1, part_sh, vt, pacc, red_sh, bs,
+                                                    ll_part, tag)
+                            : slab_fused<false, REG>(p, S_sh, As, yv, vs, sc, sv, c0, c1, part_sh, vt, pacc, red_sh,
+                                                     bs, ll_part, tag);
       mark(3);
       exchange(p, ll_part, ll_red, tot, tag);
       mark(4);
       // alpha_r, v_s = raw / alpha_r; rotation of step r - 1 (r >= 2) or the initial w (r = 1)
-      double vq = 0.0;
-      for (int k = tid; k < s; k += NT) vq = fma(vs[k], vs[k], vq);
-      alpha = sqrt(tot[s] + block_sum(vq, red_sh));
+      alpha = sqrt(tot[s] + vq);
       const double ia = alpha > 0.0 ? 1.0 / alpha : 0.0;
       if (r == 1) {
         rhobar = alpha;
@@ -541,7 +618,7 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
       __syncthreads();
       mark(5);
       // step r, first half: beta_{r+1} u_{r+1} = M v_r - alpha_r u_r; y = R^{-1} u; v_s raw
-      const double beta_next = s_products(p, X, vin, u, yv, vs, buf, red_sh, alpha, false);
+      const double beta_next = s_products(p, X, vin, u, yv, vs, buf, red_sh, bs, alpha, false);
       mark(6);
       sc.ia = ia;
       sc.defer = r == 1 ? 1 : 2;
@@ -562,14 +639,14 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
     {
       const double rho = st_sh.rho, cm = (1.0 - rho) / (1.0 + rho);
       for (long long j = c0 + tid; j < c1; j += NT) {
-        const double v = p.vn[j] * sc.ia;
+        const double v = sv.vn[j] * sc.ia;
         double xn, wn;
         if (sc.defer == 1) {
           wn = v;
           xn = 0.0;
         } else {
-          const double w = p.wn[j];
-          xn = fma(sc.f1, w, p.xn[j]);
+          const double w = sv.wn[j];
+          xn = fma(sc.f1, w, sv.xn[j]);
           wn = fma(-sc.f2, w, v);
         }
         const double wt = fma(f1_last, wn, xn);
@@ -590,13 +667,16 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
     mark(7);
   }
   if (g == 0 && tid == 0) *p.st = st_sh;
+  if (prof)
+    for (int i = 0; i < 8; ++i) p.prof[i] += pr[i];
 }
 
 }  // namespace
 
-size_t lsqr_smem_bytes(int s, int a_smem, int sl, int x_smem) {
+size_t lsqr_smem_bytes(int s, int a_smem, int sl, int x_smem, int v_smem) {
   const int SP = (s + 31) & ~31;
-  size_t d = (size_t)(8 * SP + 32 + NT + NW * TW + 2 * TW + SP / 2);
+  size_t d = (size_t)(9 * SP + 32 + 2 * NT + NW * TW + 2 * TW + SP / 2);
+  if (v_smem) d += 3 * (size_t)sl;
   if (a_smem) d += (size_t)s * sl;
   if (x_smem) d += (size_t)s * s;
   return d * sizeof(double);
@@ -632,7 +712,7 @@ cudaError_t launch_lsqr_window(cudaStream_t st, const LsqrParams& p) {
   static int attr_smem[2] = {0, 0};
   const bool reg = p.s <= NW * RA;
   const void* fn = reg ? (const void*)lsqr_persistent_kernel<true> : (const void*)lsqr_persistent_kernel<false>;
-  const size_t smem = lsqr_smem_bytes(p.s, p.a_smem, p.sl, p.x_smem);
+  const size_t smem = lsqr_smem_bytes(p.s, p.a_smem, p.sl, p.x_smem, p.v_smem);
   if ((int)smem > attr_smem[reg]) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
