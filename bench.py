@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=-1)
     ap.add_argument("--rht", action="store_true", help="randomized Hadamard preprocessing (SURVEY 8(f) NEXT-1)")
+    ap.add_argument("--proj", type=int, default=0, choices=[0, 1],
+                    help="K++ projection: 0 exact (memoized factor), 1 sketch + LSQR (Alg 6, SURVEY 8(f) NEXT-2)")
+    ap.add_argument("--tmax", type=int, default=8, help="LSQR steps per iteration with --proj 1 (P:1322)")
     return ap.parse_args()
 
 
@@ -127,11 +130,11 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic(cfg_name):
-    """dram bytes per launch of the iteration kernel from the committed ncu capture."""
+def ncu_traffic(cfg_name, kernel="iterate_kernel"):
+    """dram bytes per iteration of the Phase-2 kernel from the committed ncu capture."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        e = d.get(cfg_name, {}).get("iterate_kernel")
+        e = d.get(cfg_name, {}).get(kernel)
         return e.get("dram_bytes_per_iter") if e else None
     except Exception:
         return None
@@ -151,7 +154,7 @@ def phase1_flops(cfg, n_blocks, n_refined):
     return n_blocks * (s * (s + 1) * n + small) + n_refined * (s * s * n + s * (s + 1) * n + 5 * small / 3)
 
 
-def cpu_oracle_sample(cfg, A_host, b_host, seconds):
+def cpu_oracle_sample(cfg, A_host, b_host, seconds, proj=0, tmax=8):
     """Time the oracle, as it stands, on the host cores: iterations 0..T-1 of the same cold
     solve, T grown until the call takes about `seconds`."""
     import oracle
@@ -163,19 +166,23 @@ def cpu_oracle_sample(cfg, A_host, b_host, seconds):
         if cfg.kind == "cdpp":
             oracle.cdpp_run(A_host, b_host, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=threads)
         else:
-            oracle.kpp_run(A_host, b_host, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=threads)
+            oracle.kpp_run(A_host, b_host, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=threads,
+                           proj=proj, tmax=tmax)
         dt = time.perf_counter() - t0
         if dt >= seconds / 3 or T >= 1 << 20:
             break
         T = int(T * min(8.0, max(2.0, seconds / 3 / max(dt, 1e-3))))
     return {"value": T / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"{cfg.name}: iterations 0..{T - 1} of a cold solve (first-visit Householder "
-                      f"factors included), {threads} OpenMP threads over independent outputs, {dt:.1f} s"}
+            "sample": f"{cfg.name}: iterations 0..{T - 1} of a cold solve (first-visit "
+                      f"{'sketch' if proj else 'Householder'} factors included"
+                      f"{f', {tmax} LSQR steps per projection' if proj else ''}), {threads} OpenMP threads over "
+                      f"independent outputs, {dt:.1f} s"}
 
 
-def workload_config(cfg, iters, world, dist):
+def workload_config(cfg, iters, world, dist, proj=0, tmax=8):
     """The `config` object of the JSON line (shared by both arms)."""
-    return {"workload": f"{cfg.name}: {'CD++' if cfg.kind == 'cdpp' else 'Kaczmarz++'} "
+    algo = "CD++" if cfg.kind == "cdpp" else ("Kaczmarz++(LSQR-%d)" % tmax if proj else "Kaczmarz++")
+    return {"workload": f"{cfg.name}: {algo} "
                         f"m={cfg.m} n={cfg.n} s={cfg.s} lam={cfg.lam:g}",
             "iters_per_step": iters, "step": "cold solve (memo cache cleared)",
             "parallelism": f"column-sharded x{world}" if dist else "1 GPU",
@@ -193,7 +200,7 @@ def run_reference(args, cfg):
     cb = None
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        r = cpu_oracle_sample(cfg, A_host, b_host, args.cpu_seconds / max(1, args.steps))
+        r = cpu_oracle_sample(cfg, A_host, b_host, args.cpu_seconds / max(1, args.steps), args.proj, args.tmax)
         if i >= args.warmup:
             per_step.append(r["value"])
             step_ms.append((time.perf_counter() - t0) * 1e3)
@@ -204,7 +211,7 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(step_ms)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(cfg, iters, 1, False),
+            "data": "synthetic", "config": workload_config(cfg, iters, 1, False, args.proj, args.tmax),
             "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -253,6 +260,11 @@ def main():
     ctx.set_stream(stream)
     if args.engine >= 0:
         ctx.set_option(kpp.OPT_ENGINE, args.engine)
+    if args.proj:
+        if cfg.kind != "kpp" or dist:
+            raise SystemExit("--proj 1: single-GPU Kaczmarz++ configs only")
+        ctx.set_option(kpp.OPT_PROJ, 1)
+        ctx.set_option(kpp.OPT_TMAX, args.tmax)
     rht_ms = None
     if args.rht:
         ctx.enable_rht()  # one-time transform of A (not part of a step: the paper's Alg 5/3 line 2-3)
@@ -350,8 +362,10 @@ def main():
     achieved = bpi * total_iters / (p2max / 1e3) / 1e9 if p2max > 0 else None
     # per launch: one persistent launch per window of min(iters, window) iterations
     iters_per_launch = min(iters, 8192)
-    tr = ncu_traffic(cfg.name)
-    roof = {"bound": "hbm", "kernel": "Phase-2 persistent kernel (iterate_kernel / cdpp_stream_kernel)",
+    tr = ncu_traffic(cfg.name, "lsqr_persistent_kernel" if args.proj else "iterate_kernel")
+    kname = ("lsqr_persistent_kernel (t_max + 1 exchange rounds per iteration)" if args.proj
+             else "Phase-2 persistent kernel (iterate_kernel / cdpp_stream_kernel)")
+    roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": (achieved / hbm_peak) if achieved else None,
             "traffic": tr * iters_per_launch if tr else None,
@@ -361,14 +375,14 @@ def main():
             "iter_kernel_share": p2max / ms if ms > 0 else None}
     cpu = None
     if not args.no_cpu and not dist:
-        cpu = cpu_oracle_sample(cfg, A_keep.cpu().numpy(), b.cpu().numpy(), args.cpu_seconds)
+        cpu = cpu_oracle_sample(cfg, A_keep.cpu().numpy(), b.cpu().numpy(), args.cpu_seconds, args.proj, args.tmax)
     elif not args.no_cpu and dist and rank == 0:
         cpu = None  # N>1: the oracle baseline is reported by the N=1 run only
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(cfg, iters, world, dist),
+        "config": workload_config(cfg, iters, world, dist, args.proj, args.tmax),
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
