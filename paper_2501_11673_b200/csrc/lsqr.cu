@@ -9,10 +9,10 @@
 // selected (scaled by 1/sqrt(tau)), and A_hat A_hat^T goes through the batched DMMA GEMM.
 //
 // Phase 2 (per iteration): w_t = the first n entries of t_max steps of LSQR (Paige & Saunders) on
-// M z = R^{-T} r_t with M = R^{-T} [A_S, sqrt(lam) I], from zero.  Every LSQR step needs M v (a pass over
-// A_S and a reduction over all columns) and M^T u (a second pass) plus a norm over n: on the GPU that
-// is five small kernels per step (column-slab partials, fixed-order reductions, one-CTA s-vector
-// algebra), captured with the whole iteration into a CUDA graph.  Every sum has a fixed order.
+// M z = R^{-T} r_t with M = R^{-T} [A_S, sqrt(lam) I], from zero.  Every LSQR step needs M v and M^T u
+// (products with A_S, reduced over all columns) plus a norm over n: one persistent cooperative kernel
+// per window, t_max + 1 exchange rounds per iteration (see the Phase-2 section below and DESIGN.md
+// section 7).  Every sum has a fixed order.
 #include <cmath>
 #include <cstdint>
 
