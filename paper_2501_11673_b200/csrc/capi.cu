@@ -115,6 +115,7 @@ struct kpp_ctx {
   long long* d_trace = nullptr;
   // phase-1 workspace
   Buf p1;
+  Buf p1q;  // Q1 of the refined sub-batch (adaptive CholeskyQR2), sized on demand
   int* d_info = nullptr;
   long long info_cap = 0;
   // graph engine
@@ -317,7 +318,7 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   const size_t o_L = cqr2 ? carve((size_t)B * ss) : 0;
   const size_t o_X2 = cqr2 ? carve((size_t)B * ss) : 0;
   const size_t o_X = cqr2 ? carve((size_t)B * ss) : 0;
-  const size_t o_Q = cqr2 ? carve((size_t)B * s * n) : 0;
+  const size_t o_Q = (cqr2 && !adaptive) ? carve((size_t)B * s * n) : 0;  // adaptive: p1q
   const size_t wsb = chol_inv_workspace(s);
   const size_t o_W = wsb ? carve((size_t)B * wsb / sizeof(double)) : 0;
   const size_t o_X1c = adaptive ? carve((size_t)B * ss) : 0;         // refined sub-batch: X1, S, M
@@ -414,29 +415,43 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
     if (nref > 0) {
       // shifted CholeskyQR2 of A_aug = [A_S, sqrt(lam) I]:
       //   Q1 = R1^{-T} A_aug,  G2 = Q1 Q1^T = X1^T A_S A_S^T X1 + lam X1^T X1  (Q1 formed explicitly)
-      const int Bn = nref;
+      // Adaptive mode: Q1 (s x n per block) only for the refined blocks, in chunks of <= 16 GiB.
       double* L = (double*)(base + o_L);
       double* X2 = (double*)(base + o_X2);
       double* X = (double*)(base + o_X);
       double* Q = (double*)(base + o_Q);
-      Operand x1t{X1r, s, ss, nullptr, 0, 1}, as{ctx->A, ctx->lda, 0, Sr, s, 0};
-      launch_dgemm(st, Bn, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);  // Q1 = X1^T A_S (X1^T lower)
-      pp.mark("Q1");
-      Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
-      const int z2 = launch_dgemm(st, Bn, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
-      pp.mark("gram2");
-      Operand x1n{X1r, s, ss, nullptr, 0, 0};
-      launch_dgemm(st, Bn, s, s, s, x1t, x1n, L, s, ss, 1, 0, 1);  // X1^T X1 (X1^T lower)
-      const double lscale = (dist && ctx->rank != 0) ? 0.0 : ctx->lam;
-      launch_splitk_reduce(st, Bn, s, s, z2, part, ss, 0.0, L, lscale, ss, G, ss, 1);
-      pp.mark("reduce");
-      if (dist) CKS(allreduce(ctx, G, (size_t)Bn * ss));
-      launch_chol_trtri(st, Bn, G, X2, s, ctx->d_info + 0, W);  // R2, X2 = R2^{-1}
-      pp.mark("chol");
-      Operand x1a{X1r, s, ss, nullptr, 0, 0}, x2b{X2, s, ss, nullptr, 0, 0};
-      launch_dgemm(st, Bn, s, s, s, x1a, x2b, X, s, ss, 1, 0, 2);  // X = R^{-1} = X1 X2 (upper)
-      Operand xa{X, s, ss, nullptr, 0, 0}, xb{X, s, ss, nullptr, 0, 1};
-      launch_dgemm(st, Bn, s, s, s, xa, xb, Mr, s, ss, 1, 0, 2);  // M = X X^T
+      int chunk = nref;
+      if (adaptive) {
+        const long long qb = (long long)s * n * (long long)sizeof(double);
+        chunk = (int)std::max<long long>(1, std::min<long long>(nref, (16LL << 30) / qb));
+        CKS(ensure_buf(ctx, ctx->p1q, (size_t)chunk * qb));
+        Q = (double*)ctx->p1q.p;
+      }
+      for (int c0 = 0; c0 < nref; c0 += chunk) {
+        const int Bn = std::min(chunk, nref - c0);
+        const double* X1b = X1r + (long long)c0 * ss;
+        const int32_t* Sb = Sr + (long long)c0 * s;
+        double* Mb = Mr + (long long)c0 * ss;
+        Operand x1t{X1b, s, ss, nullptr, 0, 1}, as{ctx->A, ctx->lda, 0, Sb, s, 0};
+        launch_dgemm(st, Bn, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);  // Q1 = X1^T A_S (X1^T lower)
+        pp.mark("Q1");
+        Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
+        const int z2 = launch_dgemm(st, Bn, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
+        pp.mark("gram2");
+        Operand x1n{X1b, s, ss, nullptr, 0, 0};
+        launch_dgemm(st, Bn, s, s, s, x1t, x1n, L, s, ss, 1, 0, 1);  // X1^T X1 (X1^T lower)
+        const double lscale = (dist && ctx->rank != 0) ? 0.0 : ctx->lam;
+        launch_splitk_reduce(st, Bn, s, s, z2, part, ss, 0.0, L, lscale, ss, G, ss, 1);
+        pp.mark("reduce");
+        if (dist) CKS(allreduce(ctx, G, (size_t)Bn * ss));
+        launch_chol_trtri(st, Bn, G, X2, s, ctx->d_info + 0, W);  // R2, X2 = R2^{-1}
+        pp.mark("chol");
+        Operand x1a{X1b, s, ss, nullptr, 0, 0}, x2b{X2, s, ss, nullptr, 0, 0};
+        launch_dgemm(st, Bn, s, s, s, x1a, x2b, X, s, ss, 1, 0, 2);  // X = R^{-1} = X1 X2 (upper)
+        Operand xa{X, s, ss, nullptr, 0, 0}, xb{X, s, ss, nullptr, 0, 1};
+        launch_dgemm(st, Bn, s, s, s, xa, xb, Mb, s, ss, 1, 0, 2);  // M = X X^T
+      }
+      const int Bn = nref;
       if (Mr != Mout) launch_batch_move(st, Bn, Mr, Mout, list, ss * (long long)sizeof(double), 1);
       pp.mark("small");
     }
@@ -457,10 +472,11 @@ kpp_status phase1(kpp_ctx* ctx, long long k0, long long k1) {
   if (ctx->kind == KIND_KPP && ctx->proj == 1) CKS(lsqr_prepare(ctx));
   const long long s = ctx->s, n = ctx->n;
   const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor != 1 && ctx->proj == 0;
+  const bool qall = ctx->kind == KIND_KPP && ctx->factor == 0 && ctx->proj == 0;  // Q1 for every block
   // workspace of phase1_batch per block: split-K partials (Z s^2), G, X1 (+ L, X2, X, Q1 for CholeskyQR2)
   const long long Z = ctx->kind == KIND_KPP ? std::min<long long>(64, std::max<long long>(1, (n + 511) / 512)) : 1;
   const long long skw = (ctx->kind == KIND_KPP && ctx->proj == 1) ? ctx->lsqr_n2 * s + (long long)ctx->lsqr_tau * s : 0;
-  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 5 : 0)) * s * s + (cqr2 ? s * n + s : 0) + skw) +
+  const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 5 : 0)) * s * s + (qall ? s * n : 0) + (cqr2 ? s : 0) + skw) +
                               (long long)chol_inv_workspace((int)s) + 2048;
   long long Bmax = std::max<long long>(1, ctx->phase1_mb * (1LL << 20) / per_block);
   Bmax = std::min<long long>(Bmax, 4096);
@@ -1148,7 +1164,7 @@ void kpp_destroy(kpp_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   void* ptrs[] = {ctx->srht_d, ctx->srht_T, ctx->lsqr_buf, ctx->lsqr_ll, ctx->rht_A, ctx->rht_d, ctx->rht_v, ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
-                  ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->d_info};
+                  ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->p1q.p, ctx->d_info};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
