@@ -403,6 +403,9 @@ def main():
             phase1_flops(cfg, warm["n_blocks"], st.get("n_refined", 0) // max(1, args.steps)),
             st["phase1_ms"] / args.steps),
         "rht_preprocess_ms": rht_ms,
+        "phase2_engine": {0: "persistent cluster kernel", 1: "step-kernel graph", 2: "fused-exchange kernel (dist.cu)",
+                          3: "sketch + LSQR kernel"}.get(st.get("engine"), st.get("engine")),
+        "exchange": ("NVLink peer buffers (fused)" if st.get("xchg") else "NCCL allreduce") if dist else None,
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -75,8 +75,10 @@ typedef enum {
   KPP_OPT_PHASE1_MB = 7,  /* device workspace budget for a Phase-1 batch, MiB (default 4096) */
   KPP_OPT_RESIDENT = 8,   /* 1 (default): keep the block slab on chip across both passes when it
                              fits; 0: always stream A_S from HBM/L2 */
-  KPP_OPT_ENGINE = 9,     /* 0 (default on one GPU): persistent cluster kernel; 1: replayed CUDA
-                             graph of step kernels (the multi-GPU engine, NCCL between steps) */
+  KPP_OPT_ENGINE = 9,     /* -1 (default): automatic -- one GPU: 0; column-sharded: 2 when the peer
+                             buffers are mapped, else 1.  0: persistent cluster kernel (one GPU);
+                             1: replayed CUDA graph of step kernels (exchange per KPP_OPT_XCHG);
+                             2: persistent kernel with the cross-GPU exchange fused in (dist.cu) */
   KPP_OPT_CLUSTER = 10,   /* 0 (default): choose the thread-block cluster size automatically;
                              1, 2, 4, 8 or 16: force it (the grid shrinks to co-resident clusters) */
   KPP_OPT_YGL = 11,       /* where the persistent kernel computes y = M r: -1 (default) automatic;
@@ -91,6 +93,11 @@ typedef enum {
                              R^{-1} of the sketch factor. */
   KPP_OPT_TMAX = 14,      /* LSQR steps per iteration t_max (default 8) */
   KPP_OPT_TAU = 15,       /* sketch size tau (default 0 = 2 s); before the first solve only */
+  KPP_OPT_XCHG = 16,      /* column-sharded contexts: the per-iteration exchange of the s-vector.
+                             1 (default): fused into the reduce kernel -- each rank stores its tagged partial
+                             into every rank's receive buffer over NVLink (CUDA IPC mappings made at setup)
+                             and sums the ranks in rank order; 0: ncclAllReduce between kernels.  Falls back
+                             to 0 when the buffers cannot be mapped (stats.xchg tells which runs). */
   KPP_OPT_REASSOC = 12,   /* CD++ only.  1 (default): blocks that stream from HBM use the kernel that
                              re-associates r_{t+1} = A_{S'} (x_t + eta c m_t) - (1 + eta c) A[S', S] y_t
                              - b_{S'} (exact in real arithmetic, from Alg 3 l.11-13 P:756-759) so the
@@ -167,6 +174,9 @@ typedef struct {
   int32_t reassoc;       /* 1 if the CD++ re-associated streaming kernel runs (KPP_OPT_REASSOC) */
   int64_t n_refined;     /* blocks that received the second CholeskyQR pass (since reset) */
   double rht_ms;         /* device time of the randomized Hadamard preprocessing (kpp_enable_rht) */
+  int32_t xchg;          /* column-sharded: 1 fused NVLink peer exchange, 0 NCCL allreduce */
+  int32_t engine;        /* Phase-2 engine of the last solve: 0 persistent, 1 step graph, 2 fused exchange,
+                            3 sketch + LSQR */
 } kpp_stats;
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */

@@ -19,13 +19,14 @@ __all__ = [
     "KppError", "Ctx", "SolveResult", "kpp_setup", "cdpp_setup", "kpp_solve", "cdpp_solve",
     "kpp_destroy", "kpp_get_unique_id", "kpp_setup_dist", "cdpp_setup_dist", "load_library",
     "OPT_ACCEL", "OPT_MEMO", "OPT_ETA", "OPT_RHO_FIXED", "OPT_FACTOR", "OPT_WINDOW",
-    "OPT_PHASE1_MB", "OPT_RESIDENT", "OPT_ENGINE", "OPT_CLUSTER", "OPT_YGL", "OPT_REASSOC", "OPT_PROJ", "OPT_TMAX", "OPT_TAU",
+    "OPT_PHASE1_MB", "OPT_RESIDENT", "OPT_ENGINE", "OPT_CLUSTER", "OPT_YGL", "OPT_REASSOC", "OPT_PROJ", "OPT_TMAX", "OPT_TAU", "OPT_XCHG",
 ]
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENOTPD, EDIVERGED, EMAXITER = range(8)
 OPT_ACCEL, OPT_MEMO, OPT_ETA, OPT_RHO_FIXED, OPT_FACTOR, OPT_WINDOW, OPT_PHASE1_MB, OPT_RESIDENT = range(1, 9)
 OPT_ENGINE = 9  # 0: persistent kernel (1 GPU default); 1: graph of step kernels (+NCCL)
 OPT_CLUSTER = 10  # 0: automatic; 1/2/4/8/16: forced thread-block cluster size
+OPT_XCHG = 16  # column-sharded exchange: 1 fused NVLink peer exchange (default), 0 NCCL
 OPT_PROJ, OPT_TMAX, OPT_TAU = 13, 14, 15  # K++ projection: 1 = sketch + LSQR (Alg 6), t_max, tau
 OPT_REASSOC = 12  # CD++: 1 re-associated streaming kernel when blocks stream (default), 0 off, 2 always
 OPT_YGL = 11  # -1: automatic; 0: y = M r per cluster; 1: once per GPU (L2 gather); 4: per cluster from partials
@@ -47,7 +48,8 @@ class _Stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64), ("grid_ctas", ctypes.c_int32),
                 ("resident", ctypes.c_int32), ("cluster", ctypes.c_int32), ("m_in_smem", ctypes.c_int32),
                 ("tma", ctypes.c_int32), ("ygl", ctypes.c_int32), ("reassoc", ctypes.c_int32),
-                ("n_refined", ctypes.c_int64), ("rht_ms", ctypes.c_double)]
+                ("n_refined", ctypes.c_int64), ("rht_ms", ctypes.c_double), ("xchg", ctypes.c_int32),
+                ("engine", ctypes.c_int32)]
 
 
 def load_library():

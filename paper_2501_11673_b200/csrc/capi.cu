@@ -58,7 +58,7 @@ struct kpp_ctx {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   // options
-  int accel = 1, memo = 1, factor = 2, resident_opt = 1, engine = 0, cluster_opt = 0, ygl_opt = -1, reassoc = 1;
+  int accel = 1, memo = 1, factor = 2, resident_opt = 1, engine = -1, cluster_opt = 0, ygl_opt = -1, reassoc = 1;
   double eta_opt = -1.0, rho_fixed = -1.0;
   long long window = 8192, phase1_mb = 4096;
   cudaStream_t stream = nullptr;
@@ -122,7 +122,16 @@ struct kpp_ctx {
   cudaGraphExec_t gexec = nullptr;
   int graph_unroll = 0;
   const void* gkey[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-  double gkeyv[3] = {0, 0, 0};
+  double gkeyv[4] = {0, 0, 0, 0};
+  // fused cross-GPU exchange (steps.cu peer mode): own LL receive buffer, the peers' buffers mapped
+  // through CUDA IPC, and a one-double scratch for the start-of-solve barrier
+  unsigned long long* xeng_ll = nullptr;  // engine 2: LL words of the grid exchange
+  long long xeng_ll_cap = 0;
+  int xchg = 1;                  // KPP_OPT_XCHG: 1 peer exchange when available, 0 NCCL allreduce
+  int peer_ok = 0;
+  unsigned long long* peer_buf = nullptr;
+  unsigned long long* peer_map[KPP_MAX_PEERS] = {};
+  double* peer_bar = nullptr;
   // events / stats
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   kpp_stats stats{};
@@ -235,6 +244,57 @@ kpp_status ensure_sched(kpp_ctx* ctx, long long count) {
   return KPP_OK;
 }
 
+// Peer exchange setup (collective over the context's ranks): allocate this rank's LL receive buffer,
+// all-gather the CUDA IPC handles through NCCL, map every peer's buffer.  Any failure (no P2P, too
+// many ranks) leaves peer_ok = 0 and the per-iteration exchange on the NCCL allreduce.
+kpp_status peer_setup(kpp_ctx* ctx) {
+  const int R = ctx->nranks;
+  if (R > KPP_MAX_PEERS || getenv("KPP_NO_PEER")) return KPP_OK;
+  const size_t words = 4ULL * R * ctx->s;
+  CK(cudaMalloc((void**)&ctx->peer_buf, words * sizeof(unsigned long long)));
+  CK(cudaMemset(ctx->peer_buf, 0, words * sizeof(unsigned long long)));
+  CKS(dalloc(ctx, &ctx->peer_bar, 1));
+  CK(cudaMemset(ctx->peer_bar, 0, sizeof(double)));
+  ctx->peer_map[ctx->rank] = ctx->peer_buf;
+  int ok = 1;
+  if (R > 1) {
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, ctx->peer_buf));
+    char* dh = nullptr;
+    CK(cudaMalloc((void**)&dh, sizeof(h) * R));
+    CK(cudaMemcpy(dh + sizeof(h) * ctx->rank, &h, sizeof(h), cudaMemcpyHostToDevice));
+    CKN(ncclAllGather(dh + sizeof(h) * ctx->rank, dh, sizeof(h), ncclChar, ctx->comm, ctx->stream));
+    std::vector<cudaIpcMemHandle_t> hs((size_t)R);
+    CK(cudaMemcpyAsync(hs.data(), dh, sizeof(h) * R, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(dh);
+    for (int r = 0; r < R; ++r) {
+      if (r == ctx->rank) continue;
+      void* ptr = nullptr;
+      if (cudaIpcOpenMemHandle(&ptr, hs[(size_t)r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      ctx->peer_map[r] = (unsigned long long*)ptr;
+    }
+    // every rank must agree on the mode: min over ranks
+    double* d = nullptr;
+    CK(cudaMalloc((void**)&d, sizeof(double)));
+    const double okd = ok;
+    CK(cudaMemcpy(d, &okd, sizeof(double), cudaMemcpyHostToDevice));
+    CKN(ncclAllReduce(d, d, 1, ncclDouble, ncclMin, ctx->comm, ctx->stream));
+    double all = 0.0;
+    CK(cudaMemcpyAsync(&all, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d);
+    ok = all > 0.5;
+  }
+  ctx->peer_ok = ok;
+  ctx->stats.xchg = ok && ctx->xchg;
+  return KPP_OK;
+}
+
 kpp_status allreduce(kpp_ctx* ctx, double* buf, size_t count) {
   if (ctx->nranks <= 1 && !ctx->comm) return KPP_OK;
   CKN(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
@@ -301,6 +361,8 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   (void)tiles_up;
   int Z = 1;
   if (ctx->kind == KIND_KPP) Z = (int)std::min<long long>(64, std::max<long long>(1, (n + 511) / 512));
+  if (const char* ez = getenv("KPP_GRAM_KCHUNK"))  // experiment: K chunk per split
+    if (ctx->kind == KIND_KPP) Z = (int)std::min<long long>(64, std::max<long long>(1, (n + atoi(ez) - 1) / atoi(ez)));
   // factor 0: shifted CholeskyQR2 for every block; 2 (default): the second CholeskyQR pass only for
   // blocks whose estimated u * kappa(A_S)^2 exceeds 1e-11;
   // 1: the literal Gram + Cholesky for every block
@@ -686,7 +748,7 @@ kpp_status plan_cdpp_stream(kpp_ctx* ctx) {
 }
 
 bool use_cdpp_stream(const kpp_ctx* ctx) {
-  return ctx->kind == KIND_CDPP && ctx->cs_ok && ctx->engine == 0 && ctx->nranks == 1 &&
+  return ctx->kind == KIND_CDPP && ctx->cs_ok && ctx->engine <= 0 && ctx->nranks == 1 &&
          (ctx->reassoc == 2 || (ctx->reassoc == 1 && !ctx->pplan.resident));
 }
 
@@ -757,7 +819,7 @@ kpp_status build_graph(kpp_ctx* ctx, const StepParams& sp, int U) {
   for (int u = 0; u < U; ++u) {
     launch_step_partial(cs, sp);
     launch_step_reduce(cs, sp);
-    if (ctx->comm) {
+    if (ctx->comm && !sp.peer) {
       ncclResult_t rr = ncclAllReduce(sp.rsum, sp.rsum, (size_t)ctx->s, ncclDouble, ncclSum, ctx->comm, cs);
       if (rr != ncclSuccess) {
         cudaStreamEndCapture(cs, &g);
@@ -885,8 +947,30 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   const double eta = ctx->accel ? (ctx->eta_opt >= 0.0 ? ctx->eta_opt : (double)ctx->s / (2.0 * (double)ctx->n_global)) : 0.0;
   const long long W = std::max<long long>(1, ctx->window);
   const bool use_lsqr = ctx->kind == KIND_KPP && ctx->proj == 1;
-  const bool use_graph = !use_lsqr && (ctx->engine == 1 || ctx->nranks > 1);
+  // engine: -1 automatic (one GPU: persistent kernel; column-sharded: the fused-exchange kernel
+  // when the peer buffers are mapped, else the graph of step kernels with NCCL)
+  int eng = ctx->engine;
+  if (eng < 0) eng = ctx->nranks > 1 ? ((ctx->xchg && ctx->peer_ok) ? 2 : 1) : 0;
+  if (eng == 0 && ctx->nranks > 1) eng = 1;
+  if (eng == 2 && !ctx->peer_buf) {
+    if (ctx->nranks > 1) eng = 1;  // no peer mapping: NCCL engine
+    else CKS(peer_setup(ctx));      // one rank: a self-mapped buffer
+  }
+  const bool use_xeng = !use_lsqr && eng == 2;
+  const bool use_graph = !use_lsqr && eng == 1;
+  ctx->stats.engine = use_lsqr ? 3 : eng;
   if (use_lsqr) CKS(lsqr_prepare(ctx));
+  if (use_xeng) {
+    const long long words = (long long)xeng_ll_words((int)ctx->s, ctx->grid);
+    if (words > ctx->xeng_ll_cap) {
+      if (ctx->xeng_ll) cudaFree(ctx->xeng_ll);
+      CK(cudaMalloc((void**)&ctx->xeng_ll, (size_t)words * sizeof(unsigned long long)));
+      ctx->xeng_ll_cap = words;
+    }
+    // fresh tags for this solve: clear the receive buffer, then (multi-rank) a barrier
+    CK(cudaMemsetAsync(ctx->peer_buf, 0, 4ULL * ctx->nranks * ctx->s * sizeof(unsigned long long), st));
+    if (ctx->comm) CKN(ncclAllReduce(ctx->peer_bar, ctx->peer_bar, 1, ncclDouble, ncclSum, ctx->comm, st));
+  }
   float p1ms = 0.f, p2ms = 0.f;
   DevState fin = hs;
   for (long long t0 = 0; t0 < max_iters; t0 += W) {
@@ -899,7 +983,41 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     p1ms += ms;
     CK(cudaEventRecord(ctx->ev0, st));
-    if (use_lsqr) {
+    if (use_xeng) {
+      XParams q{};
+      q.A = ctx->A; q.lda = ctx->lda; q.n = n; q.s = (int)ctx->s; q.cd = ctx->kind == KIND_CDPP;
+      q.grid = ctx->grid; q.slab = ctx->slab; q.col_base = ctx->col_begin;
+      q.b = b_dev; q.tol2bb = tol * tol * bb; q.bb = bb;
+      q.S_pool = ctx->S_pool; q.M_pool = ctx->M_pool; q.bid = ctx->bid;
+      q.t0 = t0; q.t1 = t0 + cnt; q.t_base = t0;
+      q.x = ctx->x; q.mom = ctx->mom; q.eta = eta; q.zeta = ctx->zeta;
+      q.adaptive = ctx->rho_fixed < 0.0; q.writer = ctx->rank == 0;
+      q.ll = ctx->xeng_ll; q.rank = ctx->rank; q.nranks = ctx->nranks;
+      for (int r = 0; r < KPP_MAX_PEERS; ++r) q.peer_recv[r] = ctx->peer_map[r];
+      q.err = ctx->d_err; q.st = ctx->dstate;
+      q.hist_res = ctx->hist_res; q.hist_rho = ctx->hist_rho; q.hist_cap = ctx->hist_capd;
+      const size_t budget = 227 * 1024 - 4096;
+      q.sl = ctx->slab;
+      const size_t fixed = xeng_smem_bytes(q.s, 0, q.sl, 0);
+      const size_t as_b = (size_t)q.s * q.sl * sizeof(double), m_b = (size_t)q.s * q.s * sizeof(double);
+      // shared memory: the double-buffered slab of A_S first (the next block streams in behind the
+      // current iteration), then M (y computed by every CTA instead of spread over the grid)
+      q.a_smem = fixed + 2 * as_b <= budget ? 2 : (!q.cd && fixed + as_b <= budget) ? 1 : 0;
+      if (const char* ea = getenv("KPP_XENG_ASMEM")) q.a_smem = std::min(q.a_smem, atoi(ea));
+      q.m_smem = q.s % 2 == 0 && fixed + (size_t)q.a_smem * as_b + m_b <= budget;
+      if (getenv("KPP_XENG_NO_MSMEM")) q.m_smem = 0;
+      q.pf_at = 1;
+      if (const char* ep = getenv("KPP_XENG_PF")) q.pf_at = atoi(ep);
+      if (getenv("KPP_PHASE_PROFILE")) {
+        if (!ctx->d_prof) {
+          CKS(dalloc(ctx, &ctx->d_prof, 16));
+          CK(cudaMemset(ctx->d_prof, 0, 16 * sizeof(long long)));
+        }
+        q.prof = ctx->d_prof;
+      }
+      CK(launch_xeng_window(st, q));
+      ctx->stats.iter_launches += 1;
+    } else if (use_lsqr) {
       // K++ with Proj = Alg 6: one persistent cooperative launch per window
       LsqrParams q = lsqr_params(ctx, b_dev, tol * tol * bb, bb, eta);
       q.t0 = t0; q.t1 = t0 + cnt; q.t_base = t0;
@@ -967,7 +1085,18 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       sp.part = ctx->part; sp.rsum = ctx->r; sp.y = ctx->y; sp.st = ctx->dstate; sp.sp = ctx->dstep;
       sp.hist_res = ctx->hist_res; sp.hist_rho = ctx->hist_rho; sp.hist_cap = ctx->hist_capd;
       // the graph bakes in pointers and scalars: re-capture when any of them changed
-      const double keyv[3] = {sp.tol2bb, sp.eta, (double)sp.adaptive};
+      sp.peer = ctx->xchg && ctx->peer_ok;
+      sp.rank = ctx->rank;
+      sp.nranks = ctx->nranks;
+      sp.err = ctx->d_err;
+      for (int r = 0; r < KPP_MAX_PEERS; ++r) sp.peer_recv[r] = ctx->peer_map[r];
+      if (sp.peer && t0 == 0) {
+        // fresh tags for this solve: every rank clears its receive buffer, then a barrier, before
+        // any rank publishes (tags are t + 1)
+        CK(cudaMemsetAsync(ctx->peer_buf, 0, 4ULL * ctx->nranks * ctx->s * sizeof(unsigned long long), st));
+        CKN(ncclAllReduce(ctx->peer_bar, ctx->peer_bar, 1, ncclDouble, ncclSum, ctx->comm, st));
+      }
+      const double keyv[4] = {sp.tol2bb, sp.eta, (double)sp.adaptive, (double)sp.peer};
       const void* key[5] = {ctx->S_pool, ctx->M_pool, b_dev, ctx->hist_res, ctx->bid};
       if (ctx->gexec && (memcmp(key, ctx->gkey, sizeof key) != 0 || memcmp(keyv, ctx->gkeyv, sizeof keyv) != 0)) {
         cudaGraphExecDestroy(ctx->gexec);
@@ -1037,7 +1166,9 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
                                 "ch:A", "-", "ch:gather", "ch:r_wait", "ch:y_rows", "ch:y_gather", "ch:barrier", "-"};
     const char* names_ls[16] = {"r0_pass", "r0_xchg", "r0_spart", "pass", "xchg", "rot", "spart", "update", "-", "-", "-", "-",
                                 "-", "-", "-", "-"};
-    const char* const* names = use_lsqr ? names_ls : use_cdpp_stream(ctx) ? names_cs : names_it;
+    const char* names_x[16] = {"a_rowsums", "b_exchange", "d_solve", "e_update", "f_window", "-", "-", "-",
+                               "-", "-", "-", "-", "-", "-", "-", "-"};
+    const char* const* names = use_xeng ? names_x : use_lsqr ? names_ls : use_cdpp_stream(ctx) ? names_cs : names_it;
     fprintf(stderr, "[kpp phase cycles/iter, CTA 0]");
     for (int i = 0; i < 16; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
     fprintf(stderr, "\n");
@@ -1097,6 +1228,7 @@ static kpp_status setup_any(kpp_ctx** out, int kind, const double* A, long long 
     memcpy(&uid, id, sizeof uid);
     ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, uid, rank);
     if (r != ncclSuccess) st = fail(ctx, KPP_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    if (st == KPP_OK) st = peer_setup(ctx);
   }
   if (st != KPP_OK) {
     kpp_destroy(ctx);
@@ -1161,6 +1293,10 @@ kpp_status cdpp_solve(kpp_ctx* ctx, const double* b, const double* x0, int64_t m
 void kpp_destroy(kpp_ctx* ctx) {
   if (!ctx) return;
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  for (int r = 0; r < KPP_MAX_PEERS; ++r)
+    if (ctx->peer_map[r] && r != ctx->rank) cudaIpcCloseMemHandle(ctx->peer_map[r]);
+  if (ctx->peer_buf) cudaFree(ctx->peer_buf);
+  if (ctx->xeng_ll) cudaFree(ctx->xeng_ll);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   void* ptrs[] = {ctx->srht_d, ctx->srht_T, ctx->lsqr_buf, ctx->lsqr_ll, ctx->rht_A, ctx->rht_d, ctx->rht_v, ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
@@ -1228,6 +1364,11 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
       if (v < 0 || ctx->lsqr_ready) return KPP_EINVAL;  // fixed once the sketch exists
       ctx->tau_opt = (int)v;
       return KPP_OK;
+    case KPP_OPT_XCHG:
+      if (v != 0.0 && v != 1.0) return KPP_EINVAL;
+      ctx->xchg = (int)v;
+      ctx->stats.xchg = ctx->xchg && ctx->peer_ok;
+      return KPP_OK;
     case KPP_OPT_REASSOC:
       if (v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;
       ctx->reassoc = (int)v;
@@ -1238,7 +1379,7 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
       ctx->ygl_opt = (int)v;
       return plan_persistent(ctx);
     case KPP_OPT_ENGINE:
-      if (v != 0.0 && v != 1.0) return KPP_EINVAL;
+      if (v != -1.0 && v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;
       ctx->engine = (int)v;
       break;
     default: return KPP_EINVAL;

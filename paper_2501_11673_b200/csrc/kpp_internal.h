@@ -159,6 +159,7 @@ struct DevStep {
   long long t_end;   // end of the current window
   long long t_base;  // iteration of bid[0]
 };
+constexpr int KPP_MAX_PEERS = 8;
 struct StepParams {
   const double* A;
   long long lda, m, n;
@@ -183,9 +184,47 @@ struct StepParams {
   double* hist_res;
   double* hist_rho;
   long long hist_cap;
+  // fused cross-GPU exchange (KPP_OPT_XCHG = 1): every rank's LL receive buffer
+  // [2 (iteration parity)][nranks][s] x 2 words, mapped into this process (peer_recv[rank] = own)
+  int peer, rank, nranks;
+  unsigned long long* peer_recv[KPP_MAX_PEERS];
+  int* err;
 };
+// ------------------------------------------------------------------ dist.cu (engine 2)
+struct XParams {
+  const double* A;
+  long long lda, n;  // n: local columns (the rank's slab)
+  int s, cd, grid, slab;
+  long long col_base;
+  const double* b;
+  double tol2bb, bb;
+  const int32_t* S_pool;
+  const double* M_pool;
+  const int32_t* bid;
+  long long t0, t1, t_base;
+  double* x;
+  double* mom;
+  double eta;
+  long long zeta;
+  int adaptive, writer;
+  unsigned long long* ll;  // [grid][s] x 2 words (local grid exchange)
+  int rank, nranks;
+  unsigned long long* peer_recv[KPP_MAX_PEERS];  // every rank's [2][nranks][s] x 2 words, mapped here
+  int a_smem, sl, m_smem;
+  int pf_at;  // where the next slab's prefetch is issued: 0 after (a), 1 after (b), 2 after (d)
+  int* err;
+  DevState* st;
+  double* hist_res;
+  double* hist_rho;
+  long long hist_cap;
+  long long* prof;
+};
+size_t xeng_smem_bytes(int s, int a_smem, int sl, int m_smem);
+size_t xeng_ll_words(int s, int grid);
+cudaError_t launch_xeng_window(cudaStream_t st, const XParams& p);
+
 void launch_step_partial(cudaStream_t st, const StepParams& p);
-void launch_step_reduce(cudaStream_t st, const StepParams& p);   // rsum = sum_g part[g]
+void launch_step_reduce(cudaStream_t st, const StepParams& p);   // rsum = sum_g part[g] (peer: + sum over ranks)
 void launch_step_solve(cudaStream_t st, const StepParams& p);    // y = M (rsum - b_S)
 void launch_step_update(cudaStream_t st, const StepParams& p);   // w, momentum, x
 void launch_step_window(cudaStream_t st, const StepParams& p);   // e, checkpoint, t_cur++

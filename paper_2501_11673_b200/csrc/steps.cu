@@ -48,6 +48,19 @@ __global__ void __launch_bounds__(ST_THREADS) step_partial_kernel(StepParams p) 
   }
 }
 
+__device__ __noinline__ void peer_fail(int* err) {
+  atomicExch(err, 4);
+  __trap();
+}
+
+// rsum[k] = sum_g part[g][k] (fixed order).  Peer mode (the B200-native replacement of the NCCL
+// allreduce between this kernel and the solve): lane 0 publishes the rank's sum as two
+// tagged 8-byte words (32 data bits + 32-bit tag t+1; an aligned 8-byte store is single-copy atomic,
+// so seeing the tag means seeing the data) into slot [t mod 2][rank][k] of EVERY rank's receive
+// buffer over NVLink (system-scope stores to the peers' mapped memory), then lanes r < nranks poll
+// slot [t mod 2][r][k] of the local buffer and the warp sums the ranks in rank order -- the same
+// bits on every rank.  Two parity slots suffice: a rank can only publish t+2 after every rank has
+// published t+1, i.e. after every rank has consumed t.
 __global__ void __launch_bounds__(ST_THREADS) step_reduce_kernel(StepParams p) {
   long long t;
   if (!step_active(p.st, p.sp, &t)) return;
@@ -57,7 +70,41 @@ __global__ void __launch_bounds__(ST_THREADS) step_reduce_kernel(StepParams p) {
   double acc = 0.0;
   for (int q = lane; q < p.grid; q += 32) acc += p.part[(long long)q * p.s + kk];
   acc = wsum(acc);
-  if (lane == 0) p.rsum[kk] = acc;
+  if (!p.peer) {
+    if (lane == 0) p.rsum[kk] = acc;
+    return;
+  }
+  const unsigned tag = (unsigned)(t + 1);
+  const long long slot = ((long long)(t & 1) * p.nranks) * p.s;
+  if (lane < p.nranks) {  // lane r stores into rank r's buffer
+    const unsigned long long u = (unsigned long long)__double_as_longlong(acc);
+    const unsigned long long tg = (unsigned long long)tag << 32;
+    unsigned long long* dst = p.peer_recv[lane] + 2 * (slot + (long long)p.rank * p.s + kk);
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};\n" ::"l"(dst), "l"(tg | (u & 0xffffffffull)),
+                 "l"(tg | (u >> 32))
+                 : "memory");
+  }
+  double v = 0.0;
+  if (lane < p.nranks) {
+    const unsigned long long* src = p.peer_recv[p.rank] + 2 * (slot + (long long)lane * p.s + kk);
+    unsigned long long a, b;
+    unsigned long long t0 = 0;
+    unsigned n = 0;
+    for (;;) {
+      asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+      if ((unsigned)(a >> 32) == tag && (unsigned)(b >> 32) == tag) break;
+      if (n == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      if ((++n & 1023u) == 0) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > 20000000000ull) peer_fail(p.err);
+      }
+    }
+    v = __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
+  }
+  double tot = 0.0;  // ranks in order 0 .. nranks-1
+  for (int r = 0; r < p.nranks; ++r) tot += __shfl_sync(0xffffffffu, v, r);
+  if (lane == 0) p.rsum[kk] = tot;
 }
 
 __global__ void __launch_bounds__(ST_THREADS) step_solve_kernel(StepParams p) {

@@ -187,12 +187,37 @@ def test_engines_agree(kpp, ora, cfg):
     A, b, _ = synth.make_problem(cfg)
     ref = (ora.cdpp_run if cfg.kind == "cdpp" else ora.kpp_run)(A.numpy(), b.numpy(), cfg.s, max_iters=300, threads=8)
     outs = []
-    for eng in (0, 1):
+    for eng in (0, 1, 2):
         ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A.to(DEV), cfg.s, 1e-8, 0)
         ctx.set_option(kpp.OPT_ENGINE, eng)
         outs.append(ctx.solve(b.to(DEV), max_iters=300).x.cpu().numpy())
+        assert ctx.stats()["engine"] == eng
         assert rel(outs[-1], ref.x) <= 1e-10, eng
     assert rel(outs[0], outs[1]) <= 1e-10
+    assert rel(outs[0], outs[2]) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg", TWINS, ids=[c.name for c in TWINS])
+def test_fused_exchange_engine(kpp, ora, cfg):
+    """Engine 2 (dist.cu: grid reduce + peer-buffer exchange + replicated solve in one persistent
+    kernel; the multi-GPU default) on one GPU, self-mapped, against the oracle; a second solve on the
+    same context re-arms the tags and gives the same bits."""
+    A, b, _ = synth.make_problem(cfg)
+    T = 200
+    if cfg.kind == "cdpp":
+        ctx = kpp.cdpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+        ref = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8)
+    else:
+        ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+        ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8)
+    ctx.set_option(kpp.OPT_ENGINE, 2)
+    ctx.set_option(kpp.OPT_WINDOW, 64)  # several launches per solve
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    assert ctx.stats()["engine"] == 2
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    x1 = res.x.clone()
+    assert torch.equal(ctx.solve(b.to(DEV), max_iters=T).x, x1)
 
 
 def test_deterministic_and_warm_cache(kpp):
@@ -404,10 +429,28 @@ def test_dist_path_single_rank(kpp, ora, cfg):
     else:
         ctx = kpp.kpp_setup_dist(A.to(DEV), A.shape[0], n, 0, n, cfg.s, cfg.lam, 0, uid, 0, 1)
         ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=300, threads=8)
+    ctx.set_option(kpp.OPT_ENGINE, 1)  # one rank would otherwise run the persistent kernel
+    assert ctx.stats()["xchg"] == 1  # the fused peer exchange (self-mapped with one rank)
+    res2 = ctx.solve(b.to(DEV), max_iters=300)
+    assert ctx.stats()["engine"] == 1
+    ctx.set_option(kpp.OPT_ENGINE, 2)  # the multi-rank default: fused-exchange persistent kernel
+    res_e2 = ctx.solve(b.to(DEV), max_iters=300)
+    assert ctx.stats()["engine"] == 2
+    assert rel(res_e2.x.cpu().numpy(), ref.x) <= 1e-10
+    assert rel(res_e2.x.cpu().numpy(), res2.x.cpu().numpy()) <= 1e-12
+    ctx.set_option(kpp.OPT_ENGINE, 1)
     res = ctx.solve(b.to(DEV), max_iters=300)
     assert res.iters == 300
     assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
     assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    # the same solve with the NCCL allreduce between kernels: identical bits (rank-order sums)
+    x_peer = res.x.clone()
+    res2 = ctx.solve(b.to(DEV), max_iters=300)  # a second solve re-arms the tags
+    assert torch.equal(res2.x, x_peer)
+    ctx.set_option(kpp.OPT_XCHG, 0)
+    assert ctx.stats()["xchg"] == 0
+    res3 = ctx.solve(b.to(DEV), max_iters=300)
+    assert torch.equal(res3.x, x_peer)
     ctx.destroy()
 
 
