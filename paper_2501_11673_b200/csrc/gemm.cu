@@ -173,6 +173,34 @@ __device__ __forceinline__ void stage_tile(double* sm, const double* base, long 
   }
 }
 
+// KC tiles (k contiguous in memory): the memory row of each of the thread's chunks is fixed across
+// the K loop, so it is resolved once (row gather included) into NI registers; -1 = out of range.
+template <int OUTER>
+struct KcRows {
+  static constexpr int NI = OUTER * (B2K / 2) / B2T;
+  int r[NI];
+  __device__ __forceinline__ void init(const int32_t* idx, int outer0, int outer_lim) {
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int go = outer0 + (threadIdx.x + B2T * i) / (B2K / 2);
+      r[i] = go < outer_lim ? (idx ? idx[go] : go) : -1;
+    }
+  }
+};
+template <int OUTER>
+__device__ __forceinline__ void stage_tile_kc(double* sm, const double* base, long long ld, const KcRows<OUTER>& rows,
+                                              int k0, int k_lim) {
+#pragma unroll
+  for (int i = 0; i < KcRows<OUTER>::NI; ++i) {
+    const int c = threadIdx.x + B2T * i;
+    const int o = c / (B2K / 2), kc = (c % (B2K / 2)) * 2;
+    const int gk = k0 + kc;
+    const int valid = rows.r[i] >= 0 ? min(2, max(0, k_lim - gk)) : 0;
+    const double* src = valid ? base + (long long)rows.r[i] * ld + gk : base;
+    cp_async16z(sm + o * KC_LD + kc, src, valid * 8);
+  }
+}
+
 // ATRI: 0 general A; 1 logical A lower triangular (A(i,k) = 0 for k > i); 2 upper (A(i,k) = 0 for
 // k < i) -- the K range of each row tile / warp is clipped (the stored zeros are skipped, not
 // assumed).  Epilogue: C = alpha * A B (+ C when beta1).
@@ -210,12 +238,19 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
   const bool wskip = upper_only && wrow0 >= wcol0 + 32;
   const int wrow_end = wrow0 + 32;
   // A logical (i,k): !AT -> memory row i (k contiguous); B logical (k,j): BT -> memory row j
+  KcRows<B2M> arows;
+  KcRows<B2N> brows;
+  if (!AT) arows.init(aidx, tm * B2M, M);
+  if (BT) brows.init(bidx, tn * B2N, N);
+  auto stage = [&](int slot, int k0) {
+    if (!AT) stage_tile_kc<B2M>(As + slot * A_STAGE, abase, a.ld, arows, k0, kend);
+    else stage_tile<false, B2M, AM_LD>(As + slot * A_STAGE, abase, a.ld, aidx, tm * B2M, M, k0, kend);
+    if (BT) stage_tile_kc<B2N>(Bs + slot * B_STAGE, bbase, b.ld, brows, k0, kend);
+    else stage_tile<false, B2N, BN_LD>(Bs + slot * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, k0, kend);
+  };
 #pragma unroll
   for (int st = 0; st < B2S - 1; ++st) {
-    if (st < nk) {
-      stage_tile<!AT, B2M, AM_LD>(As + st * A_STAGE, abase, a.ld, aidx, tm * B2M, M, kbeg_t + st * B2K, kend);
-      stage_tile<BT, B2N, BN_LD>(Bs + st * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, kbeg_t + st * B2K, kend);
-    }
+    if (st < nk) stage(st, kbeg_t + st * B2K);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
   for (int kt = 0; kt < nk; ++kt) {
@@ -223,11 +258,7 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
     __syncthreads();
     {
       const int ln = kt + B2S - 1;
-      if (ln < nk) {
-        const int sl = ln % B2S;
-        stage_tile<!AT, B2M, AM_LD>(As + sl * A_STAGE, abase, a.ld, aidx, tm * B2M, M, kbeg_t + ln * B2K, kend);
-        stage_tile<BT, B2N, BN_LD>(Bs + sl * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, kbeg_t + ln * B2K, kend);
-      }
+      if (ln < nk) stage(ln % B2S, kbeg_t + ln * B2K);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     const double* Ast = As + (kt % B2S) * A_STAGE;
