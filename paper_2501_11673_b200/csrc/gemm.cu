@@ -142,6 +142,7 @@ constexpr int BN_LD = B2N + 4;      // [k][outer] row stride of B
 constexpr int A_STAGE = (B2M * KC_LD > B2K * AM_LD) ? B2M * KC_LD : B2K * AM_LD;  // doubles
 constexpr int B_STAGE = (B2N * KC_LD > B2K * BN_LD) ? B2N * KC_LD : B2K * BN_LD;
 constexpr size_t B2_SMEM = (size_t)B2S * (A_STAGE + B_STAGE) * sizeof(double);
+constexpr int KIDX_MAX = 1024;      // K-gathered operand: staged gather list (s <= 1024)
 
 __device__ __forceinline__ void cp_async16z(double* dst, const double* src, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
@@ -242,11 +243,25 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
   KcRows<B2N> brows;
   if (!AT) arows.init(aidx, tm * B2M, M);
   if (BT) brows.init(bidx, tn * B2N, N);
+  // operands whose memory rows run along K with a row gather: the CTA's K range of the gather list
+  // is staged in shared memory once (the per-stage address then needs no global load)
+  __shared__ int32_t kidx_sh[KIDX_MAX];
+  const int32_t* kidx_a = nullptr;
+  const int32_t* kidx_b = nullptr;
+  {
+    const int32_t* g = (AT && aidx) ? aidx : (!BT && bidx) ? bidx : nullptr;
+    if (g && kend - kbeg_t <= KIDX_MAX && !(AT && aidx && !BT && bidx)) {
+      for (int i = threadIdx.x; i < kend - kbeg_t; i += B2T) kidx_sh[i] = g[kbeg_t + i];
+      __syncthreads();
+      if (AT && aidx) kidx_a = kidx_sh - kbeg_t;
+      else kidx_b = kidx_sh - kbeg_t;
+    }
+  }
   auto stage = [&](int slot, int k0) {
     if (!AT) stage_tile_kc<B2M>(As + slot * A_STAGE, abase, a.ld, arows, k0, kend);
-    else stage_tile<false, B2M, AM_LD>(As + slot * A_STAGE, abase, a.ld, aidx, tm * B2M, M, k0, kend);
+    else stage_tile<false, B2M, AM_LD>(As + slot * A_STAGE, abase, a.ld, kidx_a ? kidx_a : aidx, tm * B2M, M, k0, kend);
     if (BT) stage_tile_kc<B2N>(Bs + slot * B_STAGE, bbase, b.ld, brows, k0, kend);
-    else stage_tile<false, B2N, BN_LD>(Bs + slot * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, k0, kend);
+    else stage_tile<false, B2N, BN_LD>(Bs + slot * B_STAGE, bbase, b.ld, kidx_b ? kidx_b : bidx, tn * B2N, N, k0, kend);
   };
 #pragma unroll
   for (int st = 0; st < B2S - 1; ++st) {
