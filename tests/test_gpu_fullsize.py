@@ -1,0 +1,90 @@
+"""Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py times (default options,
+cold solve, default window, the input generated on the device exactly as bench.py does).
+
+- c1, c2, c3, c5: the first 200 iterations against the oracle run on all host cores (the BJ bar,
+  ||x_gpu - x_cpu|| / ||x_cpu|| <= 1e-10), plus the checkpoint residual history;
+- c4: 3 iterations (each fresh c4 block costs the oracle a 256 x 131072 Householder QR);
+- every config: the block schedule and the fresh index sets of the solve bit-exact;
+- every config: a property of one step that holds at any size (no oracle):
+  from x_0 = 0, r_0 = -b_S, m_1 = -w_0 (rho_0 = 0) and x_1 = -(1+eta) w_0, so for K++
+  A_S x_1 = (1+eta)(b_S - lam y) with y = (A_S A_S^T + lam I)^{-1} b_S, and for CD++
+  (A_SS + lam I) x_1[S] = (1+eta) b_S with x_1 zero outside S.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def kpp():
+    import paper_2501_11673_b200 as k
+    from paper_2501_11673_b200 import build
+    build.build()
+    k.load_library()
+    assert torch.cuda.is_available()
+    return k
+
+
+def setup(kpp, cfg):
+    A, b, _ = synth.make_problem(cfg, seed=0, device=DEV)  # bench.py's instance
+    ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A, cfg.s, cfg.lam, 0)
+    return A, b, ctx
+
+
+@pytest.mark.parametrize("name,T", [("c1", 200), ("c2", 200), ("c3", 200), ("c5", 200), ("c4", 3)])
+def test_fullsize_parity(kpp, ora, name, T):
+    cfg = synth.CONFIGS[name]
+    A, b, ctx = setup(kpp, cfg)
+    res = ctx.solve(b, max_iters=T)
+    assert res.iters == T
+    x_gpu = res.x.cpu().numpy()
+    pop = cfg.n if cfg.kind == "cdpp" else cfg.m
+    # schedule and fresh index sets, bit-exact (the oracle's schedule is data independent)
+    C = ora.cdpp_C(cfg.n, cfg.s) if cfg.kind == "cdpp" else ora.kpp_C(cfg.m, cfg.n, cfg.s)
+    bid, fresh, _ = ora.schedule(0, C, T)
+    g_bid, g_fresh = ctx.schedule(0, T)
+    assert np.array_equal(g_bid.numpy(), bid) and np.array_equal(g_fresh.numpy(), fresh)
+    for k in sorted({0, int(bid.max()) // 2, int(bid.max())}):
+        assert np.array_equal(ctx.block(k).numpy(), ora.fresh_block(0, pop, cfg.s, k))
+    An, bn = A.cpu().numpy(), b.cpu().numpy()
+    del A
+    torch.cuda.empty_cache()
+    run = ora.cdpp_run if cfg.kind == "cdpp" else ora.kpp_run
+    ref = run(An, bn, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=os.cpu_count() or 1)
+    assert rel(x_gpu, ref.x) <= 1e-10, rel(x_gpu, ref.x)
+    if len(ref.hist_res):
+        assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_fullsize_first_step_property(kpp, name):
+    cfg = synth.CONFIGS[name]
+    A, b, ctx = setup(kpp, cfg)
+    x1 = ctx.solve(b, max_iters=1).x
+    S = ctx.block(0).to(DEV).long()
+    eta = cfg.s / (2.0 * cfg.n)  # P:1340 / P:748
+    bS = b[S]
+    if cfg.kind == "kpp":
+        AS = A[S]
+        y = torch.linalg.solve(AS @ AS.T + cfg.lam * torch.eye(cfg.s, dtype=A.dtype, device=DEV), bS)
+        lhs = AS @ x1
+        # A_S w = r - lam y with r = -b_S, x_1 = -(1+eta) w  =>  A_S x_1 = (1+eta)(b_S - lam y)
+        want = (1 + eta) * (bS - cfg.lam * y)
+    else:
+        ASS = A[S][:, S]
+        lhs = (ASS + cfg.lam * torch.eye(cfg.s, dtype=A.dtype, device=DEV)) @ x1[S]
+        want = (1 + eta) * bS
+        off = x1.clone()
+        off[S] = 0
+        assert float(off.abs().max()) == 0.0  # CD++ touches only the coordinates in S
+    err = float(torch.linalg.vector_norm(lhs - want) / torch.linalg.vector_norm(want))
+    assert err <= 1e-9, err
