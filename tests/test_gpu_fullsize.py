@@ -88,3 +88,23 @@ def test_fullsize_first_step_property(kpp, name):
         assert float(off.abs().max()) == 0.0  # CD++ touches only the coordinates in S
     err = float(torch.linalg.vector_norm(lhs - want) / torch.linalg.vector_norm(want))
     assert err <= 1e-9, err
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fullsize_lsqr_parity(kpp, ora, name):
+    """K++ with the sketch + LSQR projection (NEXT-2, bench.py --proj 1) at full size, 200 iterations,
+    under the DESIGN.md R5 bar max(1e-10, 4 u kappa(G))."""
+    cfg = synth.CONFIGS[name]
+    A, b, ctx = setup(kpp, cfg)
+    ctx.set_option(kpp.OPT_PROJ, 1)
+    T = 200
+    res = ctx.solve(b, max_iters=T)
+    x_gpu = res.x.cpu().numpy()
+    S0 = [ctx.block(k).numpy() for k in range(4)]
+    An, bn = A.cpu().numpy(), b.cpu().numpy()
+    del A
+    torch.cuda.empty_cache()
+    ref = ora.kpp_run(An, bn, cfg.s, lam=cfg.lam, seed=0, max_iters=T, proj=1, tmax=8, threads=os.cpu_count() or 1)
+    kap = max(np.linalg.cond(ora.sketch_factor(An, S, cfg.lam, 0, 2 * cfg.s)) ** 2 for S in S0)
+    bar = max(1e-10, 4 * 2.2e-16 * kap)
+    assert rel(x_gpu, ref.x) <= bar, (rel(x_gpu, ref.x), kap)
