@@ -164,3 +164,23 @@ def make_bell_psd(n: int = 4096, effective_rank: int = 25, tail_strength: float 
     A.diagonal().add_(phi)
     b = torch.randn((n,), generator=g, dtype=torch.float64, device=device)
     return A, b
+
+
+@torch.no_grad()
+def make_bell_general(m: int = 4096, n: int = 1024, effective_rank: int = 50, tail_strength: float = 0.01,
+                      seed: int = 0, device="cpu"):
+    """K++ test system of App F (Fig lsqr_steps): an m x n matrix with the
+    bell singular value profile, A = U diag(sigma) V^T with U (m x n, orthonormal columns) and V
+    (n x n) Haar-random (QR of Gaussians, signs fixed by diag(R)); b ~ N(0, I) (inconsistent, as in
+    the paper).  Returns (A, b)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    U, R = torch.linalg.qr(torch.randn((m, n), generator=g, dtype=torch.float64, device=device))
+    U = U * torch.sign(torch.diagonal(R))
+    V, R2 = torch.linalg.qr(torch.randn((n, n), generator=g, dtype=torch.float64, device=device))
+    V = V * torch.sign(torch.diagonal(R2))
+    sig = bell_profile(n, effective_rank, tail_strength).to(device)
+    A = (U * sig) @ V.T
+    b = torch.randn((m,), generator=g, dtype=torch.float64, device=device)
+    return A, b
+
