@@ -544,6 +544,15 @@ def test_bell_spectrum_generator():
     assert np.allclose(ev, want, rtol=0, atol=1e-12)
 
 
+def test_bell_general_generator():
+    """K++ bell-spectrum systems (App F): the singular values of A are the profile."""
+    A, b = synth.make_bell_general(256, 64, 10, seed=5)
+    sv = np.linalg.svd(A.numpy(), compute_uv=False)
+    want = np.sort(synth.bell_profile(64, 10).numpy())[::-1]
+    assert np.allclose(sv, want, rtol=0, atol=1e-13)
+    assert A.shape == (256, 64) and b.shape == (256,)
+
+
 # ----------------------------------------------------------------- sketch + LSQR (NEXT-2)
 def test_srht_full_sketch_is_orthogonal(ora):
     """tau = n2 (T = every index): Pi = H D/sqrt(n2) is orthogonal, so A_hat A_hat^T = A_S A_S^T."""
