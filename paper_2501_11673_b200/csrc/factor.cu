@@ -230,6 +230,54 @@ __global__ void gather_principal_kernel(const double* A, long long lda, const in
   }
 }
 
+// Symmetric gather: only the upper 32 x 32 tiles (k-tile <= l-tile) are read from A -- the upper
+// triangle A[S_k][S_l], k <= l, is all the Cholesky of Alg 3 l.8 consumes (the oracle's factor reads
+// exactly these entries) -- and each off-diagonal tile is written twice, as is and transposed
+// through shared memory, so G is the full symmetric matrix.  ~Half the random 8-byte reads.
+__global__ void __launch_bounds__(256) gather_sym_kernel(const double* A, long long lda, const int32_t* Sall, int s,
+                                                         double lam, long long cb, long long ce, double* Gall) {
+  __shared__ double tile[32][33];
+  __shared__ long long rowoff[32];
+  const int T = (s + 31) / 32;
+  int idx = blockIdx.x, ti = 0;
+  while (idx >= T - ti) {  // upper tile index -> (ti, tj), row-major over the upper triangle
+    idx -= T - ti;
+    ++ti;
+  }
+  const int tj = ti + idx;
+  const int32_t* S = Sall + (long long)blockIdx.y * s;
+  double* G = Gall + (long long)blockIdx.y * s * s;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  if (threadIdx.x < 32) {
+    const int k = ti * 32 + threadIdx.x;
+    rowoff[threadIdx.x] = k < s ? (long long)S[k] * lda : 0;
+  }
+  const int l = tj * 32 + tx;
+  const long long c = l < s ? (long long)S[l] : -1;
+  const bool own = l < s && c >= cb && c < ce;
+  __syncthreads();
+  double v[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int kk = ty + 8 * r, k = ti * 32 + kk;
+    v[r] = (k < s && own) ? __ldg(A + rowoff[kk] + (c - cb)) : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int kk = ty + 8 * r, k = ti * 32 + kk;
+    const double g = v[r] + ((k == l) ? lam : 0.0);
+    tile[kk][tx] = g;
+    if (k < s && l < s && (ti != tj || k <= l)) G[(long long)k * s + l] = g;
+  }
+  __syncthreads();
+  // the mirror image (for the diagonal tile: its lower half, from the upper entries)
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int ll = ty + 8 * r, lr = tj * 32 + ll, k = ti * 32 + tx;
+    if (lr < s && k < s && (ti != tj || lr > k)) G[(long long)lr * s + k] = tile[tx][ll];
+  }
+}
+
 __global__ void add_diag_kernel(double* Gall, int s, double lam) {
   double* G = Gall + (long long)blockIdx.x * s * s;
   for (int i = threadIdx.x; i < s; i += blockDim.x) G[(long long)i * s + i] += lam;
@@ -518,8 +566,13 @@ void launch_gather_principal(cudaStream_t st, int batch, const double* A, long l
                              const int32_t* S, int s, double lam, long long col_begin,
                              long long col_end, double* G) {
   if (batch <= 0) return;
-  dim3 grid((s + 3) / 4, batch);
-  gather_principal_kernel<<<grid, 512, 0, st>>>(A, lda, S, s, lam, col_begin, col_end, G);
+  if (!getenv("KPP_GATHER_FULL")) {
+    const int T = (s + 31) / 32;
+    gather_sym_kernel<<<dim3(T * (T + 1) / 2, batch), 256, 0, st>>>(A, lda, S, s, lam, col_begin, col_end, G);
+  } else {
+    dim3 grid((s + 3) / 4, batch);
+    gather_principal_kernel<<<grid, 512, 0, st>>>(A, lda, S, s, lam, col_begin, col_end, G);
+  }
   count_launches(1);
 }
 
