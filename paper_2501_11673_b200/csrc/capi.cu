@@ -410,7 +410,8 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
     launch_chol_trtri(st, B, G, X1, s, ctx->d_info, W);
     pp.mark("chol");
     Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
-    launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);  // M = X X^T (X upper)
+    launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 1, 2);  // M = X X^T (X upper): upper tiles
+    launch_mirror_upper(st, B, Mout, s);                          // ... and its mirror image
     pp.mark("M");
   } else if (ctx->proj == 1) {
     // Alg 6 l.2-5: A_hat = A_S Pi^T (SRHT), R = chol(A_hat A_hat^T + lam I), memoized as X = R^{-1}
@@ -448,7 +449,8 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
     pp.mark("chol");
     if (!cqr2 || adaptive) {
       Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
-      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 0, 2);  // M = X1 X1^T
+      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 1, 2);  // M = X1 X1^T (upper tiles)
+      launch_mirror_upper(st, B, Mout, s);
     }
     int nref = cqr2 ? B : 0;
     const int32_t* Sr = S;
@@ -511,7 +513,8 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
         Operand x1a{X1b, s, ss, nullptr, 0, 0}, x2b{X2, s, ss, nullptr, 0, 0};
         launch_dgemm(st, Bn, s, s, s, x1a, x2b, X, s, ss, 1, 0, 2);  // X = R^{-1} = X1 X2 (upper)
         Operand xa{X, s, ss, nullptr, 0, 0}, xb{X, s, ss, nullptr, 0, 1};
-        launch_dgemm(st, Bn, s, s, s, xa, xb, Mb, s, ss, 1, 0, 2);  // M = X X^T
+        launch_dgemm(st, Bn, s, s, s, xa, xb, Mb, s, ss, 1, 1, 2);  // M = X X^T (upper tiles)
+        launch_mirror_upper(st, Bn, Mb, s);
       }
       const int Bn = nref;
       if (Mr != Mout) launch_batch_move(st, Bn, Mr, Mout, list, ss * (long long)sizeof(double), 1);

@@ -278,6 +278,31 @@ __global__ void __launch_bounds__(256) gather_sym_kernel(const double* A, long l
   }
 }
 
+// M[l][k] = M[k][l] for l > k: the lower triangle from the upper one (tiled transpose).
+__global__ void __launch_bounds__(256) mirror_upper_kernel(double* Mall, int s) {
+  __shared__ double tile[32][33];
+  const int T = (s + 31) / 32;
+  int idx = blockIdx.x, ti = 0;
+  while (idx >= T - ti) {
+    idx -= T - ti;
+    ++ti;
+  }
+  const int tj = ti + idx;
+  double* M = Mall + (long long)blockIdx.y * s * s;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int kk = ty + 8 * r, k = ti * 32 + kk, l = tj * 32 + tx;
+    tile[kk][tx] = (k < s && l < s) ? M[(long long)k * s + l] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int ll = ty + 8 * r, lr = tj * 32 + ll, k = ti * 32 + tx;
+    if (lr < s && k < s && (ti != tj || lr > k)) M[(long long)lr * s + k] = tile[tx][ll];
+  }
+}
+
 __global__ void add_diag_kernel(double* Gall, int s, double lam) {
   double* G = Gall + (long long)blockIdx.x * s * s;
   for (int i = threadIdx.x; i < s; i += blockDim.x) G[(long long)i * s + i] += lam;
@@ -573,6 +598,13 @@ void launch_gather_principal(cudaStream_t st, int batch, const double* A, long l
     dim3 grid((s + 3) / 4, batch);
     gather_principal_kernel<<<grid, 512, 0, st>>>(A, lda, S, s, lam, col_begin, col_end, G);
   }
+  count_launches(1);
+}
+
+void launch_mirror_upper(cudaStream_t st, int batch, double* M, int s) {
+  if (batch <= 0) return;
+  const int T = (s + 31) / 32;
+  mirror_upper_kernel<<<dim3(T * (T + 1) / 2, batch), 256, 0, st>>>(M, s);
   count_launches(1);
 }
 

@@ -69,6 +69,7 @@ void launch_gather_principal(cudaStream_t st, int batch, const double* A, long l
                              const int32_t* S, int s, double lam, long long col_begin,
                              long long col_end, double* G);
 // G[b] += lam on the diagonal
+void launch_mirror_upper(cudaStream_t st, int batch, double* M, int s);  // lower triangle := upper^T
 void launch_add_diag(cudaStream_t st, int batch, double* G, int s, double lam);
 // In place: G[b] -> R[b] upper with R^T R = G (lower part zeroed); X[b] = R^{-1}.
 // info[b] = 0 on success, 1 + pivot index on a non-positive pivot.
