@@ -231,9 +231,6 @@ void launch_step_update(cudaStream_t st, const StepParams& p);   // w, momentum,
 void launch_step_window(cudaStream_t st, const StepParams& p);   // e, checkpoint, t_cur++
 
 // ------------------------------------------------------------------ lsqr.cu (NEXT-2: Alg 6)
-struct LsqrScal {
-  double alpha, beta, phibar, rhobar, f1, f2;
-};
 struct LsqrParams {
   const double* A;
   long long lda, n;

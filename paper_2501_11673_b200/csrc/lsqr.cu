@@ -24,8 +24,6 @@ namespace kpp {
 namespace {
 using namespace gx;
 
-constexpr int LT = 512;  // threads per CTA (grid kernels and the one-CTA s-vector kernels, s <= 1024)
-
 __device__ __forceinline__ void philox4(uint32_t c[4], uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int round = 0; round < 10; ++round) {
