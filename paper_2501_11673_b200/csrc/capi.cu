@@ -338,6 +338,15 @@ struct P1Prof {
 
 kpp_status lsqr_prepare(kpp_ctx* ctx);
 
+// Split-K count of the Gram products: a function of n only (K chunks of 1024 columns, at most 64),
+// so the summation order -- and the bits of M -- do not depend on how fresh blocks are batched.
+int gram_splits(const kpp_ctx* ctx) {
+  if (ctx->kind != KIND_KPP) return 1;
+  long long kc = 1024;
+  if (const char* ez = getenv("KPP_GRAM_KCHUNK")) kc = std::max(16, atoi(ez));  // experiments
+  return (int)std::min<long long>(64, std::max<long long>(1, (ctx->n + kc - 1) / kc));
+}
+
 kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   P1Prof pp;
   pp.on = getenv("KPP_P1_PROFILE") != nullptr;
@@ -359,10 +368,7 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   // split-K count depends on n only, so the summation order (and the bits of M) does not
   // depend on how fresh blocks happen to be batched
   (void)tiles_up;
-  int Z = 1;
-  if (ctx->kind == KIND_KPP) Z = (int)std::min<long long>(64, std::max<long long>(1, (n + 511) / 512));
-  if (const char* ez = getenv("KPP_GRAM_KCHUNK"))  // experiment: K chunk per split
-    if (ctx->kind == KIND_KPP) Z = (int)std::min<long long>(64, std::max<long long>(1, (n + atoi(ez) - 1) / atoi(ez)));
+  const int Z = gram_splits(ctx);
   // factor 0: shifted CholeskyQR2 for every block; 2 (default): the second CholeskyQR pass only for
   // blocks whose estimated u * kappa(A_S)^2 exceeds 1e-11;
   // 1: the literal Gram + Cholesky for every block
@@ -539,7 +545,7 @@ kpp_status phase1(kpp_ctx* ctx, long long k0, long long k1) {
   const bool cqr2 = ctx->kind == KIND_KPP && ctx->factor != 1 && ctx->proj == 0;
   const bool qall = ctx->kind == KIND_KPP && ctx->factor == 0 && ctx->proj == 0;  // Q1 for every block
   // workspace of phase1_batch per block: split-K partials (Z s^2), G, X1 (+ L, X2, X, Q1 for CholeskyQR2)
-  const long long Z = ctx->kind == KIND_KPP ? std::min<long long>(64, std::max<long long>(1, (n + 511) / 512)) : 1;
+  const long long Z = gram_splits(ctx);
   const long long skw = (ctx->kind == KIND_KPP && ctx->proj == 1) ? ctx->lsqr_n2 * s + (long long)ctx->lsqr_tau * s : 0;
   const long long per_block = (long long)sizeof(double) * ((Z + 2 + (cqr2 ? 5 : 0)) * s * s + (qall ? s * n : 0) + (cqr2 ? s : 0) + skw) +
                               (long long)chol_inv_workspace((int)s) + 2048;
