@@ -204,8 +204,9 @@ kpp_status cdpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t n, int64
    A_pad = [[A, 0], [0, I]] of size n2 and returns x = (Q^T x~)[0:n]; x0 is mapped by Q.
    The transformed matrix is computed once, here, into a buffer the context owns (m2 x n or
    n2 x n2 doubles; A is no longer read); the memo cache is dropped.  Later kpp_solve calls take
-   and return the caller's sizes (b: m values, x0 / x_out: n).  Single-GPU contexts only
-   (KPP_EINVAL on a column-sharded context).  Idempotent. */
+   and return the caller's sizes (b: m values, x0 / x_out: n).  K++ column-sharded contexts
+   transform their own column slab (Q mixes rows only; every rank uses the same D); CD++ needs the
+   whole matrix (Q A Q^T mixes columns): KPP_EINVAL on a column-sharded CD++ context.  Idempotent. */
 kpp_status kpp_enable_rht(kpp_ctx* ctx);
 /* The transformed matrix (HOST, m2 x n or n2 x n2 row-major); requires kpp_enable_rht. */
 kpp_status kpp_get_rht_matrix(kpp_ctx* ctx, double* out);

@@ -1445,7 +1445,9 @@ kpp_status kpp_get_rho_history(kpp_ctx* ctx, double* rho_hist, int64_t cap, int6
 }
 
 kpp_status kpp_enable_rht(kpp_ctx* ctx) {
-  if (!ctx || ctx->nranks > 1) return KPP_EINVAL;
+  // K++ mixes rows only, so a column-sharded rank transforms its own slab (the same D and H on
+  // every rank: exactly the columns of the single-GPU transform); CD++ mixes columns: one GPU only
+  if (!ctx || (ctx->nranks > 1 && ctx->kind == KIND_CDPP)) return KPP_EINVAL;
   if (ctx->rht) return KPP_OK;
   cudaStream_t st = ctx->stream;
   auto np2 = [](long long v) { long long p = 1; while (p < v) p <<= 1; return p; };

@@ -498,6 +498,26 @@ def test_rht_solve_parity(kpp, ora, cfg):
         assert rel(res0.x.cpu().numpy(), ref0.x) <= 1e-10
 
 
+def test_rht_dist_kpp(kpp, ora):
+    """K++ RHT on a column-sharded context (one rank): the slab transform + the fused-exchange engine
+    against the oracle's transformed solve; CD++ column-sharded RHT is refused."""
+    cfg = synth.twin("c3", 1000, 100, 25, k=6)
+    A, b, _ = synth.make_problem(cfg)
+    uid = kpp.kpp_get_unique_id()
+    ctx = kpp.kpp_setup_dist(A.to(DEV), A.shape[0], A.shape[1], 0, A.shape[1], cfg.s, cfg.lam, 4, uid, 0, 1)
+    ctx.enable_rht()
+    ctx.set_option(kpp.OPT_ENGINE, 2)
+    res = ctx.solve(b.to(DEV), max_iters=300)
+    ref = ora.kpp_run_rht(A.numpy(), b.numpy(), cfg.s, seed=4, lam=cfg.lam, max_iters=300, threads=8)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    ctx.destroy()
+    c5 = synth.twin("c5", 300, 300, 37, k=10)
+    A5, b5, _ = synth.make_problem(c5)
+    cd = kpp.cdpp_setup_dist(A5.to(DEV), 300, 0, 300, 37, c5.lam, 4, kpp.kpp_get_unique_id(), 0, 1)
+    cd.enable_rht()  # one rank holds the whole matrix: allowed
+    cd.destroy()
+
+
 MAX_CASES = [synth.twin("c3", 2048, 1100, 1024, k=8), synth.twin("c4", 1030, 3000, 1023, k=8),
              synth.twin("c5", 1100, 1100, 1024, k=16), synth.twin("c5", 1100, 1100, 1023, k=16)]
 
