@@ -170,19 +170,14 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
       double a = 0.0;
       for (int q0 = lane; q0 < G; q0 += 32 * 8) a += ll_sum<8>(p.ll + 2LL * k, 2LL * s, q0, G, tag, p.err);
       a = wsum(a);
-      // system scope across GPUs; one rank: GPU scope suffices (and polls through L2 faster)
-      if (lane < R) {
-        unsigned long long* dst = p.peer_recv[lane] + 2 * (slot + (long long)p.rank * s + k);
-        if (R > 1) ll_put_sys(dst, a, tag);
-        else ll_put(dst, a, tag);
-      }
+      // system scope: the destination may be a peer GPU's memory (one rank runs the same code)
+      if (lane < R) ll_put_sys(p.peer_recv[lane] + 2 * (slot + (long long)p.rank * s + k), a, tag);
     }
     double e = 0.0;
     for (int k = tid; k < s; k += NT) {
       double v = 0.0;
       for (int r = 0; r < R; ++r) {
-        const unsigned long long* src = p.peer_recv[p.rank] + 2 * (slot + (long long)r * s + k);
-        v += R > 1 ? ll_get_sys(src, tag, p.err) : ll_sum<1>(src, 0, 0, 1, tag, p.err);
+        v += ll_get_sys(p.peer_recv[p.rank] + 2 * (slot + (long long)r * s + k), tag, p.err);
       }
       const double rk = v - bS[k];
       tot[k] = rk;
