@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=list(synth.CONFIGS))
     ap.add_argument("--iters", type=int, default=0, help="block iterations per step (0: config default)")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-8 measurement")
-    ap.add_argument("--ttt-cap", type=int, default=4_000_000, help="iteration cap of the time-to-tolerance solve")
+    ap.add_argument("--ttt-cap", type=int, default=0,
+                    help="iteration cap of the time-to-tolerance solve (0: 25M, or 1M with --proj 1)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=-1)
@@ -338,7 +339,8 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        r = ctx.solve(b, max_iters=args.ttt_cap, tol=cfg.tol if cfg.tol > 0 else 1e-8, x_out=x_out)
+        cap = args.ttt_cap or (1_000_000 if args.proj else 25_000_000)  # c2 needs 19.3M (DESIGN 12)
+        r = ctx.solve(b, max_iters=cap, tol=cfg.tol if cfg.tol > 0 else 1e-8, x_out=x_out)
         e1.record(stream)
         torch.cuda.synchronize()
         tms = e0.elapsed_time(e1)
