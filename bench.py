@@ -339,7 +339,8 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        cap = args.ttt_cap or (1_000_000 if args.proj else 25_000_000)  # c2 needs 19.3M (DESIGN 12)
+        # c2 needs 19.3M iterations (DESIGN 12); multi-GPU runs keep a bounded 4M cap
+        cap = args.ttt_cap or (1_000_000 if args.proj else 25_000_000 if world == 1 else 4_000_000)
         r = ctx.solve(b, max_iters=cap, tol=cfg.tol if cfg.tol > 0 else 1e-8, x_out=x_out)
         e1.record(stream)
         torch.cuda.synchronize()
