@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(double* Gall, long long 
   extern __shared__ double dsm[];
   double (*a)[65] = reinterpret_cast<double (*)[65]>(dsm);             // working copy
   double (*rx)[65] = reinterpret_cast<double (*)[65]>(dsm + 64 * 65);  // R, then X row by row
-  double* rrow = dsm + 2 * 64 * 65;
+  double* dinv_sh = dsm + 2 * 64 * 65;  // 1 / R[i][i]
   __shared__ int fail_sh;
   double* G = Gall + (long long)blockIdx.x * gstride;
   double* X = Xall + (long long)blockIdx.x * xstride;
@@ -349,8 +349,9 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(double* Gall, long long 
     const double v = a[i][i];
     const bool ok = v > 0.0;
     if (!ok && tid == 0 && fail_sh == 0) fail_sh = i + 1;
-    const double d = ok ? sqrt(v) : 1.0;
-    const double dinv = 1.0 / d;
+    const double dinv = ok ? rsqrt(v) : 1.0;  // (one reciprocal square root on the pivot chain)
+    const double d = ok ? v * dinv : 1.0;
+    if (tid == 0) dinv_sh[i] = dinv;
     // row i of R: R[i][j] = a[i][j] / d
     if (tid < kb && tid >= i) rx[i][tid] = (tid == i) ? d : a[i][tid] * dinv;
     // trailing update with the scaled row: a[p][q] -= R[i][p] R[i][q], i < p <= q
@@ -374,26 +375,27 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(double* Gall, long long 
     }
     __syncthreads();
   }
-  // X = R^{-1}, rows from the bottom: X[i][j] = (delta_ij - sum_{l=i+1..j} R[i][l] X[l][j]) / R[i][i]
-  const int lane = tid & 31;
-  const int col = tid >> 2, sub = tid & 3;  // 4 threads per column
-  for (int i = kb - 1; i >= 0; --i) {
-    if (tid < kb) rrow[tid] = rx[i][tid];
-    __syncthreads();
-    double acc = 0.0;
-    if (col < kb && col > i)
-      for (int l = i + 1 + sub; l <= col; l += 4) acc = fma(rrow[l], rx[l][col], acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    (void)lane;
-    const double rinv = 1.0 / rrow[i];
-    if (sub == 0 && col < kb && col >= i) rx[i][col] = (col == i) ? rinv : -acc * rinv;
-    __syncthreads();
+  // X = R^{-1} by COLUMNS, each an independent back substitution R x = e_j (no CTA barriers):
+  // 4 lanes per column split the dot products, x_i = (delta_ij - sum_{l=i+1..j} R[i][l] x_l) / R[i][i];
+  // X is built in `a` (the working copy is no longer needed), R stays in rx.
+  {
+    const int col = tid >> 2, sub = tid & 3;  // 64 columns x 4 lanes = 256 threads
+    const bool live = col < kb;
+    for (int i = kb - 1; i >= 0; --i) {
+      double acc = 0.0;
+      if (live && col > i)
+        for (int l = i + 1 + sub; l <= col; l += 4) acc = fma(rx[i][l], a[l][col], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (live && sub == 0 && col >= i) a[i][col] = ((col == i) ? 1.0 - acc : -acc) * dinv_sh[i];
+      __syncwarp();
+    }
   }
+  __syncthreads();
   // only X_kk is needed by the blocked driver (R_kk itself is never read again)
   for (int e = tid; e < kb * kb; e += 256) {
     const int i = e / kb, j = e - i * kb;
-    X[(long long)i * ldx + j] = (j >= i) ? rx[i][j] : 0.0;
+    X[(long long)i * ldx + j] = (j >= i) ? a[i][j] : 0.0;
   }
   if (tid == 0 && fail_sh) info[blockIdx.x] = info_base + fail_sh;
 }
