@@ -117,3 +117,21 @@ def test_lsqr_option_errors(kpp):
     ctx.solve(b.to(DEV), max_iters=4)
     with pytest.raises(kpp.KppError):
         ctx.set_option(kpp.OPT_TAU, 80)  # the sketch already exists
+
+
+@pytest.mark.parametrize("cfg", [synth.twin("c3", 1000, 100, 25, k=6), synth.twin("c2", 512, 500, 64)],
+                         ids=["tall_ragged", "square_ragged"])
+def test_full_kpp_alg5(kpp, ora, cfg):
+    """Alg 5 exactly as printed: RHT preprocessing (l.2-3, rows padded to 2^k) AND the
+    sketch + LSQR projection (l.10, Alg 6), against the oracle's transcription."""
+    A, b, _ = synth.make_problem(cfg)
+    T = 200
+    ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 6)
+    ctx.enable_rht()
+    ctx.set_option(kpp.OPT_PROJ, 1)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    ref = ora.kpp_run_rht(A.numpy(), b.numpy(), cfg.s, seed=6, lam=cfg.lam, max_iters=T, proj=1, tmax=8)
+    At, _ = ora.rht_rows(A.numpy(), b.numpy(), 6)
+    kap = max(np.linalg.cond(ora.sketch_factor(At, ctx.block(k).numpy(), cfg.lam, 6, 2 * cfg.s)) ** 2
+              for k in range(4))
+    assert rel(res.x.cpu().numpy(), ref.x) <= max(1e-10, 4 * 2.2e-16 * kap)
