@@ -69,7 +69,7 @@ typedef enum {
   KPP_OPT_RHO_FIXED = 4,  /* < 0 (default): adaptive rho; >= 0: fixed rho, never updated */
   KPP_OPT_FACTOR = 5,     /* K++ factor route (same R in exact arithmetic): 2 (default) Gram + Cholesky,
                              then a second (shifted CholeskyQR2) pass only for blocks whose power-
-                             iteration estimate of u*kappa(A_S)^2 exceeds 1e-11; 0 shifted CholeskyQR2
+                             iteration estimate 4 u kappa(A_S)^2 exceeds 3e-11; 0 shifted CholeskyQR2
                              of [A_S, sqrt(lam) I] for every block; 1 literal Gram + Cholesky */
   KPP_OPT_WINDOW = 6,     /* iterations per device window (default 8192; rounded to >= 1) */
   KPP_OPT_PHASE1_MB = 7,  /* device workspace budget for a Phase-1 batch, MiB (default 4096) */

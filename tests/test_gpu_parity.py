@@ -394,7 +394,7 @@ def test_cdpp_reassociated_parity(kpp, ora, cfg, cluster):
                          ids=["c2twin", "c3twin"])
 def test_adaptive_refinement(kpp, ora, cfg, expect):
     """Default factor route: Gram + Cholesky, second CholeskyQR pass only for ill-conditioned blocks
-    (estimated u kappa(A_S)^2 > 1e-11).  Iterates within 1e-10 of the oracle either way; the spiked
+    (estimated 4 u kappa(A_S)^2 > 3e-11).  Iterates within 1e-10 of the oracle either way; the spiked
     over-determined twin (kappa ~ 3e3) refines every block."""
     A, b, _ = synth.make_problem(cfg)
     ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
