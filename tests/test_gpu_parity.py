@@ -218,6 +218,13 @@ def test_fused_exchange_engine(kpp, ora, cfg):
     assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
     x1 = res.x.clone()
     assert torch.equal(ctx.solve(b.to(DEV), max_iters=T).x, x1)
+    # a start vector and the tolerance stop (checkpoint logic inside the fused kernel)
+    x0 = np.random.default_rng(3).standard_normal(A.shape[1])
+    run = ora.cdpp_run if cfg.kind == "cdpp" else ora.kpp_run
+    ref2 = run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=3000, tol=0.05, x0=x0, threads=8)
+    res2 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=3000, tol=0.05)
+    assert res2.iters == ref2.iters
+    assert rel(res2.x.cpu().numpy(), ref2.x) <= 1e-10
 
 
 def test_deterministic_and_warm_cache(kpp):
