@@ -24,7 +24,7 @@ __all__ = [
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENOTPD, EDIVERGED, EMAXITER = range(8)
 OPT_ACCEL, OPT_MEMO, OPT_ETA, OPT_RHO_FIXED, OPT_FACTOR, OPT_WINDOW, OPT_PHASE1_MB, OPT_RESIDENT = range(1, 9)
-OPT_ENGINE = 9  # 0: persistent kernel (1 GPU default); 1: graph of step kernels (+NCCL)
+OPT_ENGINE = 9  # -1 auto (default); 0 persistent kernel; 1 graph of step kernels; 2 fused-exchange kernel
 OPT_CLUSTER = 10  # 0: automatic; 1/2/4/8/16: forced thread-block cluster size
 OPT_XCHG = 16  # column-sharded exchange: 1 fused NVLink peer exchange (default), 0 NCCL
 OPT_PROJ, OPT_TMAX, OPT_TAU = 13, 14, 15  # K++ projection: 1 = sketch + LSQR (Alg 6), t_max, tau
