@@ -543,3 +543,43 @@ def test_max_block_size(kpp, ora, cfg):
         ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8)
     res = ctx.solve(b.to(DEV), max_iters=T)
     assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["default", "engine2", "lsqr"])
+@pytest.mark.parametrize("pad", [3, 4])
+@pytest.mark.parametrize("cfg", [synth.twin("c3", 1000, 777, 50, k=8), synth.twin("c5", 301, 301, 37, k=10)],
+                         ids=["kpp", "cdpp"])
+def test_padded_leading_dimension(kpp, ora, cfg, pad, mode):
+    """The C ABI with lda > n (A as the left part of a wider row-major buffer; odd lda disables the
+    16-byte paths: TMA, vector loads, the pipelined GEMM) against the oracle."""
+    import ctypes
+    A, b, _ = synth.make_problem(cfg)
+    m, n = A.shape
+    buf = torch.full((m, n + pad), float("nan"), dtype=torch.float64, device=DEV)  # padding poisoned
+    buf[:, :n] = A.to(DEV)
+    L = kpp.load_library()
+    h = ctypes.c_void_p()
+    if cfg.kind == "cdpp":
+        st = L.cdpp_setup(ctypes.byref(h), ctypes.c_void_p(buf.data_ptr()), n, n + pad, cfg.s, cfg.lam, 0)
+    else:
+        st = L.kpp_setup(ctypes.byref(h), ctypes.c_void_p(buf.data_ptr()), m, n, n + pad, cfg.s, cfg.lam, 0)
+    assert st == kpp.OK
+    if mode == "lsqr" and cfg.kind == "cdpp":
+        L.kpp_destroy(h)
+        pytest.skip("sketch + LSQR is a K++ projection")
+    if mode == "engine2":
+        assert L.kpp_set_option(h, kpp.OPT_ENGINE, 2.0) == kpp.OK
+    if mode == "lsqr":
+        assert L.kpp_set_option(h, kpp.OPT_PROJ, 1.0) == kpp.OK
+    T = 200
+    bd = b.to(DEV)
+    x = torch.zeros(n, dtype=torch.float64, device=DEV)
+    iters = ctypes.c_int64()
+    st = L.kpp_solve(h, ctypes.c_void_p(bd.data_ptr()), None, T, 0.0, ctypes.c_void_p(x.data_ptr()), None, 0,
+                     None, ctypes.byref(iters))
+    assert st in (kpp.OK, kpp.EMAXITER) and iters.value == T
+    run = ora.cdpp_run if cfg.kind == "cdpp" else ora.kpp_run
+    kw = dict(proj=1, tmax=8) if mode == "lsqr" else {}
+    ref = run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8, **kw)
+    assert rel(x.cpu().numpy(), ref.x) <= 1e-10
+    L.kpp_destroy(h)
