@@ -297,6 +297,7 @@ void srht_params(uint64_t seed, int64_t n2, int32_t tau, std::vector<double>& d,
 int sketch_factor(const double* A, int64_t lda, int64_t n, const int32_t* S, int32_t s, double lam, uint64_t seed,
                   int32_t tau, double* R) {
   const int64_t n2 = next_pow2_(n);
+  if (tau < 1 || tau > n2) return ORA_EINVAL;  // T is tau distinct rows of the n2-point transform
   std::vector<double> d;
   std::vector<int32_t> T;
   srht_params(seed, n2, tau, d, T);
@@ -459,7 +460,8 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
       fresh_block(seed, pop, s, opt.memo ? nfresh : t, nbk.S.data());
       int rc;
       const bool lsqr = !cd && opt.proj == 1;
-      const int32_t tau = opt.tau > 0 ? opt.tau : 2 * s;
+      // tau = 2s (Alg 5 l.4), at most the padded dimension n2 (R5)
+      const int32_t tau = opt.tau > 0 ? opt.tau : (int32_t)std::min<int64_t>(2 * (int64_t)s, next_pow2_(n));
       if (cd)
         rc = cdpp_factor(A, lda, nbk.S.data(), s, lam, par, nbk.R.data());
       else if (lsqr)

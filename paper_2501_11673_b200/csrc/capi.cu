@@ -861,6 +861,8 @@ kpp_status lsqr_prepare(kpp_ctx* ctx) {
   while (n2 < n) n2 <<= 1;
   ctx->lsqr_n2 = n2;
   ctx->lsqr_tau = ctx->tau_opt > 0 ? ctx->tau_opt : (int)std::min<long long>(2 * s, n2);
+  if (ctx->lsqr_tau > n2)  // T is tau distinct rows of the n2-point transform
+    return fail(ctx, KPP_EINVAL, "sketch size tau = %d exceeds the padded dimension %lld", ctx->lsqr_tau, n2);
   CKS(dalloc(ctx, &ctx->srht_d, (size_t)n2));
   CKS(dalloc(ctx, &ctx->srht_T, (size_t)ctx->lsqr_tau));
   int32_t* perm = nullptr;

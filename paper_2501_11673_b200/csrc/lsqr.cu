@@ -167,8 +167,8 @@ __device__ __forceinline__ void slab_rowsums_x(const LsqrParams& p, const int32_
 }
 
 struct SlabScal {
-  double ia;      // 1 / alpha_{r-1}: normalises the previous v_n (0: no previous v)
-  int defer;      // 0 none, 1 the initial w = v, x = 0 (step 1), 2 x += f1 w, w = v - f2 w
+  double ia;      // 1 / alpha_{r-1} (0 when alpha_{r-1} = 0): normalises the previous v_n
+  int defer;      // 0 no previous v (round 1), 1 the initial w = v, x = 0 (step 1), 2 x += f1 w, w = v - f2 w
   double f1, f2;  // deferred coefficients
   double beta;    // beta_r of the C term (0 in round 1)
 };
@@ -206,7 +206,7 @@ __device__ __forceinline__ double slab_fused(const LsqrParams& p, const int32_t*
     if (tid < TW) {
       const long long j = jb + tid;
       double v = 0.0;
-      if (j < c1 && sc.ia != 0.0) {
+      if (j < c1 && sc.defer != 0) {  // (not sc.ia: a zero alpha at an LSQR breakdown still defers)
         v = sv.vn[j] * sc.ia;
         if (sc.defer == 1) {
           sv.wn[j] = v;

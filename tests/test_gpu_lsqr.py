@@ -135,3 +135,19 @@ def test_full_kpp_alg5(kpp, ora, cfg):
     kap = max(np.linalg.cond(ora.sketch_factor(At, ctx.block(k).numpy(), cfg.lam, 6, 2 * cfg.s)) ** 2
               for k in range(4))
     assert rel(res.x.cpu().numpy(), ref.x) <= max(1e-10, 4 * 2.2e-16 * kap)
+
+
+@pytest.mark.parametrize("s", [1, 2, 33, 64])
+def test_lsqr_block_size_edges(kpp, ora, s):
+    """Degenerate block sizes for the sketch + LSQR projection: s = 1 (tau = 2), odd s, and s = m
+    (every row in one block), on a 64 x 48 system (n padded to 64 for the SRHT)."""
+    cfg = synth.twin("c3", 64, 48, s, k=4)
+    A, b, _ = synth.make_problem(cfg)
+    T = 60
+    ref = ora.kpp_run(A.numpy(), b.numpy(), s, lam=cfg.lam, seed=9, max_iters=T, proj=1, tmax=8)
+    ctx = lsqr_ctx(kpp, A, s, cfg.lam, 9)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    An = A.numpy()
+    kap = max(np.linalg.cond(ora.sketch_factor(An, ctx.block(k).numpy(), cfg.lam, 9, min(2 * s, 64))) ** 2
+              for k in range(min(3, len(ctx.block(0)))))
+    assert rel(res.x.cpu().numpy(), ref.x) <= max(1e-10, 4 * 2.2e-16 * kap)
