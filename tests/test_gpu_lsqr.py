@@ -151,3 +151,27 @@ def test_lsqr_block_size_edges(kpp, ora, s):
     kap = max(np.linalg.cond(ora.sketch_factor(An, ctx.block(k).numpy(), cfg.lam, 9, min(2 * s, 64))) ** 2
               for k in range(min(3, len(ctx.block(0)))))
     assert rel(res.x.cpu().numpy(), ref.x) <= max(1e-10, 4 * 2.2e-16 * kap)
+
+
+@pytest.mark.parametrize("opts", [dict(accel=False), dict(memo=False), dict(rho_fixed=0.3), dict(eta=0.01)],
+                         ids=["no_accel", "no_memo", "fixed_rho", "eta"])
+def test_lsqr_with_options_and_x0(kpp, ora, opts):
+    """The LSQR projection under the algorithm options and a start vector, against the oracle."""
+    cfg = synth.twin("c2", 256, 200, 32)
+    A, b, _ = synth.make_problem(cfg)
+    x0 = np.random.default_rng(5).standard_normal(200)
+    T = 150
+    ref = ora.kpp_run(A.numpy(), b.numpy(), 32, lam=cfg.lam, seed=3, max_iters=T, x0=x0, proj=1, tmax=8, **opts)
+    ctx = lsqr_ctx(kpp, A, 32, cfg.lam, 3)
+    if "accel" in opts:
+        ctx.set_option(kpp.OPT_ACCEL, 0)
+    if "memo" in opts:
+        ctx.set_option(kpp.OPT_MEMO, 0)
+    if "rho_fixed" in opts:
+        ctx.set_option(kpp.OPT_RHO_FIXED, opts["rho_fixed"])
+    if "eta" in opts:
+        ctx.set_option(kpp.OPT_ETA, opts["eta"])
+    res = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=T)
+    An = A.numpy()
+    kap = max(np.linalg.cond(ora.sketch_factor(An, ctx.block(k).numpy(), cfg.lam, 3, 64)) ** 2 for k in range(3))
+    assert rel(res.x.cpu().numpy(), ref.x) <= max(1e-10, 4 * 2.2e-16 * kap)

@@ -583,3 +583,29 @@ def test_padded_leading_dimension(kpp, ora, cfg, pad, mode):
     ref = run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8, **kw)
     assert rel(x.cpu().numpy(), ref.x) <= 1e-10
     L.kpp_destroy(h)
+
+
+@pytest.mark.parametrize("engine", [0, 1, 2])
+@pytest.mark.parametrize("cfg,s", [(synth.twin("c3", 96, 40, 1, k=4), 1), (synth.twin("c3", 96, 40, 96, k=4), 96),
+                                   (synth.twin("c5", 70, 70, 1, k=4), 1), (synth.twin("c5", 70, 70, 70, k=4), 70)],
+                         ids=["kpp_s1", "kpp_sm", "cdpp_s1", "cdpp_sn"])
+def test_block_size_extremes_engines(kpp, ora, cfg, s, engine):
+    """s = 1 and s = m (K++) / n (CD++) on the persistent and fused-exchange engines, with RHT for
+    s = 1 (padding of a non-power-of-2 size)."""
+    A, b, _ = synth.make_problem(cfg)
+    T = 120
+    setup = kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup
+    run = ora.cdpp_run if cfg.kind == "cdpp" else ora.kpp_run
+    ctx = setup(A.to(DEV), s, cfg.lam, 2)
+    ctx.set_option(kpp.OPT_ENGINE, engine)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    ref = run(A.numpy(), b.numpy(), s, lam=cfg.lam, seed=2, max_iters=T, threads=8)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    if s == 1:
+        ctx2 = setup(A.to(DEV), s, cfg.lam, 2)
+        ctx2.set_option(kpp.OPT_ENGINE, engine)
+        ctx2.enable_rht()
+        res2 = ctx2.solve(b.to(DEV), max_iters=T)
+        runr = ora.cdpp_run_rht if cfg.kind == "cdpp" else ora.kpp_run_rht
+        ref2 = runr(A.numpy(), b.numpy(), s, seed=2, lam=cfg.lam, max_iters=T, threads=8)
+        assert rel(res2.x.cpu().numpy(), ref2.x) <= 1e-10
