@@ -609,3 +609,20 @@ def test_block_size_extremes_engines(kpp, ora, cfg, s, engine):
         runr = ora.cdpp_run_rht if cfg.kind == "cdpp" else ora.kpp_run_rht
         ref2 = runr(A.numpy(), b.numpy(), s, seed=2, lam=cfg.lam, max_iters=T, threads=8)
         assert rel(res2.x.cpu().numpy(), ref2.x) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["engine0", "engine1", "engine2", "lsqr"])
+def test_zero_rhs(kpp, ora, mode):
+    """b = 0 from x0 = 0: every residual is zero, x stays 0 and the solve stops at the first checkpoint
+    (E1 = 0 <= tol^2 ||b||^2 = 0), as in the oracle."""
+    A = torch.from_numpy(np.random.default_rng(8).standard_normal((96, 50)))
+    b = torch.zeros(96, dtype=torch.float64)
+    ctx = kpp.kpp_setup(A.to(DEV), 12, 1e-8, 0)
+    if mode == "lsqr":
+        ctx.set_option(kpp.OPT_PROJ, 1)
+    else:
+        ctx.set_option(kpp.OPT_ENGINE, int(mode[-1]))
+    res = ctx.solve(b.to(DEV), max_iters=1000)
+    ref = ora.kpp_run(A.numpy(), b.numpy(), 12, lam=1e-8, seed=0, max_iters=1000, proj=1 if mode == "lsqr" else 0)
+    assert res.iters == ref.iters == 2 * 8  # zeta = ceil(96 / 12)
+    assert float(res.x.abs().max()) == 0.0
