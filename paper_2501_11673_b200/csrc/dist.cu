@@ -4,15 +4,17 @@
 // One persistent cooperative kernel per window, one CTA per SM.  Per block iteration (Alg 5 l.9-12
 // P:1346-1349 / Alg 3 l.10-13 P:755-759) on rank p's column slab A[:, cols_p]:
 //   (a) CTA g: row sums of its slab, part[g][k] = sum_{j in slab g} A[S_k][j] x_j, as tagged LL
-//       words in L2 (the slab is kept in shared memory for (e) when it fits);
+//       words in L2 (the slab sits in shared memory when it fits: double-buffered, the next block's
+//       slab streaming in by cp.async behind the current iteration, or a single copy reused by (e));
 //   (b) exchange: the owner warp of k (CTA k mod grid) sums the grid's words in a fixed order and
 //       stores the rank's partial into slot [t mod 2][p][k] of EVERY rank's receive buffer -- over
 //       NVLink for the peers (CUDA IPC mappings, system-scope stores of 32 data bits + 32-bit tag per
 //       8-byte word) -- and every CTA gathers slot [t mod 2][0..P-1][k] of its own buffer, summing
 //       the ranks in rank order: the same bits on every rank, no NCCL call and no kernel boundary
 //       between the partial products and the solve;
-//   (c) r = (A_S x)_total - b_S, e = ||r||^2;  (d) y = M r (M row-major, staged in shared memory
-//       when it fits), computed redundantly and bit-identically by every CTA of every rank;
+//   (c) r = (A_S x)_total - b_S, e = ||r||^2;  (d) y = M r: by every CTA from M staged in shared
+//       memory when it fits, else row k by CTA k mod grid and gathered through L2 (one more hop);
+//       bit-identical on every CTA of every rank either way;
 //   (e) w = A_S^T y on the slab (K++) or the scatter of y (CD++), m <- c (m - w), x <- x - w + eta m;
 //   (f) window logic (row 8), replicated.
 // Two parity slots suffice for the peer buffers: a rank publishes t+2 only after every rank has
