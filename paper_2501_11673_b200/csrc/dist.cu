@@ -55,10 +55,11 @@ __device__ __forceinline__ void prefetch_slab(const XParams& p, const int32_t* S
                                               long long c1) {
   const int w = (int)(c1 - c0);
   if (w <= 0) return;
-  const long long tot = (long long)p.s * w;
-  for (long long i = threadIdx.x; i < tot; i += NT) {
-    const int k = (int)(i / w), c = (int)(i % w);
-    cp_async8(dst + (long long)k * p.sl + c, p.A + (long long)S[k] * p.lda + c0 + c);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < p.s; k += NW) {  // a warp per row, lanes across the slab (no divisions)
+    const double* src = p.A + (long long)S[k] * p.lda + c0;
+    double* d = dst + (long long)k * p.sl;
+    for (int c = lane; c < w; c += 32) cp_async8(d + c, src + c);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
