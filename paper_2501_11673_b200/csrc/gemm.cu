@@ -135,13 +135,17 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(int M, int N, int K, int
 // orientation in shared memory ([outer][k] when k is contiguous in memory, [k][outer] otherwise),
 // padded so that the fragment loads of a half-warp hit distinct banks.  Requires 16-byte aligned
 // rows (even ld and batch strides, aligned base pointers); launch_dgemm falls back otherwise.
+// The M tile is a template parameter BM (128: 8 warps as 4 x 2; 64: 4 warps as 2 x 2, used for the
+// upper-only Gram products, whose diagonal-crossing 128 x 64 tiles leave up to 5 of 8 warps idle).
 constexpr int B2M = 128, B2N = 64, B2K = 16, B2S = 3, B2T = 256;
 constexpr int KC_LD = B2K + 4;      // [outer][k] row stride (doubles)
-constexpr int AM_LD = B2M + 4;      // [k][outer] row stride of A
 constexpr int BN_LD = B2N + 4;      // [k][outer] row stride of B
-constexpr int A_STAGE = (B2M * KC_LD > B2K * AM_LD) ? B2M * KC_LD : B2K * AM_LD;  // doubles
+__host__ __device__ constexpr int am_ld(int bm) { return bm + 4; }  // [k][outer] row stride of A
+__host__ __device__ constexpr int a_stage(int bm) { return (bm * KC_LD > B2K * am_ld(bm)) ? bm * KC_LD : B2K * am_ld(bm); }
 constexpr int B_STAGE = (B2N * KC_LD > B2K * BN_LD) ? B2N * KC_LD : B2K * BN_LD;
-constexpr size_t B2_SMEM = (size_t)B2S * (A_STAGE + B_STAGE) * sizeof(double);
+constexpr size_t b2_smem(int bm) { return (size_t)B2S * (a_stage(bm) + B_STAGE) * sizeof(double); }
+constexpr int AM_LD = am_ld(B2M);
+constexpr size_t B2_SMEM = b2_smem(B2M);
 constexpr int KIDX_MAX = 1024;      // K-gathered operand: staged gather list (s <= 1024)
 
 __device__ __forceinline__ void cp_async16z(double* dst, const double* src, int bytes) {
@@ -152,12 +156,12 @@ __device__ __forceinline__ void cp_async16z(double* dst, const double* src, int 
 
 // Stage one OUTER x 16 operand tile.  KC: memory rows are `outer` (k contiguous) -> sm[outer][k];
 // otherwise memory rows are k (outer contiguous) -> sm[k][outer].
-template <bool KC, int OUTER, int LDO>
+template <bool KC, int OUTER, int LDO, int NTT = B2T>
 __device__ __forceinline__ void stage_tile(double* sm, const double* base, long long ld, const int32_t* idx,
                                            int outer0, int outer_lim, int k0, int k_lim) {
   constexpr int CH = KC ? OUTER * (B2K / 2) : B2K * (OUTER / 2);  // 16-byte chunks
 #pragma unroll
-  for (int c = threadIdx.x; c < CH; c += B2T) {
+  for (int c = threadIdx.x; c < CH; c += NTT) {
     if (KC) {
       const int o = c / (B2K / 2), kc = (c % (B2K / 2)) * 2;
       const int go = outer0 + o, gk = k0 + kc;
@@ -176,24 +180,24 @@ __device__ __forceinline__ void stage_tile(double* sm, const double* base, long 
 
 // KC tiles (k contiguous in memory): the memory row of each of the thread's chunks is fixed across
 // the K loop, so it is resolved once (row gather included) into NI registers; -1 = out of range.
-template <int OUTER>
+template <int OUTER, int NTT = B2T>
 struct KcRows {
-  static constexpr int NI = OUTER * (B2K / 2) / B2T;
+  static constexpr int NI = OUTER * (B2K / 2) / NTT;
   int r[NI];
   __device__ __forceinline__ void init(const int32_t* idx, int outer0, int outer_lim) {
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
-      const int go = outer0 + (threadIdx.x + B2T * i) / (B2K / 2);
+      const int go = outer0 + (threadIdx.x + NTT * i) / (B2K / 2);
       r[i] = go < outer_lim ? (idx ? idx[go] : go) : -1;
     }
   }
 };
-template <int OUTER>
-__device__ __forceinline__ void stage_tile_kc(double* sm, const double* base, long long ld, const KcRows<OUTER>& rows,
-                                              int k0, int k_lim) {
+template <int OUTER, int NTT = B2T>
+__device__ __forceinline__ void stage_tile_kc(double* sm, const double* base, long long ld,
+                                              const KcRows<OUTER, NTT>& rows, int k0, int k_lim) {
 #pragma unroll
-  for (int i = 0; i < KcRows<OUTER>::NI; ++i) {
-    const int c = threadIdx.x + B2T * i;
+  for (int i = 0; i < KcRows<OUTER, NTT>::NI; ++i) {
+    const int c = threadIdx.x + NTT * i;
     const int o = c / (B2K / 2), kc = (c % (B2K / 2)) * 2;
     const int gk = k0 + kc;
     const int valid = rows.r[i] >= 0 ? min(2, max(0, k_lim - gk)) : 0;
@@ -205,23 +209,25 @@ __device__ __forceinline__ void stage_tile_kc(double* sm, const double* base, lo
 // ATRI: 0 general A; 1 logical A lower triangular (A(i,k) = 0 for k > i); 2 upper (A(i,k) = 0 for
 // k < i) -- the K range of each row tile / warp is clipped (the stored zeros are skipped, not
 // assumed).  Epilogue: C = alpha * A B (+ C when beta1).
-template <bool AT, bool BT, int ATRI>
-__global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int Z, int kchunk, Operand a,
-                                                        Operand b, double* C, long long ldc, long long c_bstride,
-                                                        int upper_only, double alpha, int beta1) {
+template <bool AT, bool BT, int ATRI, int BM = B2M>
+__global__ void __launch_bounds__(2 * BM, BM == 128 ? 2 : 3) dgemm2_kernel(int M, int N, int K, int Z, int kchunk,
+                                                                           Operand a, Operand b, double* C,
+                                                                           long long ldc, long long c_bstride,
+                                                                           int upper_only, double alpha, int beta1) {
+  constexpr int NTT = 2 * BM, A_ST = a_stage(BM), AMLD = am_ld(BM);
   constexpr bool ALOWER = ATRI == 1;
   extern __shared__ __align__(16) double g2sm[];
   const int tn = blockIdx.x, tm = blockIdx.y;
-  if (upper_only && tm * B2M >= (tn + 1) * B2N) return;  // tile entirely below the diagonal
+  if (upper_only && tm * BM >= (tn + 1) * B2N) return;  // tile entirely below the diagonal
   const int bz = blockIdx.z;
   const int batch = bz / Z, z = bz % Z;
   const int kbeg = z * kchunk;
   int kbeg_t = kbeg;
   int kend = min(K, kbeg + kchunk);
-  if (ALOWER) kend = min(kend, (tm + 1) * B2M);  // A(i,k) = 0 for k > i
-  if (ATRI == 2) kbeg_t = max(kbeg, (tm * B2M) / B2K * B2K);  // A(i,k) = 0 for k < i
+  if (ALOWER) kend = min(kend, (tm + 1) * BM);  // A(i,k) = 0 for k > i
+  if (ATRI == 2) kbeg_t = max(kbeg, (tm * BM) / B2K * B2K);  // A(i,k) = 0 for k < i
   double* As = g2sm;
-  double* Bs = g2sm + B2S * A_STAGE;
+  double* Bs = g2sm + B2S * A_ST;
   const double* abase = a.ptr + (long long)batch * a.bstride;
   const double* bbase = b.ptr + (long long)batch * b.bstride;
   const int32_t* aidx = a.idx ? a.idx + (long long)batch * a.idx_bstride : nullptr;
@@ -235,13 +241,13 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int nk = kend > kbeg_t ? (kend - kbeg_t + B2K - 1) / B2K : 0;
-  const int wrow0 = tm * B2M + wm * 32, wcol0 = tn * B2N + wn * 32;
+  const int wrow0 = tm * BM + wm * 32, wcol0 = tn * B2N + wn * 32;
   const bool wskip = upper_only && wrow0 >= wcol0 + 32;
   const int wrow_end = wrow0 + 32;
   // A logical (i,k): !AT -> memory row i (k contiguous); B logical (k,j): BT -> memory row j
-  KcRows<B2M> arows;
-  KcRows<B2N> brows;
-  if (!AT) arows.init(aidx, tm * B2M, M);
+  KcRows<BM, NTT> arows;
+  KcRows<B2N, NTT> brows;
+  if (!AT) arows.init(aidx, tm * BM, M);
   if (BT) brows.init(bidx, tn * B2N, N);
   // operands whose memory rows run along K with a row gather: the CTA's K range of the gather list
   // is staged in shared memory once (the per-stage address then needs no global load)
@@ -251,17 +257,17 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
   {
     const int32_t* g = (AT && aidx) ? aidx : (!BT && bidx) ? bidx : nullptr;
     if (g && kend - kbeg_t <= KIDX_MAX && !(AT && aidx && !BT && bidx)) {
-      for (int i = threadIdx.x; i < kend - kbeg_t; i += B2T) kidx_sh[i] = g[kbeg_t + i];
+      for (int i = threadIdx.x; i < kend - kbeg_t; i += NTT) kidx_sh[i] = g[kbeg_t + i];
       __syncthreads();
       if (AT && aidx) kidx_a = kidx_sh - kbeg_t;
       else kidx_b = kidx_sh - kbeg_t;
     }
   }
   auto stage = [&](int slot, int k0) {
-    if (!AT) stage_tile_kc<B2M>(As + slot * A_STAGE, abase, a.ld, arows, k0, kend);
-    else stage_tile<false, B2M, AM_LD>(As + slot * A_STAGE, abase, a.ld, kidx_a ? kidx_a : aidx, tm * B2M, M, k0, kend);
-    if (BT) stage_tile_kc<B2N>(Bs + slot * B_STAGE, bbase, b.ld, brows, k0, kend);
-    else stage_tile<false, B2N, BN_LD>(Bs + slot * B_STAGE, bbase, b.ld, kidx_b ? kidx_b : bidx, tn * B2N, N, k0, kend);
+    if (!AT) stage_tile_kc<BM, NTT>(As + slot * A_ST, abase, a.ld, arows, k0, kend);
+    else stage_tile<false, BM, AMLD, NTT>(As + slot * A_ST, abase, a.ld, kidx_a ? kidx_a : aidx, tm * BM, M, k0, kend);
+    if (BT) stage_tile_kc<B2N, NTT>(Bs + slot * B_STAGE, bbase, b.ld, brows, k0, kend);
+    else stage_tile<false, B2N, BN_LD, NTT>(Bs + slot * B_STAGE, bbase, b.ld, kidx_b ? kidx_b : bidx, tn * B2N, N, k0, kend);
   };
 #pragma unroll
   for (int st = 0; st < B2S - 1; ++st) {
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
       if (ln < nk) stage(ln % B2S, kbeg_t + ln * B2K);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-    const double* Ast = As + (kt % B2S) * A_STAGE;
+    const double* Ast = As + (kt % B2S) * A_ST;
     const double* Bst = Bs + (kt % B2S) * B_STAGE;
     if (wskip) continue;  // this warp's 32 x 32 tile lies below the diagonal (Gram, upper only)
     // logical A lower triangular: k-steps past this warp's last row contribute nothing
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int m = wm * 32 + i * 8 + fr;
-        af[i] = !AT ? Ast[m * KC_LD + kk + fc] : Ast[(kk + fc) * AM_LD + m];
+        af[i] = !AT ? Ast[m * KC_LD + kk + fc] : Ast[(kk + fc) * AMLD + m];
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(B2T, 2) dgemm2_kernel(int M, int N, int K, int
   double* Cb = C + (long long)bz * c_bstride;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int gi = tm * B2M + wm * 32 + i * 8 + fr;
+    const int gi = tm * BM + wm * 32 + i * 8 + fr;
     if (gi >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -343,17 +349,38 @@ static bool aligned16(const Operand& o) {
   return (reinterpret_cast<uintptr_t>(o.ptr) & 15) == 0 && (o.ld & 1) == 0 && (o.bstride & 1) == 0;
 }
 
+// M tile of the pipelined kernel: 64 for upper-only (Gram) products unless KPP_GEMM_BM=128
+static int gram_bm() {
+  static int bm = [] {
+    const char* e = getenv("KPP_GEMM_BM");
+    return (e && atoi(e) == 128) ? 128 : 64;
+  }();
+  return bm;
+}
+
+template <bool AT, bool BT, int TRI, int TBM>
+static void launch2m(cudaStream_t st, int M, int N, int Zb, int Z, int K, int kchunk, const Operand& a,
+                     const Operand& b, double* C, long long ldc, long long c_bstride, int upper_only, double alpha,
+                     int beta1) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dgemm2_kernel<AT, BT, TRI, TBM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)b2_smem(TBM));
+    attr = true;
+  }
+  dim3 grid((N + B2N - 1) / B2N, (M + TBM - 1) / TBM, Zb);
+  dgemm2_kernel<AT, BT, TRI, TBM><<<grid, 2 * TBM, b2_smem(TBM), st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride,
+                                                                       upper_only, alpha, beta1);
+}
+
 template <bool AT, bool BT, int TRI>
 static void launch2(cudaStream_t st, dim3 grid, int M, int N, int K, int Z, int kchunk, const Operand& a,
                     const Operand& b, double* C, long long ldc, long long c_bstride, int upper_only, double alpha,
                     int beta1) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dgemm2_kernel<AT, BT, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)B2_SMEM);
-    attr = true;
-  }
-  dgemm2_kernel<AT, BT, TRI><<<grid, B2T, B2_SMEM, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only,
-                                                         alpha, beta1);
+  if (upper_only && gram_bm() == 64)
+    launch2m<AT, BT, TRI, 64>(st, M, N, grid.z, Z, K, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
+  else
+    launch2m<AT, BT, TRI, B2M>(st, M, N, grid.z, Z, K, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
 }
 
 template <bool AT, bool BT>
