@@ -137,7 +137,15 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(int M, int N, int K, int
 // rows (even ld and batch strides, aligned base pointers); launch_dgemm falls back otherwise.
 // The M tile is a template parameter BM (128: 8 warps as 4 x 2; 64: 4 warps as 2 x 2, used for the
 // upper-only Gram products, whose diagonal-crossing 128 x 64 tiles leave up to 5 of 8 warps idle).
-constexpr int B2M = 128, B2N = 64, B2K = 16, B2S = 3, B2T = 256;
+// K step and pipeline depth: measured alternatives (K 32 / 3 stages, K 16 / 4, K 32 / 2) all lose
+// occupancy and were slower or equal; overridable for such experiments
+#ifndef KPP_B2K
+#define KPP_B2K 16
+#endif
+#ifndef KPP_B2S
+#define KPP_B2S 3
+#endif
+constexpr int B2M = 128, B2N = 64, B2K = KPP_B2K, B2S = KPP_B2S, B2T = 256;
 constexpr int KC_LD = B2K + 4;      // [outer][k] row stride (doubles)
 constexpr int BN_LD = B2N + 4;      // [k][outer] row stride of B
 __host__ __device__ constexpr int am_ld(int bm) { return bm + 4; }  // [k][outer] row stride of A
