@@ -251,6 +251,9 @@ __global__ void __launch_bounds__(2 * BM, BM == 128 ? 2 : 3) dgemm2_kernel(int M
   const int nk = kend > kbeg_t ? (kend - kbeg_t + B2K - 1) / B2K : 0;
   const int wrow0 = tm * BM + wm * 32, wcol0 = tn * B2N + wn * 32;
   const bool wskip = upper_only && wrow0 >= wcol0 + 32;
+  // a warp tile on the diagonal (upper only): its 8 x 8 fragments strictly below the diagonal
+  // (6 of 16) are not computed either
+  const bool wdiag = upper_only == 2 && wrow0 == wcol0;  // 2: fragment skipping on
   const int wrow_end = wrow0 + 32;
   // A logical (i,k): !AT -> memory row i (k contiguous); B logical (k,j): BT -> memory row j
   KcRows<BM, NTT> arows;
@@ -309,10 +312,17 @@ __global__ void __launch_bounds__(2 * BM, BM == 128 ? 2 : 3) dgemm2_kernel(int M
         const int nn = wn * 32 + j * 8 + fr;
         bf[j] = BT ? Bst[nn * KC_LD + kk + fc] : Bst[(kk + fc) * BN_LD + nn];
       }
+      if (wdiag) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) mma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = i; j < 4; ++j) mma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -385,6 +395,11 @@ template <bool AT, bool BT, int TRI>
 static void launch2(cudaStream_t st, dim3 grid, int M, int N, int K, int Z, int kchunk, const Operand& a,
                     const Operand& b, double* C, long long ldc, long long c_bstride, int upper_only, double alpha,
                     int beta1) {
+  static const int fskip = [] {
+    const char* e = getenv("KPP_GEMM_FSKIP");  // 0: compute diagonal warp tiles whole (A/B switch)
+    return e ? atoi(e) : 1;
+  }();
+  if (upper_only && fskip) upper_only = 2;
   if (upper_only && gram_bm() == 64)
     launch2m<AT, BT, TRI, 64>(st, M, N, grid.z, Z, K, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
   else
