@@ -338,11 +338,11 @@ struct P1Prof {
 
 kpp_status lsqr_prepare(kpp_ctx* ctx);
 
-// Split-K count of the Gram products: a function of n only (K chunks of 1024 columns, at most 64),
+// Split-K count of the Gram products: a function of n only (K chunks of 4096 columns, at most 64),
 // so the summation order -- and the bits of M -- do not depend on how fresh blocks are batched.
 int gram_splits(const kpp_ctx* ctx) {
   if (ctx->kind != KIND_KPP) return 1;
-  long long kc = 1024;
+  long long kc = 4096;  // measured: 1024 / 2048 / 4096 / 8192
   if (const char* ez = getenv("KPP_GRAM_KCHUNK")) kc = std::max(16, atoi(ez));  // experiments
   return (int)std::min<long long>(64, std::max<long long>(1, (ctx->n + kc - 1) / kc));
 }
