@@ -152,8 +152,6 @@ __host__ __device__ constexpr int am_ld(int bm) { return bm + 4; }  // [k][outer
 __host__ __device__ constexpr int a_stage(int bm) { return (bm * KC_LD > B2K * am_ld(bm)) ? bm * KC_LD : B2K * am_ld(bm); }
 constexpr int B_STAGE = (B2N * KC_LD > B2K * BN_LD) ? B2N * KC_LD : B2K * BN_LD;
 constexpr size_t b2_smem(int bm) { return (size_t)B2S * (a_stage(bm) + B_STAGE) * sizeof(double); }
-constexpr int AM_LD = am_ld(B2M);
-constexpr size_t B2_SMEM = b2_smem(B2M);
 constexpr int KIDX_MAX = 1024;      // K-gathered operand: staged gather list (s <= 1024)
 
 __device__ __forceinline__ void cp_async16z(double* dst, const double* src, int bytes) {

@@ -117,6 +117,41 @@ def test_factor_operator(kpp, ora, factor):
         assert np.allclose(M, M.T, rtol=0, atol=1e-12 * np.abs(M).max())
 
 
+@pytest.mark.parametrize("s", [31, 33, 64, 65, 100, 129, 200])
+@pytest.mark.parametrize("factor", [1, 2])
+def test_factor_operator_ragged(kpp, ora, s, factor):
+    """The Gram products' tile edges: 64-row upper-only tiles, the diagonal warp tiles whose
+    fragments below the diagonal are skipped, and a split-K whose last 4096-column chunk is ragged
+    (n = 4100). M against the oracle's Householder factor, same bound as above."""
+    m, n, lam = 300, 4100, 1e-8
+    cfg = synth.twin("c3", m, n, s, k=8)
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), s, lam, 5)
+    ctx.set_option(kpp.OPT_FACTOR, factor)
+    ctx.prepare(6)
+    An = A.numpy()
+    for k in (0, 2):
+        S = ctx.block(k).numpy()
+        M = ctx.factor(k).numpy()
+        Ri = np.linalg.inv(ora.kpp_factor(An, S, lam))
+        G = An[S] @ An[S].T + lam * np.eye(s)
+        assert rel(M, Ri @ Ri.T) < 200 * 2.2e-16 * np.linalg.cond(G), (s, k, rel(M, Ri @ Ri.T))
+        assert np.allclose(M, M.T, rtol=0, atol=1e-12 * np.abs(M).max())
+
+
+@pytest.mark.parametrize("s", [33, 100])
+def test_cdpp_factor_operator_ragged(kpp, ora, s):
+    cfg = synth.twin("c5", 700, 700, s, k=25)
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.cdpp_setup(A.to(DEV), s, 1e-8, 2)
+    ctx.prepare(4)
+    An = A.numpy()
+    for k in (0, 1):
+        S = ctx.block(k).numpy()
+        Ri = np.linalg.inv(ora.cdpp_factor(An, S, 1e-8))
+        assert rel(ctx.factor(k).numpy(), Ri @ Ri.T) < 1e-10
+
+
 def test_cdpp_factor_operator(kpp, ora):
     cfg = synth.twin("c5", 1024, 1024, 128, k=25)
     A, b, _ = synth.make_problem(cfg)
