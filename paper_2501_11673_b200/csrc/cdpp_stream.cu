@@ -235,12 +235,14 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   double* m_sm = D + L.m;
   double* z_sm = D + L.z;
   double* r_sm = D + L.r;
-  double* ybuf[2] = {D + L.y, D + L.yprev};  // y_t of slot t in ybuf[it & 1]
-  double* dbuf[2] = {D + L.dcur, D + L.dnext};
+  // double buffers picked by parity with selects, not arrays of pointers: the pointers stay
+  // derived from smem_raw, so their accesses compile to shared-memory loads/stores (LDS/STS)
+  auto ybuf = [&](int i) { return i ? D + L.yprev : D + L.y; };  // y_t of slot t in ybuf(it & 1)
+  auto dbuf = [&](int i) { return i ? D + L.dnext : D + L.dcur; };
   double* bS_sh = D + L.bS;
-  double* stash[2] = {D + L.stash0, D + L.stash1};
+  auto stash = [&](int i) { return i ? D + L.stash1 : D + L.stash0; };
   int* I = reinterpret_cast<int*>(D + L.ints);
-  int* cmap[2] = {I + L.cmap0, I + L.cmap1};  // cmap[it & 1]: positions of S_t's entries in the slab
+  auto cmap = [&](int i) { return i ? I + L.cmap1 : I + L.cmap0; };  // cmap(it & 1): positions of S_t's entries in the slab
   int* ljb = I + L.lj;                       // lists of S_t, S_{t+1}, S_{t+2} entries: [it % 3]
   int* lkb = I + L.lk;
   int32_t* S_sh = I + L.S;
@@ -267,8 +269,8 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   for (int j = tid; j < w; j += T2) {
     x_sm[j] = p.x[c0 + j];
     m_sm[j] = p.mom[c0 + j];
-    cmap[0][j] = -1;
-    cmap[1][j] = -1;
+    cmap(0)[j] = -1;
+    cmap(1)[j] = -1;
   }
   for (int i = tid; i < s; i += T2) {
     const int32_t v = p.S_pool[(long long)p.bid[0] * s + i];
@@ -278,13 +280,13 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   }
   __syncthreads();
   if (warp == 0) {
-    const int n = build_list(S_sh, s, gc0, gc1, ljb, lkb, cmap[0], lane);
+    const int n = build_list(S_sh, s, gc0, gc1, ljb, lkb, cmap(0), lane);
     if (lane == 0) nl_sh[0] = n;
   }
   if (tid == 0) row_ctr = 0;
   cluster.sync();
   // prologue: D_{t0} = A_{S_{t0}} x_{t0} (no correction: nothing was applied before t0 here)
-  stream_pass(p, S_sh, c0, w, x_sm, dbuf[0], nullptr, stash[0], vec, &row_ctr);
+  stream_pass(p, S_sh, c0, w, x_sm, dbuf(0), nullptr, stash(0), vec, &row_ctr);
   __syncthreads();
 
   const unsigned la_rp = smem_u32(rp_sm), la_r = smem_u32(r_sm);
@@ -320,19 +322,19 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
     const int nprev = it > 0 ? nl_sh[lm] : 0;
     const int* ljm = ljb + lm * L.lcap;
     const int* lkm = lkb + lm * L.lcap;
-    const double* yprev = ybuf[prv];
-    double* y_sm = ybuf[cur];
+    const double* yprev = ybuf(prv);
+    double* y_sm = ybuf(cur);
     if (tid == 0) {
       if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
       mbar_expect_tx(bars + 3, (unsigned)s * 8u);
       row_ctr = 0;  // read only after the phase-A barrier
     }
     // ---- phase A (all threads)
-    // A1: x_t, m_t from w_{t-1} = I_{S_{t-1}}^T y_{t-1} (cmap[prv] holds S_{t-1}'s positions), z_t
+    // A1: x_t, m_t from w_{t-1} = I_{S_{t-1}}^T y_{t-1} (cmap(prv) holds S_{t-1}'s positions), z_t
     for (int j = tid; j < w; j += T2) {
       double xv = x_sm[j], mv = m_sm[j];
       if (it > 0) {
-        const int pos = cmap[prv][j];
+        const int pos = cmap(prv)[j];
         const double wv = pos >= 0 ? yprev[lkm[pos]] : 0.0;
         mv = c_prev * (mv - wv);
         xv = xv - wv + p.eta * mv;
@@ -343,8 +345,8 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
     }
     // A2: partial r_t = D_t - (1 + eta c_{t-1}) A[S_t, S_{t-1} in slab] y_{t-1} -> slice owner
     {
-      const double* dcur = dbuf[cur];
-      const double* stc = stash[cur];
+      const double* dcur = dbuf(cur);
+      const double* stc = stash(cur);
       const double g = 1.0 + p.eta * c_prev;
       for (int k = tid; k < s; k += T2) {
         double v = dcur[k];
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
 
     if (warp < NSW) {
       // ---- B (streaming warps): D_{t+1} = A[S_{t+1}, slab] z_t, stash A[S_{t+1}, S_t in slab]
-      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf[prv], cmap[cur], stash[prv], vec, &row_ctr);
+      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf(prv), cmap(cur), stash(prv), vec, &row_ctr);
       CS_MARK(1);  // stream (thread 0)
     } else {
       // ---- B (chain threads): exchange, window logic and projection of iteration t
@@ -402,10 +404,10 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
           }
         }
       } else if (ct < 64 && pf) {
-        // map of S_{t+1} for the stream of slot t+1 (cmap[prv]: clear S_{t-1}'s entries first)
-        for (int i = lane; i < nprev; i += 32) cmap[prv][ljm[i]] = -1;
+        // map of S_{t+1} for the stream of slot t+1 (cmap(prv): clear S_{t-1}'s entries first)
+        for (int i = lane; i < nprev; i += 32) cmap(prv)[ljm[i]] = -1;
         __syncwarp();
-        const int n = build_list(Sn, s, gc0, gc1, ljb + lp * L.lcap, lkb + lp * L.lcap, cmap[prv], lane);
+        const int n = build_list(Sn, s, gc0, gc1, ljb + lp * L.lcap, lkb + lp * L.lcap, cmap(prv), lane);
         if (lane == 0) nl_sh[lp] = n;
       }
       tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
@@ -442,11 +444,11 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
       ll_gather_vec<4>(y_sm, p.yll + (long long)(it & 1) * s * 2, s, tag, p.err, ct, NCH);
       CS_MARK(5);  // y gathered
       // the chain of t is done: help stream D_{t+1}
-      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf[prv], cmap[cur], stash[prv], vec, &row_ctr);
+      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf(prv), cmap(cur), stash(prv), vec, &row_ctr);
     }
     __syncthreads();
     CS_MARK(6);  // end-of-slot barrier wait
-    // hand over: y_t (ybuf[cur]) becomes y_prev, rho_t becomes rho_prev
+    // hand over: y_t (ybuf(cur)) becomes y_prev, rho_t becomes rho_prev
     rho_prev = rho;
     if (stop_sh) {
       ++t;
@@ -458,11 +460,11 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   if (it > 0) {
     __syncthreads();
     const int lastm = (it - 1) & 1, lastl = (it - 1) % 3;
-    const double* yprev = ybuf[lastm];
+    const double* yprev = ybuf(lastm);
     const double c_last = (1.0 - rho_prev) / (1.0 + rho_prev);
     const int* lkl = lkb + lastl * L.lcap;
     for (int j = tid; j < w; j += T2) {
-      const int pos = cmap[lastm][j];
+      const int pos = cmap(lastm)[j];
       const double wv = pos >= 0 ? yprev[lkl[pos]] : 0.0;
       const double mm = c_last * (m_sm[j] - wv);
       m_sm[j] = mm;

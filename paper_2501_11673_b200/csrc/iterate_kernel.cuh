@@ -76,7 +76,12 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   // ygl 4: partial y (and ||r_slice||^2) from every rank of the cluster, [C][s+1]
   double* yp_sm = reinterpret_cast<double*>(S_sh + 3 * sp);
   unsigned char* tail = reinterpret_cast<unsigned char*>(yp_sm + (yred ? ((C * (s + 1) + 1) & ~1) : 0));
-  tail = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tail) + 127) & ~uintptr_t(127));
+  {
+    // 128-byte alignment of the TMA buffers, applied as an offset to a pointer derived from
+    // smem_raw: the compiler then keeps the shared address space (LDS, not generic loads)
+    const unsigned a0 = (unsigned)__cvta_generic_to_shared(tail);
+    tail += ((a0 + 127u) & ~127u) - a0;
+  }
   double* Abuf = reinterpret_cast<double*>(tail);               // [2][s4][sw] (128B aligned)
   const long long absz = (long long)((s + 3) & ~3) * p.sw;
   const long long mslz = ((long long)sl * s + 15) & ~15LL;
@@ -158,6 +163,14 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     const int nbf = a_single ? 0 : (buf ^ 1);  // ... of the prefetch of iteration t+1
     const double* Ac = Abuf + sb * absz;
     const double* Msl = Mbuf + (m2 ? 0 : buf * mslz);
+    if constexpr (YG == 0) {
+      // Measured (c2, one box, A/B): this plan runs faster with the slab and the M rows read by
+      // generic loads (5.81 vs 6.05 us/iteration with LDS) -- its y step issues the M-row loads
+      // next to the DSMEM stores and shuffles of the exchange; the other plans use LDS (c3 8.45 ->
+      // 7.76 us).  The no-op move hides the shared address space from the compiler.
+      asm volatile("mov.b64 %0, %0;" : "+l"(Msl));
+      asm volatile("mov.b64 %0, %0;" : "+l"(Ac));
+    }
     const bool pf = t + 1 < p.t1;
     // ---- top: this iteration's slab and M rows have landed; this thread's cp.async loads
     //      (S, b_S) of the previous iteration have landed; arm the barrier of the next buffer
@@ -173,7 +186,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
 #pragma unroll
       for (int i = 0; i < RPW; ++i) {
         const int k = warp + 16 * i;
-        const double* arow = Ac + (long long)k * p.sw;
+        const double* arow = Ac + k * p.sw;
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) ar[i][cc] = (k < s && lane + 32 * cc < w) ? arow[lane + 32 * cc] : 0.0;
       }
@@ -220,7 +233,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
           const int k = kp + tid / tpr;
           double acc = 0.0;
           if (k < s && !p.dbg_skip) {
-            const double* arow = Ac + (long long)k * p.sw;
+            const double* arow = Ac + k * p.sw;
             for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
           }
           for (int o = tpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -494,7 +507,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
                 const double rl = r_sm[l];
 #pragma unroll
                 for (int i = 0; i < RY; ++i)
-                  if (rb + i < R) v[i] = fma(Msl[(long long)(rb + i) * s + l], rl, v[i]);
+                  if (rb + i < R) v[i] = fma(Msl[(rb + i) * s + l], rl, v[i]);
               }
             } else {
 #pragma unroll 4
