@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       for (int l = tid; l < s; l += T2) {
         double v = 0.0;
         if (!p.dbg_skip)
-          for (int k = 0; k < R; ++k) v = fma(Msl[(long long)k * s + l], r_sm[r0 + k], v);
+          for (int k = 0; k < R; ++k) v = fma(Msl[k * s + l], r_sm[r0 + k], v);
         for (int cc = 0; cc < C; ++cc)
           st_async_f64(mapa_u32(la_yp + (unsigned)(c * (s + 1) + l) * 8u, cc), v, mapa_u32(lb_y, cc));
       }
@@ -501,7 +501,19 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
           const int rb = gi * RY;
           double v[RY] = {0.0, 0.0, 0.0, 0.0};
           if (!p.dbg_skip) {
-            if (p.m_in_smem) {
+            if (p.m_in_smem && regpath) {
+              // s <= 16 RPW: at most RPW / 2 column chunks per lane, fully unrolled
+#pragma unroll
+              for (int jc = 0; jc < (RPW + 1) / 2; ++jc) {
+                const int l = lane + 32 * jc;
+                if (l < s) {
+                  const double rl = r_sm[l];
+#pragma unroll
+                  for (int i = 0; i < RY; ++i)
+                    if (rb + i < R) v[i] = fma(Msl[(rb + i) * s + l], rl, v[i]);
+                }
+              }
+            } else if (p.m_in_smem) {
 #pragma unroll 4
               for (int l = lane; l < s; l += 32) {
                 const double rl = r_sm[l];
