@@ -398,7 +398,11 @@ static void launch2(cudaStream_t st, dim3 grid, int M, int N, int K, int Z, int 
     return e ? atoi(e) : 1;
   }();
   if (upper_only && fskip) upper_only = 2;
-  if (upper_only && gram_bm() == 64)
+  static const int tri64 = [] {
+    const char* e = getenv("KPP_GEMM_TRI64");  // 64-row tiles for triangular left operands (A/B switch)
+    return e ? atoi(e) : 1;
+  }();
+  if ((upper_only || (TRI != 0 && tri64)) && gram_bm() == 64)
     launch2m<AT, BT, TRI, 64>(st, M, N, grid.z, Z, K, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
   else
     launch2m<AT, BT, TRI, B2M>(st, M, N, grid.z, Z, K, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
