@@ -378,7 +378,9 @@ __device__ __forceinline__ double s_products(const LsqrParams& p, const double* 
   return beta;
 }
 
-template <bool REG>
+// XS / VS: X and the slab vectors in shared memory (p.x_smem / p.v_smem), as template parameters so
+// that their accesses compile to shared-memory loads rather than generic ones
+template <bool REG, bool XS, bool VS>
 __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
   extern __shared__ double sm[];
   __shared__ DevState st_sh;
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
   double(*part_sh)[TW] = reinterpret_cast<double(*)[TW]>(buf + 2 * NT);
   double* vt = buf + 2 * NT + NW * TW;  // [2 TW]
   double* slv = vt + 2 * TW;        // [3 sl] when v_smem
-  int32_t* S_sh = reinterpret_cast<int32_t*>(slv + (p.v_smem ? 3LL * p.sl : 0));
+  int32_t* S_sh = reinterpret_cast<int32_t*>(slv + (VS ? 3LL * p.sl : 0));
   // on-chip operands (lsqr_plan): the CTA's slab of A_S (s x sl) and X (s x s), reused by all
   // t_max + 1 rounds of the iteration
   double* As = reinterpret_cast<double*>(S_sh) + SP / 2;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
   const long long c0 = (long long)g * p.slab;
   const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
   SlabVec sv;
-  if (p.v_smem) {
+  if constexpr (VS) {
     sv.vn = slv - c0;
     sv.wn = slv + p.sl - c0;
     sv.xn = slv + 2LL * p.sl - c0;
@@ -417,6 +419,14 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
     sv.vn = p.vn;
     sv.wn = p.wn;
     sv.xn = p.xn;
+  }
+  if constexpr (!XS) {
+    // measured (c3, X in global memory): generic accesses to X and the slab vectors run faster
+    // here than shared/global-specific ones (192.6 vs 212.1 us/iteration); the no-op moves hide
+    // the address spaces.  With X in shared memory (c2) the specific loads win (119.1 -> 105.2).
+    asm volatile("mov.b64 %0, %0;" : "+l"(sv.vn));
+    asm volatile("mov.b64 %0, %0;" : "+l"(sv.wn));
+    asm volatile("mov.b64 %0, %0;" : "+l"(sv.xn));
   }
   if (tid == 0) st_sh = *p.st;
   __syncthreads();
@@ -436,12 +446,13 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
     if (st_sh.stopped) break;
     const long long kb = p.bid[t - p.t_base];
     const double* Xg = p.X_pool + kb * (long long)s * s;
-    if (p.x_smem) {  // asynchronous copy, overlapped with round 0
+    if constexpr (XS) {  // asynchronous copy, overlapped with round 0
       const long long nx = (long long)s * s;
       for (long long i = 2LL * tid; i < nx; i += 2LL * NT) cp_async16(Xs + i, Xg + i);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-    const double* X = p.x_smem ? Xs : Xg;
+    const double* X = XS ? Xs : Xg;
+    if constexpr (!XS) asm volatile("mov.b64 %0, %0;" : "+l"(X));
     for (int i = tid; i < s; i += NT) {
       const int32_t row = p.S_pool[kb * s + i];
       S_sh[i] = row;
@@ -461,7 +472,7 @@ __global__ void __launch_bounds__(NT, 1) lsqr_persistent_kernel(LsqrParams p) {
       vin[k] = r;
       e = fma(r, r, e);
     }
-    if (p.x_smem) asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if constexpr (XS) asm volatile("cp.async.wait_all;\n" ::: "memory");
     e = block_sum(e, red_sh, bs);  // (its barrier also publishes vin and the copied X)
     double beta = s_products(p, X, vin, u, yv, vs, buf, red_sh, bs, 0.0, true);
     mark(2);
@@ -598,14 +609,20 @@ size_t lsqr_ll_words(int s, int grid) { return 2 * ((size_t)grid * (s + 1) + s +
 
 // One window [p.t0, p.t1) of K++ with Proj = Alg 6 (one cooperative launch: all CTAs co-resident).
 cudaError_t launch_lsqr_window(cudaStream_t st, const LsqrParams& p) {
-  static int attr_smem[2] = {0, 0};
+  static int attr_smem[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const bool reg = p.s <= NW * RA;
-  const void* fn = reg ? (const void*)lsqr_persistent_kernel<true> : (const void*)lsqr_persistent_kernel<false>;
+  static const void* const fns[8] = {
+      (const void*)lsqr_persistent_kernel<false, false, false>, (const void*)lsqr_persistent_kernel<false, false, true>,
+      (const void*)lsqr_persistent_kernel<false, true, false>,  (const void*)lsqr_persistent_kernel<false, true, true>,
+      (const void*)lsqr_persistent_kernel<true, false, false>,  (const void*)lsqr_persistent_kernel<true, false, true>,
+      (const void*)lsqr_persistent_kernel<true, true, false>,   (const void*)lsqr_persistent_kernel<true, true, true>};
+  const int ki = (reg ? 4 : 0) + (p.x_smem ? 2 : 0) + (p.v_smem ? 1 : 0);
+  const void* fn = fns[ki];
   const size_t smem = lsqr_smem_bytes(p.s, p.a_smem, p.sl, p.x_smem, p.v_smem);
-  if ((int)smem > attr_smem[reg]) {
+  if ((int)smem > attr_smem[ki]) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_smem[reg] = (int)smem;
+    attr_smem[ki] = (int)smem;
   }
   if (p.grid > NT) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(p.ll, 0, lsqr_ll_words(p.s, p.grid) * sizeof(unsigned long long), st);
