@@ -95,6 +95,9 @@ __device__ __forceinline__ void rowsums(const XParams& p, const int32_t* S_sh, d
   }
 }
 
+// MS: M staged in shared memory (p.m_smem) as a template parameter, so that the y products read it
+// with shared-memory loads rather than generic ones
+template <bool MS>
 __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
   extern __shared__ double sm[];
   __shared__ DevState st_sh;
@@ -139,12 +142,12 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
     if (st_sh.stopped) break;
     const long long kb = p.bid[t - p.t_base];
     const double* Mg = p.M_pool + kb * (long long)s * s;
-    if (p.m_smem) {  // asynchronous copy, overlapped with (a) and (b)
+    if constexpr (MS) {  // asynchronous copy, overlapped with (a) and (b)
       const long long nm = (long long)s * s;
       for (long long i = 2LL * tid; i < nm; i += 2LL * NT) cp_async16(Ms + i, Mg + i);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-    const double* M = p.m_smem ? Ms : Mg;
+    const double* M = MS ? Ms : Mg;
     for (int i = tid; i < s; i += NT) {
       const int32_t row = p.S_pool[kb * s + i];
       S_sh[i] = row;
@@ -186,13 +189,13 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
       tot[k] = rk;
       e = fma(rk, rk, e);
     }
-    if (p.m_smem) asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if constexpr (MS) asm volatile("cp.async.wait_all;\n" ::: "memory");
     e = block_sum(e, red_sh, bs);  // (its barrier publishes r and the staged M)
     mark(1);
     if (p.pf_at == 1) issue_prefetch();
     // (d) y = M r.  M staged in shared memory: every CTA computes all of y; else the rows are spread
     // over the grid (row k by CTA k mod grid) and gathered through L2 like (b)
-    if (!p.m_smem) {
+    if (!MS) {
       for (int k = g + warp * G; k < s; k += NW * G) {
         const double* Mrow = M + (long long)k * s;
         double a = 0.0;
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
       }
       for (int k = tid; k < s; k += NT) yv[k] = ll_sum<1>(ll_y + 2LL * k, 0, 0, 1, tag, p.err);
     }
-    for (int r0 = warp * YR; p.m_smem && r0 < s; r0 += NW * YR) {
+    for (int r0 = warp * YR; MS && r0 < s; r0 += NW * YR) {
       double a[YR];
 #pragma unroll
       for (int r = 0; r < YR; ++r) a[r] = 0.0;
@@ -301,19 +304,21 @@ size_t xeng_smem_bytes(int s, int a_smem, int sl, int m_smem) {
 size_t xeng_ll_words(int s, int grid) { return 2 * ((size_t)grid * s + s); }
 
 cudaError_t launch_xeng_window(cudaStream_t st, const XParams& p) {
-  static int attr_smem = 0;
+  static int attr_smem[2] = {0, 0};
+  const int ms = p.m_smem ? 1 : 0;
+  const void* fn = ms ? (const void*)xeng_kernel<true> : (const void*)xeng_kernel<false>;
   const size_t smem = xeng_smem_bytes(p.s, p.a_smem, p.sl, p.m_smem);
-  if ((int)smem > attr_smem) {
-    cudaError_t e = cudaFuncSetAttribute(xeng_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if ((int)smem > attr_smem[ms]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_smem = (int)smem;
+    attr_smem[ms] = (int)smem;
   }
   if (p.nranks > KPP_MAX_PEERS || p.nranks > 32) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(p.ll, 0, xeng_ll_words(p.s, p.grid) * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   XParams q = p;
   void* args[] = {&q};
-  e = cudaLaunchCooperativeKernel((const void*)xeng_kernel, dim3(p.grid), dim3(NT), args, smem, st);
+  e = cudaLaunchCooperativeKernel(fn, dim3(p.grid), dim3(NT), args, smem, st);
   count_launches(1);
   return e;
 }
