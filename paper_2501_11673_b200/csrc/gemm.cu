@@ -272,11 +272,15 @@ __global__ void __launch_bounds__(2 * BM, BM == 128 ? 2 : 3) dgemm2_kernel(int M
       else kidx_b = kidx_sh - kbeg_t;
     }
   }
+  // (separate calls for the staged and the global gather list: each pointer keeps its address space,
+  // so the staged list is read with shared-memory loads)
   auto stage = [&](int slot, int k0) {
     if (!AT) stage_tile_kc<BM, NTT>(As + slot * A_ST, abase, a.ld, arows, k0, kend);
-    else stage_tile<false, BM, AMLD, NTT>(As + slot * A_ST, abase, a.ld, kidx_a ? kidx_a : aidx, tm * BM, M, k0, kend);
+    else if (kidx_a) stage_tile<false, BM, AMLD, NTT>(As + slot * A_ST, abase, a.ld, kidx_sh - kbeg_t, tm * BM, M, k0, kend);
+    else stage_tile<false, BM, AMLD, NTT>(As + slot * A_ST, abase, a.ld, aidx, tm * BM, M, k0, kend);
     if (BT) stage_tile_kc<B2N, NTT>(Bs + slot * B_STAGE, bbase, b.ld, brows, k0, kend);
-    else stage_tile<false, B2N, BN_LD, NTT>(Bs + slot * B_STAGE, bbase, b.ld, kidx_b ? kidx_b : bidx, tn * B2N, N, k0, kend);
+    else if (kidx_b) stage_tile<false, B2N, BN_LD, NTT>(Bs + slot * B_STAGE, bbase, b.ld, kidx_sh - kbeg_t, tn * B2N, N, k0, kend);
+    else stage_tile<false, B2N, BN_LD, NTT>(Bs + slot * B_STAGE, bbase, b.ld, bidx, tn * B2N, N, k0, kend);
   };
 #pragma unroll
   for (int st = 0; st < B2S - 1; ++st) {
