@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "kpp_internal.h"
 
 namespace kpp {
@@ -507,6 +509,20 @@ static void chol_tile(cudaStream_t st, int batch, double* G, long long ldg, long
     chol_trtri_blocked_kernel<16><<<batch, CT, sm, st>>>(G, ldg, gstride, X, ldx, xstride, s, info, info_base);
   }
   count_launches(1);
+}
+
+// Matrices one launch of the diagonal-tile kernel runs in a single wave (SMs x resident CTAs).
+int chol_diag_wave() {
+  static int wave = [] {
+    constexpr size_t kSmem = (2 * 64 * 65 + 64) * sizeof(double);
+    cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chol_diag_kernel, 256, kSmem);
+    return std::max(1, sms * per);
+  }();
+  return wave;
 }
 
 size_t chol_inv_workspace(int s) {

@@ -76,6 +76,7 @@ void launch_add_diag(cudaStream_t st, int batch, double* G, int s, double lam);
 // ws: workspace of chol_inv_workspace(s) bytes per matrix (nullptr: one CTA per matrix).
 void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, int* info, double* ws);
 size_t chol_inv_workspace(int s);
+int chol_diag_wave();  // matrices the diagonal-tile kernel runs in one wave
 // lam[b] = power-iteration estimate (lower bound) of lambda_max of A[b] (mode 0, symmetric) or of
 // A[b] A[b]^T with A[b] upper triangular (mode 1)
 // (other != nullptr: stop as soon as lam * other[b] > stop)
