@@ -98,6 +98,10 @@ typedef enum {
                              into every rank's receive buffer over NVLink (CUDA IPC mappings made at setup)
                              and sums the ranks in rank order; 0: ncclAllReduce between kernels.  Falls back
                              to 0 when the buffers cannot be mapped (stats.xchg tells which runs). */
+  KPP_OPT_RHO0 = 17,      /* initial momentum parameter rho_0 in [0, 1) (default 0, Alg 5 l.4 P:1340,
+                             Alg 3 l.4 P:748); ignored when KPP_OPT_RHO_FIXED >= 0 */
+  KPP_OPT_RHO_MAX = 18,   /* upper clamp of the adaptive rho = clamp(1 - r_hat^{1/zeta}, 0, rho_max),
+                             in [0, 1) (default 0.99; the paper does not bound rho, DESIGN reading Q9) */
   KPP_OPT_REASSOC = 12,   /* CD++ only.  1 (default): blocks that stream from HBM use the kernel that
                              re-associates r_{t+1} = A_{S'} (x_t + eta c m_t) - (1 + eta c) A[S', S] y_t
                              - b_{S'} (exact in real arithmetic, from Alg 3 l.11-13 P:756-759) so the

@@ -231,13 +231,13 @@ void chol_solve(const double* R, int32_t s, const double* r, bool rev, double* y
 // rho = 1 - rhat^{1/zeta}, clamped to [0, 0.99] (Q9).
 // a_{i-1}/a_i = exp(ln(i)^2 - ln(i+1)^2)  (same value; avoids overflow of a_i).
 void rho_update(int64_t i, double rhat_prev, double E0, double E1, int64_t zeta, double* rhat,
-                double* rho) {
+                double* rho, double rho_max = 0.99) {
   double li = std::log((double)i), li1 = std::log((double)(i + 1));
   double omega = std::exp(li * li - li1 * li1);
   double rh = omega * rhat_prev + (1.0 - omega) * (E1 / E0);
   double rr = 1.0 - std::pow(rh, 1.0 / (double)zeta);
   if (rr < 0.0) rr = 0.0;
-  if (rr > 0.99) rr = 0.99;
+  if (rr > rho_max) rr = rho_max;
   *rhat = rh;
   *rho = rr;
 }
@@ -423,7 +423,7 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
         const double* x0, int32_t s, double lam, uint64_t seed, int64_t max_iters, double tol,
         const ora_opts* opt_in, double* x_out, double* hist_res, double* hist_rho,
         int64_t hist_cap, int64_t* n_hist, int64_t* iters_out, int64_t* nfresh_out) {
-  ora_opts opt = {1, 1, -1.0, -1.0, ORA_FACTOR_HOUSEHOLDER, 0, 1, 0, 8, 0};
+  ora_opts opt = {1, 1, -1.0, -1.0, ORA_FACTOR_HOUSEHOLDER, 0, 1, 0, 8, 0, 0.0, 0.99};
   if (opt_in) opt = *opt_in;
   const int64_t pop = cd ? n : m;  // sampling population: rows (K++) or coordinates (CD++)
   if (s < 1 || s > pop || lam < 0.0 || tol < 0.0 || max_iters < 0 || lda < n) return ORA_EINVAL;
@@ -433,7 +433,7 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
   const double C = cd ? ora_cdpp_C(n, s) : ora_kpp_C(m, n, s);
   const int64_t zeta = (pop + s - 1) / s;
   const double eta = opt.accel ? (opt.eta_override >= 0.0 ? opt.eta_override : (double)s / (2.0 * (double)n)) : 0.0;
-  double rho = opt.rho_fixed >= 0.0 ? opt.rho_fixed : 0.0;
+  double rho = opt.rho_fixed >= 0.0 ? opt.rho_fixed : opt.rho0;  // rho_0 (Alg 5 l.4 P:1340: 0)
   double rhat = 1.0, E0 = 0.0, E1 = 0.0;
   int64_t ichk = 0, nh = 0;
   std::vector<double> x((size_t)n), mom((size_t)n, 0.0), w((size_t)n, 0.0);
@@ -536,7 +536,7 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
     if (t % (2 * zeta) == 2 * zeta - 1) {
       ++ichk;
       bool stop = E1 <= tol * tol * bb;
-      if (!stop && opt.rho_fixed < 0.0 && E0 > 0.0) rho_update(ichk, rhat, E0, E1, zeta, &rhat, &rho);
+      if (!stop && opt.rho_fixed < 0.0 && E0 > 0.0) rho_update(ichk, rhat, E0, E1, zeta, &rhat, &rho, opt.rho_max);
       if (nh < hist_cap) {
         if (hist_res) hist_res[nh] = std::sqrt(E1 / bb);
         if (hist_rho) hist_rho[nh] = rho;

@@ -56,6 +56,8 @@ typedef struct {
                           precondition LSQR (Alg 6) */
   int32_t tmax;        /* LSQR iterations t_max (default 8) */
   int32_t tau;         /* sketch size tau (<= 0: 2 s) */
+  double rho0;         /* initial rho (Alg 5 l.4 P:1340: 0) */
+  double rho_max;      /* upper clamp of the adaptive rho (reading Q9: 0.99) */
 } ora_opts;
 
 /* Philox-4x32-10 (Salmon et al., SC'11): out = philox(ctr, key). */

@@ -19,7 +19,7 @@ __all__ = [
     "KppError", "Ctx", "SolveResult", "kpp_setup", "cdpp_setup", "kpp_solve", "cdpp_solve",
     "kpp_destroy", "kpp_get_unique_id", "kpp_setup_dist", "cdpp_setup_dist", "load_library",
     "OPT_ACCEL", "OPT_MEMO", "OPT_ETA", "OPT_RHO_FIXED", "OPT_FACTOR", "OPT_WINDOW",
-    "OPT_PHASE1_MB", "OPT_RESIDENT", "OPT_ENGINE", "OPT_CLUSTER", "OPT_YGL", "OPT_REASSOC", "OPT_PROJ", "OPT_TMAX", "OPT_TAU", "OPT_XCHG",
+    "OPT_PHASE1_MB", "OPT_RESIDENT", "OPT_ENGINE", "OPT_CLUSTER", "OPT_YGL", "OPT_REASSOC", "OPT_PROJ", "OPT_TMAX", "OPT_TAU", "OPT_XCHG", "OPT_RHO0", "OPT_RHO_MAX",
 ]
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENOTPD, EDIVERGED, EMAXITER = range(8)
@@ -29,6 +29,7 @@ OPT_CLUSTER = 10  # 0: automatic; 1/2/4/8/16: forced thread-block cluster size
 OPT_XCHG = 16  # column-sharded exchange: 1 fused NVLink peer exchange (default), 0 NCCL
 OPT_PROJ, OPT_TMAX, OPT_TAU = 13, 14, 15  # K++ projection: 1 = sketch + LSQR (Alg 6), t_max, tau
 OPT_REASSOC = 12  # CD++: 1 re-associated streaming kernel when blocks stream (default), 0 off, 2 always
+OPT_RHO0, OPT_RHO_MAX = 17, 18  # initial rho (default 0); adaptive-rho upper clamp (default 0.99, Q9)
 OPT_YGL = 11  # -1: automatic; 0: y = M r per cluster; 1: once per GPU (L2 gather); 4: per cluster from partials
 
 LIB_PATH = _build.LIB
@@ -261,6 +262,15 @@ def kpp_solve(ctx: Ctx, b: torch.Tensor, x0: torch.Tensor | None = None, max_ite
         x0 = _dev_f64(x0, "x0")
     if x_out is None:
         x_out = torch.empty(ctx.n, dtype=torch.float64, device=b.device)
+    # the C ABI takes bare pointers: sizes are checked here (b has the m rows of the problem --
+    # the caller's m with RHT, the full m on a column-sharded context; x0 / x_out the n local columns)
+    if b.numel() != ctx.m:
+        raise KppError(EINVAL, f"b has {b.numel()} entries, expected m = {ctx.m}")
+    if x0 is not None and x0.numel() != ctx.n:
+        raise KppError(EINVAL, f"x0 has {x0.numel()} entries, expected n = {ctx.n}")
+    if not isinstance(x_out, torch.Tensor) or x_out.dtype != torch.float64 or not x_out.is_contiguous() \
+            or x_out.numel() != ctx.n:
+        raise KppError(EINVAL, f"x_out must be a contiguous float64 tensor of n = {ctx.n} entries")
     L = load_library()
     hist = torch.zeros(max(hist_cap, 1), dtype=torch.float64)
     nh, it = ctypes.c_int64(), ctypes.c_int64()

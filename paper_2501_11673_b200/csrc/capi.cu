@@ -60,6 +60,7 @@ struct kpp_ctx {
   // options
   int accel = 1, memo = 1, factor = 2, resident_opt = 1, engine = -1, cluster_opt = 0, ygl_opt = -1, reassoc = 1;
   double eta_opt = -1.0, rho_fixed = -1.0;
+  double rho0 = 0.0, rho_max = 0.99;  // KPP_OPT_RHO0, KPP_OPT_RHO_MAX (reading Q9)
   long long window = 8192, phase1_mb = 4096;
   cudaStream_t stream = nullptr;
   int device = 0, num_sms = 0;
@@ -122,7 +123,7 @@ struct kpp_ctx {
   cudaGraphExec_t gexec = nullptr;
   int graph_unroll = 0;
   const void* gkey[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-  double gkeyv[4] = {0, 0, 0, 0};
+  double gkeyv[6] = {0, 0, 0, 0, 0, 0};
   // fused cross-GPU exchange (steps.cu peer mode): own LL receive buffer, the peers' buffers mapped
   // through CUDA IPC, and a one-double scratch for the start-of-solve barrier
   unsigned long long* xeng_ll = nullptr;  // engine 2: LL words of the grid exchange
@@ -359,7 +360,8 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   const int32_t* S = ctx->S_pool + k0 * s;
   double* Mout = ctx->M_pool + k0 * ss;
   if ((long long)B > ctx->info_cap) {
-    CKS(dalloc(ctx, &ctx->d_info, (size_t)B));
+    // [0, B): first factor pass, block order; [B, 2B): the CholeskyQR2 second pass, sub-batch order
+    CKS(dalloc(ctx, &ctx->d_info, 2 * (size_t)B));
     ctx->info_cap = B;
   }
   // workspace carve-up
@@ -397,12 +399,13 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   const size_t o_Y = skp ? carve((size_t)ctx->lsqr_n2 * B * s) : 0;    // sketch: n2 x (B s)
   const size_t o_Ah = skp ? carve((size_t)B * ctx->lsqr_tau * s) : 0;
   CKS(ensure_buf(ctx, ctx->p1, off));
-  CK(cudaMemsetAsync(ctx->d_info, 0, (size_t)B * sizeof(int), st));  // the factor kernel only records failures
+  CK(cudaMemsetAsync(ctx->d_info, 0, 2 * (size_t)B * sizeof(int), st));  // the factor kernel only records failures
   char* base = (char*)ctx->p1.p;
   double* part = (double*)(base + o_part);
   double* G = (double*)(base + o_G);
   double* X1 = (double*)(base + o_X1);
   double* W = wsb ? (double*)(base + o_W) : nullptr;
+  const int* refined_list = nullptr;  // device: block index of each refined sub-batch entry
 
   if (ctx->kind == KIND_CDPP) {
     // G = A_SS + lam I (Alg 3 l.8); multi-GPU: disjoint column supports summed exactly
@@ -483,6 +486,7 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
         launch_batch_move(st, nref, X1, X1c, list, ss * (long long)sizeof(double), 0);
         Sr = Sc;
         X1r = X1c;
+        refined_list = list;
         Mr = (double*)(base + o_Mc);
       }
     }
@@ -518,7 +522,7 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
         launch_splitk_reduce(st, Bn, s, s, z2, part, ss, 0.0, L, lscale, ss, G, ss, 1);
         pp.mark("reduce");
         if (dist) CKS(allreduce(ctx, G, (size_t)Bn * ss));
-        launch_chol_trtri(st, Bn, G, X2, s, ctx->d_info + 0, W);  // R2, X2 = R2^{-1}
+        launch_chol_trtri(st, Bn, G, X2, s, ctx->d_info + B + c0, W);  // R2, X2 = R2^{-1}
         pp.mark("chol");
         Operand x1a{X1b, s, ss, nullptr, 0, 0}, x2b{X2, s, ss, nullptr, 0, 0};
         launch_dgemm(st, Bn, s, s, s, x1a, x2b, X, s, ss, 1, 0, 2);  // X = R^{-1} = X1 X2 (upper)
@@ -533,12 +537,20 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   }
   pp.report();
   CK(cudaGetLastError());
-  std::vector<int> info((size_t)B);
-  CK(cudaMemcpyAsync(info.data(), ctx->d_info, (size_t)B * sizeof(int), cudaMemcpyDeviceToHost, st));
+  std::vector<int> info(2 * (size_t)B);
+  CK(cudaMemcpyAsync(info.data(), ctx->d_info, 2 * (size_t)B * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int i = 0; i < B; ++i)
     if (info[(size_t)i])
       return fail(ctx, KPP_ENOTPD, "non-positive pivot %d in block %lld", info[(size_t)i] - 1, k0 + i);
+  for (int i = 0; i < B; ++i)
+    if (info[(size_t)B + i]) {
+      // second CholeskyQR pass: sub-batch index i is block list[i] when a sub-batch was gathered
+      int blk = i;
+      if (refined_list) CK(cudaMemcpy(&blk, refined_list + i, sizeof(int), cudaMemcpyDeviceToHost));
+      return fail(ctx, KPP_ENOTPD, "non-positive pivot %d in block %lld (second CholeskyQR pass)",
+                  info[(size_t)B + i] - 1, k0 + blk);
+    }
   ctx->stats.n_fresh_last += B;
   return KPP_OK;
 }
@@ -951,8 +963,9 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   launch_sumsq(st, b_dev, m, ctx->d_bb);
   // state
   DevState hs{};
-  hs.rho = ctx->rho_fixed >= 0.0 ? ctx->rho_fixed : 0.0;  // rho_0 = 0
+  hs.rho = ctx->rho_fixed >= 0.0 ? ctx->rho_fixed : ctx->rho0;  // rho_0 = 0 unless KPP_OPT_RHO0
   hs.rhat = 1.0;
+  hs.rho_max = ctx->rho_max;
   CK(cudaMemcpyAsync(ctx->dstate, &hs, sizeof hs, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(ctx->d_nb, 0, sizeof(long long), st));
   double bb = 0.0;
@@ -1117,7 +1130,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
         CK(cudaMemsetAsync(ctx->peer_buf, 0, 4ULL * ctx->nranks * ctx->s * sizeof(unsigned long long), st));
         CKN(ncclAllReduce(ctx->peer_bar, ctx->peer_bar, 1, ncclDouble, ncclSum, ctx->comm, st));
       }
-      const double keyv[4] = {sp.tol2bb, sp.eta, (double)sp.adaptive, (double)sp.peer};
+      const double keyv[6] = {sp.tol2bb, sp.eta, (double)sp.adaptive, (double)sp.peer, sp.bb, (double)sp.hist_cap};
       const void* key[5] = {ctx->S_pool, ctx->M_pool, b_dev, ctx->hist_res, ctx->bid};
       if (ctx->gexec && (memcmp(key, ctx->gkey, sizeof key) != 0 || memcmp(keyv, ctx->gkeyv, sizeof keyv) != 0)) {
         cudaGraphExecDestroy(ctx->gexec);
@@ -1349,6 +1362,14 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
     case KPP_OPT_RHO_FIXED:
       if (v > 1.0) return KPP_EINVAL;
       ctx->rho_fixed = v;
+      break;
+    case KPP_OPT_RHO0:
+      if (!(v >= 0.0 && v < 1.0)) return KPP_EINVAL;
+      ctx->rho0 = v;
+      break;
+    case KPP_OPT_RHO_MAX:
+      if (!(v >= 0.0 && v < 1.0)) return KPP_EINVAL;
+      ctx->rho_max = v;
       break;
     case KPP_OPT_FACTOR:
       if (v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;

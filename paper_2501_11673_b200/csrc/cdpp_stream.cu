@@ -496,7 +496,7 @@ cudaError_t launch_cdpp_stream(cudaStream_t stream, const IterParams& p, int gri
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (C > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(itk::T2);
   cfg.dynamicSmemBytes = smem;
@@ -507,8 +507,7 @@ cudaError_t launch_cdpp_stream(cudaStream_t stream, const IterParams& p, int gri
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  count_launches(1);
-  return cudaLaunchKernelEx(&cfg, fn, p);
+  return launch_coresident(cfg, attr, fn, p);
 }
 
 int cdpp_stream_max_clusters(const IterParams& p, int C, size_t smem) {

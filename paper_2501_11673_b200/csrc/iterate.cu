@@ -89,10 +89,9 @@ static cudaLaunchConfig_t make_cfg(int grid, int C, size_t smem, cudaStream_t st
 cudaError_t launch_iterate(cudaStream_t stream, const IterParams& p, int grid, int C, size_t smem) {
   KernelFn fn = pick_kernel(p);
   set_attrs(fn, smem, C);
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   cudaLaunchConfig_t cfg = make_cfg(grid, C, smem, stream, attr);
-  count_launches(1);
-  return cudaLaunchKernelEx(&cfg, fn, p);
+  return launch_coresident(cfg, attr, fn, p);
 }
 
 int iterate_max_clusters(const IterParams& p, int C, size_t smem) {

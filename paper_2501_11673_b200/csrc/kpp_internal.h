@@ -9,6 +9,29 @@ namespace kpp {
 
 // Number of kernels this library has launched (process-wide; read by kpp_get_stats).
 void count_launches(long long k);
+
+// Launch of a persistent kernel whose CTAs wait on one another (LL polling, DSMEM): every CTA must
+// be resident at once.  The launch carries the cooperative attribute next to the cluster size, so
+// the driver rejects a grid that cannot be co-resident (MPS / green-context partitions, SMs held by
+// another kernel) with an error instead of the waits spinning into the watchdog.  If the driver
+// refuses the attribute combination itself, co-residency is re-checked with the occupancy API and
+// the kernel is launched without it.
+template <typename P>
+cudaError_t launch_coresident(cudaLaunchConfig_t cfg, cudaLaunchAttribute* attr, void (*fn)(P), const P& p) {
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  count_launches(1);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, p);
+  if (e == cudaSuccess || e == cudaErrorCooperativeLaunchTooLarge) return e;
+  cudaGetLastError();
+  cfg.numAttrs = 1;
+  int nclu = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)fn, &cfg) != cudaSuccess) return cudaGetLastError();
+  if ((long long)nclu * attr[0].val.clusterDim.x < (long long)cfg.gridDim.x) return cudaErrorCooperativeLaunchTooLarge;
+  return cudaLaunchKernelEx(&cfg, fn, p);
+}
 long long launches_total();
 
 // Replicated solver state of one solve, persisted in device memory between
@@ -24,6 +47,7 @@ struct DevState {
   long long nb;      // fresh blocks created by the schedule in [0, t_sched)
   int stopped;       // 0 running, 1 tolerance met, 2 non-finite residual
   int pad;
+  double rho_max;    // upper clamp of the adaptive rho (reading Q9; KPP_OPT_RHO_MAX, default 0.99)
 };
 
 // ------------------------------------------------------------------ schedule.cu

@@ -10,7 +10,7 @@ namespace kpp {
 // Accumulate e = ||r_t||^2 into the window sums; at a checkpoint (t mod 2 zeta == 2 zeta - 1):
 // stop test E1 <= tol^2 ||b||^2, else the adaptive rho update of Eq (weighted)
 // with omega_i = a_{i-1}/a_i, a_i = (i+1)^{ln(i+1)} (reading Q8), rho = 1 - rhat^{1/zeta}
-// clamped to [0, 0.99] (Q9).  Returns 0 continue, 1 tolerance met, 2 non-finite residual.
+// clamped to [0, rho_max] (Q9; rho_max = 0.99 unless KPP_OPT_RHO_MAX).  Returns 0 continue, 1 tolerance met, 2 non-finite residual.
 // tm = t mod 2 zeta is passed in (the persistent kernel keeps it incrementally: no 64-bit division).
 __device__ __forceinline__ int window_step_dev(DevState& st, long long tm, double e, long long zeta,
                                                double tol2bb, double bb, int adaptive, bool writer,
@@ -26,7 +26,7 @@ __device__ __forceinline__ int window_step_dev(DevState& st, long long tm, doubl
     const double om = exp(li * li - li1 * li1);
     st.rhat = om * st.rhat + (1.0 - om) * (st.E1 / st.E0);
     double rr = 1.0 - pow(st.rhat, 1.0 / (double)zeta);
-    rr = fmin(fmax(rr, 0.0), 0.99);
+    rr = fmin(fmax(rr, 0.0), st.rho_max);
     st.rho = rr;
   }
   if (writer && st.nh < hist_cap) {

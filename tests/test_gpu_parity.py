@@ -661,3 +661,36 @@ def test_zero_rhs(kpp, ora, mode):
     ref = ora.kpp_run(A.numpy(), b.numpy(), 12, lam=1e-8, seed=0, max_iters=1000, proj=1 if mode == "lsqr" else 0)
     assert res.iters == ref.iters == 2 * 8  # zeta = ceil(96 / 12)
     assert float(res.x.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("engine", [0, 1, 2])
+@pytest.mark.parametrize("kind", ["kpp", "cdpp"])
+def test_window_checkpoint_closed_form_gpu(kpp, kind, engine):
+    """Alg 5 l.13-18 / Alg 3 l.14-20 on the GPU against the hand-derived closed form (no oracle):
+    A = I_64, s = n (zeta = 1), lam = 0, x0 = 0, eta = 1/2: hist_res[0] = 0.5 exactly,
+    rho_1 = 1 - (omega_1 + (1 - omega_1)/4) = 0.286122647, then the scalar recursion
+    (tests/closed_forms.py) for the next checkpoints; every engine."""
+    from closed_forms import full_block_window_trace
+    b = torch.from_numpy(np.random.default_rng(21).standard_normal(64))
+    A = torch.eye(64, dtype=torch.float64, device=DEV)
+    ctx = (kpp.kpp_setup if kind == "kpp" else kpp.cdpp_setup)(A, 64, 0.0, 0)
+    ctx.set_option(kpp.OPT_ENGINE, engine)
+    res = ctx.solve(b.to(DEV), max_iters=8)
+    hr, hp = full_block_window_trace(0.5, 4)
+    assert res.iters == 8 and len(res.res_hist) == 4
+    assert abs(float(res.res_hist[0]) - 0.5) < 1e-15
+    rh = ctx.rho_history().numpy()
+    assert abs(rh[0] - 0.286122647) < 1e-9
+    np.testing.assert_allclose(res.res_hist.numpy(), hr, rtol=1e-10, atol=0)
+    np.testing.assert_allclose(rh, hp, rtol=1e-10, atol=1e-15)
+    # KPP_OPT_RHO0 / KPP_OPT_RHO_MAX (closed form with rho_0 = 0.6, the clamp 0.25 active)
+    ctx.set_option(kpp.OPT_RHO0, 0.6)
+    ctx.set_option(kpp.OPT_RHO_MAX, 0.25)
+    res = ctx.solve(b.to(DEV), max_iters=8)
+    hr, hp = full_block_window_trace(0.5, 4, rho0=0.6, rho_max=0.25)
+    np.testing.assert_allclose(res.res_hist.numpy(), hr, rtol=1e-10, atol=0)
+    np.testing.assert_allclose(ctx.rho_history().numpy(), hp, rtol=1e-10, atol=1e-15)
+    with pytest.raises(kpp.KppError):
+        ctx.set_option(kpp.OPT_RHO_MAX, 1.0)
+    with pytest.raises(kpp.KppError):
+        ctx.set_option(kpp.OPT_RHO0, -0.1)

@@ -14,6 +14,7 @@ import pytest
 import torch
 
 import synth
+from closed_forms import full_block_window_trace as _full_block_window_trace
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
@@ -293,6 +294,103 @@ def test_zero_residual_stops_at_first_checkpoint(ora):
     zeta = 96 // 16
     assert res.status == ora.OK and res.iters == 2 * zeta
     assert res.hist_res[0] < 1e-14  # zero up to the rounding of b = A x*
+
+
+def test_window_checkpoint_closed_form(ora):
+    """Alg 5 l.13-18 / Alg 3 l.14-20 wiring pinned by a closed form (not by the oracle):
+    A = I_64, s = n (zeta = 1), lam = 0, x0 = 0, eta = s/(2n) = 1/2.  First checkpoint:
+    hist_res[0] = eta = 0.5 exactly (r_1 = eta b) and rho_1 = 1 - (omega_1 + (1 - omega_1) eta^2)
+    with omega_1 = e^{-(ln 2)^2}, i.e. 0.286122647; second checkpoint hist_res[1] = c_1 / 8 with
+    c_1 = (1 - rho_1)/(1 + rho_1), and rho_2 from r_hat_2 = omega_2 r_hat_1 + (1 - omega_2) c_1^2 / 4.  Swapping E0/E1 or feeding the wrong checkpoint index to
+    omega fails here."""
+    om1 = math.exp(-math.log(2) ** 2)
+    rho1 = 1.0 - (om1 + (1.0 - om1) * 0.25)
+    assert abs(rho1 - 0.286122647) < 1e-9
+    c1 = (1 - rho1) / (1 + rho1)
+    b = _rng(21).standard_normal(64)
+    hr, hp = _full_block_window_trace(0.5, 6)
+    # the hand-derived values of the first two checkpoints, restated
+    assert hr[0] == 0.5 and abs(hp[0] - rho1) < 1e-15
+    assert abs(hr[1] - 0.125 * c1) < 1e-15
+    om2 = math.exp(math.log(2) ** 2 - math.log(3) ** 2)
+    rhat1 = 1.0 - rho1
+    rho2 = min(max(1.0 - (om2 * rhat1 + (1 - om2) * 0.25 * c1 * c1), 0.0), 0.99)
+    assert abs(hp[1] - rho2) < 1e-15
+    for run in (ora.kpp_run, ora.cdpp_run):
+        # 4 checkpoints: the residual falls to ~1e-5 (later ones reach the rounding floor)
+        res = run(np.eye(64), b, 64, lam=0.0, max_iters=8)
+        hr, hp = hr[:4], hp[:4]
+        assert res.iters == 8 and len(res.hist_res) == 4
+        assert abs(res.hist_res[0] - 0.5) < 1e-15
+        assert abs(res.hist_rho[0] - 0.286122647) < 1e-9
+        # rounding: alpha_t - 1 cancels to ~1e-5, so ~1e-11 relative at the 4th checkpoint
+        np.testing.assert_allclose(res.hist_res, hr, rtol=1e-10, atol=0)
+        np.testing.assert_allclose(res.hist_rho, hp, rtol=1e-10, atol=1e-15)
+
+
+@pytest.mark.parametrize("rho0,rho_max", [(0.3, 0.99), (0.0, 0.2), (0.6, 0.25)])
+def test_window_rho0_rho_max_closed_form(ora, rho0, rho_max):
+    """The options rho_0 (Alg 5 l.4 P:1340 fixes 0) and the upper clamp of Q9 (0.99) on the same
+    closed form: with rho_max = 0.2 the first update (0.286) is clamped."""
+    b = _rng(24).standard_normal(64)
+    hr, hp = _full_block_window_trace(0.5, 4, rho0=rho0, rho_max=rho_max)
+    if rho0 > 0:
+        c0 = (1 - rho0) / (1 + rho0)  # first checkpoint with rho_0: r_1 = eta c_0 b
+        assert abs(hr[0] - 0.5 * c0) < 1e-15
+    if rho_max < 0.286:
+        assert hp[0] == rho_max
+    for run in (ora.kpp_run, ora.cdpp_run):
+        res = run(np.eye(64), b, 64, lam=0.0, max_iters=8, rho0=rho0, rho_max=rho_max)
+        np.testing.assert_allclose(res.hist_res, hr, rtol=1e-10, atol=0)
+        np.testing.assert_allclose(res.hist_rho, hp, rtol=1e-10, atol=1e-15)
+
+
+def test_window_checkpoint_closed_form_general(ora):
+    """Same reduction on a general full-row-rank A (32 x 80, s = m = 32, eta = s/(2n) = 0.2):
+    hist_res[0] = eta for any A; the whole checkpoint trajectory follows the scalar recursion.
+    The final iterate is alpha_T x_mn with x_mn the min-norm solution by LAPACK."""
+    rng = _rng(22)
+    A = rng.standard_normal((32, 80))
+    b = rng.standard_normal(32)
+    eta = 32 / (2 * 80)
+    n_chk = 4  # residual ~1e-4 at the 4th checkpoint: E1/E0 still far above rounding
+    hr, hp = _full_block_window_trace(eta, n_chk)
+    res = ora.kpp_run(A, b, 32, lam=0.0, max_iters=2 * n_chk)
+    assert abs(res.hist_res[0] - eta) < 1e-12
+    np.testing.assert_allclose(res.hist_res, hr, rtol=1e-9, atol=1e-14)
+    np.testing.assert_allclose(res.hist_rho, hp, rtol=1e-9, atol=1e-12)
+    # x_T = alpha_T x_mn: recompute alpha_T with the same recursion
+    alpha, mu, rho = 0.0, 0.0, 0.0
+    for t in range(2 * n_chk):
+        if t >= 2 and t % 2 == 0:
+            rho = hp[t // 2 - 1]
+        c = (1 - rho) / (1 + rho)
+        mu = c * (mu - (alpha - 1.0))
+        alpha = 1.0 + eta * mu
+    x_mn = A.T @ np.linalg.solve(A @ A.T, b)
+    assert rel(res.x, alpha * x_mn) < 1e-10
+
+
+def test_window_estimator_partition_identity(ora):
+    """SPEC's partition identity for Eq (residual): when the blocks of a window partition
+    the row set (here s = m, zeta = 1: one block = all rows) the window sum E equals ||A x - b||^2
+    of the iterate the block residual was taken at.  With x0 given and accel off, E0 of the first
+    checkpoint is ||A x0 - b||^2 and hist_res[0]^2 ||b||^2 = E1 = ||A x1 - b||^2 with
+    x1 = x0 - A^T (A A^T)^{-1} (A x0 - b) = the projection of x0, so E1 = 0 up to rounding; with
+    lam > 0 the residual of the regularised step is lam (A A^T + lam I)^{-1} (A x0 - b)."""
+    rng = _rng(23)
+    A = rng.standard_normal((24, 60))
+    b = rng.standard_normal(24)
+    x0 = rng.standard_normal(60)
+    lam = 0.5
+    G = A @ A.T + lam * np.eye(24)
+    r0 = A @ x0 - b
+    x1 = x0 - A.T @ np.linalg.solve(G, r0)
+    res = ora.kpp_run(A, b, 24, lam=lam, max_iters=2, accel=False, x0=x0)
+    bb = float(b @ b)
+    r1 = A @ x1 - b
+    assert abs(res.hist_res[0] ** 2 * bb - float(r1 @ r1)) < 1e-10 * float(r1 @ r1)
+    np.testing.assert_allclose(r1, lam * np.linalg.solve(G, r0), rtol=1e-10, atol=1e-12)
 
 
 # ----------------------------------------------------------------- end-to-end limits
