@@ -48,13 +48,16 @@ def parse():
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-8 measurement")
     ap.add_argument("--ttt-cap", type=int, default=0,
                     help="iteration cap of the time-to-tolerance solve (0: 25M, or 1M with --proj 1)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=24.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", type=int, default=-1)
     ap.add_argument("--rht", action="store_true", help="randomized Hadamard preprocessing (SURVEY 8(f) NEXT-1)")
     ap.add_argument("--proj", type=int, default=0, choices=[0, 1],
                     help="K++ projection: 0 exact (memoized factor), 1 sketch + LSQR (Alg 6, SURVEY 8(f) NEXT-2)")
     ap.add_argument("--tmax", type=int, default=8, help="LSQR steps per iteration with --proj 1 (P:1322)")
+    ap.add_argument("--secondary", default="c5,c4",
+                    help="N=1 only: configs measured after the headline one and reported under 'secondary' "
+                         "(the HBM-bound configs, so their roofline is in the driver's line); '' for none")
     return ap.parse_args()
 
 
@@ -155,29 +158,64 @@ def phase1_flops(cfg, n_blocks, n_refined):
     return n_blocks * (s * (s + 1) * n + small) + n_refined * (s * s * n + s * (s + 1) * n + 5 * small / 3)
 
 
-def cpu_oracle_sample(cfg, A_host, b_host, seconds, proj=0, tmax=8):
-    """Time the oracle, as it stands, on the host cores: iterations 0..T-1 of the same cold
-    solve, T grown until the call takes about `seconds`."""
+def cpu_model():
+    try:
+        for l in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if l.startswith("Model name:"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _oracle_timed(cfg, A_host, b_host, T, threads, proj, tmax):
+    import oracle
+    tm = np.zeros(3)
+    run = oracle.cdpp_run if cfg.kind == "cdpp" else oracle.kpp_run
+    kw = {} if cfg.kind == "cdpp" else {"proj": proj, "tmax": tmax}
+    run(A_host, b_host, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=threads, timing=tm, **kw)
+    return float(tm[0]), float(tm[1]), int(tm[2])
+
+
+def cpu_oracle_sample(cfg, A_host, b_host, seconds, iters, proj=0, tmax=8):
+    """Time the oracle, as it stands, on the host cores (SURVEY 8(d) protocol): iterations 0..T-1
+    of the same cold solve, T grown until a run takes about its share of `seconds`, once with ONE
+    thread (primary) and once with every core (OpenMP over independent outputs, secondary).  The
+    oracle times its first-visit factorisations apart (instrumentation only), which gives
+      - the warm (memoized, Phase-2-only) rate: T / (wall - factor seconds),
+      - seconds per fresh-block factorisation (the paper's s^3/3-per-fresh-block split),
+      - the cold-prefix rate T / wall (mostly fresh blocks: labelled as such),
+    and `value` = the like-for-like rate of ONE bench step: `iters` iterations with the step's own
+    number of fresh blocks (the schedule is data independent and bit-identical on both sides):
+    iters / (iters / warm + n_fresh * factor seconds)."""
     import oracle
     oracle.build()
-    threads = os.cpu_count() or 1
-    T = 8
-    while True:
-        t0 = time.perf_counter()
-        if cfg.kind == "cdpp":
-            oracle.cdpp_run(A_host, b_host, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=threads)
-        else:
-            oracle.kpp_run(A_host, b_host, cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=threads,
-                           proj=proj, tmax=tmax)
-        dt = time.perf_counter() - t0
-        if dt >= seconds / 3 or T >= 1 << 20:
-            break
-        T = int(T * min(8.0, max(2.0, seconds / 3 / max(dt, 1e-3))))
-    return {"value": T / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"{cfg.name}: iterations 0..{T - 1} of a cold solve (first-visit "
-                      f"{'sketch' if proj else 'Householder'} factors included"
-                      f"{f', {tmax} LSQR steps per projection' if proj else ''}), {threads} OpenMP threads over "
-                      f"independent outputs, {dt:.1f} s"}
+    C = oracle.cdpp_C(cfg.n, cfg.s) if cfg.kind == "cdpp" else oracle.kpp_C(cfg.m, cfg.n, cfg.s)
+    n_fresh = int(oracle.schedule(0, C, iters)[2])
+    allc = os.cpu_count() or 1
+    out = {}
+    for label, threads, share in (("1_thread", 1, 0.5), ("all_cores", allc, 0.5)):
+        T = 4
+        while True:
+            wall, fac, nf = _oracle_timed(cfg, A_host, b_host, T, threads, proj, tmax)
+            if wall >= seconds * share / 2 or T >= 1 << 16:
+                break
+            T = int(T * min(8.0, max(2.0, seconds * share / 2 / max(wall, 1e-3))))
+        warm = T / max(wall - fac, 1e-9)
+        per_f = fac / nf if nf else None
+        step = iters / (iters / warm + (n_fresh * per_f if per_f else 0.0))
+        out[label] = {"threads": threads, "iters_timed": T, "wall_s": wall, "fresh_blocks_timed": nf,
+                      "factor_s": fac, "warm_block_iters_per_s": warm, "s_per_fresh_factor": per_f,
+                      "cold_prefix_block_iters_per_s": T / wall, "step_block_iters_per_s": step}
+    main = out["all_cores"]
+    return {"value": main["step_block_iters_per_s"], "unit": UNIT, "cores": allc, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"{cfg.name}: iterations 0..T-1 of the cold solve timed on the host "
+                      f"({main['iters_timed']} on {allc} threads, {out['1_thread']['iters_timed']} on 1), "
+                      f"first-visit {'sketch' if proj else 'Householder'} factors timed apart; value = one bench "
+                      f"step of {iters} iterations with its {n_fresh} fresh blocks at the measured warm rate "
+                      f"and seconds per factor, all cores",
+            "step_fresh_blocks": n_fresh, "single_thread": out["1_thread"], "all_cores": out["all_cores"]}
 
 
 def workload_config(cfg, iters, world, dist, proj=0, tmax=8):
@@ -188,6 +226,62 @@ def workload_config(cfg, iters, world, dist, proj=0, tmax=8):
             "iters_per_step": iters, "step": "cold solve (memo cache cleared)",
             "parallelism": f"column-sharded x{world}" if dist else "1 GPU",
             "l2": f"inputs larger than L2 (A = {cfg.m * cfg.n * 8 / 2**20:.0f} MiB)"}
+
+
+def measure_secondary(name, steps, warmup, dev, hbm_peak):
+    """A short N=1 block for an HBM-bound config (c4/c5): cold bench steps of the config's default
+    iteration count, one warm solve (pure Phase 2) with its roofline against the measured copy
+    bandwidth, and the time to 1e-8.  Device time with CUDA events on the solve's stream."""
+    import paper_2501_11673_b200 as kpp
+    cfg = synth.CONFIGS[name]
+    iters = DEFAULT_ITERS[name]
+    A, b, _ = synth.make_problem(cfg, seed=0, device=dev)
+    ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A, cfg.s, cfg.lam, 0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream)
+    x_out = torch.empty(cfg.n, dtype=torch.float64, device=dev)
+    for _ in range(warmup):
+        ctx.clear_cache()
+        ctx.solve(b, max_iters=iters, x_out=x_out)
+    torch.cuda.synchronize()
+    ctx.reset_stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ctx.clear_cache()
+        ctx.solve(b, max_iters=iters, x_out=x_out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    cold = ctx.stats()
+    ctx.reset_stats()
+    ctx.solve(b, max_iters=iters, x_out=x_out)  # warm: every factor memoized
+    warm = ctx.stats()
+    bpi = bytes_per_iter(cfg)
+    ach = bpi * iters / (warm["phase2_ms"] / 1e3) / 1e9 if warm["phase2_ms"] > 0 else None
+    tr = ncu_traffic(name, "iterate_kernel")
+    ctx.clear_cache()
+    zeta = -(-(cfg.n if cfg.kind == "cdpp" else cfg.m) // cfg.s)
+    e0.record(stream)
+    r = ctx.solve(b, max_iters=200000, tol=1e-8, x_out=x_out, hist_cap=200000 // (2 * zeta) + 2)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    true_res = float(torch.linalg.vector_norm(A @ x_out - b) / torch.linalg.vector_norm(b))
+    out = {"workload": workload_config(cfg, iters, 1, False)["workload"], "iters_per_step": iters,
+           "value": steps * iters / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps,
+           "phase1_ms_per_step": cold["phase1_ms"] / steps, "phase2_ms_per_step": cold["phase2_ms"] / steps,
+           "warm_block_iters_per_s": iters / (warm["phase2_ms"] / 1e3) if warm["phase2_ms"] > 0 else None,
+           "roofline": {"bound": "hbm", "kernel": "Phase-2 persistent kernel, warm (iterate_kernel / cdpp_stream_kernel)",
+                        "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak if ach else None,
+                        "bytes_per_iter": bpi, "traffic": tr * iters if tr else None,
+                        "traffic_note": "ncu dram read+write bytes per iteration (profiles/ncu_summary.json) x iterations per launch"},
+           "time_to_tol": {"seconds": e0.elapsed_time(e1) / 1e3, "iters": r.iters, "converged": r.status == kpp.OK,
+                           "est_rel_res": float(r.res_hist[-1]) if len(r.res_hist) else None,
+                           "true_rel_res": true_res, "tol": 1e-8}}
+    ctx.destroy()
+    del A, b, x_out
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_reference(args, cfg):
@@ -201,7 +295,8 @@ def run_reference(args, cfg):
     cb = None
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        r = cpu_oracle_sample(cfg, A_host, b_host, args.cpu_seconds / max(1, args.steps), args.proj, args.tmax)
+        r = cpu_oracle_sample(cfg, A_host, b_host, args.cpu_seconds / max(1, args.steps),
+                              args.iters or DEFAULT_ITERS[cfg.name], args.proj, args.tmax)
         if i >= args.warmup:
             per_step.append(r["value"])
             step_ms.append((time.perf_counter() - t0) * 1e3)
@@ -341,14 +436,17 @@ def main():
         e0.record(stream)
         # c2 needs 19.3M iterations (DESIGN 12); multi-GPU runs keep a bounded 4M cap
         cap = args.ttt_cap or (1_000_000 if args.proj else 25_000_000 if world == 1 else 4_000_000)
-        r = ctx.solve(b, max_iters=cap, tol=cfg.tol if cfg.tol > 0 else 1e-8, x_out=x_out)
+        zeta = -(-(cfg.n if cfg.kind == "cdpp" else cfg.m) // cfg.s)
+        # history sized for every checkpoint of the capped solve, so res_hist[-1] is the stopping one
+        r = ctx.solve(b, max_iters=cap, tol=cfg.tol if cfg.tol > 0 else 1e-8, x_out=x_out,
+                      hist_cap=cap // (2 * zeta) + 2)
         e1.record(stream)
         torch.cuda.synchronize()
         tms = e0.elapsed_time(e1)
         true_res = None
         if not dist:
             true_res = float(torch.linalg.vector_norm(A_keep @ x_out - b) / torch.linalg.vector_norm(b))
-        ttt = {"seconds": tms / 1e3, "iters": r.iters, "converged": r.status == kpp.OK,
+        ttt = {"seconds": tms / 1e3, "iters": r.iters, "converged": r.status == kpp.OK, "checkpoints": len(r.res_hist),
                "est_rel_res": float(r.res_hist[-1]) if len(r.res_hist) else None,
                "true_rel_res": true_res, "tol": 1e-8}
 
@@ -378,9 +476,20 @@ def main():
             "iter_kernel_share": p2max / ms if ms > 0 else None}
     cpu = None
     if not args.no_cpu and not dist:
-        cpu = cpu_oracle_sample(cfg, A_keep.cpu().numpy(), b.cpu().numpy(), args.cpu_seconds, args.proj, args.tmax)
+        cpu = cpu_oracle_sample(cfg, A_keep.cpu().numpy(), b.cpu().numpy(), args.cpu_seconds, iters, args.proj,
+                                args.tmax)
     elif not args.no_cpu and dist and rank == 0:
         cpu = None  # N>1: the oracle baseline is reported by the N=1 run only
+    secondary = None
+    if world == 1 and args.secondary and not args.proj and not args.rht:
+        ctx.destroy()
+        A = A_keep = None  # free the headline problem before the next one is generated
+        torch.cuda.empty_cache()
+        secondary = {}
+        for nm in [c for c in args.secondary.split(",") if c and c != cfg.name]:
+            with ClockSampler(local) as clk2:
+                secondary[nm] = measure_secondary(nm, max(2, args.steps // 2), 2, dev, hbm_peak)
+            secondary[nm]["clocks"] = clk2.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -409,6 +518,7 @@ def main():
         "phase2_engine": {0: "persistent cluster kernel", 1: "step-kernel graph", 2: "fused-exchange kernel (dist.cu)",
                           3: "sketch + LSQR kernel"}.get(st.get("engine"), st.get("engine")),
         "exchange": ("NVLink peer buffers (fused)" if st.get("xchg") else "NCCL allreduce") if dist else None,
+        "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
     if dist:

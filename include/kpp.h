@@ -102,6 +102,12 @@ typedef enum {
                              Alg 3 l.4 P:748); ignored when KPP_OPT_RHO_FIXED >= 0 */
   KPP_OPT_RHO_MAX = 18,   /* upper clamp of the adaptive rho = clamp(1 - r_hat^{1/zeta}, 0, rho_max),
                              in [0, 1) (default 0.99; the paper does not bound rho, DESIGN reading Q9) */
+  KPP_OPT_VRANKS = 19,    /* one-GPU contexts, engine 2 only: emulate P column-sharded ranks (1..8, default 1)
+                             inside the one launch -- rank v's CTAs own the columns [v n/P, (v+1) n/P),
+                             reduce them over their own grid, publish the rank partial into every rank's
+                             receive buffer and sum the P partials in rank order, exactly the protocol of
+                             the multi-GPU path, with the buffers in this device's memory.
+                             Test vehicle for the P > 1 exchange on a single GPU; not a performance mode */
   KPP_OPT_REASSOC = 12,   /* CD++ only.  1 (default): blocks that stream from HBM use the kernel that
                              re-associates r_{t+1} = A_{S'} (x_t + eta c m_t) - (1 + eta c) A[S', S] y_t
                              - b_{S'} (exact in real arithmetic, from Alg 3 l.11-13 P:756-759) so the

@@ -41,7 +41,8 @@ class _Opts(ctypes.Structure):
                 ("eta_override", ctypes.c_double), ("rho_fixed", ctypes.c_double),
                 ("factor", ctypes.c_int32), ("reverse", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("proj", ctypes.c_int32), ("tmax", ctypes.c_int32),
-                ("tau", ctypes.c_int32), ("rho0", ctypes.c_double), ("rho_max", ctypes.c_double)]
+                ("tau", ctypes.c_int32), ("rho0", ctypes.c_double), ("rho_max", ctypes.c_double),
+                ("timing", ctypes.c_void_p)]
 
 
 _lib = None
@@ -161,7 +162,7 @@ class Result:
 
 
 def _run(cd, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed, factor,
-         reverse, threads, hist_cap, proj=0, tmax=8, tau=0, rho0=0.0, rho_max=0.99):
+         reverse, threads, hist_cap, proj=0, tmax=8, tau=0, rho0=0.0, rho_max=0.99, timing=None):
     A = _f64(A)
     b = _f64(b)
     n = A.shape[1]
@@ -176,7 +177,8 @@ def _run(cd, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed
     nh, it, nf = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     o = _Opts(int(accel), int(memo), -1.0 if eta is None else float(eta),
               -1.0 if rho_fixed is None else float(rho_fixed), int(factor), int(reverse),
-              int(threads), int(proj), int(tmax), int(tau), float(rho0), float(rho_max))
+              int(threads), int(proj), int(tmax), int(tau), float(rho0), float(rho_max),
+              ctypes.c_void_p(timing.ctypes.data) if timing is not None else None)
     if cd:
         rc = lib().ora_cdpp_run(_p(A), n, n, _p(b), x0p, s, lam, seed, max_iters, tol,
                                 ctypes.byref(o), _p(x), _p(hr), _p(hp), hist_cap,
@@ -191,19 +193,19 @@ def _run(cd, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed
 
 def kpp_run(A, b, s, lam=1e-8, seed=0, max_iters=100, tol=0.0, x0=None, accel=True, memo=True,
             eta=None, rho_fixed=None, factor=HOUSEHOLDER, reverse=False, threads=1,
-            hist_cap=1 << 16, proj=0, tmax=8, tau=0, rho0=0.0, rho_max=0.99) -> Result:
+            hist_cap=1 << 16, proj=0, tmax=8, tau=0, rho0=0.0, rho_max=0.99, timing=None) -> Result:
     """Kaczmarz++ (Alg 5; proj=0 exact projections (K++(Cholesky)), proj=1 sketch + LSQR, Alg 6)
     -- see kpp_oracle.h."""
     return _run(False, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed,
-                factor, reverse, threads, hist_cap, proj, tmax, tau, rho0, rho_max)
+                factor, reverse, threads, hist_cap, proj, tmax, tau, rho0, rho_max, timing)
 
 
 def cdpp_run(A, b, s, lam=1e-8, seed=0, max_iters=100, tol=0.0, x0=None, accel=True, memo=True,
              eta=None, rho_fixed=None, reverse=False, threads=1, hist_cap=1 << 16, rho0=0.0,
-             rho_max=0.99) -> Result:
+             rho_max=0.99, timing=None) -> Result:
     """CD++ (Alg 3 without SymFHT) -- see kpp_oracle.h."""
     return _run(True, A, b, s, lam, seed, max_iters, tol, x0, accel, memo, eta, rho_fixed,
-                HOUSEHOLDER, reverse, threads, hist_cap, rho0=rho0, rho_max=rho_max)
+                HOUSEHOLDER, reverse, threads, hist_cap, rho0=rho0, rho_max=rho_max, timing=timing)
 
 
 # ---------------------------------------------------------------- RHT (SURVEY 8(f) NEXT-1)

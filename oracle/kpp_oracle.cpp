@@ -423,7 +423,7 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
         const double* x0, int32_t s, double lam, uint64_t seed, int64_t max_iters, double tol,
         const ora_opts* opt_in, double* x_out, double* hist_res, double* hist_rho,
         int64_t hist_cap, int64_t* n_hist, int64_t* iters_out, int64_t* nfresh_out) {
-  ora_opts opt = {1, 1, -1.0, -1.0, ORA_FACTOR_HOUSEHOLDER, 0, 1, 0, 8, 0, 0.0, 0.99};
+  ora_opts opt = {1, 1, -1.0, -1.0, ORA_FACTOR_HOUSEHOLDER, 0, 1, 0, 8, 0, 0.0, 0.99, nullptr};
   if (opt_in) opt = *opt_in;
   const int64_t pop = cd ? n : m;  // sampling population: rows (K++) or coordinates (CD++)
   if (s < 1 || s > pop || lam < 0.0 || tol < 0.0 || max_iters < 0 || lda < n) return ORA_EINVAL;
@@ -448,6 +448,8 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
   std::vector<double> r((size_t)s), y((size_t)s);
   Block scratch;
   int status = ORA_EMAXITER;
+  const double t_run0 = omp_get_wtime();
+  double t_factor = 0.0;
   int64_t t = 0;
   for (; t < max_iters; ++t) {
     // line 6-8: block selection with memoization
@@ -458,6 +460,7 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
       nbk.S.resize((size_t)s);
       nbk.R.resize((size_t)s * s);
       fresh_block(seed, pop, s, opt.memo ? nfresh : t, nbk.S.data());
+      const double tf0 = omp_get_wtime();
       int rc;
       const bool lsqr = !cd && opt.proj == 1;
       // tau = 2s (Alg 5 l.4), at most the padded dimension n2 (R5)
@@ -470,6 +473,7 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
         rc = gram_factor(A, lda, n, nbk.S.data(), s, lam, par, nbk.R.data());
       else
         rc = householder_factor(A, lda, n, nbk.S.data(), s, lam, par, nbk.R.data());
+      t_factor += omp_get_wtime() - tf0;
       if (rc != ORA_OK) { status = rc; break; }
       ++nfresh;
       if (opt.memo) {
@@ -547,6 +551,11 @@ int run(bool cd, const double* A, int64_t m, int64_t n, int64_t lda, const doubl
     }
   }
   for (int64_t j = 0; j < n; ++j) x_out[j] = x[(size_t)j];
+  if (opt.timing) {
+    opt.timing[0] = omp_get_wtime() - t_run0;
+    opt.timing[1] = t_factor;
+    opt.timing[2] = (double)nfresh;
+  }
   if (n_hist) *n_hist = nh;
   if (iters_out) *iters_out = t;
   if (nfresh_out) *nfresh_out = nfresh;

@@ -58,6 +58,8 @@ typedef struct {
   int32_t tau;         /* sketch size tau (<= 0: 2 s) */
   double rho0;         /* initial rho (Alg 5 l.4 P:1340: 0) */
   double rho_max;      /* upper clamp of the adaptive rho (reading Q9: 0.99) */
+  double* timing;      /* optional out (instrumentation, no arithmetic): [0] wall seconds of the
+                          run, [1] seconds inside first-visit factorisations, [2] their count */
 } ora_opts;
 
 /* Philox-4x32-10 (Salmon et al., SC'11): out = philox(ctr, key). */

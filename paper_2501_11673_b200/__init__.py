@@ -19,7 +19,7 @@ __all__ = [
     "KppError", "Ctx", "SolveResult", "kpp_setup", "cdpp_setup", "kpp_solve", "cdpp_solve",
     "kpp_destroy", "kpp_get_unique_id", "kpp_setup_dist", "cdpp_setup_dist", "load_library",
     "OPT_ACCEL", "OPT_MEMO", "OPT_ETA", "OPT_RHO_FIXED", "OPT_FACTOR", "OPT_WINDOW",
-    "OPT_PHASE1_MB", "OPT_RESIDENT", "OPT_ENGINE", "OPT_CLUSTER", "OPT_YGL", "OPT_REASSOC", "OPT_PROJ", "OPT_TMAX", "OPT_TAU", "OPT_XCHG", "OPT_RHO0", "OPT_RHO_MAX",
+    "OPT_PHASE1_MB", "OPT_RESIDENT", "OPT_ENGINE", "OPT_CLUSTER", "OPT_YGL", "OPT_REASSOC", "OPT_PROJ", "OPT_TMAX", "OPT_TAU", "OPT_XCHG", "OPT_RHO0", "OPT_RHO_MAX", "OPT_VRANKS",
 ]
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENOTPD, EDIVERGED, EMAXITER = range(8)
@@ -29,6 +29,7 @@ OPT_CLUSTER = 10  # 0: automatic; 1/2/4/8/16: forced thread-block cluster size
 OPT_XCHG = 16  # column-sharded exchange: 1 fused NVLink peer exchange (default), 0 NCCL
 OPT_PROJ, OPT_TMAX, OPT_TAU = 13, 14, 15  # K++ projection: 1 = sketch + LSQR (Alg 6), t_max, tau
 OPT_REASSOC = 12  # CD++: 1 re-associated streaming kernel when blocks stream (default), 0 off, 2 always
+OPT_VRANKS = 19  # engine 2 on one GPU: emulate P column-sharded ranks in one launch (protocol test)
 OPT_RHO0, OPT_RHO_MAX = 17, 18  # initial rho (default 0); adaptive-rho upper clamp (default 0.99, Q9)
 OPT_YGL = 11  # -1: automatic; 0: y = M r per cluster; 1: once per GPU (L2 gather); 4: per cluster from partials
 

@@ -128,6 +128,11 @@ struct kpp_ctx {
   // through CUDA IPC, and a one-double scratch for the start-of-solve barrier
   unsigned long long* xeng_ll = nullptr;  // engine 2: LL words of the grid exchange
   long long xeng_ll_cap = 0;
+  // KPP_OPT_VRANKS (one-GPU context): P ranks emulated inside the engine-2 launch, each with its own
+  // column slab, grid exchange and receive buffer (vpeer: P buffers of [2][P][s] LL words)
+  int vranks = 1;
+  unsigned long long* vpeer = nullptr;
+  long long vpeer_cap = 0;
   int xchg = 1;                  // KPP_OPT_XCHG: 1 peer exchange when available, 0 NCCL allreduce
   int peer_ok = 0;
   unsigned long long* peer_buf = nullptr;
@@ -994,8 +999,11 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   const bool use_graph = !use_lsqr && eng == 1;
   ctx->stats.engine = use_lsqr ? 3 : eng;
   if (use_lsqr) CKS(lsqr_prepare(ctx));
+  // emulated ranks (KPP_OPT_VRANKS, one-GPU context): grid vg per rank, all in one launch
+  const int vr = (use_xeng && ctx->nranks == 1) ? ctx->vranks : 1;
+  const int vg = vr > 1 ? ctx->num_sms / vr : ctx->grid;
   if (use_xeng) {
-    const long long words = (long long)xeng_ll_words((int)ctx->s, ctx->grid);
+    const long long words = (long long)vr * (long long)xeng_ll_words((int)ctx->s, vg);
     if (words > ctx->xeng_ll_cap) {
       if (ctx->xeng_ll) cudaFree(ctx->xeng_ll);
       CK(cudaMalloc((void**)&ctx->xeng_ll, (size_t)words * sizeof(unsigned long long)));
@@ -1003,6 +1011,15 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
     }
     // fresh tags for this solve: clear the receive buffer, then (multi-rank) a barrier
     CK(cudaMemsetAsync(ctx->peer_buf, 0, 4ULL * ctx->nranks * ctx->s * sizeof(unsigned long long), st));
+    if (vr > 1) {
+      const long long vw = 4LL * vr * vr * ctx->s;  // P receive buffers of [2][P][s] x 2 words
+      if (vw > ctx->vpeer_cap) {
+        if (ctx->vpeer) cudaFree(ctx->vpeer);
+        CK(cudaMalloc((void**)&ctx->vpeer, (size_t)vw * sizeof(unsigned long long)));
+        ctx->vpeer_cap = vw;
+      }
+      CK(cudaMemsetAsync(ctx->vpeer, 0, (size_t)vw * sizeof(unsigned long long), st));
+    }
     if (ctx->comm) CKN(ncclAllReduce(ctx->peer_bar, ctx->peer_bar, 1, ncclDouble, ncclSum, ctx->comm, st));
   }
   float p1ms = 0.f, p2ms = 0.f;
@@ -1028,10 +1045,22 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       q.adaptive = ctx->rho_fixed < 0.0; q.writer = ctx->rank == 0;
       q.ll = ctx->xeng_ll; q.rank = ctx->rank; q.nranks = ctx->nranks;
       for (int r = 0; r < KPP_MAX_PEERS; ++r) q.peer_recv[r] = ctx->peer_map[r];
+      q.vranks = vr;
+      q.vcol[0] = 0;
+      q.vcol[1] = n;
+      if (vr > 1) {  // rank v owns the contiguous columns [v n / P, (v + 1) n / P)
+        q.nranks = vr;
+        q.grid = vg;
+        long long wmax = 0;
+        for (int v = 0; v <= vr; ++v) q.vcol[v] = (long long)v * n / vr;
+        for (int v = 0; v < vr; ++v) wmax = std::max(wmax, q.vcol[v + 1] - q.vcol[v]);
+        q.slab = (int)((wmax + vg - 1) / vg);
+        for (int r = 0; r < vr; ++r) q.peer_recv[r] = ctx->vpeer + 4LL * vr * ctx->s * r;
+      }
       q.err = ctx->d_err; q.st = ctx->dstate;
       q.hist_res = ctx->hist_res; q.hist_rho = ctx->hist_rho; q.hist_cap = ctx->hist_capd;
       const size_t budget = 227 * 1024 - 4096;
-      q.sl = ctx->slab;
+      q.sl = q.slab;
       const size_t fixed = xeng_smem_bytes(q.s, 0, q.sl, 0);
       const size_t as_b = (size_t)q.s * q.sl * sizeof(double), m_b = (size_t)q.s * q.s * sizeof(double);
       // shared memory: the double-buffered slab of A_S first (the next block streams in behind the
@@ -1331,6 +1360,7 @@ void kpp_destroy(kpp_ctx* ctx) {
     if (ctx->peer_map[r] && r != ctx->rank) cudaIpcCloseMemHandle(ctx->peer_map[r]);
   if (ctx->peer_buf) cudaFree(ctx->peer_buf);
   if (ctx->xeng_ll) cudaFree(ctx->xeng_ll);
+  if (ctx->vpeer) cudaFree(ctx->vpeer);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   void* ptrs[] = {ctx->srht_d, ctx->srht_T, ctx->lsqr_buf, ctx->lsqr_ll, ctx->rht_A, ctx->rht_d, ctx->rht_v, ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
@@ -1423,6 +1453,11 @@ kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double v) {
     case KPP_OPT_ENGINE:
       if (v != -1.0 && v != 0.0 && v != 1.0 && v != 2.0) return KPP_EINVAL;
       ctx->engine = (int)v;
+      break;
+    case KPP_OPT_VRANKS:
+      if (!(v >= 1.0 && v <= (double)KPP_MAX_PEERS) || v != (double)(int)v || ctx->nranks > 1) return KPP_EINVAL;
+      if ((long long)v > ctx->n || (int)v > ctx->num_sms) return KPP_EINVAL;
+      ctx->vranks = (int)v;
       break;
     default: return KPP_EINVAL;
   }

@@ -67,7 +67,7 @@ __device__ __forceinline__ void prefetch_slab(const XParams& p, const int32_t* S
 // MODE 0: A_S from global; 1: from global, filling As; 2: from As (prefetched)
 template <int MODE>
 __device__ __forceinline__ void rowsums(const XParams& p, const int32_t* S_sh, double* As, long long c0, long long c1,
-                                        unsigned long long* ll_part, unsigned tag) {
+                                        unsigned long long* ll_part, unsigned tag, int g) {
   const int s = p.s, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int k0 = warp * RW; k0 < s; k0 += NW * RW) {
     double acc[RW];
@@ -91,7 +91,7 @@ __device__ __forceinline__ void rowsums(const XParams& p, const int32_t* S_sh, d
     }
     const double tot = warp_multi_sum<RW>(acc);
     const int r = warp_multi_index<RW>();
-    if ((lane & (32 / RW - 1)) == 0 && k0 + r < s) ll_put(ll_part + 2LL * ((long long)blockIdx.x * s + k0 + r), tot, tag);
+    if ((lane & (32 / RW - 1)) == 0 && k0 + r < s) ll_put(ll_part + 2LL * ((long long)g * s + k0 + r), tot, tag);
   }
 }
 
@@ -113,10 +113,16 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
   double* As0 = yv + SP + NW * TW + SP;
   double* As1 = As0 + (p.a_smem == 2 ? (long long)s * p.sl : 0);
   double* Ms = As1 + (p.a_smem ? (long long)s * p.sl : 0);
-  unsigned long long* ll_y = p.ll + 2LL * G * s;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = blockIdx.x;
-  const long long c0 = (long long)g * p.slab;
-  const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
+  // virtual rank vr of this CTA (one rank per launch unless emulated, see XParams::vranks)
+  const int vr = (int)blockIdx.x / G;
+  const int rank = p.rank + vr;
+  const bool lead = vr == 0;  // the CTAs of the first rank of the launch write the shared state
+  unsigned long long* llr = p.ll + (long long)vr * 2LL * ((long long)G * s + s);
+  unsigned long long* ll_y = llr + 2LL * G * s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = (int)blockIdx.x - vr * G;
+  const long long cr1 = p.vcol[vr + 1];
+  const long long c0 = min(p.vcol[vr] + (long long)g * p.slab, cr1);
+  const long long c1 = (c0 + p.slab < cr1) ? c0 + p.slab : cr1;
   if (tid == 0) st_sh = *p.st;
   int cur = 0;
   if (p.a_smem == 2 && p.t0 < p.t1) {  // prefetch mode: the first block of the window, synchronously
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
   }
   __syncthreads();
   long long tm = p.t0 % (2 * p.zeta);
-  const bool prof = p.prof != nullptr && g == 0 && tid == 0;
+  const bool prof = p.prof != nullptr && g == 0 && lead && tid == 0;
   long long tp = prof ? clock64() : 0;
   long long pr[6] = {0, 0, 0, 0, 0, 0};
   auto mark = [&](int i) {
@@ -157,9 +163,9 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
     const unsigned tag = (unsigned)(t + 1);
     double* As = cur ? As1 : As0;
     // (a)
-    if (p.a_smem == 2) rowsums<2>(p, S_sh, As, c0, c1, p.ll, tag);
-    else if (p.a_smem == 1) rowsums<1>(p, S_sh, As, c0, c1, p.ll, tag);
-    else rowsums<0>(p, S_sh, As, c0, c1, p.ll, tag);
+    if (p.a_smem == 2) rowsums<2>(p, S_sh, As, c0, c1, llr, tag, g);
+    else if (p.a_smem == 1) rowsums<1>(p, S_sh, As, c0, c1, llr, tag, g);
+    else rowsums<0>(p, S_sh, As, c0, c1, llr, tag, g);
     mark(0);
     auto issue_prefetch = [&]() {  // the next block's slab streams in behind this iteration
       if (p.a_smem == 2 && t + 1 < p.t1) {
@@ -174,16 +180,16 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
     const long long slot = (long long)(t & 1) * R * s;
     for (int k = g + warp * G; k < s; k += NW * G) {
       double a = 0.0;
-      for (int q0 = lane; q0 < G; q0 += 32 * 8) a += ll_sum<8>(p.ll + 2LL * k, 2LL * s, q0, G, tag, p.err);
+      for (int q0 = lane; q0 < G; q0 += 32 * 8) a += ll_sum<8>(llr + 2LL * k, 2LL * s, q0, G, tag, p.err);
       a = wsum(a);
       // system scope: the destination may be a peer GPU's memory (one rank runs the same code)
-      if (lane < R) ll_put_sys(p.peer_recv[lane] + 2 * (slot + (long long)p.rank * s + k), a, tag);
+      if (lane < R) ll_put_sys(p.peer_recv[lane] + 2 * (slot + (long long)rank * s + k), a, tag);
     }
     double e = 0.0;
     for (int k = tid; k < s; k += NT) {
       double v = 0.0;
       for (int r = 0; r < R; ++r) {
-        v += ll_get_sys(p.peer_recv[p.rank] + 2 * (slot + (long long)r * s + k), tag, p.err);
+        v += ll_get_sys(p.peer_recv[rank] + 2 * (slot + (long long)r * s + k), tag, p.err);
       }
       const double rk = v - bS[k];
       tot[k] = rk;
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
     // (f)
     __syncthreads();
     if (tid == 0) {
-      const int res = window_step_dev(st_sh, tm, e, p.zeta, p.tol2bb, p.bb, p.adaptive, p.writer && g == 0,
+      const int res = window_step_dev(st_sh, tm, e, p.zeta, p.tol2bb, p.bb, p.adaptive, p.writer && g == 0 && lead,
                                       p.hist_res, p.hist_rho, p.hist_cap);
       if (res) st_sh.stopped = res;
       st_sh.t_done = t + 1;
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(NT, 1) xeng_kernel(XParams p) {
     __syncthreads();
     mark(4);
   }
-  if (g == 0 && tid == 0) *p.st = st_sh;
+  if (g == 0 && lead && tid == 0) *p.st = st_sh;
   if (prof)
     for (int i = 0; i < 6; ++i) p.prof[i] += pr[i];
 }
@@ -313,12 +319,13 @@ cudaError_t launch_xeng_window(cudaStream_t st, const XParams& p) {
     if (e != cudaSuccess) return e;
     attr_smem[ms] = (int)smem;
   }
-  if (p.nranks > KPP_MAX_PEERS || p.nranks > 32) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(p.ll, 0, xeng_ll_words(p.s, p.grid) * sizeof(unsigned long long), st);
+  if (p.nranks > KPP_MAX_PEERS || p.nranks > 32 || p.vranks < 1 || p.rank + p.vranks > p.nranks)
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(p.ll, 0, (size_t)p.vranks * xeng_ll_words(p.s, p.grid) * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   XParams q = p;
   void* args[] = {&q};
-  e = cudaLaunchCooperativeKernel(fn, dim3(p.grid), dim3(NT), args, smem, st);
+  e = cudaLaunchCooperativeKernel(fn, dim3(p.grid * p.vranks), dim3(NT), args, smem, st);
   count_launches(1);
   return e;
 }

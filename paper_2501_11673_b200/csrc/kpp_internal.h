@@ -236,6 +236,12 @@ struct XParams {
   unsigned long long* ll;  // [grid][s] x 2 words (local grid exchange)
   int rank, nranks;
   unsigned long long* peer_recv[KPP_MAX_PEERS];  // every rank's [2][nranks][s] x 2 words, mapped here
+  // Ranks emulated inside this launch (one GPU standing in for several, B200_PROFILING.md: "emulate
+  // the ranks as one kernel over all ranks' data"): CTAs [v*grid, (v+1)*grid) act as rank rank + v
+  // on the local columns [vcol[v], vcol[v+1]), with their own grid-exchange words (ll + v * words)
+  // and receive buffer peer_recv[rank + v].  1 on a real rank (vcol = {0, n}).
+  int vranks;
+  long long vcol[KPP_MAX_PEERS + 1];
   int a_smem, sl, m_smem;
   int pf_at;  // where the next slab's prefetch is issued: 0 after (a), 1 after (b), 2 after (d)
   int* err;

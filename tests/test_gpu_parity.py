@@ -694,3 +694,47 @@ def test_window_checkpoint_closed_form_gpu(kpp, kind, engine):
         ctx.set_option(kpp.OPT_RHO_MAX, 1.0)
     with pytest.raises(kpp.KppError):
         ctx.set_option(kpp.OPT_RHO0, -0.1)
+
+
+VR_TWINS = [synth.twin("c3", 8192, 512, 256), synth.twin("c4", 512, 8192, 256),
+            synth.twin("c5", 2048, 2048, 512, k=100), synth.twin("c4", 300, 5003, 37, k=8)]
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("cfg", VR_TWINS, ids=[c.name for c in VR_TWINS])
+def test_emulated_ranks_exchange(kpp, ora, cfg, P):
+    """SURVEY 8(e) per-iteration exchange with P > 1 ranks, emulated on one GPU inside one cooperative
+    launch (B200_PROFILING.md: ranks whose kernels wait on one another are emulated as one kernel over
+    all ranks' data): rank v owns columns [v n/P, (v+1) n/P), reduces them over its own grid, publishes
+    its tagged partial into EVERY rank's receive buffer and sums the P partials in rank order.  Against
+    the oracle at the BJ bar after 200 iterations, the checkpoint history, a start vector with the
+    tolerance stop at the oracle's iteration, and bit-identical repeats (the rank-order sum is
+    deterministic)."""
+    A, b, _ = synth.make_problem(cfg)
+    run = ora.cdpp_run if cfg.kind == "cdpp" else ora.kpp_run
+    ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A.to(DEV), cfg.s, cfg.lam, 0)
+    ctx.set_option(kpp.OPT_ENGINE, 2)
+    ctx.set_option(kpp.OPT_VRANKS, P)
+    ctx.set_option(kpp.OPT_WINDOW, 64)
+    T = 200
+    ref = run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    assert ctx.stats()["engine"] == 2
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    x1 = res.x.clone()
+    assert torch.equal(ctx.solve(b.to(DEV), max_iters=T).x, x1)
+    x0 = np.random.default_rng(3).standard_normal(A.shape[1])
+    ref2 = run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=3000, tol=0.05, x0=x0, threads=8)
+    res2 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=3000, tol=0.05)
+    assert res2.iters == ref2.iters
+    assert rel(res2.x.cpu().numpy(), ref2.x) <= 1e-10
+
+
+def test_emulated_ranks_options(kpp):
+    A = torch.zeros(64, 64, dtype=torch.float64, device=DEV)
+    ctx = kpp.kpp_setup(A, 8, 1e-8, 0)
+    for bad in (0, 9, 2.5):
+        with pytest.raises(kpp.KppError):
+            ctx.set_option(kpp.OPT_VRANKS, bad)
+    ctx.set_option(kpp.OPT_VRANKS, 8)
