@@ -1109,6 +1109,8 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       // p.ygl comes from the launch plan
       p.yll = ctx->d_ll + ctx->ll_bytes / sizeof(unsigned long long) - 4LL * ctx->s;
       p.dbg_skip = getenv("KPP_DBG_SKIP") ? 1 : 0;
+      p.g2max = getenv("KPP_G2MAX") ? atoi(getenv("KPP_G2MAX")) : 0;
+      p.poll_ns = getenv("KPP_POLL_NS") ? atoi(getenv("KPP_POLL_NS")) : 0;
       if (getenv("KPP_TRACE")) {
         static long long* dtr = nullptr;
         if (!dtr) CK(cudaMalloc((void**)&dtr, 16LL * ctx->pgrid * 8 * sizeof(long long)));

@@ -379,17 +379,17 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     PHASE_MARK(3);
     TRACE(3);
     // ---- r slice: every (row, cluster-group) polls at once; fixed-order combine over the groups
-    const int G2 = (R > 0 && R <= T2) ? min(16, T2 / R) : 1;
+    const int G2 = (R > 0 && R <= T2) ? min(p.g2max > 0 ? min(p.g2max, 16) : 16, T2 / R) : 1;
     if (R > 0 && R <= T2) {
       if (tid < R * G2) {
         const int row = tid % R, grp = tid / R;
         double v = 0.0;
         if ((NQ - grp + G2 - 1) / G2 <= 4) {
-          v = ll_gather_sum<4>(gll + (long long)(r0 + row) * 2, (long long)s * 2, grp, G2, NQ, tag, p.err);
+          v = ll_gather_sum<4>(gll + (long long)(r0 + row) * 2, (long long)s * 2, grp, G2, NQ, tag, p.err, p.poll_ns);
         } else {
           // many clusters per thread: batches of 8 loads in flight (one L2 round trip per batch)
           for (int q0 = grp; q0 < NQ; q0 += 8 * G2)
-            v += ll_gather_sum<8>(gll + (long long)(r0 + row) * 2, (long long)s * 2, q0, G2, NQ, tag, p.err);
+            v += ll_gather_sum<8>(gll + (long long)(r0 + row) * 2, (long long)s * 2, q0, G2, NQ, tag, p.err, p.poll_ns);
         }
         red_sm[grp * R + row] = v;
       }

@@ -64,7 +64,7 @@ __device__ __forceinline__ double ll_wait_global(const unsigned long long* src, 
 // should not flood L2 with requests)
 template <int KQ, int BACKOFF = 0>
 __device__ __forceinline__ double ll_gather_sum(const unsigned long long* src, long long stride, int q0, int dq, int nq,
-                                                unsigned tag, int* err) {
+                                                unsigned tag, int* err, int backoff_ns = 0) {
   unsigned long long a[KQ], b[KQ];
   int cnt = 0;
 #pragma unroll
@@ -90,6 +90,7 @@ __device__ __forceinline__ double ll_gather_sum(const unsigned long long* src, l
     }
     if (all) break;
     if (BACKOFF) __nanosleep(BACKOFF);
+    if (backoff_ns) __nanosleep(backoff_ns);
     if ((++n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) spin_fail(err);
   }
   double v = 0.0;

@@ -153,6 +153,8 @@ struct alignas(64) IterParams {
   long long* prof;       // optional [16] phase cycle counters (CTA 0), nullptr = off
   long long* trace;      // debug: [16][grid][8] globaltimer event stamps (iterations 64..79)
   int dbg_skip;          // debug: 1 skips the arithmetic of rows 3-5 (exchange-latency floor)
+  int g2max;             // pollers per r row in the cross-cluster gather (<= 16; 0 = 16)
+  int poll_ns;           // back-off between unsuccessful polling rounds of the gather (ns; 0 = none)
 };
 // Persistent Phase-2 kernel: grid = C * clusters CTAs, cluster size C.
 cudaError_t launch_iterate(cudaStream_t st, const IterParams& p, int grid, int C, size_t smem);

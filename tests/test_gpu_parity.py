@@ -738,3 +738,38 @@ def test_emulated_ranks_options(kpp):
         with pytest.raises(kpp.KppError):
             ctx.set_option(kpp.OPT_VRANKS, bad)
     ctx.set_option(kpp.OPT_VRANKS, 8)
+
+
+@pytest.mark.parametrize("rht", [False, True], ids=["plain", "rht"])
+@pytest.mark.parametrize("er", [25, 200])
+def test_bell_psd_parity(kpp, ora, er, rht):
+    """NEXT-3: the paper's CD++ test systems, App F P:1302-1306 -- A = Phi Phi^T + 0.001 I,
+    n = 4096, bell singular-value profile of effective rank er, b ~ N(0, I), s = 200 --
+    GPU against the oracle after 200 iterations at the BJ bar, with and without the randomized Hadamard
+    preprocessing (Alg 3 l.2-3 and the back-rotation of l.16: "Full CD++")."""
+    A, b = synth.make_bell_psd(4096, effective_rank=er, phi=1e-3, seed=0)
+    s, lam, T = 200, 1e-8, 200
+    ctx = kpp.cdpp_setup(A.to(DEV), s, lam, 0)
+    if rht:
+        ctx.enable_rht()
+        ref = ora.cdpp_run_rht(A.numpy(), b.numpy(), s, seed=0, lam=lam, max_iters=T, threads=8)
+    else:
+        ref = ora.cdpp_run(A.numpy(), b.numpy(), s, lam=lam, seed=0, max_iters=T, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("accel", [True, False], ids=["momentum", "no_momentum"])
+def test_bell_general_parity(kpp, ora, accel):
+    """NEXT-3: the paper's K++ system of Fig lsqr_steps (App F): 4096 x 1024 with
+    the bell profile (effective rank 50), b ~ N(0, I) (inconsistent), s = 100; GPU against the oracle
+    after 200 iterations at the BJ bar, momentum on and off (Table 1 ablation toggle)."""
+    A, b = synth.make_bell_general(4096, 1024, effective_rank=50, seed=0)
+    s, lam, T = 100, 1e-8, 200
+    ctx = kpp.kpp_setup(A.to(DEV), s, lam, 0)
+    ctx.set_option(kpp.OPT_ACCEL, 1 if accel else 0)
+    ref = ora.kpp_run(A.numpy(), b.numpy(), s, lam=lam, seed=0, max_iters=T, accel=accel, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
