@@ -1,6 +1,7 @@
 // iterate.cu -- host side of the persistent Phase-2 kernel (iterate_kernel.cuh): shared-memory
 // budget, choice of the compile-time instantiation, launch with thread-block clusters.
 #include <cstdint>
+#include <cstdlib>
 
 #include "kpp_internal.h"
 
@@ -37,6 +38,8 @@ KernelFn iterate_pick_reg_y0(int rpw, int cpl);
 KernelFn iterate_pick_reg_y1(int rpw, int cpl);
 KernelFn iterate_pick_reg_y4(int rpw, int cpl);
 KernelFn iterate_pick_generic(int resident, int yg, int cd);
+KernelFn iterate_pick_lean(const IterParams& p, int C, int rpw, int cpl);
+size_t iterate_lean_smem_bytes(const IterParams& p, int C);
 
 static bool reg_shape(const IterParams& p, int* rpw_out, int* cpl_out) {
   if (!p.resident || p.cd || NW2 * p.slab > 2 * T2) return false;
@@ -86,7 +89,24 @@ static cudaLaunchConfig_t make_cfg(int grid, int C, size_t smem, cudaStream_t st
   return cfg;
 }
 
+// The lean instantiation (iterate_lean.cu) when the plan is one it serves (KPP_NO_LEAN=1: off).
+static KernelFn pick_lean(const IterParams& p, int C) {
+  static const bool off = getenv("KPP_NO_LEAN") != nullptr;
+  int rpw = 0, cpl = 0;
+  if (off || p.prof || !reg_shape(p, &rpw, &cpl)) return nullptr;
+  return iterate_pick_lean(p, C, rpw, cpl);
+}
+
+bool iterate_uses_lean(const IterParams& p, int C) { return pick_lean(p, C) != nullptr; }
+
 cudaError_t launch_iterate(cudaStream_t stream, const IterParams& p, int grid, int C, size_t smem) {
+  if (KernelFn lf = pick_lean(p, C)) {
+    const size_t ls = iterate_lean_smem_bytes(p, C);
+    set_attrs(lf, ls, C);
+    cudaLaunchAttribute attr[2];
+    cudaLaunchConfig_t cfg = make_cfg(grid, C, ls, stream, attr);
+    return launch_coresident(cfg, attr, lf, p);
+  }
   KernelFn fn = pick_kernel(p);
   set_attrs(fn, smem, C);
   cudaLaunchAttribute attr[2];

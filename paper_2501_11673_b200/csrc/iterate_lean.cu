@@ -1,0 +1,354 @@
+// iterate_lean.cu -- the persistent Phase-2 kernel for Kaczmarz++ blocks held in a register tile
+// (the c1/c2 launch plans), written for the shortest loop body.
+//
+// Same method and same exchange as iterate_kernel.cuh (Alg 5 l.9-18 P:1346-1357):
+//   r = A_S x - b_S (row 3), y = M r with the memoized M = (A_S A_S^T + lam I)^{-1} (row 4),
+//   w = A_S^T y (row 5), m <- c (m - w), x <- x - w + eta m (row 6), window sums / checkpoint (row 8),
+// with the s-vector all-reduce as partials --st.async--> slice owner --LL words in L2--> every
+// cluster's slice owner --st.async--> r, then y slices --st.async--> every CTA of the cluster.
+// What differs is the code, not the arithmetic: every plan decision of this instantiation is
+// compile-time (TMA gather4 slabs, M rows double-buffered in shared memory, y per cluster, one slab
+// buffer under a register tile), the rare paths (watchdog time-outs, the checkpoint's log/exp/pow)
+// are out of line, and each prefetch duty has its own warp.  The generic kernel's loop body spans
+// ~165 KB of SASS (instruction fetches on every stage of the critical path); measured on B200, its
+// exchange skeleton alone runs at 2.2 us per iteration against 5.9 us for the whole iteration.
+#include "kernel_common.cuh"
+
+namespace kpp {
+namespace itk {
+namespace {
+
+static __device__ __noinline__ void lean_wait_slow(unsigned long long* bar, unsigned parity, int code) {
+  const unsigned long long t0 = globaltimer();
+  unsigned n = 0;
+  while (!mbar_try_cta(bar, parity))
+    if ((++n & 255u) == 0 && globaltimer() - t0 > 10000000000ull) mbar_hang(code, parity);
+}
+__device__ __forceinline__ void lwait(unsigned long long* bar, unsigned parity, int code) {
+  if (!mbar_try_cta(bar, parity)) lean_wait_slow(bar, parity, code);
+}
+
+struct LeanLayout {
+  int sp, sl, s4, red, mslz;
+  size_t o_rp, o_x, o_m, o_r, o_y, o_red, o_bS, o_S, o_A, o_M, bytes;
+};
+__host__ __device__ inline LeanLayout lean_layout(int s, int slab, int sw, int C) {
+  LeanLayout L{};
+  L.sp = (s + 1) & ~1;
+  L.sl = (s + C - 1) / C;
+  L.s4 = (s + 3) & ~3;
+  L.red = NW2 * slab > 16 * L.sl ? NW2 * slab : 16 * L.sl;
+  L.red = (L.red + 1) & ~1;
+  L.mslz = (L.sl * s + 15) & ~15;
+  size_t o = 64;  // 8 mbarriers
+  L.o_rp = o; o += (size_t)((C * L.sl + 1) & ~1) * 8;
+  L.o_x = o; o += (size_t)slab * 8;
+  L.o_m = o; o += (size_t)slab * 8;
+  L.o_r = o; o += (size_t)L.sp * 8;
+  L.o_y = o; o += (size_t)L.sp * 8;
+  L.o_red = o; o += (size_t)L.red * 8;
+  L.o_bS = o; o += 3 * (size_t)L.sp * 8;
+  L.o_S = o; o += 3 * (size_t)L.sp * 4;
+  o = (o + 127) & ~(size_t)127;  // TMA destinations: 128-byte aligned
+  L.o_A = o; o += (size_t)L.s4 * sw * 8;
+  L.o_M = o; o += 2 * (size_t)L.mslz * 8;
+  L.bytes = o;
+  return L;
+}
+
+// RPW: rows per warp of the register tile (warp wi holds rows wi + 16 i), CPL: columns per lane
+// (lane l holds columns l + 32 c).  PROF: globaltimer stamps (p.trace) compiled in.
+template <int RPW, int CPL, bool PROF>
+__global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_constant__ IterParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int s = p.s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int c = (int)cluster.block_rank();
+  const int q = blockIdx.x / C;
+  const int NQ = gridDim.x / C;
+  const LeanLayout L = lean_layout(s, p.slab, p.sw, C);
+  const int sl = L.sl, sp = L.sp;
+  const int r0 = min(s, c * sl), r1 = min(s, r0 + sl);
+  const int R = r1 - r0;  // rows of the slice this CTA owns (<= 32)
+
+  // shared memory: offsets derived from smem_raw keep the shared address space (LDS / STS)
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // [0] slab + M rows of
+  // block t landed (TMA), [2] partials of my slice, [3] r, [4] y (DSMEM st.async transactions)
+  double* rp_sm = reinterpret_cast<double*>(smem_raw + L.o_rp);  // [C][sl]
+  double* x_sm = reinterpret_cast<double*>(smem_raw + L.o_x);
+  double* m_sm = reinterpret_cast<double*>(smem_raw + L.o_m);
+  double* r_sm = reinterpret_cast<double*>(smem_raw + L.o_r);
+  double* y_sm = reinterpret_cast<double*>(smem_raw + L.o_y);
+  double* red_sm = reinterpret_cast<double*>(smem_raw + L.o_red);  // gather [16][R], then w [16][slab]
+  double* bS_sh = reinterpret_cast<double*>(smem_raw + L.o_bS);    // [3][sp] b_S of t, t+1, t+2
+  int32_t* S_sh = reinterpret_cast<int32_t*>(smem_raw + L.o_S);    // [3][sp]
+  double* Abuf = reinterpret_cast<double*>(smem_raw + L.o_A);      // [s4][sw] slab of the next block
+  double* Mbuf = reinterpret_cast<double*>(smem_raw + L.o_M);      // [2][sl][s] my rows of M
+  __shared__ DevState st;
+  __shared__ int stop_sh;
+
+  const long long c0 = (long long)blockIdx.x * p.slab;
+  const int w = (int)max(0LL, min((long long)p.slab, p.n - c0));
+  const long long ss = (long long)s * s;
+  const CUtensorMap* tm = &p.tmA;
+  const int nops = (s + 3) >> 2;
+  const unsigned slab_bytes = (unsigned)nops * 4u * (unsigned)p.sw * 8u;
+  const unsigned m_bytes = (unsigned)(R * s) * 8u;
+
+  if (tid == 0) {
+    st = *p.st;
+    stop_sh = 0;
+    for (int i = 0; i < 6; ++i) mbar_init(bars + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int j = tid; j < w; j += T2) {
+    x_sm[j] = p.x[c0 + j];
+    m_sm[j] = p.mom[c0 + j];
+  }
+  for (int i = tid; i < s; i += T2) {
+    const int32_t v = p.S_pool[(long long)p.bid[0] * s + i];
+    S_sh[i] = v;
+    bS_sh[i] = p.b[v];
+  }
+  if (p.t0 + 1 < p.t1)
+    for (int i = tid; i < s; i += T2) S_sh[sp + i] = p.S_pool[(long long)p.bid[1] * s + i];
+  long long qb1 = (p.t0 + 1 < p.t1) ? p.bid[1] : 0;
+  long long qb2 = (p.t0 + 2 < p.t1) ? p.bid[2] : 0;
+  long long qb3 = 0;
+  __syncthreads();
+  if (warp == 0)  // block t0: slab (gather4) + my M rows on bars[0]
+    issue_loads(true, tm, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, true,
+                R > 0 ? p.M_pool + (long long)p.bid[0] * ss + (long long)r0 * s : nullptr, R * s, Mbuf, bars + 0);
+  cluster.sync();  // every peer's barriers are initialised before any DSMEM store
+  long long tmod = p.t0 % (2 * p.zeta);
+
+  const unsigned la_rp = smem_u32(rp_sm), la_r = smem_u32(r_sm), la_y = smem_u32(y_sm);
+  const unsigned lb_rp = smem_u32(bars + 2), lb_r = smem_u32(bars + 3), lb_y = smem_u32(bars + 4);
+  // pollers per row of my slice: warps 0..14 only -- the last warp issues block t+1's copies (a
+  // warp issuing 32 serialised TMA gathers must not hold up a polling group) and runs row 8
+  const int G2 = R > 0 ? min(15, (T2 - 32) / R) : 1;
+  const int ngy = min(NW2 - 1, (R + 3) >> 2);   // warps computing y (4 rows each)
+  long long t = p.t0;
+  unsigned it = 0, ph0 = 0;
+  for (; t < p.t1; ++t, ++it) {
+    const int buf = it & 1;
+    const unsigned tag = it + 1;
+    const int32_t* Sc = S_sh + (it % 3) * sp;
+    const double* bSc = bS_sh + (it % 3) * sp;
+    const double* Msl = Mbuf + buf * L.mslz;
+    const bool pf = t + 1 < p.t1;
+    (void)Sc;
+    // ---- top: slab + M rows of block t have landed; register tile of the slab
+    lwait(bars + 0, ph0, 10);
+    ph0 ^= 1u;
+    double ar[RPW][CPL];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int k = warp + 16 * i;
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) ar[i][cc] = (k < s && lane + 32 * cc < w) ? Abuf[k * p.sw + lane + 32 * cc] : 0.0;
+    }
+    cp_async_wait_all();  // this thread's b_S(t) / S(t+1) copies
+    if (tid == 0) {
+      if (pf) mbar_expect_tx(bars + 0, slab_bytes + m_bytes);
+      if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
+      mbar_expect_tx(bars + 3, (unsigned)s * 8u);
+      mbar_expect_tx(bars + 4, (unsigned)s * 8u);
+    }
+    __syncthreads();
+    if constexpr (PROF) TRACE(0);
+    const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
+
+    // ---- row 3: partial block residual over the slab, row k to its slice owner
+    {
+      double xr[CPL];
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) xr[cc] = (lane + 32 * cc < w) ? x_sm[lane + 32 * cc] : 0.0;
+      double v[RPW];
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        v[i] = 0.0;
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) v[i] = fma(ar[i][cc], xr[cc], v[i]);
+      }
+      warp_reduce_scatter<RPW>(v, lane);
+      const int k = warp + 16 * rs_row<RPW>(lane);
+      if ((lane & (32 / RPW - 1)) == 0 && k < s) {
+        const int owner = k / sl;
+        st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), v[0], mapa_u32(lb_rp, owner));
+      }
+    }
+    if constexpr (PROF) TRACE(1);
+
+    unsigned long long* gll = p.ll + (long long)(it & 1) * NQ * s * 2;
+    if (warp == 0) {
+      // ---- owner warp: cluster partial of my slice -> L2 (LL words) for every cluster
+      if (R > 0) lwait(bars + 2, it & 1u, 12);
+      if constexpr (PROF) TRACE(2);
+      if (lane < R) {
+        double v = 0.0;
+        for (int cc = 0; cc < C; ++cc) v += rp_sm[cc * sl + lane];
+        ll_store_global(gll + ((long long)q * s + r0 + lane) * 2, v, tag);
+      }
+    } else if (warp == NW2 - 1) {
+      // ---- the last warp requests block t+1 behind this iteration (M rows first: one bulk copy)
+      if (pf) {
+        const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
+        if (lane == 0 && R > 0) {
+          fence_proxy_async();
+          bulk_g2s(Mbuf + (buf ^ 1) * L.mslz, p.M_pool + qb1 * ss + (long long)r0 * s, m_bytes, bars + 0);
+        }
+        for (int j = lane; j < nops; j += 32) {
+          const int k = 4 * j;
+          fence_proxy_async();
+          tma_gather4(Abuf + (long long)k * p.sw, tm, (int)c0, S1[k], S1[min(k + 1, s - 1)], S1[min(k + 2, s - 1)],
+                      S1[min(k + 3, s - 1)], bars + 0);
+        }
+        double* b1 = bS_sh + ((it + 1) % 3) * sp;
+        for (int i = lane; i < s; i += 32) cp_async8(b1 + i, p.b + S1[i]);
+      }
+      if (t + 2 < p.t1) {
+        int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
+        const int32_t* src = p.S_pool + qb2 * s;
+        for (int i = lane; i < s; i += 32) cp_async4(S2 + i, src + i);
+      }
+      cp_async_commit();
+    }
+    if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
+    if constexpr (PROF) TRACE(3);
+
+    // ---- the slice over all clusters: G2 pollers per row, fixed-order sums
+    if (tid < R * G2) {
+      const int row = tid % R, grp = tid / R;
+      double v = 0.0;
+      if ((NQ - grp + G2 - 1) / G2 <= 4) {
+        v = ll_gather_sum<4>(gll + (long long)(r0 + row) * 2, (long long)s * 2, grp, G2, NQ, tag, p.err);
+      } else {
+        for (int q0 = grp; q0 < NQ; q0 += 8 * G2)
+          v += ll_gather_sum<8>(gll + (long long)(r0 + row) * 2, (long long)s * 2, q0, G2, NQ, tag, p.err);
+      }
+      red_sm[grp * R + row] = v;
+    }
+    __syncthreads();
+    if constexpr (PROF) TRACE(4);
+    // ---- r = A_S x - b_S for my slice, to every CTA of the cluster
+    if (tid < R) {
+      double g[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) g[i] = (i < G2) ? red_sm[i * R + tid] : 0.0;
+#pragma unroll
+      for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+        for (int i = 0; i < h; ++i) g[i] += g[i + h];
+      const double v = g[0] - bSc[r0 + tid];
+      for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + tid) * 8u, cc), v, mapa_u32(lb_r, cc));
+    }
+    lwait(bars + 3, it & 1u, 13);
+    if constexpr (PROF) TRACE(5);
+    // ---- row 8 (last warp, beside y): ||r||^2 in a fixed order and the replicated window logic
+    if (warp == NW2 - 1) {
+      double e = 0.0;
+      for (int i = lane; i < s; i += 32) e = fma(r_sm[i], r_sm[i], e);
+      e = warp_sum(e);
+      if (lane == 0) {
+        const int res = window_step_dev(st, tmod, e, p.zeta, p.tol2bb, p.bb, p.adaptive, blockIdx.x == 0 && p.writer,
+                                        p.hist_res, p.hist_rho, p.hist_cap);
+        if (res) {
+          st.stopped = res;
+          stop_sh = 1;
+        }
+      }
+    }
+    tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
+    // ---- row 4: my slice of y = M r (4 rows per warp from the staged M rows), to every CTA
+    if (warp < ngy) {
+      const int rb = warp * 4;
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int jc = 0; jc < (RPW + 1) / 2; ++jc) {  // s <= 16 RPW: at most RPW / 2 column chunks
+        const int l = lane + 32 * jc;
+        if (l < s) {
+          const double rl = r_sm[l];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (rb + i < R) v[i] = fma(Msl[(rb + i) * s + l], rl, v[i]);
+        }
+      }
+      warp_reduce_scatter<4>(v, lane);
+      const int row = rb + rs_row<4>(lane);
+      const int cc = lane & 7;  // the 8 lanes holding a row send it to peer (lane & 7), C <= 8
+      if (row < R && cc < C) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v[0], mapa_u32(lb_y, cc));
+    }
+    lwait(bars + 4, it & 1u, 14);
+    if constexpr (PROF) TRACE(6);
+
+    // ---- rows 5-6: w = A_S^T y from the register tile, fixed-order sum over warps, momentum, x
+    const double cm = (1.0 - rho) / (1.0 + rho);
+#pragma unroll
+    for (int cc = 0; cc < CPL; ++cc) {
+      double a = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int k = warp + 16 * i;
+        if (k < s) a = fma(ar[i][cc], y_sm[k], a);
+      }
+      if (lane + 32 * cc < w) red_sm[warp * p.slab + lane + 32 * cc] = a;
+    }
+    __syncthreads();
+    for (int jj = tid; jj < w; jj += T2) {
+      double wv = 0.0;
+      for (int ww = 0; ww < NW2; ++ww) wv += red_sm[ww * p.slab + jj];
+      const double mm = cm * (m_sm[jj] - wv);
+      m_sm[jj] = mm;
+      x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
+    }
+    if constexpr (PROF) TRACE(7);
+    qb1 = qb2;
+    qb2 = qb3;
+    if (stop_sh) {  // written before the y barrier of this iteration: every thread sees it
+      ++t;
+      break;
+    }
+  }
+  // an early stop leaves block t's slab / M rows in flight: they must land before exit
+  if (t < p.t1) lwait(bars + 0, ph0, 30);
+  cp_async_wait_all();
+  __syncthreads();
+  for (int j = tid; j < w; j += T2) {
+    p.x[c0 + j] = x_sm[j];
+    p.mom[c0 + j] = m_sm[j];
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    st.t_done = t;
+    *p.st = st;
+  }
+  cluster.sync();  // keep shared memory alive until every peer is done with DSMEM
+}
+
+}  // namespace
+}  // namespace itk
+
+using KernelFn = void (*)(const IterParams);
+
+// The lean kernel serves K++ plans with the slab in a register tile, TMA gather4, M rows
+// double-buffered in shared memory, y per cluster (ygl 0), clusters of at most 8 and slices of at
+// most 32 rows; nullptr otherwise.
+KernelFn iterate_pick_lean(const IterParams& p, int C, int rpw, int cpl) {
+  if (p.cd || !p.resident || !p.a_single || !p.tma || p.ygl != 0 || p.m_in_smem != 1 || C > 8) return nullptr;
+  if ((p.s + C - 1) / C > 32 || (p.s & 1)) return nullptr;
+  const bool prof = p.trace != nullptr;
+#define K(R, CP)                                                                              \
+  if (rpw == R && cpl == CP)                                                                  \
+    return prof ? itk::iterate_lean_kernel<R, CP, true> : itk::iterate_lean_kernel<R, CP, false>;
+  K(2, 1) K(4, 1) K(8, 1) K(16, 1) K(2, 2) K(4, 2) K(8, 2) K(16, 2)
+#undef K
+  return nullptr;
+}
+
+size_t iterate_lean_smem_bytes(const IterParams& p, int C) {
+  return itk::lean_layout(p.s, p.slab, p.sw, C).bytes + 128;
+}
+
+}  // namespace kpp

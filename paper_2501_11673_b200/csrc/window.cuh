@@ -12,13 +12,11 @@ namespace kpp {
 // with omega_i = a_{i-1}/a_i, a_i = (i+1)^{ln(i+1)} (reading Q8), rho = 1 - rhat^{1/zeta}
 // clamped to [0, rho_max] (Q9; rho_max = 0.99 unless KPP_OPT_RHO_MAX).  Returns 0 continue, 1 tolerance met, 2 non-finite residual.
 // tm = t mod 2 zeta is passed in (the persistent kernel keeps it incrementally: no 64-bit division).
-__device__ __forceinline__ int window_step_dev(DevState& st, long long tm, double e, long long zeta,
-                                               double tol2bb, double bb, int adaptive, bool writer,
-                                               double* hist_res, double* hist_rho,
-                                               long long hist_cap) {
-  if (!isfinite(e)) return 2;
-  if (tm < zeta) st.E0 += e; else st.E1 += e;
-  if (tm != 2 * zeta - 1) return 0;
+// The checkpoint itself (every 2 zeta iterations: log/exp/pow) is kept out of line so that the
+// persistent kernels' loop bodies stay small (instruction-cache footprint).
+static __device__ __noinline__ int window_checkpoint_dev(DevState& st, long long zeta, double tol2bb, double bb,
+                                                         int adaptive, bool writer, double* hist_res,
+                                                         double* hist_rho, long long hist_cap) {
   st.ichk += 1;
   const bool stop = st.E1 <= tol2bb;
   if (!stop && adaptive && st.E0 > 0.0) {
@@ -37,6 +35,16 @@ __device__ __forceinline__ int window_step_dev(DevState& st, long long tm, doubl
   st.E0 = 0.0;
   st.E1 = 0.0;
   return stop ? 1 : 0;
+}
+
+__device__ __forceinline__ int window_step_dev(DevState& st, long long tm, double e, long long zeta,
+                                               double tol2bb, double bb, int adaptive, bool writer,
+                                               double* hist_res, double* hist_rho,
+                                               long long hist_cap) {
+  if (!isfinite(e)) return 2;
+  if (tm < zeta) st.E0 += e; else st.E1 += e;
+  if (tm != 2 * zeta - 1) return 0;
+  return window_checkpoint_dev(st, zeta, tol2bb, bb, adaptive, writer, hist_res, hist_rho, hist_cap);
 }
 
 }  // namespace kpp

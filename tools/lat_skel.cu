@@ -28,11 +28,19 @@ __device__ __forceinline__ void st_async(unsigned ra, double v, unsigned rb) {
 __device__ __forceinline__ void expect(unsigned long long* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void wait(unsigned long long* b, unsigned par) {
-  asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"(
-                   smem_u32(b)),
-               "r"(par)
-               : "memory");
+__device__ __forceinline__ bool try_w(unsigned long long* b, unsigned par) {
+  unsigned ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+               : "=r"(ok) : "r"(smem_u32(b)), "r"(par) : "memory");
+  return ok != 0;
+}
+__device__ void wait(unsigned long long* b, unsigned par, int site, int it) {
+  long long t0 = clock64();
+  while (!try_w(b, par))
+    if (clock64() - t0 > 4000000000LL) {
+      printf("hang: site %d iter %d block %d thread %d\n", site, it, blockIdx.x, threadIdx.x);
+      __trap();
+    }
 }
 __device__ __forceinline__ void ll_st(unsigned long long* d, double v, unsigned tag) {
   unsigned long long u = __double_as_longlong(v), t = (unsigned long long)tag << 32;
@@ -43,23 +51,47 @@ __device__ __forceinline__ void ll_ld(const unsigned long long* s, unsigned long
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(s) : "memory");
 }
 
+__device__ __forceinline__ void bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, int mode, int g2max, int backoff,
-                                               long long* out) {
-  __shared__ __align__(8) unsigned long long bars[4];
+                                               long long* out, const double* big) {
+  extern __shared__ __align__(128) double dyn[];  // 96 KB landing zone of the simulated prefetch
+  __shared__ __align__(8) unsigned long long bars[5];
   __shared__ double rp[4 * 32], r_sm[S], y_sm[S], red[16 * 32];
   cg::cluster_group cl = cg::this_cluster();
   const int C = cl.num_blocks(), c = cl.block_rank(), q = blockIdx.x / C, NQ = gridDim.x / C;
   const int sl = S / C, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
+    for (int i = 0; i < 5; ++i) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cl.sync();
   const unsigned la_rp = smem_u32(rp), la_r = smem_u32(r_sm), la_y = smem_u32(y_sm);
   long long t0 = clock64();
   double acc = 0.0;
+  const bool traffic = (mode & 6) != 0;
+  auto prefetch = [&](int it) {  // 128 rows x 512 B (slab) + 32 KB (M rows) from a 512 MB buffer
+    if (tid == 0) {
+      expect(bars + 4, 96 * 1024);
+      for (int k = 0; k < 128; ++k) {
+        const long long row = ((long long)it * 131 + k * 61 + blockIdx.x * 7) % 8192;  // 512 MB = 8192 x 8192 doubles
+        bulk(dyn + k * 64, big + row * 8192 + (blockIdx.x % 128) * 64, 512, bars + 4);
+      }
+      bulk(dyn + 128 * 64, big + (long long)(it % 64) * 4096 * 4 + (blockIdx.x % 4) * 4096, 32768, bars + 4);
+    }
+  };
+  if (traffic) prefetch(0);
   for (int it = 0; it < iters; ++it) {
     const unsigned tag = it + 1, par = it & 1;
+    if (traffic) {
+      wait(bars + 4, par, 4, it);
+      __syncthreads();
+      if ((mode & 4) && it + 1 < iters) prefetch(it + 1);
+    }
     unsigned long long* g = ll + (long long)(it & 1) * NQ * S * 2;
     if (tid == 0) {
       expect(bars + 0, C * sl * 8);
@@ -72,9 +104,10 @@ __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, 
       const int k = warp + 16 * lane, owner = k / sl;
       st_async(mapa(la_rp + (c * sl + k - owner * sl) * 8, owner), 1.0 + acc, mapa(smem_u32(bars + 0), owner));
     }
+    if ((mode & 2) && it + 1 < iters && warp == 15) prefetch(it + 1);
     // stage 2
     if (warp == 0) {
-      wait(bars + 0, par);
+      wait(bars + 0, par, 0, it);
       double v = 0.0;
       for (int cc = 0; cc < C; ++cc) v += rp[cc * sl + lane];
       ll_st(g + ((long long)q * S + c * sl + lane) * 2, v, tag);
@@ -88,9 +121,14 @@ __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, 
         unsigned long long a, b;
         const unsigned long long* src = g + ((long long)qq * S + c * sl + row) * 2;
         ll_ld(src, a, b);
+        long long t0 = clock64();
         while ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
           if (backoff) __nanosleep(backoff);
           ll_ld(src, a, b);
+          if (clock64() - t0 > 4000000000LL) {
+            printf("hang: poll iter %d block %d thread %d q %d\n", it, blockIdx.x, threadIdx.x, qq);
+            __trap();
+          }
         }
         v += __longlong_as_double((a & 0xffffffffull) | (b << 32));
       }
@@ -103,14 +141,14 @@ __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, 
       for (int i = 0; i < G2; ++i) v += red[i * sl + tid];
       for (int cc = 0; cc < C; ++cc) st_async(mapa(la_r + (c * sl + tid) * 8, cc), v, mapa(smem_u32(bars + 1), cc));
     }
-    wait(bars + 1, par);
+    wait(bars + 1, par, 1, it);
     // stage 5
     if (!(mode & 1)) {
       if (tid < sl) {
         const double v = r_sm[c * sl + tid] * 0.5;
         for (int cc = 0; cc < C; ++cc) st_async(mapa(la_y + (c * sl + tid) * 8, cc), v, mapa(smem_u32(bars + 2), cc));
       }
-      wait(bars + 2, par);
+      wait(bars + 2, par, 2, it);
       acc += y_sm[lane] * 1e-300;
     } else {
       acc += r_sm[lane] * 1e-300;
@@ -128,15 +166,19 @@ int main(int argc, char** argv) {
   long long* out;
   cudaMalloc(&ll, 2LL * 160 * S * 2 * 8);
   cudaMalloc(&out, 64);
+  double* big;
+  cudaMalloc(&big, 512LL << 20);
+  cudaMemset(big, 0, 512LL << 20);
+  cudaFuncSetAttribute(skel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   struct V { int C, grid, mode, g2, bo; } vs[] = {
-      {4, 132, 0, 16, 0}, {4, 132, 1, 16, 0}, {4, 132, 0, 4, 0}, {4, 132, 0, 1, 0}, {4, 132, 0, 16, 64},
-      {4, 132, 0, 4, 64}, {8, 128, 0, 16, 0}, {8, 128, 0, 4, 0}, {2, 132, 0, 16, 0}, {4, 64, 0, 16, 0},
-      {4, 32, 0, 16, 0}, {4, 8, 0, 16, 0}};
+      {4, 132, 0, 16, 0}, {4, 132, 1, 16, 0}, {4, 132, 2, 16, 0}, {4, 132, 4, 16, 0}, {4, 132, 0, 4, 0},
+      {4, 132, 0, 16, 64}, {8, 128, 0, 16, 0}, {8, 128, 2, 16, 0}, {4, 64, 0, 16, 0}, {4, 8, 0, 16, 0}};
   for (auto v : vs) {
     cudaMemset(ll, 0, 2LL * 160 * S * 2 * 8);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(v.grid);
     cfg.blockDim = dim3(T);
+    cfg.dynamicSmemBytes = 100 * 1024;
     cudaLaunchAttribute a[1];
     a[0].id = cudaLaunchAttributeClusterDimension;
     a[0].val.clusterDim.x = v.C;
@@ -144,12 +186,15 @@ int main(int argc, char** argv) {
     a[0].val.clusterDim.z = 1;
     cfg.attrs = a;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, skel, ll, 4000, v.mode, v.g2, v.bo, out);
+    cudaLaunchKernelEx(&cfg, skel, ll, 4000, v.mode, v.g2, v.bo, out, (const double*)big);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[2];
     cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
+    fflush(stdout);
     printf("C=%d grid=%d %s G2max=%d backoff=%d: %lld cycles/iter (%.2f us at 1965 MHz) %s\n", v.C, v.grid,
-           v.mode & 1 ? "r only " : "r and y", v.g2, v.bo, h[0], h[0] / 1965.0, cudaGetErrorString(e));
+           v.mode & 1 ? "r only " : v.mode & 2 ? "r+y, 96KB TMA after stage 1" : v.mode & 4 ? "r+y, 96KB TMA at top" : "r and y", v.g2, v.bo, h[0], h[0] / 1965.0, cudaGetErrorString(e));
+    fflush(stdout);
+    if (e != cudaSuccess) return 1;
   }
   return 0;
 }
