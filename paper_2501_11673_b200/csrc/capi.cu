@@ -31,6 +31,7 @@ using namespace kpp;
 
 #include <atomic>
 namespace kpp {
+bool iterate_uses_lean(const IterParams& p, int C);
 static std::atomic<long long> g_launches{0};
 void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 long long launches_total() { return g_launches.load(std::memory_order_relaxed); }
@@ -1108,7 +1109,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       // blocks that stream from HBM (c4/c5 sizes): y once per GPU, gathered through L2
       // p.ygl comes from the launch plan
       p.yll = ctx->d_ll + ctx->ll_bytes / sizeof(unsigned long long) - 4LL * ctx->s;
-      p.dbg_skip = getenv("KPP_DBG_SKIP") ? 1 : 0;
+      p.dbg_skip = getenv("KPP_DBG_SKIP") ? atoi(getenv("KPP_DBG_SKIP")) : 0;
       p.g2max = getenv("KPP_G2MAX") ? atoi(getenv("KPP_G2MAX")) : 0;
       p.poll_ns = getenv("KPP_POLL_NS") ? atoi(getenv("KPP_POLL_NS")) : 0;
       if (getenv("KPP_TRACE")) {
@@ -1233,7 +1234,10 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
                                 "-", "-", "-", "-"};
     const char* names_x[16] = {"a_rowsums", "b_exchange", "d_solve", "e_update", "f_window", "-", "-", "-",
                                "-", "-", "-", "-", "-", "-", "-", "-"};
-    const char* const* names = use_xeng ? names_x : use_lsqr ? names_ls : use_cdpp_stream(ctx) ? names_cs : names_it;
+    const char* names_ln[16] = {"top_wait", "tile+bar", "P1", "owner_wait", "owner_st", "gather_poll", "gather_bar",
+                                "r_comb", "r_wait", "y_comp", "y_wait", "w_fma", "w_bar", "x_upd", "-", "-"};
+    const char* const* names = use_xeng ? names_x : use_lsqr ? names_ls : use_cdpp_stream(ctx) ? names_cs
+                             : iterate_uses_lean(ctx->pplan, ctx->pC) ? names_ln : names_it;
     fprintf(stderr, "[kpp phase cycles/iter, CTA 0]");
     for (int i = 0; i < 16; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)pr[i] / (double)fin.t_done);
     fprintf(stderr, "\n");

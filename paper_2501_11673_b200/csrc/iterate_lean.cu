@@ -12,17 +12,32 @@
 // are out of line, and each prefetch duty has its own warp.  The generic kernel's loop body spans
 // ~165 KB of SASS (instruction fetches on every stage of the critical path); measured on B200, its
 // exchange skeleton alone runs at 2.2 us per iteration against 5.9 us for the whole iteration.
+#include <cstdlib>
+
 #include "kernel_common.cuh"
 
 namespace kpp {
 namespace itk {
 namespace {
 
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes (or 0.2 ms
+// pass) instead of re-issuing the test -- waiting warps share the SMSP issue slots with the warps on
+// the critical path (ncu: the spin loop was ~20 % of all instructions issued per iteration)
+__device__ __forceinline__ bool mbar_try_sleep(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(200000u)
+      : "memory");
+  return ok != 0;
+}
 static __device__ __noinline__ void lean_wait_slow(unsigned long long* bar, unsigned parity, int code) {
   const unsigned long long t0 = globaltimer();
-  unsigned n = 0;
-  while (!mbar_try_cta(bar, parity))
-    if ((++n & 255u) == 0 && globaltimer() - t0 > 10000000000ull) mbar_hang(code, parity);
+  while (!mbar_try_sleep(bar, parity))
+    if (globaltimer() - t0 > 10000000000ull) mbar_hang(code, parity);
 }
 __device__ __forceinline__ void lwait(unsigned long long* bar, unsigned parity, int code) {
   if (!mbar_try_cta(bar, parity)) lean_wait_slow(bar, parity, code);
@@ -37,7 +52,8 @@ __host__ __device__ inline LeanLayout lean_layout(int s, int slab, int sw, int C
   L.sp = (s + 1) & ~1;
   L.sl = (s + C - 1) / C;
   L.s4 = (s + 3) & ~3;
-  L.red = NW2 * slab > 16 * L.sl ? NW2 * slab : 16 * L.sl;
+  // gather partials [row][RS] and w partials [column][RS] (RS = 17: conflict-free, compile-time offsets)
+  L.red = (slab > L.sl ? slab : L.sl) * 17;
   L.red = (L.red + 1) & ~1;
   L.mslz = (L.sl * s + 15) & ~15;
   size_t o = 64;  // 8 mbarriers
@@ -72,6 +88,20 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   const int sl = L.sl, sp = L.sp;
   const int r0 = min(s, c * sl), r1 = min(s, r0 + sl);
   const int R = r1 - r0;  // rows of the slice this CTA owns (<= 32)
+  // PROF: cycle counters of thread 0 of CTA 0 per stage (p.prof[16]), printed by the host
+  const bool lprof = PROF && p.prof != nullptr && blockIdx.x == 0 && tid == 0;
+  long long lacc[14] = {};
+  long long llast = lprof ? clock64() : 0;
+#define LM(i)                                   \
+  do {                                          \
+    if constexpr (PROF) {                       \
+      if (lprof) {                              \
+        const long long now_ = clock64();       \
+        lacc[i] += now_ - llast;                \
+        llast = now_;                           \
+      }                                         \
+    }                                           \
+  } while (0)
 
   // shared memory: offsets derived from smem_raw keep the shared address space (LDS / STS)
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // [0] slab + M rows of
@@ -81,7 +111,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   double* m_sm = reinterpret_cast<double*>(smem_raw + L.o_m);
   double* r_sm = reinterpret_cast<double*>(smem_raw + L.o_r);
   double* y_sm = reinterpret_cast<double*>(smem_raw + L.o_y);
-  double* red_sm = reinterpret_cast<double*>(smem_raw + L.o_red);  // gather [16][R], then w [16][slab]
+  double* red_sm = reinterpret_cast<double*>(smem_raw + L.o_red);  // gather [R][17], then w [slab][17]
+  constexpr int RS = 17;
   double* bS_sh = reinterpret_cast<double*>(smem_raw + L.o_bS);    // [3][sp] b_S of t, t+1, t+2
   int32_t* S_sh = reinterpret_cast<int32_t*>(smem_raw + L.o_S);    // [3][sp]
   double* Abuf = reinterpret_cast<double*>(smem_raw + L.o_A);      // [s4][sw] slab of the next block
@@ -94,8 +125,12 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   const long long ss = (long long)s * s;
   const CUtensorMap* tm = &p.tmA;
   const int nops = (s + 3) >> 2;
-  const unsigned slab_bytes = (unsigned)nops * 4u * (unsigned)p.sw * 8u;
-  const unsigned m_bytes = (unsigned)(R * s) * 8u;
+  // (timing experiments only, results wrong: p.dbg_skip & 2 skips the slab copies of t+1, & 4 the M rows)
+  // & 16: the slab rows of t+1 are prefetched into L2 only (gather4 prefetch), not copied to shared memory
+  const bool no_slab = (p.dbg_skip & 18) != 0, no_m = (p.dbg_skip & 4) != 0, l2_only = (p.dbg_skip & 16) != 0;
+  const unsigned slab_bytes = no_slab ? 0u : (unsigned)nops * 4u * (unsigned)p.sw * 8u;
+  const unsigned m_bytes = no_m ? 0u : (unsigned)(R * s) * 8u;
+  const bool full = (s == 16 * RPW) && (w == 32 * CPL);  // the tile needs no bounds predicates
 
   if (tid == 0) {
     st = *p.st;
@@ -121,6 +156,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   if (warp == 0)  // block t0: slab (gather4) + my M rows on bars[0]
     issue_loads(true, tm, p.A, p.lda, S_sh, s, c0, w, Abuf, p.sw, true,
                 R > 0 ? p.M_pool + (long long)p.bid[0] * ss + (long long)r0 * s : nullptr, R * s, Mbuf, bars + 0);
+
   cluster.sync();  // every peer's barriers are initialised before any DSMEM store
   long long tmod = p.t0 % (2 * p.zeta);
 
@@ -141,24 +177,36 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     const bool pf = t + 1 < p.t1;
     (void)Sc;
     // ---- top: slab + M rows of block t have landed; register tile of the slab
+    LM(13);
     lwait(bars + 0, ph0, 10);
     ph0 ^= 1u;
+    LM(0);
     double ar[RPW][CPL];
+    if (full) {  // (uniform per CTA) no bounds predicates
+      const double* a0 = Abuf + warp * p.sw + lane;
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int k = warp + 16 * i;
+      for (int i = 0; i < RPW; ++i)
 #pragma unroll
-      for (int cc = 0; cc < CPL; ++cc) ar[i][cc] = (k < s && lane + 32 * cc < w) ? Abuf[k * p.sw + lane + 32 * cc] : 0.0;
+        for (int cc = 0; cc < CPL; ++cc) ar[i][cc] = a0[16 * i * p.sw + 32 * cc];
+    } else {
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int k = warp + 16 * i;
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc)
+          ar[i][cc] = (k < s && lane + 32 * cc < w) ? Abuf[k * p.sw + lane + 32 * cc] : 0.0;
+      }
     }
     cp_async_wait_all();  // this thread's b_S(t) / S(t+1) copies
     if (tid == 0) {
-      if (pf) mbar_expect_tx(bars + 0, slab_bytes + m_bytes);
+      if (pf) mbar_expect_tx(bars + 0, slab_bytes + m_bytes);  // (0 bytes: the arrive completes the phase)
       if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
       mbar_expect_tx(bars + 3, (unsigned)s * 8u);
       mbar_expect_tx(bars + 4, (unsigned)s * 8u);
     }
     __syncthreads();
     if constexpr (PROF) TRACE(0);
+    LM(1);
     const double rho = st.rho;  // set at the last checkpoint strictly before t (reading Q11)
 
     // ---- row 3: partial block residual over the slab, row k to its slice owner
@@ -181,12 +229,14 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
       }
     }
     if constexpr (PROF) TRACE(1);
+    LM(2);
 
     unsigned long long* gll = p.ll + (long long)(it & 1) * NQ * s * 2;
     if (warp == 0) {
       // ---- owner warp: cluster partial of my slice -> L2 (LL words) for every cluster
       if (R > 0) lwait(bars + 2, it & 1u, 12);
       if constexpr (PROF) TRACE(2);
+      LM(3);
       if (lane < R) {
         double v = 0.0;
         for (int cc = 0; cc < C; ++cc) v += rp_sm[cc * sl + lane];
@@ -196,28 +246,39 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
       // ---- the last warp requests block t+1 behind this iteration (M rows first: one bulk copy)
       if (pf) {
         const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
-        if (lane == 0 && R > 0) {
+        if (lane == 0 && R > 0 && !no_m) {
           fence_proxy_async();
           bulk_g2s(Mbuf + (buf ^ 1) * L.mslz, p.M_pool + qb1 * ss + (long long)r0 * s, m_bytes, bars + 0);
         }
-        for (int j = lane; j < nops; j += 32) {
+        if (l2_only) {
+#pragma unroll 1
+          for (int j = lane; j < nops; j += 32) {
+            const int k = 4 * j;
+            tma_prefetch_gather4(tm, (int)c0, S1[k], S1[min(k + 1, s - 1)], S1[min(k + 2, s - 1)], S1[min(k + 3, s - 1)]);
+          }
+        }
+#pragma unroll 1
+        for (int j = lane; j < (no_slab ? 0 : nops); j += 32) {  // (no unrolling: a TMA issue is a per-lane waterfall)
           const int k = 4 * j;
           fence_proxy_async();
           tma_gather4(Abuf + (long long)k * p.sw, tm, (int)c0, S1[k], S1[min(k + 1, s - 1)], S1[min(k + 2, s - 1)],
                       S1[min(k + 3, s - 1)], bars + 0);
         }
         double* b1 = bS_sh + ((it + 1) % 3) * sp;
+#pragma unroll 1
         for (int i = lane; i < s; i += 32) cp_async8(b1 + i, p.b + S1[i]);
       }
       if (t + 2 < p.t1) {
         int32_t* S2 = S_sh + ((it + 2) % 3) * sp;
         const int32_t* src = p.S_pool + qb2 * s;
+#pragma unroll 1
         for (int i = lane; i < s; i += 32) cp_async4(S2 + i, src + i);
       }
       cp_async_commit();
     }
     if (t + 3 < p.t1) qb3 = p.bid[t + 3 - p.t0];
     if constexpr (PROF) TRACE(3);
+    LM(4);
 
     // ---- the slice over all clusters: G2 pollers per row, fixed-order sums
     if (tid < R * G2) {
@@ -229,23 +290,32 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
         for (int q0 = grp; q0 < NQ; q0 += 8 * G2)
           v += ll_gather_sum<8>(gll + (long long)(r0 + row) * 2, (long long)s * 2, q0, G2, NQ, tag, p.err);
       }
-      red_sm[grp * R + row] = v;
+      red_sm[row * RS + grp] = v;
     }
-    __syncthreads();
+    LM(5);
+    // warps 0..14 only (named barrier 1): the last warp may still be issuing block t+1's copies
+    // (a serialised TMA issue of ~2000 cycles) and joins at the r barrier below
+    if (warp < NW2 - 1) asm volatile("bar.sync 1, %0;\n" ::"r"(T2 - 32) : "memory");
     if constexpr (PROF) TRACE(4);
-    // ---- r = A_S x - b_S for my slice, to every CTA of the cluster
+    LM(6);
+    // ---- r = A_S x - b_S for my slice (fixed-order tree over the pollers' partial sums)
+    double rv = 0.0;
     if (tid < R) {
       double g[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) g[i] = (i < G2) ? red_sm[i * R + tid] : 0.0;
+      for (int i = 0; i < 16; ++i) g[i] = (i < G2) ? red_sm[tid * RS + i] : 0.0;
 #pragma unroll
       for (int h = 8; h >= 1; h >>= 1)
 #pragma unroll
         for (int i = 0; i < h; ++i) g[i] += g[i + h];
-      const double v = g[0] - bSc[r0 + tid];
-      for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + tid) * 8u, cc), v, mapa_u32(lb_r, cc));
+      rv = g[0] - bSc[r0 + tid];
     }
+    // ---- r slice to every CTA of the cluster
+    if (tid < R)
+      for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + tid) * 8u, cc), rv, mapa_u32(lb_r, cc));
+    LM(7);
     lwait(bars + 3, it & 1u, 13);
+    LM(8);
     if constexpr (PROF) TRACE(5);
     // ---- row 8 (last warp, beside y): ||r||^2 in a fixed order and the replicated window logic
     if (warp == NW2 - 1) {
@@ -255,7 +325,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
       if (lane == 0) {
         const int res = window_step_dev(st, tmod, e, p.zeta, p.tol2bb, p.bb, p.adaptive, blockIdx.x == 0 && p.writer,
                                         p.hist_res, p.hist_rho, p.hist_cap);
-        if (res) {
+        if (res && !(res == 2 && (p.dbg_skip & 22))) {  // (timing experiments run on stale data)
           st.stopped = res;
           stop_sh = 1;
         }
@@ -281,25 +351,35 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
       const int cc = lane & 7;  // the 8 lanes holding a row send it to peer (lane & 7), C <= 8
       if (row < R && cc < C) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v[0], mapa_u32(lb_y, cc));
     }
+    LM(9);
     lwait(bars + 4, it & 1u, 14);
+    LM(10);
     if constexpr (PROF) TRACE(6);
 
     // ---- rows 5-6: w = A_S^T y from the register tile, fixed-order sum over warps, momentum, x
     const double cm = (1.0 - rho) / (1.0 + rho);
-#pragma unroll
-    for (int cc = 0; cc < CPL; ++cc) {
-      double a = 0.0;
+    {
+      double yk[RPW];  // y rows of this warp's tile rows (tile rows past s are zero: any value works)
 #pragma unroll
       for (int i = 0; i < RPW; ++i) {
-        const int k = warp + 16 * i;
-        if (k < s) a = fma(ar[i][cc], y_sm[k], a);
+        yk[i] = y_sm[min(warp + 16 * i, s - 1)];
       }
-      if (lane + 32 * cc < w) red_sm[warp * p.slab + lane + 32 * cc] = a;
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        double a = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) a = fma(ar[i][cc], yk[i], a);
+        if (lane + 32 * cc < w) red_sm[(lane + 32 * cc) * RS + warp] = a;
+      }
     }
+
+    LM(11);
     __syncthreads();
+    LM(12);
     for (int jj = tid; jj < w; jj += T2) {
       double wv = 0.0;
-      for (int ww = 0; ww < NW2; ++ww) wv += red_sm[ww * p.slab + jj];
+#pragma unroll
+      for (int ww = 0; ww < NW2; ++ww) wv += red_sm[jj * RS + ww];
       const double mm = cm * (m_sm[jj] - wv);
       m_sm[jj] = mm;
       x_sm[jj] = x_sm[jj] - wv + p.eta * mm;
@@ -324,6 +404,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     st.t_done = t;
     *p.st = st;
   }
+  if constexpr (PROF)
+    if (lprof)
+      for (int i = 0; i < 14; ++i) p.prof[i] += lacc[i];
+#undef LM
   cluster.sync();  // keep shared memory alive until every peer is done with DSMEM
 }
 
@@ -338,10 +422,9 @@ using KernelFn = void (*)(const IterParams);
 KernelFn iterate_pick_lean(const IterParams& p, int C, int rpw, int cpl) {
   if (p.cd || !p.resident || !p.a_single || !p.tma || p.ygl != 0 || p.m_in_smem != 1 || C > 8) return nullptr;
   if ((p.s + C - 1) / C > 32 || (p.s & 1)) return nullptr;
-  const bool prof = p.trace != nullptr;
-#define K(R, CP)                                                                              \
-  if (rpw == R && cpl == CP)                                                                  \
-    return prof ? itk::iterate_lean_kernel<R, CP, true> : itk::iterate_lean_kernel<R, CP, false>;
+  const bool prof = p.trace != nullptr || p.prof != nullptr;
+#define K(R, CP) \
+  if (rpw == R && cpl == CP) return prof ? itk::iterate_lean_kernel<R, CP, true> : itk::iterate_lean_kernel<R, CP, false>;
   K(2, 1) K(4, 1) K(8, 1) K(16, 1) K(2, 2) K(4, 2) K(8, 2) K(16, 2)
 #undef K
   return nullptr;

@@ -148,6 +148,14 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
       "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA gather4 prefetch into L2 only (no shared-memory destination, no mbarrier)
+__device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap* tm, int c0, int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(
+          reinterpret_cast<unsigned long long>(tm)),
+      "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 // DSMEM: remote shared::cluster address of a local shared variable in CTA `rank`
 __device__ __forceinline__ unsigned mapa_u32(unsigned la, int rank) {
   unsigned ra;

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace kpp {
 
@@ -16,8 +17,16 @@ void count_launches(long long k);
 // another kernel) with an error instead of the waits spinning into the watchdog.  If the driver
 // refuses the attribute combination itself, co-residency is re-checked with the occupancy API and
 // the kernel is launched without it.
+// (KPP_NO_COOP=1: plain cluster launch, for tools that cannot replay cooperative launches.)
 template <typename P>
 cudaError_t launch_coresident(cudaLaunchConfig_t cfg, cudaLaunchAttribute* attr, void (*fn)(P), const P& p) {
+  static const bool no_coop = getenv("KPP_NO_COOP") != nullptr;
+  if (no_coop) {
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    count_launches(1);
+    return cudaLaunchKernelEx(&cfg, fn, p);
+  }
   attr[1].id = cudaLaunchAttributeCooperative;
   attr[1].val.cooperative = 1;
   cfg.attrs = attr;

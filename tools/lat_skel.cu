@@ -6,10 +6,15 @@
 //   stage 4  r slice -> every CTA of the cluster (st.async), wait
 //   stage 5  y slice -> every CTA of the cluster (st.async), wait      (mode & 1: skipped)
 //   stage 6  __syncthreads (the w / x update barrier)
-// Prints cycles per iteration for each variant.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
+// Simulated prefetch of the next block (mode bits): 2 issued after stage 1 by the last warp, 4 at the
+// top; 64 KB of slab rows as 128 bulk copies of 512 B (default), 32 TMA gather4 ops (+64) or 16-byte
+// cp.async from every thread (+128); +8 no 32 KB M-row copy, +16 no slab rows, +32 slab rows from an
+// L2-resident region.  Prints cycles per iteration for each variant.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 namespace cg = cooperative_groups;
 
@@ -57,8 +62,19 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, unsigned bytes,
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void gather4(void* dst, const CUtensorMap* tm, int c0, int r0, int r1, int r2, int r3,
+                                        unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, int mode, int g2max, int backoff,
-                                               long long* out, const double* big) {
+                                               long long* out, const double* big, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) double dyn[];  // 96 KB landing zone of the simulated prefetch
   __shared__ __align__(8) unsigned long long bars[5];
   __shared__ double rp[4 * 32], r_sm[S], y_sm[S], red[16 * 32];
@@ -71,26 +87,44 @@ __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, 
   }
   cl.sync();
   const unsigned la_rp = smem_u32(rp), la_r = smem_u32(r_sm), la_y = smem_u32(y_sm);
-  long long t0 = clock64();
+  long long t0 = clock64(), twait = 0;
   double acc = 0.0;
   const bool traffic = (mode & 6) != 0;
+  auto rowof = [&](int it, int k) { return (int)(((long long)it * 131 + k * 61 + blockIdx.x * 7) % ((mode & 32) ? 256 : 8192)); };
+  // mode 128: the slab rows by 16-byte cp.async from every thread (LSU path, not the TMA engine)
+  auto cpa_slab = [&](int it) {
+    for (int e = tid; e < 128 * 32; e += T) {
+      const int k = e >> 5, j = e & 31;
+      cpa16(dyn + k * 64 + 2 * j, big + (long long)rowof(it, k) * 8192 + (blockIdx.x % 128) * 64 + 2 * j);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   auto prefetch = [&](int it) {  // 128 rows x 512 B (slab) + 32 KB (M rows) from a 512 MB buffer
-    if (tid == 0) {
-      expect(bars + 4, 96 * 1024);
-      for (int k = 0; k < 128; ++k) {
-        const long long row = ((long long)it * 131 + k * 61 + blockIdx.x * 7) % 8192;  // 512 MB = 8192 x 8192 doubles
-        bulk(dyn + k * 64, big + row * 8192 + (blockIdx.x % 128) * 64, 512, bars + 4);
-      }
-      bulk(dyn + 128 * 64, big + (long long)(it % 64) * 4096 * 4 + (blockIdx.x % 4) * 4096, 32768, bars + 4);
+    if (lane == 0) {
+      expect(bars + 4, ((mode & (16 | 128)) ? 0 : 64 * 1024) + ((mode & 8) ? 0 : 32 * 1024));
+      if (!(mode & (16 | 128)) && (mode & 64)) {  // TMA gather4: 32 ops of 4 rows x 512 B
+        for (int k = 0; k < 128; k += 4)
+          gather4(dyn + k * 64, &tmap, (blockIdx.x % 128) * 64, rowof(it, k), rowof(it, k + 1), rowof(it, k + 2),
+                  rowof(it, k + 3), bars + 4);
+      } else if (!(mode & (16 | 128)))
+        for (int k = 0; k < 128; ++k) {
+          // 512 MB = 8192 x 8192 doubles; mode 32: rows from the first 256 (16 MB, L2-resident)
+          bulk(dyn + k * 64, big + (long long)rowof(it, k) * 8192 + (blockIdx.x % 128) * 64, 512, bars + 4);
+        }
+      if (!(mode & 8)) bulk(dyn + 128 * 64, big + (long long)(it % 64) * 4096 * 4 + (blockIdx.x % 4) * 4096, 32768, bars + 4);
     }
   };
-  if (traffic) prefetch(0);
+  if (traffic && warp == 15) prefetch(0);
+  if (mode & 128) cpa_slab(0);
   for (int it = 0; it < iters; ++it) {
     const unsigned tag = it + 1, par = it & 1;
     if (traffic) {
+      const long long tw = clock64();
       wait(bars + 4, par, 4, it);
+      if (mode & 128) asm volatile("cp.async.wait_all;" ::: "memory");
+      twait += clock64() - tw;
       __syncthreads();
-      if ((mode & 4) && it + 1 < iters) prefetch(it + 1);
+      if ((mode & 4) && it + 1 < iters && warp == 15) prefetch(it + 1);
     }
     unsigned long long* g = ll + (long long)(it & 1) * NQ * S * 2;
     if (tid == 0) {
@@ -105,6 +139,7 @@ __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, 
       st_async(mapa(la_rp + (c * sl + k - owner * sl) * 8, owner), 1.0 + acc, mapa(smem_u32(bars + 0), owner));
     }
     if ((mode & 2) && it + 1 < iters && warp == 15) prefetch(it + 1);
+    if ((mode & 128) && it + 1 < iters) cpa_slab(it + 1);
     // stage 2
     if (warp == 0) {
       wait(bars + 0, par, 0, it);
@@ -156,7 +191,10 @@ __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, 
     // stage 6
     __syncthreads();
   }
-  if (blockIdx.x == 0 && tid == 0) out[0] = (clock64() - t0) / iters;
+  if (blockIdx.x == 0 && tid == 0) {
+    out[0] = (clock64() - t0) / iters;
+    out[2] = twait / iters;
+  }
   if (acc == 12345.0) out[1] = 1;
   cl.sync();
 }
@@ -170,9 +208,19 @@ int main(int argc, char** argv) {
   cudaMalloc(&big, 512LL << 20);
   cudaMemset(big, 0, 512LL << 20);
   cudaFuncSetAttribute(skel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &qr);
+  CUtensorMap tmap;
+  cuuint64_t dims[2] = {8192, 8192};
+  cuuint64_t strides[1] = {8192 * 8};
+  cuuint32_t box[2] = {64, 1}, estr[2] = {1, 1};
+  CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, big, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  printf("tensor map: %d\n", (int)cr);
   struct V { int C, grid, mode, g2, bo; } vs[] = {
-      {4, 132, 0, 16, 0}, {4, 132, 1, 16, 0}, {4, 132, 2, 16, 0}, {4, 132, 4, 16, 0}, {4, 132, 0, 4, 0},
-      {4, 132, 0, 16, 64}, {8, 128, 0, 16, 0}, {8, 128, 2, 16, 0}, {4, 64, 0, 16, 0}, {4, 8, 0, 16, 0}};
+      {4, 132, 0, 16, 0}, {4, 132, 0, 15, 0}, {4, 132, 2, 15, 0}, {4, 132, 2 | 64, 15, 0}, {4, 132, 2 | 64 | 8, 15, 0},
+      {4, 132, 2 | 16, 15, 0}, {4, 132, 4 | 64, 15, 0}};
   for (auto v : vs) {
     cudaMemset(ll, 0, 2LL * 160 * S * 2 * 8);
     cudaLaunchConfig_t cfg = {};
@@ -186,13 +234,13 @@ int main(int argc, char** argv) {
     a[0].val.clusterDim.z = 1;
     cfg.attrs = a;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, skel, ll, 4000, v.mode, v.g2, v.bo, out, (const double*)big);
+    cudaLaunchKernelEx(&cfg, skel, ll, 4000, v.mode, v.g2, v.bo, out, (const double*)big, tmap);
     cudaError_t e = cudaDeviceSynchronize();
-    long long h[2];
-    cudaMemcpy(h, out, 16, cudaMemcpyDeviceToHost);
+    long long h[3];
+    cudaMemcpy(h, out, 24, cudaMemcpyDeviceToHost);
     fflush(stdout);
-    printf("C=%d grid=%d %s G2max=%d backoff=%d: %lld cycles/iter (%.2f us at 1965 MHz) %s\n", v.C, v.grid,
-           v.mode & 1 ? "r only " : v.mode & 2 ? "r+y, 96KB TMA after stage 1" : v.mode & 4 ? "r+y, 96KB TMA at top" : "r and y", v.g2, v.bo, h[0], h[0] / 1965.0, cudaGetErrorString(e));
+    printf("C=%d grid=%d mode=%d G2max=%d: %lld cycles/iter (%.2f us), top wait %lld %s\n", v.C, v.grid, v.mode,
+           v.g2, h[0], h[0] / 1965.0, h[2], cudaGetErrorString(e));
     fflush(stdout);
     if (e != cudaSuccess) return 1;
   }
