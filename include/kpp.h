@@ -115,23 +115,34 @@ typedef enum {
 } kpp_option;
 
 /* ---- setup ------------------------------------------------------------------ */
-/* Kaczmarz++ context for general A (m x n).  1 <= block_size <= m, lambda >= 0.
-   No device work beyond allocation is done here. */
+/* Kaczmarz++ context (Alg 5, problem statement P:78 / P:179) for a general A (m x n):
+   A DEVICE, row-major, lda >= n, borrowed; block_size = s, 1 <= s <= m; lambda >= 0 the
+   Tikhonov shift of the projection (A_S A_S^T + lam I)^{-1} (Eq (bk), default 1e-8 P:850);
+   seed keys the Philox-4x32-10 streams of the block schedule (reading R2).  *out receives the
+   context (owned by the caller, freed by kpp_destroy).  Errors: KPP_EINVAL (null pointers, sizes,
+   lambda < 0; *out untouched), KPP_ENOMEM, KPP_ECUDA.  No device work beyond allocation. */
 kpp_status kpp_setup(kpp_ctx** out, const double* A, int64_t m, int64_t n, int64_t lda,
                      int32_t block_size, double lambda, uint64_t seed);
-/* CD++ context for symmetric PSD A (n x n).  1 <= block_size <= n, lambda >= 0.
-   A must be exactly symmetric (A_SS is read from the stored rows). */
+/* CD++ context (Alg 3) for a symmetric PSD A (n x n): A DEVICE, row-major, lda >= n,
+   borrowed, exactly symmetric (A_SS is read from the stored rows); 1 <= block_size <= n; lambda >= 0
+   shifts the principal block, (A_SS + lam I)^{-1} (Alg 3 l.8-11 P:753-757).  Same ownership and
+   errors as kpp_setup. */
 kpp_status cdpp_setup(kpp_ctx** out, const double* A, int64_t n, int64_t lda,
                       int32_t block_size, double lambda, uint64_t seed);
 
 /* ---- solve ------------------------------------------------------------------ */
-/* One solve.  b: m values (n for CD++).  x0: n values or NULL (= 0).  max_iters >= 0.
+/* One solve: the block iterations of Alg 5 l.5-18 P:1341-1357 (Alg 3 l.5-20 P:749-766) from x0,
+   with the memoized factors of the context (Phase 1 runs for every block seen for the first time).
+   b: m values (n for CD++).  x0: n values or NULL (= 0).  max_iters >= 0.
    tol >= 0: stop at the first checkpoint with E1 <= tol^2 ||b||^2 (0 = run max_iters
    unless the estimate is exactly zero).  x_out: n values.  res_hist (HOST, may be
    NULL): per-checkpoint sqrt(E1/||b||^2), at most hist_cap entries; n_hist (may be
    NULL) receives the number of checkpoints; iters_out (may be NULL) receives the
-   number of block iterations performed.
-   Returns KPP_OK (tolerance met), KPP_EMAXITER, or an error. */
+   number of block iterations performed.  b / x0 / x_out: DEVICE or HOST (staged through the
+   context's stream), caller-owned, sizes unchecked by the ABI (the Python binding checks them).
+   Returns KPP_OK (tolerance met, Alg 5 l.15 P:1352), KPP_EMAXITER (x_out written), KPP_ENOTPD (a
+   block's shifted Gram / principal block is not positive definite, reading Q13), KPP_EDIVERGED
+   (non-finite block residual, reading Q13'), KPP_EINVAL (outputs untouched), KPP_ECUDA, KPP_ENCCL. */
 kpp_status kpp_solve(kpp_ctx* ctx, const double* b, const double* x0, int64_t max_iters, double tol,
                      double* x_out, double* res_hist, int64_t hist_cap, int64_t* n_hist,
                      int64_t* iters_out);
@@ -140,31 +151,42 @@ kpp_status cdpp_solve(kpp_ctx* ctx, const double* b, const double* x0, int64_t m
                       double* x_out, double* res_hist, int64_t hist_cap, int64_t* n_hist,
                       int64_t* iters_out);
 
+/* Free the context and everything it owns (factor cache, schedule, work vectors, NCCL
+   communicator, peer mappings).  NULL is a no-op.  A (borrowed) is not touched. */
 void kpp_destroy(kpp_ctx* ctx);
+/* Static string naming a status code. */
 const char* kpp_status_str(kpp_status s);
 const char* kpp_last_error(const kpp_ctx* ctx); /* owned by ctx; "" if none */
 
-/* Run the context's work on this cudaStream_t (default: the legacy default stream). */
+/* Run the context's work on this cudaStream_t (default: the legacy default stream).  The stream is
+   borrowed.  KPP_EINVAL on a null context. */
 kpp_status kpp_set_stream(kpp_ctx* ctx, void* cuda_stream);
+/* Set one kpp_option (each enumerator above cites its passage and range); KPP_EINVAL for an unknown
+   key or an out-of-range value (the option keeps its previous value).  Takes effect at the next
+   solve; changing the factor route or the projection invalidates the memoized factors (they are
+   recomputed, for the same blocks, at the next solve). */
 kpp_status kpp_set_option(kpp_ctx* ctx, int32_t key, double value);
 
 /* ---- introspection (parity tests, benchmarks) ------------------------------- */
-/* Schedule for t in [t0, t0+count): block id (fresh blocks numbered in creation
-   order) and fresh flag.  Computed on the device; HOST outputs. */
+/* Schedule for t in [t0, t0+count) (Alg 5 l.6-8 P:1342-1345, Alg 3 l.6-8 P:750-754, online
+   memoization P:653-665): block id (fresh blocks numbered in creation order) and fresh flag.
+   Computed on the device; HOST outputs of count entries.  KPP_EINVAL for t0 < 0 or count < 0. */
 kpp_status kpp_get_schedule(kpp_ctx* ctx, int64_t t0, int64_t count, int32_t* block_id,
                             uint8_t* is_fresh);
-/* Index set of memoized block `block_id` (HOST, s ints).  The block must already exist
-   (created by a solve or by kpp_get_schedule/kpp_prepare). */
+/* Index set S of memoized block `block_id` ("S ~ ([m] choose s)", P:752 / P:1344; sorted, 0-based;
+   HOST, s ints).  The block must already exist (created by a solve or by kpp_get_schedule /
+   kpp_prepare), else KPP_EINVAL. */
 kpp_status kpp_get_block(kpp_ctx* ctx, int64_t block_id, int32_t* S_out);
-/* Memoized projection operator of block `block_id`: M = (A_S A_S^T + lam I)^{-1}
-   (K++) or (A_SS + lam I)^{-1} (CD++), s x s row-major, HOST output.  Requires the
-   factor to exist (run kpp_prepare or a solve first). */
+/* Memoized projection operator of block `block_id` (Phase 1, P:104-109 / P:140 / P:753, DESIGN
+   reading R1): M = (A_S A_S^T + lam I)^{-1} (K++) or (A_SS + lam I)^{-1} (CD++), s x s row-major,
+   HOST output.  Requires the factor to exist (run kpp_prepare or a solve first), else KPP_EINVAL. */
 kpp_status kpp_get_factor(kpp_ctx* ctx, int64_t block_id, double* M_out);
 /* Drop every memoized block (the next solve regenerates and refactors them: a cold solve). */
 kpp_status kpp_clear_cache(kpp_ctx* ctx);
-/* Generate and factor (Phase 1) every fresh block needed by iterations [0, iters). */
+/* Generate and factor (Phase 1, P:653-665) every fresh block needed by iterations [0, iters). */
 kpp_status kpp_prepare(kpp_ctx* ctx, int64_t iters);
-/* Rho history of the last solve (HOST, per checkpoint, the rho in force after it). */
+/* Rho history of the last solve (Eq (weighted), reading Q8/Q9): HOST, per checkpoint, the
+   rho in force after it; at most cap entries written, *n receives the number available. */
 kpp_status kpp_get_rho_history(kpp_ctx* ctx, double* rho_hist, int64_t cap, int64_t* n);
 
 typedef struct {
@@ -188,20 +210,27 @@ typedef struct {
   int32_t engine;        /* Phase-2 engine of the last solve: 0 persistent, 1 step graph, 2 fused exchange,
                             3 sketch + LSQR */
 } kpp_stats;
+/* Timing and launch-plan counters (measurement); HOST output. */
 kpp_status kpp_get_stats(kpp_ctx* ctx, kpp_stats* out);
 /* Reset the timing counters of kpp_get_stats. */
 kpp_status kpp_reset_stats(kpp_ctx* ctx);
 
 /* ---- column-sharded multi-GPU (one process per GPU) ------------------------- */
-/* 128-byte NCCL unique id; rank 0 creates it, the harness broadcasts it through its
-   own process group (torch.distributed), every rank passes it to *_setup_dist. */
+/* Column-sharded multi-GPU (per iteration one all-reduce of the s-vector A_S x, the
+   paper's Alg 5 l.9 P:1346 split over column slabs; per fresh block one of the s x s Gram).
+   128-byte NCCL unique id; rank 0 creates it, the harness broadcasts it through its own process
+   group (torch.distributed), every rank passes it to *_setup_dist.  KPP_ENCCL on failure. */
 kpp_status kpp_get_unique_id(uint8_t id[128]);
-/* A_slab = A[:, col_begin:col_end] (m x (col_end-col_begin), row-major, lda >= width)
-   on this rank's device.  b is full and replicated; x0 / x_out are the local slab. */
+/* A_slab = A[:, col_begin:col_end] (m x (col_end-col_begin), row-major, lda >= width) on this rank's
+   device, borrowed.  b is full and replicated; x0 / x_out are the local slab.  Collective: every rank
+   calls it with the same (m, n_global, s, lambda, seed, id, nranks) and its own slab; the contiguous
+   slabs must tile [0, n_global).  Errors as kpp_setup, plus KPP_ENCCL. */
 kpp_status kpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t m, int64_t n_global,
                           int64_t col_begin, int64_t col_end, int64_t lda, int32_t block_size,
                           double lambda, uint64_t seed, const uint8_t id[128], int32_t rank,
                           int32_t nranks);
+/* CD++ on a column slab A[:, col_begin:col_end] of the symmetric A (Alg 3); fresh principal blocks
+   A_SS are assembled from the ranks' disjoint column supports by one exact sum. */
 kpp_status cdpp_setup_dist(kpp_ctx** out, const double* A_slab, int64_t n, int64_t col_begin,
                            int64_t col_end, int64_t lda, int32_t block_size, double lambda,
                            uint64_t seed, const uint8_t id[128], int32_t rank, int32_t nranks);
