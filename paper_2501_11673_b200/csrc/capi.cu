@@ -134,6 +134,8 @@ struct kpp_ctx {
   int vranks = 1;
   unsigned long long* vpeer = nullptr;
   long long vpeer_cap = 0;
+  unsigned long long* cs_vll = nullptr;  // emulated ranks of the CD++ streaming kernel: grid exchanges
+  long long cs_vll_cap = 0;
   int xchg = 1;                  // KPP_OPT_XCHG: 1 peer exchange when available, 0 NCCL allreduce
   int peer_ok = 0;
   unsigned long long* peer_buf = nullptr;
@@ -446,7 +448,8 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   } else {
     // G1 = A_S A_S^T (+ lam I): NT GEMM with row gathers on both operands, split-K
     Operand a{ctx->A, ctx->lda, 0, S, s, 0}, b{ctx->A, ctx->lda, 0, S, s, 1};
-    const int z1 = launch_dgemm(st, B, s, s, (int)n, a, b, part, s, ss, Z, 1);
+    int z1 = launch_gram_syrk(st, B, s, (int)n, ctx->A, ctx->lda, 0, S, s, part, ss, Z);
+    if (!z1) z1 = launch_dgemm(st, B, s, s, (int)n, a, b, part, s, ss, Z, 1);
     pp.mark("gram1");
     const bool dist = ctx->nranks > 1;
     launch_splitk_reduce(st, B, s, s, z1, part, ss, dist ? 0.0 : ctx->lam, nullptr, 0.0, 0, G, ss, 1);
@@ -520,7 +523,8 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
         launch_dgemm(st, Bn, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);  // Q1 = X1^T A_S (X1^T lower)
         pp.mark("Q1");
         Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
-        const int z2 = launch_dgemm(st, Bn, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
+        int z2 = launch_gram_syrk(st, Bn, s, (int)n, Q, n, (long long)s * n, nullptr, 0, part, ss, Z);
+        if (!z2) z2 = launch_dgemm(st, Bn, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
         pp.mark("gram2");
         Operand x1n{X1b, s, ss, nullptr, 0, 0};
         launch_dgemm(st, Bn, s, s, s, x1t, x1n, L, s, ss, 1, 0, 1);  // X1^T X1 (X1^T lower)
@@ -784,8 +788,11 @@ kpp_status plan_cdpp_stream(kpp_ctx* ctx) {
   return KPP_OK;
 }
 
+// (column-sharded contexts: with the peer buffers mapped and the fused exchange on, the rank stage
+// of the kernel carries the per-iteration exchange)
 bool use_cdpp_stream(const kpp_ctx* ctx) {
-  return ctx->kind == KIND_CDPP && ctx->cs_ok && ctx->engine <= 0 && ctx->nranks == 1 &&
+  return ctx->kind == KIND_CDPP && ctx->cs_ok && ctx->engine <= 0 &&
+         (ctx->nranks == 1 || (ctx->peer_ok && ctx->xchg)) &&
          (ctx->reassoc == 2 || (ctx->reassoc == 1 && !ctx->pplan.resident));
 }
 
@@ -990,8 +997,10 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   // engine: -1 automatic (one GPU: persistent kernel; column-sharded: the fused-exchange kernel
   // when the peer buffers are mapped, else the graph of step kernels with NCCL)
   int eng = ctx->engine;
-  if (eng < 0) eng = ctx->nranks > 1 ? ((ctx->xchg && ctx->peer_ok) ? 2 : 1) : 0;
-  if (eng == 0 && ctx->nranks > 1) eng = 1;
+  // CD++ on streaming blocks: the re-associated cluster kernel carries its own rank stage (engine 0)
+  const bool cs_dist = ctx->nranks > 1 && use_cdpp_stream(ctx) && !use_lsqr;
+  if (eng < 0) eng = ctx->nranks > 1 ? (cs_dist ? 0 : (ctx->xchg && ctx->peer_ok) ? 2 : 1) : 0;
+  if (eng == 0 && ctx->nranks > 1 && !cs_dist) eng = 1;
   if (eng == 2 && !ctx->peer_buf) {
     if (ctx->nranks > 1) eng = 1;  // no peer mapping: NCCL engine
     else CKS(peer_setup(ctx));      // one rank: a self-mapped buffer
@@ -1000,9 +1009,34 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   const bool use_graph = !use_lsqr && eng == 1;
   ctx->stats.engine = use_lsqr ? 3 : eng;
   if (use_lsqr) CKS(lsqr_prepare(ctx));
-  // emulated ranks (KPP_OPT_VRANKS, one-GPU context): grid vg per rank, all in one launch
-  const int vr = (use_xeng && ctx->nranks == 1) ? ctx->vranks : 1;
+  const bool use_cs = !use_lsqr && !use_xeng && !use_graph && use_cdpp_stream(ctx);
+  // emulated ranks (KPP_OPT_VRANKS, one-GPU context): grid vg per rank, all in one launch (engine 2
+  // or the CD++ streaming kernel)
+  const int vr = ((use_xeng || use_cs) && ctx->nranks == 1) ? ctx->vranks : 1;
   const int vg = vr > 1 ? ctx->num_sms / vr : ctx->grid;
+  if (use_cs && (ctx->nranks > 1 || vr > 1)) {
+    // fresh tags for this solve: clear the receive buffers, then (multi-rank) a barrier
+    if (vr > 1) {
+      const long long vw = 4LL * vr * vr * ctx->s;
+      if (vw > ctx->vpeer_cap) {
+        if (ctx->vpeer) cudaFree(ctx->vpeer);
+        CK(cudaMalloc((void**)&ctx->vpeer, (size_t)vw * sizeof(unsigned long long)));
+        ctx->vpeer_cap = vw;
+      }
+      CK(cudaMemsetAsync(ctx->vpeer, 0, (size_t)vw * sizeof(unsigned long long), st));
+      // per-rank grid-exchange regions: [2][clusters][s] + [2][s] LL words each
+      const int gpr = ctx->cs_grid / vr / ctx->cs_C * ctx->cs_C;
+      const long long vll = (long long)vr * (4LL * (gpr / ctx->cs_C) * ctx->s + 4LL * ctx->s);
+      if (vll > ctx->cs_vll_cap) {
+        if (ctx->cs_vll) cudaFree(ctx->cs_vll);
+        CK(cudaMalloc((void**)&ctx->cs_vll, (size_t)vll * sizeof(unsigned long long)));
+        ctx->cs_vll_cap = vll;
+      }
+    } else {
+      CK(cudaMemsetAsync(ctx->peer_buf, 0, 4ULL * ctx->nranks * ctx->s * sizeof(unsigned long long), st));
+      if (ctx->comm) CKN(ncclAllReduce(ctx->peer_bar, ctx->peer_bar, 1, ncclDouble, ncclSum, ctx->comm, st));
+    }
+  }
   if (use_xeng) {
     const long long words = (long long)vr * (long long)xeng_ll_words((int)ctx->s, vg);
     if (words > ctx->xeng_ll_cap) {
@@ -1135,7 +1169,28 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
         q.hist_res = p.hist_res; q.hist_rho = p.hist_rho; q.hist_cap = p.hist_cap;
         q.ygl = 1; q.yll = ctx->d_ll + ctx->ll_bytes / sizeof(unsigned long long) - 4LL * ctx->s;
         q.prof = p.prof;
-        CK(launch_cdpp_stream(st, q, ctx->cs_grid, ctx->cs_C, ctx->cs_smem));
+        // ranks: this one (vcol = all local columns), or vr emulated ones splitting the columns
+        q.rank = ctx->rank; q.nranks = ctx->nranks; q.vranks = 1; q.ll_vstride = 0;
+        q.vcol[0] = 0; q.vcol[1] = n;
+        for (int r = 0; r < KPP_MAX_PEERS; ++r) q.peer_recv[r] = ctx->peer_map[r];
+        int cgrid = ctx->cs_grid;
+        size_t csmem = ctx->cs_smem;
+        if (vr > 1) {
+          const int gpr = ctx->cs_grid / vr / ctx->cs_C * ctx->cs_C;
+          q.nranks = vr; q.rank = 0; q.vranks = vr;
+          long long wmax = 0;
+          for (int v = 0; v <= vr; ++v) q.vcol[v] = (long long)v * n / vr;
+          for (int v = 0; v < vr; ++v) wmax = std::max(wmax, q.vcol[v + 1] - q.vcol[v]);
+          q.slab = (int)std::max<long long>(4, ((wmax + gpr - 1) / gpr + 3) / 4 * 4);
+          for (int r = 0; r < vr; ++r) q.peer_recv[r] = ctx->vpeer + 4LL * vr * ctx->s * r;
+          q.ll = ctx->cs_vll;
+          q.yll = ctx->cs_vll + 4LL * (gpr / ctx->cs_C) * ctx->s;
+          q.ll_vstride = 4LL * (gpr / ctx->cs_C) * ctx->s + 4LL * ctx->s;
+          CK(cudaMemsetAsync(ctx->cs_vll, 0, (size_t)vr * q.ll_vstride * sizeof(unsigned long long), st));
+          cgrid = gpr * vr;
+          csmem = cdpp_stream_smem_bytes(q, ctx->cs_C);
+        }
+        CK(launch_cdpp_stream(st, q, cgrid, ctx->cs_C, csmem));
       } else {
         CK(launch_iterate(st, p, ctx->pgrid, ctx->pC, ctx->psmem));
       }
@@ -1367,6 +1422,7 @@ void kpp_destroy(kpp_ctx* ctx) {
   if (ctx->peer_buf) cudaFree(ctx->peer_buf);
   if (ctx->xeng_ll) cudaFree(ctx->xeng_ll);
   if (ctx->vpeer) cudaFree(ctx->vpeer);
+  if (ctx->cs_vll) cudaFree(ctx->cs_vll);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   void* ptrs[] = {ctx->srht_d, ctx->srht_T, ctx->lsqr_buf, ctx->lsqr_ll, ctx->rht_A, ctx->rht_d, ctx->rht_v, ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,

@@ -222,7 +222,12 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
   const int c = (int)cluster.block_rank();
-  const int q = blockIdx.x / C, NQ = gridDim.x / C;
+  // rank of this CTA (several ranks per launch when emulated; cluster boundaries align with them)
+  const int gpr = (int)gridDim.x / p.vranks;      // CTAs per rank
+  const int vr = (int)blockIdx.x / gpr, gb = (int)blockIdx.x - vr * gpr;
+  const int rank = p.rank + vr, P = p.nranks;
+  const bool lead = vr == 0;                       // the first rank of the launch writes shared state
+  const int q = gb / C, NQ = gpr / C;              // cluster within the rank, clusters per rank
   const int sl = (s + C - 1) / C;
   const int r0 = min(s, c * sl), r1 = min(s, r0 + sl);
   const int R = r1 - r0;
@@ -250,14 +255,17 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   __shared__ int stop_sh, nl_sh[3], row_ctr;
   __shared__ long long tmod_sh;
 
-  const long long c0 = (long long)blockIdx.x * p.slab;
-  const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
+  const long long cr1 = p.vcol[vr + 1];            // end of the rank's local columns
+  const long long c0 = min(p.vcol[vr] + (long long)gb * p.slab, cr1);
+  const long long c1 = (c0 + p.slab < cr1) ? c0 + p.slab : cr1;
   const int w = (int)(c1 > c0 ? c1 - c0 : 0);
   const long long gc0 = p.col_base + c0, gc1 = p.col_base + c1;  // global columns of the slab
+  unsigned long long* const llr = p.ll + (long long)vr * p.ll_vstride;   // this rank's grid exchange
+  unsigned long long* const ylr = p.yll + (long long)vr * p.ll_vstride;
   const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
   const long long ss = (long long)s * s;
-  const int yg0 = (int)((long long)blockIdx.x * s / gridDim.x);
-  const int yg1 = (int)((long long)(blockIdx.x + 1) * s / gridDim.x);
+  const int yg0 = (int)((long long)gb * s / gpr);
+  const int yg1 = (int)((long long)(gb + 1) * s / gpr);
 
   if (tid == 0) {
     st = *p.st;
@@ -295,7 +303,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   double rho_prev = 0.0;  // rho in force at t-1
   // optional phase timers (KPP_PHASE_PROFILE): CTA 0, thread 0 (phase A, stream) and the first
   // chain thread (chain), then the end-of-slot barrier wait of each
-  const bool prof0 = p.prof != nullptr && blockIdx.x == 0 && (tid == 0 || tid == CH0);
+  const bool prof0 = p.prof != nullptr && blockIdx.x == 0 && (tid == 0 || tid == CH0);  // (rank 0's first CTA)
   long long pacc[8] = {};
   long long plast = prof0 ? clock64() : 0;
 #define CS_MARK(i)                        \
@@ -372,7 +380,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
     } else {
       // ---- B (chain threads): exchange, window logic and projection of iteration t
       const int ct = tid - CH0;
-      unsigned long long* gll = p.ll + (long long)(it & 1) * NQ * s * 2;
+      unsigned long long* gll = llr + (long long)(it & 1) * NQ * s * 2;
       if (R > 0) mbar_wait_cluster(bars + 2, it & 1u, 42);
       for (int row = ct; row < R; row += NCH) {
         double v = 0.0;
@@ -380,10 +388,24 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
         ll_store_global(gll + ((long long)q * s + r0 + row) * 2, v, tag);
       }
       // gather my slice from every cluster (batches of 8 in flight), fixed-order sum
+      const long long pslot = (t & 1) * (long long)P * s;
+      const unsigned ptag = (unsigned)(t + 1);  // global iteration: the receive buffers persist over windows
       for (int row = ct; row < R; row += NCH) {
         double v = 0.0;
         for (int q0 = 0; q0 < NQ; q0 += 8)
           v += ll_gather_sum<8, 500>(gll + (long long)(r0 + row) * 2, (long long)s * 2, q0, 1, NQ, tag, p.err);
+        if (P > 1) {
+          // rank stage (row 9): cluster 0 of the rank stores the rank's partial into slot [t mod 2][rank]
+          // of EVERY rank's receive buffer (peer memory over NVLink; device memory when emulated),
+          // then every cluster sums the P partials in rank order: the same bits on every rank
+          if (q == 0)
+            for (int rr = 0; rr < P; ++rr)
+              ll_store_sys(p.peer_recv[rr] + 2 * (pslot + (long long)rank * s + r0 + row), v, ptag);
+          double tot = 0.0;
+          for (int rr = 0; rr < P; ++rr)
+            tot += ll_wait_sys(p.peer_recv[rank] + 2 * (pslot + (long long)rr * s + r0 + row), ptag, p.err);
+          v = tot;
+        }
         v -= bSc[r0 + row];
         for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_r, cc));
       }
@@ -397,7 +419,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
         e = warp_sum(e);
         if (lane == 0) {
           const int res = window_step_dev(st, tmod, e, p.zeta, p.tol2bb, p.bb, p.adaptive,
-                                          blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
+                                          gb == 0 && lead && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
           if (res) {
             st.stopped = res;
             stop_sh = 1;
@@ -421,7 +443,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
 #pragma unroll 4
           for (int l = lane; l < s; l += 32) v = fma(__ldg(Mrow + l), r_sm[l], v);
           v = warp_sum(v);
-          if (lane == 0) ll_store_global(p.yll + ((long long)(it & 1) * s + k) * 2, v, tag);
+          if (lane == 0) ll_store_global(ylr + ((long long)(it & 1) * s + k) * 2, v, tag);
         }
       }
       CS_MARK(4);  // window logic + y rows
@@ -441,7 +463,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
         for (int i = ct; i < s; i += NCH) S2[i] = src[i];
       }
       // y_t from every CTA's rows
-      ll_gather_vec<4>(y_sm, p.yll + (long long)(it & 1) * s * 2, s, tag, p.err, ct, NCH);
+      ll_gather_vec<4>(y_sm, ylr + (long long)(it & 1) * s * 2, s, tag, p.err, ct, NCH);
       CS_MARK(5);  // y gathered
       // the chain of t is done: help stream D_{t+1}
       if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf(prv), cmap(cur), stash(prv), vec, &row_ctr);
@@ -476,7 +498,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
     p.x[c0 + j] = x_sm[j];
     p.mom[c0 + j] = m_sm[j];
   }
-  if (blockIdx.x == 0 && tid == 0) {
+  if (gb == 0 && lead && tid == 0) {
     st.t_done = t;
     *p.st = st;
   }

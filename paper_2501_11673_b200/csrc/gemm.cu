@@ -363,6 +363,121 @@ __global__ void splitk_reduce_kernel(int M, int N, int Z, const double* part, lo
   }
 }
 
+// ---------------------------------------------------------------- balanced Gram (SYRK) kernel
+// The upper triangle of G = A_S A_S^T for one block and one K chunk per CTA, on DMMA.
+// The s x s output is cut into F x F fragments of 8 x 8 (F = ceil(s/8)); fragment rows are paired
+// (p, F-1-p), which together hold F+1 upper fragments, so every warp gets the same work (one pair,
+// or half a pair when F > 16: 17 fragments at most) -- the tile kernel's diagonal tiles left up to
+// half of their warps idle at every K step.  A_S is staged once per K step (it is both operands).
+constexpr int GS_SLOTS = 17;                 // fragments per warp
+constexpr int GS_LD = 16 + 4;                // [row][k] stride of the staged rows (doubles)
+constexpr int GS_ST = 3;                     // pipeline stages
+__host__ __device__ constexpr int gs_threads(int split) { return split == 1 ? 256 : 512; }
+__host__ __device__ constexpr size_t gs_smem(int split) {
+  return (size_t)GS_ST * (split == 1 ? 128 : 256) * GS_LD * sizeof(double);
+}
+
+// SPLIT 1: F <= 16, one warp per fragment-row pair, one CTA per (block, chunk);
+// SPLIT 2: 16 < F <= 32, two warps per pair, 8 pairs per CTA, two CTAs per (block, chunk).
+template <int SPLIT>
+__global__ void __launch_bounds__(gs_threads(SPLIT), SPLIT == 1 ? 2 : 1)
+gram_syrk_kernel(int s, int F, int K, int Z, int kchunk, const double* base, long long ld, long long bstride,
+                 const int32_t* idx, long long idx_bstride, double* part, long long ss) {
+  constexpr int NT = gs_threads(SPLIT), ROWS = SPLIT == 1 ? 128 : 256;
+  extern __shared__ __align__(16) double gs_sm[];
+  const int npairs = (F + 1) / 2;
+  const int ncta = SPLIT == 1 ? 1 : (npairs + 7) / 8;
+  const int bz = blockIdx.x / ncta, h = blockIdx.x % ncta;
+  const int batch = bz / Z, z = bz % Z;
+  const int kbeg = z * kchunk, kend = min(K, kbeg + kchunk);
+  const double* ab = base + (long long)batch * bstride;
+  const int32_t* ix = idx ? idx + (long long)batch * idx_bstride : nullptr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int p = h * 8 + warp / SPLIT, half = warp % SPLIT;
+  const bool active = p < npairs;
+  const int r1 = p, r2 = F - 1 - p;
+  const int n1 = F - r1;                          // fragments of row r1 (columns r1 .. F-1)
+  const int total = active ? (r1 != r2 ? n1 + (F - r2) : n1) : 0;
+  const int hsz = (total + SPLIT - 1) / SPLIT;
+  const int lo = half * hsz, hi = min(total, lo + hsz);
+  // the thread's staged chunks (16 bytes): row, source row of A (gathered), -1 out of range
+  constexpr int CH = ROWS * 8 / NT;               // chunks per thread per stage (4)
+  int srow[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int rr = (threadIdx.x + NT * c) >> 3;
+    srow[c] = rr < s ? (ix ? ix[rr] : rr) : -1;
+  }
+  auto stage = [&](int slot, int k0) {
+    double* dst = gs_sm + slot * ROWS * GS_LD;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int e = threadIdx.x + NT * c;
+      const int rr = e >> 3, kc = (e & 7) * 2;
+      const int gk = k0 + kc;
+      const int valid = srow[c] >= 0 ? min(2, max(0, kend - gk)) : 0;
+      const double* src = valid ? ab + (long long)srow[c] * ld + gk : ab;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(
+                       dst + rr * GS_LD + kc)),
+                   "l"(src), "r"(valid * 8)
+                   : "memory");
+    }
+  };
+  double acc[GS_SLOTS][2];
+#pragma unroll
+  for (int i = 0; i < GS_SLOTS; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const int nk = kend > kbeg ? (kend - kbeg + 15) / 16 : 0;
+#pragma unroll
+  for (int st = 0; st < GS_ST - 1; ++st) {
+    if (st < nk) stage(st, kbeg + st * 16);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(GS_ST - 2) : "memory");
+    __syncthreads();
+    {
+      const int ln = kt + GS_ST - 1;
+      if (ln < nk) stage(ln % GS_ST, kbeg + ln * 16);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    if (!active) continue;
+    const double* As = gs_sm + (kt % GS_ST) * ROWS * GS_LD + fr * GS_LD + fc;
+#pragma unroll
+    for (int kk = 0; kk < 16; kk += 4) {
+      const double a1 = As[(r1 * 8) * GS_LD + kk];
+      const double a2 = As[(r2 * 8) * GS_LD + kk];
+#pragma unroll
+      for (int i = 0; i < GS_SLOTS; ++i) {
+        const int sl = lo + i;
+        if (sl < hi) {
+          const bool first = sl < n1;
+          const int col = first ? r1 + sl : r2 + (sl - n1);
+          const double bv = As[(col * 8) * GS_LD + kk];
+          mma_f64(acc[i][0], acc[i][1], first ? a1 : a2, bv);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (!active) return;
+  double* Cb = part + (long long)bz * ss;
+#pragma unroll
+  for (int i = 0; i < GS_SLOTS; ++i) {
+    const int sl = lo + i;
+    if (sl < hi) {
+      const bool first = sl < n1;
+      const int row = first ? r1 : r2, col = first ? r1 + sl : r2 + (sl - n1);
+      const int gi = row * 8 + fr, gj = col * 8 + fc * 2;
+      if (gi < s) {
+        double* cp = Cb + (long long)gi * s + gj;
+        if (gj < s) cp[0] = acc[i][0];
+        if (gj + 1 < s) cp[1] = acc[i][1];
+      }
+    }
+  }
+}
+
 }  // namespace
 
 static bool aligned16(const Operand& o) {
@@ -448,6 +563,42 @@ int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand&
     dgemm_kernel<true, false><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
   else
     dgemm_kernel<true, true><<<grid, THREADS, 0, st>>>(M, N, K, Z, kchunk, a, b, C, ldc, c_bstride, upper_only, alpha, beta1);
+  return Z;
+}
+
+// Upper Gram of s rows (gathered through idx, or dense rows of a batched operand) per K chunk:
+// part[(b Z + z) s^2 ...] as launch_dgemm writes it (upper triangle), Z K-chunks of 16-multiples.
+// Returns Z, or 0 when the shape is not served (s > 256 or unaligned rows).
+int launch_gram_syrk(cudaStream_t st, int batch, int s, int K, const double* base, long long ld, long long bstride,
+                     const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z) {
+  static const bool off = getenv("KPP_GRAM_SYRK") && atoi(getenv("KPP_GRAM_SYRK")) == 0;
+  // measured (B200, Phase 1 ms per bench step, balanced kernel vs the tile kernel): c2 (s = 128) 14.01 vs
+  // 14.30; with two warps per pair for s = 256 it loses (c3 37.2 vs 32.1, c4 521 vs 441): s <= 128 only
+  if (off || batch <= 0 || s > 128 || (reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1) || (bstride & 1)) return 0;
+  if (Z < 1) Z = 1;
+  int kchunk = (K + Z - 1) / Z;
+  kchunk = ((kchunk + 15) / 16) * 16;
+  Z = (K + kchunk - 1) / kchunk;
+  const int F = (s + 7) / 8;
+  count_launches(1);
+  if (F <= 16) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gram_syrk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gs_smem(1));
+      attr = true;
+    }
+    gram_syrk_kernel<1><<<batch * Z, gs_threads(1), gs_smem(1), st>>>(s, F, K, Z, kchunk, base, ld, bstride, idx,
+                                                                       idx_bstride, part, ss);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gram_syrk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gs_smem(2));
+      attr = true;
+    }
+    const int ncta = ((F + 1) / 2 + 7) / 8;
+    gram_syrk_kernel<2><<<batch * Z * ncta, gs_threads(2), gs_smem(2), st>>>(s, F, K, Z, kchunk, base, ld, bstride,
+                                                                               idx, idx_bstride, part, ss);
+  }
   return Z;
 }
 

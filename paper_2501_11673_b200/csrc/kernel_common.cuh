@@ -100,6 +100,28 @@ __device__ __forceinline__ double ll_gather_sum(const unsigned long long* src, l
   return v;
 }
 
+// LL words with system scope: the destination / source may be a peer GPU's memory mapped over NVLink
+__device__ __forceinline__ void ll_store_sys(unsigned long long* dst, double v, unsigned tag) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long tg = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};\n" ::"l"(dst), "l"(tg | (u & 0xffffffffull)),
+               "l"(tg | (u >> 32))
+               : "memory");
+}
+__device__ __forceinline__ double ll_wait_sys(const unsigned long long* src, unsigned tag, int* err) {
+  unsigned long long a, b;
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+  if ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
+    const unsigned long long t0 = globaltimer();
+    unsigned n = 0;
+    while ((unsigned)(a >> 32) != tag || (unsigned)(b >> 32) != tag) {
+      asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+      if ((++n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) spin_fail(err);
+    }
+  }
+  return __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
+}
+
 // ------------------------------------------------------------------ TMA bulk copies + mbarriers
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {

@@ -90,6 +90,10 @@ int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand&
                  int upper_only, int a_tri = 0, double alpha = 1.0, int beta1 = 0);
 // out[b] = sum_z part[b*Z+z] (+ diag_add on the diagonal) (+ add_scale * add[b]);
 // with upper_only, element (i,j), i>j, is taken from (j,i).
+// Balanced Gram kernel (upper triangle of rows x rows^T per K chunk, s <= 256); returns Z, or 0 if
+// the shape is not served (then use launch_dgemm)
+int launch_gram_syrk(cudaStream_t st, int batch, int s, int K, const double* base, long long ld, long long bstride,
+                     const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
 void launch_splitk_reduce(cudaStream_t st, int batch, int M, int N, int Z, const double* part,
                           long long p_bstride, double diag_add, const double* add,
                           double add_scale, long long add_bstride, double* out,
@@ -123,6 +127,7 @@ void launch_batch_move(cudaStream_t st, int count, const void* src, void* dst, c
                        int scatter);
 
 // ------------------------------------------------------------------ iterate.cu
+constexpr int KPP_MAX_PEERS = 8;
 struct alignas(64) IterParams {
   CUtensorMap tmA;       // 2D tensor map of A (cols x rows, box {sw, 1}) for TMA gather4, if tma
   int tma;               // 1: resident slabs are gathered with cp.async.bulk.tensor ... gather4
@@ -164,6 +169,14 @@ struct alignas(64) IterParams {
   int dbg_skip;          // debug: 1 skips the arithmetic of rows 3-5 (exchange-latency floor)
   int g2max;             // pollers per r row in the cross-cluster gather (<= 16; 0 = 16)
   int poll_ns;           // back-off between unsuccessful polling rounds of the gather (ns; 0 = none)
+  // column-sharded exchange of the CD++ streaming kernel: ranks rank .. rank+vranks-1
+  // run in this launch (vranks > 1: emulated on one GPU, see XParams::vranks), rank v's CTAs own the
+  // local columns [vcol[v], vcol[v+1]); per iteration each rank publishes its partial of the
+  // s-vector into every rank's receive buffer ([2][nranks][s] LL words, tags t+1 with the global t)
+  int rank, nranks, vranks;
+  long long vcol[KPP_MAX_PEERS + 1];
+  unsigned long long* peer_recv[KPP_MAX_PEERS];
+  long long ll_vstride;  // words between the ranks' grid-exchange regions (ll and yll), 0 if one rank
 };
 // Persistent Phase-2 kernel: grid = C * clusters CTAs, cluster size C.
 cudaError_t launch_iterate(cudaStream_t st, const IterParams& p, int grid, int C, size_t smem);
@@ -196,7 +209,6 @@ struct DevStep {
   long long t_end;   // end of the current window
   long long t_base;  // iteration of bid[0]
 };
-constexpr int KPP_MAX_PEERS = 8;
 struct StepParams {
   const double* A;
   long long lda, m, n;

@@ -773,3 +773,55 @@ def test_bell_general_parity(kpp, ora, accel):
     res = ctx.solve(b.to(DEV), max_iters=T)
     assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
     assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+
+
+CS_TWINS = [synth.twin("c5", 2048, 2048, 512, k=100), synth.twin("c5", 1001, 1001, 77, k=16),
+            synth.twin("c5", 4096, 4096, 256, k=100)]
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("cfg", CS_TWINS, ids=[c.name for c in CS_TWINS])
+def test_cdpp_stream_rank_stage(kpp, ora, cfg, P):
+    """The CD++ re-associated streaming kernel (row 7) with the rank stage of the column-sharded
+    exchange (row 9: the dense pass of t+1 hides the exchange of t), P ranks emulated in
+    one cooperative launch: rank v owns columns [v n/P, (v+1) n/P), reduces them over its own clusters,
+    publishes its partial of the s-vector into every rank's receive buffer and sums the P partials in
+    rank order.  Against the oracle at the BJ bar after 200 iterations, the checkpoint history, the
+    tolerance stop with a start vector, and bit-identical repeats."""
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.cdpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+    ctx.set_option(kpp.OPT_REASSOC, 2)  # the streaming kernel even where the slab would fit on chip
+    ctx.set_option(kpp.OPT_VRANKS, P)
+    ctx.set_option(kpp.OPT_WINDOW, 64)
+    T = 200
+    ref = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    st = ctx.stats()
+    assert st["engine"] == 0 and st["reassoc"] == 1
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    x1 = res.x.clone()
+    assert torch.equal(ctx.solve(b.to(DEV), max_iters=T).x, x1)
+    x0 = np.random.default_rng(5).standard_normal(A.shape[1])
+    ref2 = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=3000, tol=0.05, x0=x0, threads=8)
+    res2 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=3000, tol=0.05)
+    assert res2.iters == ref2.iters
+    assert rel(res2.x.cpu().numpy(), ref2.x) <= 1e-10
+
+
+def test_cdpp_stream_dist_context(kpp, ora):
+    """cdpp_setup_dist at one rank (self-mapped receive buffer, one-rank NCCL communicator): the
+    automatic engine is the streaming kernel with its rank stage (system-scope peer stores)."""
+    cfg = synth.twin("c5", 2048, 2048, 512, k=100)
+    A, b, _ = synth.make_problem(cfg)
+    n = A.shape[1]
+    ctx = kpp.cdpp_setup_dist(A.to(DEV), n, 0, n, cfg.s, cfg.lam, 0, kpp.kpp_get_unique_id(), 0, 1)
+    ctx.set_option(kpp.OPT_REASSOC, 2)
+    ctx.set_option(kpp.OPT_WINDOW, 64)
+    ref = ora.cdpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=200, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=200)
+    st = ctx.stats()
+    assert st["engine"] == 0 and st["reassoc"] == 1 and st["xchg"] == 1
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert torch.equal(ctx.solve(b.to(DEV), max_iters=200).x, res.x)
+    ctx.destroy()

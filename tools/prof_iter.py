@@ -20,6 +20,7 @@ ap.add_argument("--reassoc", type=int, default=1)
 ap.add_argument("--rht", action="store_true")
 ap.add_argument("--proj", type=int, default=0)
 ap.add_argument("--tmax", type=int, default=8)
+ap.add_argument("--vranks", type=int, default=1, help="emulated column-sharded ranks (engine 2 / CD++ stream)")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 A, b, _ = synth.make_problem(cfg, device="cuda")
@@ -29,6 +30,8 @@ ctx.set_option(kpp.OPT_CLUSTER, a.cluster)
 ctx.set_option(kpp.OPT_YGL, a.ygl)
 if cfg.kind == 'cdpp':
     ctx.set_option(kpp.OPT_REASSOC, a.reassoc)
+if a.vranks > 1:
+    ctx.set_option(kpp.OPT_VRANKS, a.vranks)
 if a.proj:
     ctx.set_option(kpp.OPT_PROJ, a.proj)
     ctx.set_option(kpp.OPT_TMAX, a.tmax)
