@@ -997,10 +997,14 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   // engine: -1 automatic (one GPU: persistent kernel; column-sharded: the fused-exchange kernel
   // when the peer buffers are mapped, else the graph of step kernels with NCCL)
   int eng = ctx->engine;
-  // CD++ on streaming blocks: the re-associated cluster kernel carries its own rank stage (engine 0)
+  // column-sharded contexts with mapped peer buffers: the persistent cluster kernels carry the rank
+  // stage of the exchange (engine 0) -- the CD++ re-associated streaming kernel, or the generic K++ /
+  // CD++ kernel (the lean register-tile kernel has no rank stage: engine 2 then)
   const bool cs_dist = ctx->nranks > 1 && use_cdpp_stream(ctx) && !use_lsqr;
-  if (eng < 0) eng = ctx->nranks > 1 ? (cs_dist ? 0 : (ctx->xchg && ctx->peer_ok) ? 2 : 1) : 0;
-  if (eng == 0 && ctx->nranks > 1 && !cs_dist) eng = 1;
+  const bool it_dist = ctx->nranks > 1 && !use_lsqr && ctx->peer_ok && ctx->xchg && !use_cdpp_stream(ctx) &&
+                       !iterate_uses_lean(ctx->pplan, ctx->pC);
+  if (eng < 0) eng = ctx->nranks > 1 ? ((cs_dist || it_dist) ? 0 : (ctx->xchg && ctx->peer_ok) ? 2 : 1) : 0;
+  if (eng == 0 && ctx->nranks > 1 && !cs_dist && !it_dist) eng = 1;
   if (eng == 2 && !ctx->peer_buf) {
     if (ctx->nranks > 1) eng = 1;  // no peer mapping: NCCL engine
     else CKS(peer_setup(ctx));      // one rank: a self-mapped buffer
@@ -1010,11 +1014,13 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
   ctx->stats.engine = use_lsqr ? 3 : eng;
   if (use_lsqr) CKS(lsqr_prepare(ctx));
   const bool use_cs = !use_lsqr && !use_xeng && !use_graph && use_cdpp_stream(ctx);
+  const bool use_it = !use_lsqr && !use_xeng && !use_graph && !use_cs;  // the persistent K++ / CD++ kernel
   // emulated ranks (KPP_OPT_VRANKS, one-GPU context): grid vg per rank, all in one launch (engine 2
   // or the CD++ streaming kernel)
-  const int vr = ((use_xeng || use_cs) && ctx->nranks == 1) ? ctx->vranks : 1;
+  const int vr = ((use_xeng || use_cs || use_it) && ctx->nranks == 1) ? ctx->vranks : 1;
   const int vg = vr > 1 ? ctx->num_sms / vr : ctx->grid;
-  if (use_cs && (ctx->nranks > 1 || vr > 1)) {
+  const int pk_grid = use_cs ? ctx->cs_grid : ctx->pgrid, pk_C = use_cs ? ctx->cs_C : ctx->pC;
+  if ((use_cs || use_it) && (ctx->nranks > 1 || vr > 1)) {
     // fresh tags for this solve: clear the receive buffers, then (multi-rank) a barrier
     if (vr > 1) {
       const long long vw = 4LL * vr * vr * ctx->s;
@@ -1025,8 +1031,9 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       }
       CK(cudaMemsetAsync(ctx->vpeer, 0, (size_t)vw * sizeof(unsigned long long), st));
       // per-rank grid-exchange regions: [2][clusters][s] + [2][s] LL words each
-      const int gpr = ctx->cs_grid / vr / ctx->cs_C * ctx->cs_C;
-      const long long vll = (long long)vr * (4LL * (gpr / ctx->cs_C) * ctx->s + 4LL * ctx->s);
+      const int gpr = pk_grid / vr / pk_C * pk_C;
+      if (gpr < pk_C) return fail(ctx, KPP_EINVAL, "%d emulated ranks do not fit the launch plan", vr);
+      const long long vll = (long long)vr * (4LL * (gpr / pk_C) * ctx->s + 4LL * ctx->s);
       if (vll > ctx->cs_vll_cap) {
         if (ctx->cs_vll) cudaFree(ctx->cs_vll);
         CK(cudaMalloc((void**)&ctx->cs_vll, (size_t)vll * sizeof(unsigned long long)));
@@ -1087,7 +1094,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
         q.nranks = vr;
         q.grid = vg;
         long long wmax = 0;
-        for (int v = 0; v <= vr; ++v) q.vcol[v] = (long long)v * n / vr;
+        for (int v = 0; v <= vr; ++v) q.vcol[v] = v == vr ? n : (long long)v * n / vr / 4 * 4;  // 32-byte aligned slabs
         for (int v = 0; v < vr; ++v) wmax = std::max(wmax, q.vcol[v + 1] - q.vcol[v]);
         q.slab = (int)((wmax + vg - 1) / vg);
         for (int r = 0; r < vr; ++r) q.peer_recv[r] = ctx->vpeer + 4LL * vr * ctx->s * r;
@@ -1179,7 +1186,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
           const int gpr = ctx->cs_grid / vr / ctx->cs_C * ctx->cs_C;
           q.nranks = vr; q.rank = 0; q.vranks = vr;
           long long wmax = 0;
-          for (int v = 0; v <= vr; ++v) q.vcol[v] = (long long)v * n / vr;
+          for (int v = 0; v <= vr; ++v) q.vcol[v] = v == vr ? n : (long long)v * n / vr / 4 * 4;  // 32-byte aligned slabs
           for (int v = 0; v < vr; ++v) wmax = std::max(wmax, q.vcol[v + 1] - q.vcol[v]);
           q.slab = (int)std::max<long long>(4, ((wmax + gpr - 1) / gpr + 3) / 4 * 4);
           for (int r = 0; r < vr; ++r) q.peer_recv[r] = ctx->vpeer + 4LL * vr * ctx->s * r;
@@ -1192,7 +1199,34 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
         }
         CK(launch_cdpp_stream(st, q, cgrid, ctx->cs_C, csmem));
       } else {
-        CK(launch_iterate(st, p, ctx->pgrid, ctx->pC, ctx->psmem));
+        p.rank = ctx->rank; p.nranks = ctx->nranks; p.vranks = 1; p.ll_vstride = 0;
+        p.vcol[0] = 0; p.vcol[1] = n;
+        for (int r = 0; r < KPP_MAX_PEERS; ++r) p.peer_recv[r] = ctx->peer_map[r];
+        int igrid = ctx->pgrid;
+        if (vr > 1) {
+          const int gpr = ctx->pgrid / vr / ctx->pC * ctx->pC;
+          p.nranks = vr; p.rank = 0; p.vranks = vr;
+          long long wmax = 0;
+          for (int v = 0; v <= vr; ++v) p.vcol[v] = v == vr ? n : (long long)v * n / vr / 4 * 4;  // 32-byte aligned (TMA)
+          for (int v = 0; v < vr; ++v) wmax = std::max(wmax, p.vcol[v + 1] - p.vcol[v]);
+          const long long sl2 = std::max<long long>(4, ((wmax + gpr - 1) / gpr + 3) / 4 * 4);
+          // resident plans: shared-memory slab and TMA box are sized for the plan's slab width
+          if (p.resident && sl2 > p.slab)
+            return fail(ctx, KPP_EINVAL, "%d emulated ranks need %lld columns per CTA (plan: %d)", vr, sl2, p.slab);
+          p.slab = (int)sl2;
+          if (!p.resident && iterate_smem_bytes(p, ctx->pC) > ctx->psmem) {
+            const int maxsm = 227 * 1024;
+            if (iterate_smem_bytes(p, ctx->pC) > (size_t)maxsm)
+              return fail(ctx, KPP_EINVAL, "%d emulated ranks: %lld columns per CTA do not fit", vr, sl2);
+          }
+          for (int r = 0; r < vr; ++r) p.peer_recv[r] = ctx->vpeer + 4LL * vr * ctx->s * r;
+          p.ll = ctx->cs_vll;
+          p.yll = ctx->cs_vll + 4LL * (gpr / ctx->pC) * ctx->s;
+          p.ll_vstride = 4LL * (gpr / ctx->pC) * ctx->s + 4LL * ctx->s;
+          CK(cudaMemsetAsync(ctx->cs_vll, 0, (size_t)vr * p.ll_vstride * sizeof(unsigned long long), st));
+          igrid = gpr * vr;
+        }
+        CK(launch_iterate(st, p, igrid, ctx->pC, std::max(ctx->psmem, iterate_smem_bytes(p, ctx->pC))));
       }
       ctx->stats.iter_launches += 1;
     } else {

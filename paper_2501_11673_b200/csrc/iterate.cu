@@ -93,7 +93,7 @@ static cudaLaunchConfig_t make_cfg(int grid, int C, size_t smem, cudaStream_t st
 static KernelFn pick_lean(const IterParams& p, int C) {
   static const bool off = getenv("KPP_NO_LEAN") != nullptr;
   int rpw = 0, cpl = 0;
-  if (off || !reg_shape(p, &rpw, &cpl)) return nullptr;
+  if (off || p.vranks > 1 || p.nranks > 1 || !reg_shape(p, &rpw, &cpl)) return nullptr;  // (no rank stage)
   return iterate_pick_lean(p, C, rpw, cpl);
 }
 

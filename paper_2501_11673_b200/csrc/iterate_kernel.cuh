@@ -53,8 +53,14 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
   const int c = (int)cluster.block_rank();
-  const int q = blockIdx.x / C;    // cluster index
-  const int NQ = gridDim.x / C;    // clusters
+  // rank of this CTA: several ranks per launch when emulated (IterParams::vranks), cluster boundaries
+  // align with them; with one rank per launch vr = 0 and gb = blockIdx.x
+  const int gpr = (int)gridDim.x / p.vranks;
+  const int vr = (int)blockIdx.x / gpr, gb = (int)blockIdx.x - vr * gpr;
+  const int rank = p.rank + vr, P = p.nranks;
+  const bool lead = vr == 0;
+  const int q = gb / C;             // cluster index within the rank
+  const int NQ = gpr / C;           // clusters per rank
   const int sl = (s + C - 1) / C;  // rank cc owns rows [cc*sl, min(s, cc*sl + sl))
   const int r0 = min(s, c * sl), r1 = min(s, r0 + sl);
   const int R = r1 - r0;
@@ -93,8 +99,11 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
   __shared__ int stop_sh;
   __shared__ long long tmod_sh;
 
-  const long long c0 = (long long)blockIdx.x * p.slab;
-  const long long c1 = (c0 + p.slab < p.n) ? c0 + p.slab : p.n;
+  const long long cr1 = p.vcol[vr + 1];
+  const long long c0 = min(p.vcol[vr] + (long long)gb * p.slab, cr1);
+  const long long c1 = (c0 + p.slab < cr1) ? c0 + p.slab : cr1;
+  unsigned long long* const llr = p.ll + (long long)vr * p.ll_vstride;  // this rank's grid exchange
+  unsigned long long* const ylr = p.yll + (long long)vr * p.ll_vstride;
   const int w = (int)(c1 > c0 ? c1 - c0 : 0);
   // TMA eligibility: 16-byte aligned row segments of a multiple of 16 bytes, aligned M slices
   const bool bulkA = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((w & 1) == 0) && ((p.sw & 1) == 0) &&
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     PHASE_MARK(2);
     TRACE(1);
 
-    unsigned long long* gll = p.ll + (long long)par * NQ * s * 2;
+    unsigned long long* gll = llr + (long long)par * NQ * s * 2;
     if (pf_tid < 0) {
       // ---- slice owner warps: cluster partial of my slice -> L2 (LL) for every cluster's owner
       if (R > 0) mbar_wait_cluster(bars + 2, it & 1u, 12);
@@ -360,8 +369,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         for (int i = pf_tid; i < s; i += pf_n) cp_async8(b1 + i, p.b + S1[i]);
         if (YG == 1 && pf_tid == 0) {
           // rows [yg0, yg1) of M(t+1) into L2 ahead of the y pass of the next iteration
-          const int yg0 = (int)((long long)blockIdx.x * s / gridDim.x);
-          const int yg1 = (int)((long long)(blockIdx.x + 1) * s / gridDim.x);
+          const int yg0 = (int)((long long)gb * s / gpr);
+          const int yg1 = (int)((long long)(gb + 1) * s / gpr);
           const double* src = p.M_pool + qb1 * ss + (long long)yg0 * s;
           const unsigned bytes = (unsigned)(yg1 - yg0) * (unsigned)s * 8u;
           if (bytes > 0 && (s & 1) == 0 && (reinterpret_cast<uintptr_t>(p.M_pool) & 15) == 0)
@@ -419,6 +428,19 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       } else {
         v = red_sm[row];
       }
+      if (P > 1) {
+        // rank stage (row 9): cluster 0 of the rank stores the rank's partial, tagged with
+        // the global t + 1, into slot [t mod 2][rank] of EVERY rank's receive buffer (peer memory over
+        // NVLink; device memory when emulated); every cluster sums the P partials in rank order
+        const long long pslot = (t & 1) * (long long)P * s;
+        const unsigned ptag = (unsigned)(t + 1);
+        if (q == 0)
+          for (int rr = 0; rr < P; ++rr) ll_store_sys(p.peer_recv[rr] + 2 * (pslot + (long long)rank * s + r0 + row), v, ptag);
+        double tot = 0.0;
+        for (int rr = 0; rr < P; ++rr)
+          tot += ll_wait_sys(p.peer_recv[rank] + 2 * (pslot + (long long)rr * s + r0 + row), ptag, p.err);
+        v = tot;
+      }
       v -= bSc[r0 + row];
       if constexpr (yred) r_sm[r0 + row] = v;
       else for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_r, cc));
@@ -436,7 +458,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       e = warp_sum(e);
       if (lane == 0) {
         const int res = window_step_dev(st, tmod, e, p.zeta, p.tol2bb, p.bb, p.adaptive,
-                                        blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
+                                        gb == 0 && lead && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
         if (res) {
           st.stopped = res;
           stop_sh = 1;
@@ -476,8 +498,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     } else if constexpr (YG == 1) {
       // ---- row 4, large blocks: y rows [yg0, yg1) of this CTA (every M element read once per
       //      iteration on the whole GPU), published to L2 as LL words; all CTAs gather y below
-      const int yg0 = (int)((long long)blockIdx.x * s / gridDim.x);
-      const int yg1 = (int)((long long)(blockIdx.x + 1) * s / gridDim.x);
+      const int yg0 = (int)((long long)gb * s / gpr);
+      const int yg1 = (int)((long long)(gb + 1) * s / gpr);
       if (warp < NW2 - 1) {
         const double* Mb = p.M_pool + (long long)p.bid[t - p.t0] * ss;
         for (int k = yg0 + warp; k < yg1; k += NW2 - 1) {
@@ -486,7 +508,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
 #pragma unroll 4
           for (int l = lane; l < s; l += 32) v = fma(__ldg(Mrow + l), r_sm[l], v);
           v = warp_sum(v);
-          if (lane == 0) ll_store_global(p.yll + ((long long)par * s + k) * 2, v, tag);
+          if (lane == 0) ll_store_global(ylr + ((long long)par * s + k) * 2, v, tag);
         }
       }
     } else {
@@ -542,7 +564,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     }
     PHASE_MARK(13);  // y slice computed and sent
     if constexpr (YG == 1) {
-      for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_global(p.yll + ((long long)par * s + l) * 2, tag, p.err);
+      for (int l = tid; l < s; l += T2) y_sm[l] = ll_wait_global(ylr + ((long long)par * s + l) * 2, tag, p.err);
       __syncthreads();
     } else if constexpr (YG == 0) {
       mbar_wait_cluster(bars + 4, it & 1u, 14);  // y complete
@@ -557,7 +579,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         double e = 0.0;
         for (int cc = 0; cc < C; ++cc) e += yp_sm[cc * (s + 1) + s];
         const int res = window_step_dev(st, tmod_prev, e, p.zeta, p.tol2bb, p.bb, p.adaptive,
-                                        blockIdx.x == 0 && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
+                                        gb == 0 && lead && p.writer, p.hist_res, p.hist_rho, p.hist_cap);
         if (res) {
           st.stopped = res;
           stop_sh = 1;
@@ -692,7 +714,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
     p.x[c0 + j] = x_sm[j];
     p.mom[c0 + j] = m_sm[j];
   }
-  if (blockIdx.x == 0 && tid == 0) {
+  if (gb == 0 && lead && tid == 0) {
     st.t_done = t;
     *p.st = st;
   }

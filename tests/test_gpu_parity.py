@@ -825,3 +825,54 @@ def test_cdpp_stream_dist_context(kpp, ora):
     assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
     assert torch.equal(ctx.solve(b.to(DEV), max_iters=200).x, res.x)
     ctx.destroy()
+
+
+PK_TWINS = VR_TWINS + [synth.twin("c2", 2048, 2048, 128, k=64)]
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("cfg", PK_TWINS, ids=[c.name for c in PK_TWINS])
+def test_persistent_rank_stage(kpp, ora, cfg, P):
+    """The rank stage of the column-sharded exchange inside the persistent cluster kernel (engine 0:
+    TMA slabs, DSMEM cluster reduction, L2 exchange, then the P rank partials through every rank's
+    receive buffer, rank-order sums), P ranks emulated in one cooperative launch; the c2-shaped twin
+    leaves its one-GPU lean plan for the generic kernel.  Against the oracle (200 iterations at the BJ
+    bar, checkpoint history, tolerance stop from x0, bit-identical repeat)."""
+    A, b, _ = synth.make_problem(cfg)
+    run = ora.cdpp_run if cfg.kind == "cdpp" else ora.kpp_run
+    ctx = (kpp.cdpp_setup if cfg.kind == "cdpp" else kpp.kpp_setup)(A.to(DEV), cfg.s, cfg.lam, 0)
+    ctx.set_option(kpp.OPT_ENGINE, 0)
+    if cfg.kind == "cdpp":
+        ctx.set_option(kpp.OPT_REASSOC, 0)  # the generic kernel (the streaming one has its own test)
+    ctx.set_option(kpp.OPT_VRANKS, P)
+    ctx.set_option(kpp.OPT_WINDOW, 64)
+    T = 200
+    ref = run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=T, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=T)
+    assert ctx.stats()["engine"] == 0
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    x1 = res.x.clone()
+    assert torch.equal(ctx.solve(b.to(DEV), max_iters=T).x, x1)
+    x0 = np.random.default_rng(3).standard_normal(A.shape[1])
+    ref2 = run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=3000, tol=0.05, x0=x0, threads=8)
+    res2 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=3000, tol=0.05)
+    assert res2.iters == ref2.iters
+    assert rel(res2.x.cpu().numpy(), ref2.x) <= 1e-10
+
+
+def test_persistent_dist_context(kpp, ora):
+    """kpp_setup_dist at one rank (self-mapped receive buffer): the automatic engine of a column-sharded
+    K++ context whose plan is the generic kernel is the persistent kernel with its rank stage."""
+    cfg = synth.twin("c3", 8192, 512, 256)
+    A, b, _ = synth.make_problem(cfg)
+    n = A.shape[1]
+    ctx = kpp.kpp_setup_dist(A.to(DEV), A.shape[0], n, 0, n, cfg.s, cfg.lam, 0, kpp.kpp_get_unique_id(), 0, 1)
+    ctx.set_option(kpp.OPT_WINDOW, 64)
+    ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=200, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=200)
+    st = ctx.stats()
+    assert st["engine"] == 0 and st["xchg"] == 1
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert torch.equal(ctx.solve(b.to(DEV), max_iters=200).x, res.x)
+    ctx.destroy()
