@@ -388,24 +388,13 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
         ll_store_global(gll + ((long long)q * s + r0 + row) * 2, v, tag);
       }
       // gather my slice from every cluster (batches of 8 in flight), fixed-order sum
-      const long long pslot = (t & 1) * (long long)P * s;
-      const unsigned ptag = (unsigned)(t + 1);  // global iteration: the receive buffers persist over windows
       for (int row = ct; row < R; row += NCH) {
         double v = 0.0;
         for (int q0 = 0; q0 < NQ; q0 += 8)
           v += ll_gather_sum<8, 500>(gll + (long long)(r0 + row) * 2, (long long)s * 2, q0, 1, NQ, tag, p.err);
-        if (P > 1) {
-          // rank stage (row 9): cluster 0 of the rank stores the rank's partial into slot [t mod 2][rank]
-          // of EVERY rank's receive buffer (peer memory over NVLink; device memory when emulated),
-          // then every cluster sums the P partials in rank order: the same bits on every rank
-          if (q == 0)
-            for (int rr = 0; rr < P; ++rr)
-              ll_store_sys(p.peer_recv[rr] + 2 * (pslot + (long long)rank * s + r0 + row), v, ptag);
-          double tot = 0.0;
-          for (int rr = 0; rr < P; ++rr)
-            tot += ll_wait_sys(p.peer_recv[rank] + 2 * (pslot + (long long)rr * s + r0 + row), ptag, p.err);
-          v = tot;
-        }
+        // rank stage (row 9): the P ranks' partials of the row, summed in rank order (the dense pass of
+        // t+1 streams on the other warps meanwhile)
+        if (P > 1) v = rank_stage_sum(v, q == 0, p.peer_recv, rank, P, s, r0 + row, t, p.err);
         v -= bSc[r0 + row];
         for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_r, cc));
       }

@@ -428,19 +428,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       } else {
         v = red_sm[row];
       }
-      if (P > 1) {
-        // rank stage (row 9): cluster 0 of the rank stores the rank's partial, tagged with
-        // the global t + 1, into slot [t mod 2][rank] of EVERY rank's receive buffer (peer memory over
-        // NVLink; device memory when emulated); every cluster sums the P partials in rank order
-        const long long pslot = (t & 1) * (long long)P * s;
-        const unsigned ptag = (unsigned)(t + 1);
-        if (q == 0)
-          for (int rr = 0; rr < P; ++rr) ll_store_sys(p.peer_recv[rr] + 2 * (pslot + (long long)rank * s + r0 + row), v, ptag);
-        double tot = 0.0;
-        for (int rr = 0; rr < P; ++rr)
-          tot += ll_wait_sys(p.peer_recv[rank] + 2 * (pslot + (long long)rr * s + r0 + row), ptag, p.err);
-        v = tot;
-      }
+      // rank stage (row 9): the P ranks' partials of the row, summed in rank order
+      if (P > 1) v = rank_stage_sum(v, q == 0, p.peer_recv, rank, P, s, r0 + row, t, p.err);
       v -= bSc[r0 + row];
       if constexpr (yred) r_sm[r0 + row] = v;
       else for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + row) * 8u, cc), v, mapa_u32(lb_r, cc));

@@ -47,7 +47,7 @@ struct LeanLayout {
   int sp, sl, s4, red, mslz;
   size_t o_rp, o_x, o_m, o_r, o_y, o_red, o_bS, o_S, o_A, o_M, bytes;
 };
-__host__ __device__ inline LeanLayout lean_layout(int s, int slab, int sw, int C) {
+__host__ __device__ inline LeanLayout lean_layout(int s, int slab, int sw, int C, bool m1 = false) {
   LeanLayout L{};
   L.sp = (s + 1) & ~1;
   L.sl = (s + C - 1) / C;
@@ -67,14 +67,16 @@ __host__ __device__ inline LeanLayout lean_layout(int s, int slab, int sw, int C
   L.o_S = o; o += 3 * (size_t)L.sp * 4;
   o = (o + 127) & ~(size_t)127;  // TMA destinations: 128-byte aligned
   L.o_A = o; o += (size_t)L.s4 * sw * 8;
-  L.o_M = o; o += 2 * (size_t)L.mslz * 8;
+  L.o_M = o; o += (m1 ? 1 : 2) * (size_t)L.mslz * 8;  // M rows: double-buffered, or one buffer (m1)
   L.bytes = o;
   return L;
 }
 
 // RPW: rows per warp of the register tile (warp wi holds rows wi + 16 i), CPL: columns per lane
 // (lane l holds columns l + 32 c).  PROF: globaltimer stamps (p.trace) compiled in.
-template <int RPW, int CPL, bool PROF>
+// M1: one M-row buffer (slices of 64 rows x s = 256: 128 KB); block t+1's rows are requested once y(t)
+// is complete and land on their own barrier (bars[5]).  Slices of up to 64 rows: two owner warps.
+template <int RPW, int CPL, bool PROF, bool M1>
 __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_constant__ IterParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int s = p.s;
@@ -84,10 +86,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   const int c = (int)cluster.block_rank();
   const int q = blockIdx.x / C;
   const int NQ = gridDim.x / C;
-  const LeanLayout L = lean_layout(s, p.slab, p.sw, C);
+  const LeanLayout L = lean_layout(s, p.slab, p.sw, C, M1);
   const int sl = L.sl, sp = L.sp;
   const int r0 = min(s, c * sl), r1 = min(s, r0 + sl);
-  const int R = r1 - r0;  // rows of the slice this CTA owns (<= 32)
+  const int R = r1 - r0;  // rows of the slice this CTA owns (<= 64)
   // PROF: cycle counters of thread 0 of CTA 0 per stage (p.prof[16]), printed by the host
   const bool lprof = PROF && p.prof != nullptr && blockIdx.x == 0 && tid == 0;
   long long lacc[14] = {};
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   double* bS_sh = reinterpret_cast<double*>(smem_raw + L.o_bS);    // [3][sp] b_S of t, t+1, t+2
   int32_t* S_sh = reinterpret_cast<int32_t*>(smem_raw + L.o_S);    // [3][sp]
   double* Abuf = reinterpret_cast<double*>(smem_raw + L.o_A);      // [s4][sw] slab of the next block
-  double* Mbuf = reinterpret_cast<double*>(smem_raw + L.o_M);      // [2][sl][s] my rows of M
+  double* Mbuf = reinterpret_cast<double*>(smem_raw + L.o_M);      // [M1 ? 1 : 2][sl][s] my rows of M
   __shared__ DevState st;
   __shared__ int stop_sh;
 
@@ -165,7 +167,8 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   // pollers per row of my slice: warps 0..14 only -- the last warp issues block t+1's copies (a
   // warp issuing 32 serialised TMA gathers must not hold up a polling group) and runs row 8
   const int G2 = R > 0 ? min(15, (T2 - 32) / R) : 1;
-  const int ngy = min(NW2 - 1, (R + 3) >> 2);   // warps computing y (4 rows each)
+  const int ngroups = (R + 3) >> 2;              // groups of 4 rows of y, over warps 0..14
+  const int nown = (R + 31) >> 5;                // owner warps (<= 2)
   long long t = p.t0;
   unsigned it = 0, ph0 = 0;
   for (; t < p.t1; ++t, ++it) {
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     const unsigned tag = it + 1;
     const int32_t* Sc = S_sh + (it % 3) * sp;
     const double* bSc = bS_sh + (it % 3) * sp;
-    const double* Msl = Mbuf + buf * L.mslz;
+    const double* Msl = Mbuf + (M1 ? 0 : buf * L.mslz);
     const bool pf = t + 1 < p.t1;
     (void)Sc;
     // ---- top: slab + M rows of block t have landed; register tile of the slab
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     }
     cp_async_wait_all();  // this thread's b_S(t) / S(t+1) copies
     if (tid == 0) {
-      if (pf) mbar_expect_tx(bars + 0, slab_bytes + m_bytes);  // (0 bytes: the arrive completes the phase)
+      if (pf) mbar_expect_tx(bars + 0, slab_bytes + (M1 ? 0u : m_bytes));  // (0 bytes: the arrive completes the phase)
       if (R > 0) mbar_expect_tx(bars + 2, (unsigned)(C * R) * 8u);
       mbar_expect_tx(bars + 3, (unsigned)s * 8u);
       mbar_expect_tx(bars + 4, (unsigned)s * 8u);
@@ -232,21 +235,22 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     LM(2);
 
     unsigned long long* gll = p.ll + (long long)(it & 1) * NQ * s * 2;
-    if (warp == 0) {
-      // ---- owner warp: cluster partial of my slice -> L2 (LL words) for every cluster
+    if (warp < nown) {
+      // ---- owner warps: cluster partial of my slice -> L2 (LL words) for every cluster
       if (R > 0) lwait(bars + 2, it & 1u, 12);
       if constexpr (PROF) TRACE(2);
       LM(3);
-      if (lane < R) {
+      const int row = warp * 32 + lane;
+      if (row < R) {
         double v = 0.0;
-        for (int cc = 0; cc < C; ++cc) v += rp_sm[cc * sl + lane];
-        ll_store_global(gll + ((long long)q * s + r0 + lane) * 2, v, tag);
+        for (int cc = 0; cc < C; ++cc) v += rp_sm[cc * sl + row];
+        ll_store_global(gll + ((long long)q * s + r0 + row) * 2, v, tag);
       }
     } else if (warp == NW2 - 1) {
       // ---- the last warp requests block t+1 behind this iteration (M rows first: one bulk copy)
       if (pf) {
         const int32_t* S1 = S_sh + ((it + 1) % 3) * sp;
-        if (lane == 0 && R > 0 && !no_m) {
+        if (!M1 && lane == 0 && R > 0 && !no_m) {
           fence_proxy_async();
           bulk_g2s(Mbuf + (buf ^ 1) * L.mslz, p.M_pool + qb1 * ss + (long long)r0 * s, m_bytes, bars + 0);
         }
@@ -332,9 +336,11 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
       }
     }
     tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
-    // ---- row 4: my slice of y = M r (4 rows per warp from the staged M rows), to every CTA
-    if (warp < ngy) {
-      const int rb = warp * 4;
+    // ---- row 4: my slice of y = M r (groups of 4 rows over warps 0..14 from the staged M rows), to
+    //      every CTA (M1: the rows of block t were requested after y(t-1), on bars[5])
+    if (M1 && it > 0 && warp < min(NW2 - 1, ngroups)) lwait(bars + 5, (it - 1) & 1u, 15);
+    for (int gi = warp; gi < ngroups && warp < NW2 - 1; gi += NW2 - 1) {
+      const int rb = gi * 4;
       double v[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int jc = 0; jc < (RPW + 1) / 2; ++jc) {  // s <= 16 RPW: at most RPW / 2 column chunks
@@ -354,6 +360,14 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     LM(9);
     lwait(bars + 4, it & 1u, 14);
     LM(10);
+    if (M1 && pf && tid == 0 && R > 0 && !no_m) {
+      // every reader of the M rows of t has sent its y rows (they all arrived): block t+1's rows
+      fence_proxy_async();
+      mbar_expect_tx(bars + 5, m_bytes);
+      bulk_g2s(Mbuf, p.M_pool + qb1 * ss + (long long)r0 * s, m_bytes, bars + 5);
+    } else if (M1 && pf && tid == 0) {
+      mbar_arrive(bars + 5);
+    }
     if constexpr (PROF) TRACE(6);
 
     // ---- rows 5-6: w = A_S^T y from the register tile, fixed-order sum over warps, momentum, x
@@ -393,7 +407,10 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     }
   }
   // an early stop leaves block t's slab / M rows in flight: they must land before exit
-  if (t < p.t1) lwait(bars + 0, ph0, 30);
+  if (t < p.t1) {
+    lwait(bars + 0, ph0, 30);
+    if (M1) lwait(bars + 5, (it & 1u), 35);  // the M rows requested after y of the last iteration run
+  }
   cp_async_wait_all();
   __syncthreads();
   for (int j = tid; j < w; j += T2) {
@@ -416,22 +433,34 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
 
 using KernelFn = void (*)(const IterParams);
 
-// The lean kernel serves K++ plans with the slab in a register tile, TMA gather4, M rows
-// double-buffered in shared memory, y per cluster (ygl 0), clusters of at most 8 and slices of at
-// most 32 rows; nullptr otherwise.
+// M rows double-buffered when they fit in shared memory, else one buffer
+static bool lean_m1(const IterParams& p, int C) {
+  return itk::lean_layout(p.s, p.slab, p.sw, C, false).bytes + 128 > 227 * 1024;
+}
+
+// The lean kernel serves K++ plans with the slab in a register tile, TMA gather4, the M rows staged
+// in shared memory (its y is computed per cluster whatever the plan's y placement), clusters of at
+// most 8 and slices of at most 64 rows; nullptr otherwise.
 KernelFn iterate_pick_lean(const IterParams& p, int C, int rpw, int cpl) {
-  if (p.cd || !p.resident || !p.a_single || !p.tma || p.ygl != 0 || p.m_in_smem != 1 || C > 8) return nullptr;
-  if ((p.s + C - 1) / C > 32 || (p.s & 1)) return nullptr;
+  if (p.cd || !p.resident || !p.a_single || !p.tma || (p.ygl != 0 && p.ygl != 4) || p.m_in_smem == 0 || C > 8)
+    return nullptr;
+  if ((p.s + C - 1) / C > 64 || (p.s & 1)) return nullptr;
+  if (itk::lean_layout(p.s, p.slab, p.sw, C, true).bytes + 128 > 227 * 1024) return nullptr;
+  static const int sl64 = getenv("KPP_LEAN64") ? atoi(getenv("KPP_LEAN64")) : 1;  // 0: slices <= 32 only
+  if (!sl64 && (p.s + C - 1) / C > 32) return nullptr;
   const bool prof = p.trace != nullptr || p.prof != nullptr;
-#define K(R, CP) \
-  if (rpw == R && cpl == CP) return prof ? itk::iterate_lean_kernel<R, CP, true> : itk::iterate_lean_kernel<R, CP, false>;
+  const bool m1 = lean_m1(p, C);
+#define K(R, CP)                                                                                       \
+  if (rpw == R && cpl == CP)                                                                           \
+    return prof ? (m1 ? itk::iterate_lean_kernel<R, CP, true, true> : itk::iterate_lean_kernel<R, CP, true, false>) \
+                : (m1 ? itk::iterate_lean_kernel<R, CP, false, true> : itk::iterate_lean_kernel<R, CP, false, false>);
   K(2, 1) K(4, 1) K(8, 1) K(16, 1) K(2, 2) K(4, 2) K(8, 2) K(16, 2)
 #undef K
   return nullptr;
 }
 
 size_t iterate_lean_smem_bytes(const IterParams& p, int C) {
-  return itk::lean_layout(p.s, p.slab, p.sw, C).bytes + 128;
+  return itk::lean_layout(p.s, p.slab, p.sw, C, lean_m1(p, C)).bytes + 128;
 }
 
 }  // namespace kpp

@@ -122,6 +122,22 @@ __device__ __forceinline__ double ll_wait_sys(const unsigned long long* src, uns
   return __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
 }
 
+// Rank stage of the column-sharded exchange: cluster 0 of each rank (publish)
+// stores the rank's partial v of s-vector row `row`, tagged with the global iteration t + 1, into
+// slot [t mod 2][rank] of EVERY rank's receive buffer ([2][P][s] LL words, peer memory over NVLink or
+// device memory when emulated); then the P partials of the row are summed in rank order (the same
+// bits on every rank).  Out of line: single-GPU runs never call it and keep their loop bodies small.
+static __device__ __noinline__ double rank_stage_sum(double v, bool publish, unsigned long long* const* recv, int rank,
+                                                     int P, int s, int row, long long t, int* err) {
+  const long long pslot = (t & 1) * (long long)P * s;
+  const unsigned ptag = (unsigned)(t + 1);
+  if (publish)
+    for (int rr = 0; rr < P; ++rr) ll_store_sys(recv[rr] + 2 * (pslot + (long long)rank * s + row), v, ptag);
+  double tot = 0.0;
+  for (int rr = 0; rr < P; ++rr) tot += ll_wait_sys(recv[rank] + 2 * (pslot + (long long)rr * s + row), ptag, err);
+  return tot;
+}
+
 // ------------------------------------------------------------------ TMA bulk copies + mbarriers
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -129,6 +145,9 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 }
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try(unsigned long long* bar, unsigned parity) {
   unsigned ok;

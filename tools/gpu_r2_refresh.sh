@@ -1,7 +1,8 @@
 # Round-2 refresh under gpurun: every GPU test, smoke, bench lines, the c2 launch list and full captures of
 # the Phase-2 kernels (each ncu command preceded by the same command run plain, with &&).
 mkdir -p gpurun_out/r2f
-O=gpurun_out/r2f
+O=${O:-gpurun_out/r2f}
+mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
 timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
