@@ -863,7 +863,8 @@ def test_persistent_rank_stage(kpp, ora, cfg, P):
 
 def test_persistent_dist_context(kpp, ora):
     """kpp_setup_dist at one rank (self-mapped receive buffer): the automatic engine of a column-sharded
-    K++ context whose plan is the generic kernel is the persistent kernel with its rank stage."""
+    K++ context is the persistent kernel with its rank stage (the generic kernel: a one-GPU context of
+    this shape would run the lean one)."""
     cfg = synth.twin("c3", 8192, 512, 256)
     A, b, _ = synth.make_problem(cfg)
     n = A.shape[1]
