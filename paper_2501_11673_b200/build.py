@@ -13,7 +13,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libkpp.so")
+# A/B experiments: KPP_LIB names another library file, KPP_NVCC_FLAGS adds compiler flags (objects go
+# to a directory of their own); the product build uses neither
+LIB = os.environ.get("KPP_LIB") or os.path.join(HERE, "libkpp.so")
+EXTRA = os.environ.get("KPP_NVCC_FLAGS", "").split()
+OBJDIR = os.path.join(HERE, "build" if not os.environ.get("KPP_LIB") else "build_" + os.path.basename(LIB).replace(".so", ""))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -52,8 +56,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     # then find the library up to date; the library is linked to a temporary name and renamed, so a
     # concurrent loader never sees a partial file
     import fcntl
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
-    with open(os.path.join(HERE, "build", ".lock"), "w") as lk:
+    os.makedirs(OBJDIR, exist_ok=True)
+    with open(os.path.join(OBJDIR, ".lock"), "w") as lk:
         fcntl.flock(lk, fcntl.LOCK_EX)
         if not force and up_to_date():
             return LIB
@@ -63,13 +67,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
 def _build_locked(verbose: bool) -> str:
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    objdir = os.path.join(HERE, "build")
+    objdir = OBJDIR
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        cmd = [nvcc, *ARCH, *EXTRA, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3", "-I", inc, "-I", os.path.join(ROOT, "include"),
                "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
