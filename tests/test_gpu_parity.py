@@ -877,3 +877,30 @@ def test_persistent_dist_context(kpp, ora):
     assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
     assert torch.equal(ctx.solve(b.to(DEV), max_iters=200).x, res.x)
     ctx.destroy()
+
+
+LEAN_CASES = [synth.twin("c3", 8192, 512, 256), synth.twin("c3", 6000, 1000, 200, k=16),
+              synth.twin("c3", 4096, 300, 126, k=8), synth.twin("c2", 700, 700, 32, k=8)]
+
+
+@pytest.mark.parametrize("cfg", LEAN_CASES, ids=[c.name for c in LEAN_CASES])
+def test_lean_kernel_shapes(kpp, ora, cfg):
+    """The lean register-tile kernel at its shape limits -- slices of 64 rows with one M-row buffer
+    (s = 256, 200), ragged s and n, short windows (several launches), the tolerance stop from x0 (the
+    early-exit drain of the in-flight slab / M-row copies) -- against the oracle at the BJ bar, and a
+    repeated solve bit-identical."""
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), cfg.s, cfg.lam, 0)
+    ctx.set_option(kpp.OPT_WINDOW, 96)
+    ref = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=200, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=200)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    x0 = np.random.default_rng(7).standard_normal(A.shape[1])
+    ref2 = ora.kpp_run(A.numpy(), b.numpy(), cfg.s, lam=cfg.lam, seed=0, max_iters=5000, tol=0.02, x0=x0, threads=8)
+    res2 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=5000, tol=0.02)
+    assert res2.iters == ref2.iters and res2.status == ref2.status
+    assert rel(res2.x.cpu().numpy(), ref2.x) <= 1e-10
+    # the same solve again: the drained copies left no stale phase behind
+    res3 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=5000, tol=0.02)
+    assert torch.equal(res3.x, res2.x)
