@@ -904,3 +904,16 @@ def test_lean_kernel_shapes(kpp, ora, cfg):
     # the same solve again: the drained copies left no stale phase behind
     res3 = ctx.solve(b.to(DEV), torch.from_numpy(x0).to(DEV), max_iters=5000, tol=0.02)
     assert torch.equal(res3.x, res2.x)
+
+
+@pytest.mark.parametrize("s", [2, 4, 6, 30, 66])
+def test_lean_kernel_small_slices(kpp, ora, s):
+    """The lean kernel with slices of 0-1 rows on some CTAs of a cluster (s < cluster size x ...),
+    slices that do not fill a warp and ones just above 32 / 64 rows per cluster: against the oracle."""
+    cfg = synth.twin("c2", 600, 600, s, k=8)
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), s, cfg.lam, 1)
+    ref = ora.kpp_run(A.numpy(), b.numpy(), s, lam=cfg.lam, seed=1, max_iters=150, threads=8)
+    res = ctx.solve(b.to(DEV), max_iters=150)
+    assert rel(res.x.cpu().numpy(), ref.x) <= 1e-10
+    assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
