@@ -274,6 +274,8 @@ def measure_secondary(name, steps, warmup, dev, hbm_peak):
            "roofline": {"bound": "hbm", "kernel": "Phase-2 persistent kernel, warm (iterate_kernel / cdpp_stream_kernel)",
                         "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak if ach else None,
                         "bytes_per_iter": bpi, "traffic": tr * iters if tr else None,
+                        "frac_of_nominal_8tbs": ach / 8000.0 if ach else None,
+                        "dram_gbs_ncu": tr / (warm["phase2_ms"] / iters / 1e3) / 1e9 if (tr and warm["phase2_ms"] > 0) else None,
                         "traffic_note": "ncu dram read+write bytes per iteration (profiles/ncu_summary.json) x iterations per launch"},
            "time_to_tol": {"seconds": e0.elapsed_time(e1) / 1e3, "iters": r.iters, "converged": r.status == kpp.OK,
                            "est_rel_res": float(r.res_hist[-1]) if len(r.res_hist) else None,
@@ -473,7 +475,10 @@ def main():
             "traffic_note": "ncu dram read+write bytes per launch (per-iteration bytes from profiles/ncu_summary.json x iterations per launch)",
             "algorithmic_bytes_per_launch": bpi * iters_per_launch, "iters_per_launch": iters_per_launch,
             "peak_source": peak_note, "bytes_per_iter": bpi,
-            "iter_kernel_share": p2max / ms if ms > 0 else None}
+            "iter_kernel_share": p2max / ms if ms > 0 else None,
+            # both HBM numbers, against the nominal 8 TB/s as well as the measured copy
+            "frac_of_nominal_8tbs": (achieved / 8000.0) if achieved else None,
+            "dram_gbs_ncu": (tr * total_iters / (p2max / 1e3) / 1e9) if (tr and p2max > 0) else None}
     cpu = None
     if not args.no_cpu and not dist:
         cpu = cpu_oracle_sample(cfg, A_keep.cpu().numpy(), b.cpu().numpy(), args.cpu_seconds, iters, args.proj,
