@@ -79,6 +79,8 @@ class ClockSampler:
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.raw = []
+        self.t_enter = 0.0
 
     def __enter__(self):
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -90,21 +92,32 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            # nvidia-smi's start-up (driver initialisation) must not overlap the timed region: it
+            # held up the host thread of short steps (c1: 15 ms regions).  Wait for its first sample.
+            t_end = time.monotonic() + 5.0
+            while not self.raw and time.monotonic() < t_end:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.t_enter = time.monotonic()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.raw.append((time.monotonic(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc:
+            # a region shorter than the 200 ms period: keep the first sample after it
+            t_end = time.monotonic() + 0.5
+            while not any(t >= self.t_enter for t, _ in self.raw) and time.monotonic() < t_end:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+        self.lines = [l for t, l in self.raw if t >= self.t_enter]
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
