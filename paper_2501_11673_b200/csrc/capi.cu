@@ -448,7 +448,7 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   } else {
     // G1 = A_S A_S^T (+ lam I): NT GEMM with row gathers on both operands, split-K
     Operand a{ctx->A, ctx->lda, 0, S, s, 0}, b{ctx->A, ctx->lda, 0, S, s, 1};
-    int z1 = launch_gram_syrk(st, B, s, (int)n, ctx->A, ctx->lda, 0, S, s, part, ss, Z);
+    int z1 = launch_gram_syrk(st, B, s, (int)n, ctx->A, ctx->lda, 0, ctx->m, S, s, part, ss, Z);
     if (!z1) z1 = launch_dgemm(st, B, s, s, (int)n, a, b, part, s, ss, Z, 1);
     pp.mark("gram1");
     const bool dist = ctx->nranks > 1;
@@ -523,7 +523,7 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
         launch_dgemm(st, Bn, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);  // Q1 = X1^T A_S (X1^T lower)
         pp.mark("Q1");
         Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
-        int z2 = launch_gram_syrk(st, Bn, s, (int)n, Q, n, (long long)s * n, nullptr, 0, part, ss, Z);
+        int z2 = launch_gram_syrk(st, Bn, s, (int)n, Q, n, (long long)s * n, 0, nullptr, 0, part, ss, Z);
         if (!z2) z2 = launch_dgemm(st, Bn, s, s, (int)n, qa, qb, part, s, ss, Z, 1);
         pp.mark("gram2");
         Operand x1n{X1b, s, ss, nullptr, 0, 0};

@@ -570,7 +570,8 @@ int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand&
 // part[(b Z + z) s^2 ...] as launch_dgemm writes it (upper triangle), Z K-chunks of 16-multiples.
 // Returns Z, or 0 when the shape is not served (s > 256 or unaligned rows).
 int launch_gram_syrk(cudaStream_t st, int batch, int s, int K, const double* base, long long ld, long long bstride,
-                     const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z) {
+                     long long nrows, const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z) {
+  if (int zt = launch_gram_tma(st, batch, s, K, base, ld, bstride, nrows, idx, idx_bstride, part, ss, Z)) return zt;
   static const bool off = getenv("KPP_GRAM_SYRK") && atoi(getenv("KPP_GRAM_SYRK")) == 0;
   // measured (B200, Phase 1 ms per bench step, balanced kernel vs the tile kernel): c2 (s = 128) 14.01 vs
   // 14.30; with two warps per pair for s = 256 it loses (c3 37.2 vs 32.1, c4 521 vs 441): s <= 128 only

@@ -93,7 +93,9 @@ int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand&
 // Balanced Gram kernel (upper triangle of rows x rows^T per K chunk, s <= 256); returns Z, or 0 if
 // the shape is not served (then use launch_dgemm)
 int launch_gram_syrk(cudaStream_t st, int batch, int s, int K, const double* base, long long ld, long long bstride,
-                     const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
+                     long long nrows, const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
+int launch_gram_tma(cudaStream_t st, int batch, int s, int K, const double* base, long long ld, long long bstride,
+                    long long nrows, const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
 void launch_splitk_reduce(cudaStream_t st, int batch, int M, int N, int Z, const double* part,
                           long long p_bstride, double diag_add, const double* add,
                           double add_scale, long long add_bstride, double* out,

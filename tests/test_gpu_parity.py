@@ -117,12 +117,14 @@ def test_factor_operator(kpp, ora, factor):
         assert np.allclose(M, M.T, rtol=0, atol=1e-12 * np.abs(M).max())
 
 
-@pytest.mark.parametrize("s", [31, 33, 64, 65, 100, 129, 200])
+@pytest.mark.parametrize("s", [31, 33, 64, 65, 96, 100, 128, 129, 200, 256])
 @pytest.mark.parametrize("factor", [1, 2])
 def test_factor_operator_ragged(kpp, ora, s, factor):
     """The Gram products' tile edges: 64-row upper-only tiles, the diagonal warp tiles whose
     fragments below the diagonal are skipped, and a split-K whose last 4096-column chunk is ragged
-    (n = 4100). M against the oracle's Householder factor, same bound as above."""
+    (n = 4100: the TMA Gram's last stage is 12 columns past n, zero-filled). s = 96 .. 256 run the
+    TMA-ring Gram (one CTA per block and chunk up to s = 128, two above; rows past s ragged at 100,
+    129, 200). M against the oracle's Householder factor, same bound as above."""
     m, n, lam = 300, 4100, 1e-8
     cfg = synth.twin("c3", m, n, s, k=8)
     A, b, _ = synth.make_problem(cfg)
