@@ -118,6 +118,11 @@ struct kpp_ctx {
   // phase-1 workspace
   Buf p1;
   Buf p1q;  // Q1 of the refined sub-batch (adaptive CholeskyQR2), sized on demand
+  // int8 digit planes of A for the tensor-core Gram (gram_i8.cu), rebuilt with every memo-cache
+  // generation (kpp_clear_cache, kpp_enable_rht invalidate them)
+  int8_t* oz_planes = nullptr;
+  int* oz_erow = nullptr;
+  int oz_valid = 0;
   int* d_info = nullptr;
   long long info_cap = 0;
   // graph engine
@@ -448,7 +453,28 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
   } else {
     // G1 = A_S A_S^T (+ lam I): NT GEMM with row gathers on both operands, split-K
     Operand a{ctx->A, ctx->lda, 0, S, s, 0}, b{ctx->A, ctx->lda, 0, S, s, 1};
-    int z1 = launch_gram_syrk(st, B, s, (int)n, ctx->A, ctx->lda, 0, ctx->m, S, s, part, ss, Z);
+    int z1 = 0;
+    if (gram_i8_enabled(s)) {
+      if (!ctx->oz_valid) {
+        // the int8 digit planes of A (7/8 of A's bytes): built once per cache generation
+        if (!ctx->oz_planes) {
+          const size_t pb = (size_t)7 * ctx->m * ozaki_npad(n);
+          if (cudaMalloc((void**)&ctx->oz_planes, pb) != cudaSuccess ||
+              cudaMalloc((void**)&ctx->oz_erow, (size_t)ctx->m * sizeof(int)) != cudaSuccess) {
+            cudaGetLastError();  // no room: the fp64 DMMA Gram below
+            if (ctx->oz_planes) cudaFree(ctx->oz_planes);
+            ctx->oz_planes = nullptr;
+          }
+        }
+        if (ctx->oz_planes) {
+          launch_ozaki_planes(st, ctx->A, ctx->m, n, ctx->lda, ctx->oz_planes, ctx->oz_erow);
+          ctx->oz_valid = 1;
+        }
+        pp.mark("planes");
+      }
+      if (ctx->oz_valid) z1 = launch_gram_i8(st, B, s, (int)n, ctx->oz_planes, ctx->m, ctx->oz_erow, S, s, part, ss, Z);
+    }
+    if (!z1) z1 = launch_gram_syrk(st, B, s, (int)n, ctx->A, ctx->lda, 0, ctx->m, S, s, part, ss, Z);
     if (!z1) z1 = launch_dgemm(st, B, s, s, (int)n, a, b, part, s, ss, Z, 1);
     pp.mark("gram1");
     const bool dist = ctx->nranks > 1;
@@ -1460,7 +1486,7 @@ void kpp_destroy(kpp_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   void* ptrs[] = {ctx->srht_d, ctx->srht_T, ctx->lsqr_buf, ctx->lsqr_ll, ctx->rht_A, ctx->rht_d, ctx->rht_v, ctx->d_prof, ctx->d_ll, ctx->d_err, ctx->S_pool, ctx->M_pool, ctx->word1, ctx->fresh, ctx->bid, ctx->dstate, ctx->dstep,
                   ctx->d_nb, ctx->x, ctx->mom, ctx->part, ctx->r, ctx->y, ctx->d_bb, ctx->bstage,
-                  ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->p1q.p, ctx->d_info};
+                  ctx->bar, ctx->hist_res, ctx->hist_rho, ctx->p1.p, ctx->p1q.p, ctx->d_info, ctx->oz_planes, ctx->oz_erow};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1577,6 +1603,7 @@ kpp_status kpp_get_schedule(kpp_ctx* ctx, int64_t t0, int64_t count, int32_t* bl
 kpp_status kpp_clear_cache(kpp_ctx* ctx) {
   if (!ctx) return KPP_EINVAL;
   ctx->nb_gen = ctx->nb_ready = 0;
+  ctx->oz_valid = 0;
   return KPP_OK;
 }
 
@@ -1614,6 +1641,11 @@ kpp_status kpp_enable_rht(kpp_ctx* ctx) {
   if (!ctx || (ctx->nranks > 1 && ctx->kind == KIND_CDPP)) return KPP_EINVAL;
   if (ctx->rht) return KPP_OK;
   cudaStream_t st = ctx->stream;
+  ctx->oz_valid = 0;  // A changes (and m with it): new digit planes at the next Phase 1
+  if (ctx->oz_planes) cudaFree(ctx->oz_planes);
+  if (ctx->oz_erow) cudaFree(ctx->oz_erow);
+  ctx->oz_planes = nullptr;
+  ctx->oz_erow = nullptr;
   auto np2 = [](long long v) { long long p = 1; while (p < v) p <<= 1; return p; };
   ctx->m_user = ctx->m;
   ctx->n_user = ctx->n;

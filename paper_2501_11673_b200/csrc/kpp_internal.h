@@ -94,6 +94,12 @@ int launch_dgemm(cudaStream_t st, int batch, int M, int N, int K, const Operand&
 // the shape is not served (then use launch_dgemm)
 int launch_gram_syrk(cudaStream_t st, int batch, int s, int K, const double* base, long long ld, long long bstride,
                      long long nrows, const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
+bool gram_i8_enabled(int s);
+long long ozaki_npad(long long n);
+void launch_ozaki_planes(cudaStream_t st, const double* A, long long m, long long n, long long lda, int8_t* planes,
+                         int* erow);
+int launch_gram_i8(cudaStream_t st, int batch, int s, int K, const int8_t* planes, long long m, const int* erow,
+                   const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
 int launch_gram_tma(cudaStream_t st, int batch, int s, int K, const double* base, long long ld, long long bstride,
                     long long nrows, const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
 void launch_splitk_reduce(cudaStream_t st, int batch, int M, int N, int Z, const double* part,

@@ -141,6 +141,23 @@ def test_factor_operator_ragged(kpp, ora, s, factor):
         assert np.allclose(M, M.T, rtol=0, atol=1e-12 * np.abs(M).max())
 
 
+@pytest.mark.parametrize("prod", [0, 1, 2])
+def test_gram_i8_opt_in(prod):
+    """The opt-in int8 tensor-core Gram (gram_i8.cu, tcgen05.mma.kind::i8 on exact 7-digit splittings
+    of A, KPP_GRAM_I8=1; read once per process, hence the subprocess) with each operand producer
+    (0 TMA gather4, 1 TMA multicast across a cluster pair, 2 cp.async): M against the oracle's
+    Householder factor at s = 96, 100 (ragged), 128 with n = 4100 (ragged K), and a c2 twin solve at
+    the 1e-10 parity bar after 200 iterations."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, KPP_GRAM_I8="1", KPP_GRAM_I8_PROD=str(prod))
+    r = subprocess.run([sys.executable, os.path.join(here, "gram_i8_check.py")], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "gram_i8 ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
 @pytest.mark.parametrize("s", [33, 100])
 def test_cdpp_factor_operator_ragged(kpp, ora, s):
     cfg = synth.twin("c5", 700, 700, s, k=25)
