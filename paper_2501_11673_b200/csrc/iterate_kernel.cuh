@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         for (int kp = 0; kp < s; kp += rows_per_pass) {
           const int k = kp + tid / tpr;
           double acc = 0.0;
-          if (k < s && !p.dbg_skip) {
+          if (k < s && !(p.dbg_skip & 1)) {
             const double* arow = Ac + k * p.sw;
             for (int j = sub; j < w; j += tpr) acc = fma(arow[j], x_sm[j], acc);
           }
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
       const unsigned la_yp = smem_u32(yp_sm);
       for (int l = tid; l < s; l += T2) {
         double v = 0.0;
-        if (!p.dbg_skip)
+        if (!(p.dbg_skip & 1))
           for (int k = 0; k < R; ++k) v = fma(Msl[k * s + l], r_sm[r0 + k], v);
         for (int cc = 0; cc < C; ++cc)
           st_async_f64(mapa_u32(la_yp + (unsigned)(c * (s + 1) + l) * 8u, cc), v, mapa_u32(lb_y, cc));
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_kernel(const __grid_constant__ 
         for (int gi = warp; gi < ngroups; gi += NW2 - 1) {
           const int rb = gi * RY;
           double v[RY] = {0.0, 0.0, 0.0, 0.0};
-          if (!p.dbg_skip) {
+          if (!(p.dbg_skip & 1)) {
             if (p.m_in_smem && regpath) {
               // s <= 16 RPW: at most RPW / 2 column chunks per lane, fully unrolled
 #pragma unroll
