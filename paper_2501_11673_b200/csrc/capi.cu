@@ -546,7 +546,9 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
         const int32_t* Sb = Sr + (long long)c0 * s;
         double* Mb = Mr + (long long)c0 * ss;
         Operand x1t{X1b, s, ss, nullptr, 0, 1}, as{ctx->A, ctx->lda, 0, Sb, s, 0};
-        launch_dgemm(st, Bn, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);  // Q1 = X1^T A_S (X1^T lower)
+        // Q1 = X1^T A_S (X1^T lower): the TMA-ring stripe kernel, else the tile GEMM
+        if (!launch_trmm_tma(st, Bn, s, n, ctx->A, ctx->lda, ctx->m, Sb, X1b, Q))
+          launch_dgemm(st, Bn, s, (int)n, s, x1t, as, Q, n, (long long)s * n, 1, 0, 1);
         pp.mark("Q1");
         Operand qa{Q, n, (long long)s * n, nullptr, 0, 0}, qb{Q, n, (long long)s * n, nullptr, 0, 1};
         int z2 = launch_gram_syrk(st, Bn, s, (int)n, Q, n, (long long)s * n, 0, nullptr, 0, part, ss, Z);

@@ -198,20 +198,6 @@ gram_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
   else if (HALF) gt_consume<GT_HALF, KH>(g, tt, bz, lane, nk16, nst, stage_bytes, ring, full, empty);
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-    cudaDriverEntryPointQueryResult qr;
-    void* fn = nullptr;
-    PFN_cuTensorMapEncodeTiled_v12000 e = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
-        qr == cudaDriverEntryPointSuccess)
-      e = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    cudaGetLastError();
-    return e;
-  }();
-  return encode;
-}
-
 // Warp pieces of the TB x TB tile triangle for ncta CTAs.  Off-diagonal tiles weigh 16 DMMAs per
 // k-step, diagonal ones 10; `nsplit` off-diagonal tiles are cut into two halves of 8, which lets the
 // four sub-partitions of a CTA (warp w runs on sub-partition w % 4, so sub-partition j holds
@@ -316,6 +302,21 @@ bool plan_pieces(int TB, GramTmaArgs& g) {
 }
 
 }  // namespace
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr when unavailable)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    PFN_cuTensorMapEncodeTiled_v12000 e = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      e = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    cudaGetLastError();
+    return e;
+  }();
+  return encode;
+}
 
 // Upper Gram per K chunk through the TMA ring (see the header comment).  `nrows` is the height of
 // the row space the rows are gathered from (A's m for idx gathers; batch * bstride / ld for dense

@@ -102,6 +102,9 @@ int launch_gram_i8(cudaStream_t st, int batch, int s, int K, const int8_t* plane
                    const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
 int launch_gram_tma(cudaStream_t st, int batch, int s, int K, const double* base, long long ld, long long bstride,
                     long long nrows, const int32_t* idx, long long idx_bstride, double* part, long long ss, int Z);
+// trmm_tma.cu: Q (s x n per block) = X1^T A[S, :], X1 upper triangular (false: shape not served)
+bool launch_trmm_tma(cudaStream_t st, int batch, int s, long long n, const double* A, long long lda, long long m,
+                     const int32_t* S, const double* X1, double* Q);
 void launch_splitk_reduce(cudaStream_t st, int batch, int M, int N, int Z, const double* part,
                           long long p_bstride, double diag_add, const double* add,
                           double add_scale, long long add_bstride, double* out,

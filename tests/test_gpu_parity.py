@@ -141,6 +141,29 @@ def test_factor_operator_ragged(kpp, ora, s, factor):
         assert np.allclose(M, M.T, rtol=0, atol=1e-12 * np.abs(M).max())
 
 
+@pytest.mark.parametrize("s,n", [(64, 130), (128, 130), (64, 4100), (128, 4100), (192, 4100), (256, 4100)])
+def test_factor_cholqr2_trmm(kpp, ora, s, n):
+    """CholeskyQR2 for every block (OPT_FACTOR 0), whose Q1 = X1^T A_S runs on the TMA-ring stripe
+    kernel (trmm_tma.cu, s a multiple of 64): 64-column stripes with a ragged last one (n = 130: two
+    full stripes and 2 columns, s <= n; n = 4100: 4 columns), the triangle's boxes skipped per stage, pairs of
+    row blocks per warp (s = 64: one pair, 256: four).  M against the oracle's Householder factor,
+    the bound of test_factor_operator."""
+    m, lam = 300, 1e-8
+    cfg = synth.twin("c3", m, n, s, k=8)
+    A, b, _ = synth.make_problem(cfg)
+    ctx = kpp.kpp_setup(A.to(DEV), s, lam, 5)
+    ctx.set_option(kpp.OPT_FACTOR, 0)
+    ctx.prepare(6)
+    An = A.numpy()
+    for k in (0, 3):
+        S = ctx.block(k).numpy()
+        M = ctx.factor(k).numpy()
+        Ri = np.linalg.inv(ora.kpp_factor(An, S, lam))
+        G = An[S] @ An[S].T + lam * np.eye(s)
+        assert rel(M, Ri @ Ri.T) < 200 * 2.2e-16 * np.linalg.cond(G), (s, n, k, rel(M, Ri @ Ri.T))
+        assert np.allclose(M, M.T, rtol=0, atol=1e-12 * np.abs(M).max())
+
+
 @pytest.mark.parametrize("prod", [0, 1, 2])
 def test_gram_i8_opt_in(prod):
     """The opt-in int8 tensor-core Gram (gram_i8.cu, tcgen05.mma.kind::i8 on exact 7-digit splittings

@@ -15,7 +15,7 @@ for r in rows[2:]:
     def val(k):
         v = float(d[k].replace(",", ""))
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                    "msecond": 1e-3, "second": 1.0}.get(u[k], 1.0)
+                    "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}.get(u[k], 1.0)
 
     rd, wr, dur = val("dram__bytes_read.sum"), val("dram__bytes_write.sum"), val("gpu__time_duration.sum")
     print(f"{d['Kernel Name'][:90]}: dram read {rd / 1e6:.1f} MB write {wr / 1e6:.1f} MB, {dur * 1e3:.3f} ms, "
