@@ -16,6 +16,15 @@
 
 #include "kernel_common.cuh"
 
+// M1 plans (c3): the register tile of block t+1 is loaded from shared memory at the end of iteration t,
+// as soon as tile t's registers are dead (after the w partials), so its shared-memory latency overlaps
+// the w barrier and the x update instead of heading the next iteration.  Measured (us / iteration,
+// early / at the top): c3 6.46 / 6.68; on the double-buffered plans it loses (c2 4.79 / 4.73, c1 2.82 /
+// 2.71), so they keep the load at the top.  KPP_LEAN_EARLY_TILE=0: at the top for every plan (A/B).
+#ifndef KPP_LEAN_EARLY_TILE
+#define KPP_LEAN_EARLY_TILE 1
+#endif
+
 namespace kpp {
 namespace itk {
 namespace {
@@ -171,6 +180,25 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   const int nown = (R + 31) >> 5;                // owner warps (<= 2)
   long long t = p.t0;
   unsigned it = 0, ph0 = 0;
+  constexpr bool early = KPP_LEAN_EARLY_TILE && M1;
+  double ar[RPW][CPL];  // register tile of the slab of the current block (rows warp + 16 i, columns lane + 32 c)
+  auto load_tile = [&](double (&a)[RPW][CPL]) {
+    if (full) {  // (uniform per CTA) no bounds predicates
+      const double* a0 = Abuf + warp * p.sw + lane;
+#pragma unroll
+      for (int i = 0; i < RPW; ++i)
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) a[i][cc] = a0[16 * i * p.sw + 32 * cc];
+    } else {
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int k = warp + 16 * i;
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc)
+          a[i][cc] = (k < s && lane + 32 * cc < w) ? Abuf[k * p.sw + lane + 32 * cc] : 0.0;
+      }
+    }
+  };
   for (; t < p.t1; ++t, ++it) {
     const int buf = it & 1;
     const unsigned tag = it + 1;
@@ -181,25 +209,12 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     (void)Sc;
     // ---- top: slab + M rows of block t have landed; register tile of the slab
     LM(13);
-    lwait(bars + 0, ph0, 10);
-    ph0 ^= 1u;
-    LM(0);
-    double ar[RPW][CPL];
-    if (full) {  // (uniform per CTA) no bounds predicates
-      const double* a0 = Abuf + warp * p.sw + lane;
-#pragma unroll
-      for (int i = 0; i < RPW; ++i)
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) ar[i][cc] = a0[16 * i * p.sw + 32 * cc];
-    } else {
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const int k = warp + 16 * i;
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc)
-          ar[i][cc] = (k < s && lane + 32 * cc < w) ? Abuf[k * p.sw + lane + 32 * cc] : 0.0;
-      }
+    if (!early || it == 0) {
+      lwait(bars + 0, ph0, 10);
+      ph0 ^= 1u;
+      load_tile(ar);
     }
+    LM(0);
     cp_async_wait_all();  // this thread's b_S(t) / S(t+1) copies
     if (tid == 0) {
       if (pf) mbar_expect_tx(bars + 0, slab_bytes + (M1 ? 0u : m_bytes));  // (0 bytes: the arrive completes the phase)
@@ -386,6 +401,14 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
         if (lane + 32 * cc < w) red_sm[(lane + 32 * cc) * RS + warp] = a;
       }
     }
+    if (early && pf) {
+      // tile t is dead: block t+1's slab (requested during this iteration) into the registers now.
+      // (Not conditional on stop_sh: the window warp may still be writing it -- the flag is only
+      // read after the w barrier; a stopping iteration waits for the slab here instead of at exit.)
+      lwait(bars + 0, ph0, 10);
+      ph0 ^= 1u;
+      load_tile(ar);
+    }
 
     LM(11);
     __syncthreads();
@@ -408,7 +431,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
   }
   // an early stop leaves block t's slab / M rows in flight: they must land before exit
   if (t < p.t1) {
-    lwait(bars + 0, ph0, 30);
+    if (!early) lwait(bars + 0, ph0, 30);  // (early: waited for at the end of the last iteration)
     if (M1) lwait(bars + 5, (it & 1u), 35);  // the M rows requested after y of the last iteration run
   }
   cp_async_wait_all();
