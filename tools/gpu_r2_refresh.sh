@@ -19,6 +19,8 @@ P4="python tools/prof_iter.py --config c4 --iters 32 --reps 1"
 timeout 300 $P4 > $O/plain_p4.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:iterate_kernel -c 1 -f -o $O/iter_c4 $P4 > $O/ncu_iter_c4.log 2>&1; echo "ncu c4 rc=$?"
 P5="python tools/prof_iter.py --config c5 --iters 64 --reps 1"
 timeout 300 $P5 > $O/plain_p5.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:cdpp_stream -c 1 -f -o $O/cs_c5 $P5 > $O/ncu_cs_c5.log 2>&1; echo "ncu c5 rc=$?"
+LC4="python bench.py --config c4 --steps 1 --warmup 3 --no-cpu --no-ttt --secondary ''"
+timeout 600 bash -c "$LC4" > $O/plain_trmm.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:trmm_tma -c 1 -f -o $O/trmm_c4 bash -c "$LC4" > $O/ncu_trmm_c4.log 2>&1; echo "ncu trmm rc=$?"
 for C in c3 c4; do
   LC="python bench.py --config $C --steps 1 --warmup 3 --no-cpu --no-ttt --secondary ''"
   timeout 600 bash -c "$LC" > $O/plain_launch_$C.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_$C.csv bash -c "$LC" > $O/ncu_launch_$C.log 2>&1; echo "launch list $C rc=$?"

@@ -73,7 +73,7 @@ __device__ __forceinline__ void gather4(void* dst, const CUtensorMap* tm, int c0
 __device__ __forceinline__ void cpa16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, int mode, int g2max, int backoff,
+__global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, int mode, int g2max, int backoff, int stagger,
                                                long long* out, const double* big, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) double dyn[];  // 96 KB landing zone of the simulated prefetch
   __shared__ __align__(8) unsigned long long bars[5];
@@ -152,6 +152,45 @@ __global__ void __launch_bounds__(T, 1) skel(unsigned long long* ll, int iters, 
     if (tid < sl * G2) {
       const int row = tid % sl, grp = tid / sl;
       double v = 0.0;
+      if (mode & 256) {
+        // staggered double polling: two loads of every word in flight, the second issued half a
+        // round trip after the first, so the word is sampled twice per L2 round trip
+        constexpr int KQ = 4;
+        unsigned long long a0[KQ], b0[KQ], a1[KQ], b1[KQ];
+        int nqw = 0;
+        for (int i = 0; i < KQ; ++i) {
+          const int qq = grp + i * G2;
+          if (qq < NQ) { ll_ld(g + ((long long)qq * S + c * sl + row) * 2, a0[i], b0[i]); nqw = i + 1; }
+          else { a0[i] = b0[i] = (unsigned long long)tag << 32; }
+        }
+        __nanosleep(stagger);
+        for (int i = 0; i < KQ; ++i) {
+          const int qq = grp + i * G2;
+          if (qq < NQ) ll_ld(g + ((long long)qq * S + c * sl + row) * 2, a1[i], b1[i]);
+          else a1[i] = b1[i] = (unsigned long long)tag << 32;
+        }
+        const unsigned need = (1u << KQ) - 1u;
+        unsigned done = need & ~((1u << nqw) - 1u);  // words past NQ: nothing to poll
+        double vals[KQ];
+        for (int i = 0; i < KQ; ++i) vals[i] = 0.0;
+        long long t0 = clock64();
+        while (done != need) {
+          for (int i = 0; i < KQ; ++i) {
+            if (done >> i & 1u) continue;
+            if ((unsigned)(a0[i] >> 32) == tag && (unsigned)(b0[i] >> 32) == tag) {
+              done |= 1u << i; vals[i] = __longlong_as_double((a0[i] & 0xffffffffull) | (b0[i] << 32));
+            } else ll_ld(g + ((long long)(grp + i * G2) * S + c * sl + row) * 2, a0[i], b0[i]);
+          }
+          for (int i = 0; i < KQ; ++i) {
+            if (done >> i & 1u) continue;
+            if ((unsigned)(a1[i] >> 32) == tag && (unsigned)(b1[i] >> 32) == tag) {
+              done |= 1u << i; vals[i] = __longlong_as_double((a1[i] & 0xffffffffull) | (b1[i] << 32));
+            } else ll_ld(g + ((long long)(grp + i * G2) * S + c * sl + row) * 2, a1[i], b1[i]);
+          }
+          if (clock64() - t0 > 4000000000LL) { printf("hang: dpoll\n"); __trap(); }
+        }
+        for (int i = 0; i < KQ; ++i) v += vals[i];
+      } else
       for (int qq = grp; qq < NQ; qq += G2) {
         unsigned long long a, b;
         const unsigned long long* src = g + ((long long)qq * S + c * sl + row) * 2;
@@ -218,9 +257,11 @@ int main(int argc, char** argv) {
   CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, big, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   printf("tensor map: %d\n", (int)cr);
-  struct V { int C, grid, mode, g2, bo; } vs[] = {
-      {4, 132, 0, 16, 0}, {4, 132, 0, 15, 0}, {4, 132, 2, 15, 0}, {4, 132, 2 | 64, 15, 0}, {4, 132, 2 | 64 | 8, 15, 0},
-      {4, 132, 2 | 16, 15, 0}, {4, 132, 4 | 64, 15, 0}};
+  // mode 256: staggered double polling (stagger ns between the two loads of a word)
+  struct V { int C, grid, mode, g2, bo, st; } vs[] = {
+      {4, 132, 0, 15, 0, 0}, {4, 132, 256, 15, 0, 0}, {4, 132, 256, 15, 0, 100}, {4, 132, 256, 15, 0, 200},
+      {4, 132, 256, 15, 0, 300}, {4, 132, 256, 15, 0, 450}, {4, 132, 2 | 64, 15, 0, 0}, {4, 132, 2 | 64 | 256, 15, 0, 200},
+      {4, 132, 2 | 64 | 256, 15, 0, 300}, {4, 132, 0, 15, 0, 0}, {4, 132, 256, 15, 0, 250}};
   for (auto v : vs) {
     cudaMemset(ll, 0, 2LL * 160 * S * 2 * 8);
     cudaLaunchConfig_t cfg = {};
@@ -234,13 +275,13 @@ int main(int argc, char** argv) {
     a[0].val.clusterDim.z = 1;
     cfg.attrs = a;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, skel, ll, 4000, v.mode, v.g2, v.bo, out, (const double*)big, tmap);
+    cudaLaunchKernelEx(&cfg, skel, ll, 4000, v.mode, v.g2, v.bo, v.st, out, (const double*)big, tmap);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[3];
     cudaMemcpy(h, out, 24, cudaMemcpyDeviceToHost);
     fflush(stdout);
-    printf("C=%d grid=%d mode=%d G2max=%d: %lld cycles/iter (%.2f us), top wait %lld %s\n", v.C, v.grid, v.mode,
-           v.g2, h[0], h[0] / 1965.0, h[2], cudaGetErrorString(e));
+    printf("C=%d grid=%d mode=%d G2max=%d stagger=%d: %lld cycles/iter (%.2f us), top wait %lld %s\n", v.C, v.grid, v.mode,
+           v.g2, v.st, h[0], h[0] / 1965.0, h[2], cudaGetErrorString(e));
     fflush(stdout);
     if (e != cudaSuccess) return 1;
   }
