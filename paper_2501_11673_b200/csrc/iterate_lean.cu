@@ -51,6 +51,36 @@ static __device__ __noinline__ void lean_wait_slow(unsigned long long* bar, unsi
 __device__ __forceinline__ void lwait(unsigned long long* bar, unsigned parity, int code) {
   if (!mbar_try_cta(bar, parity)) lean_wait_slow(bar, parity, code);
 }
+// Waits that spin on test_wait (no suspension): KPP_LEAN_SPIN bit 1 the r barrier, 2 the y barrier,
+// 4 the owner's partials barrier, 8 the slab barrier (A/B of the wake-up latency of a suspended warp)
+#ifndef KPP_LEAN_SPIN
+#define KPP_LEAN_SPIN 0
+#endif
+__device__ __forceinline__ bool mbar_test_cta(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+static __device__ __noinline__ void lean_spin_slow(unsigned long long* bar, unsigned parity, int code) {
+  const unsigned long long t0 = globaltimer();
+  unsigned n = 0;
+  while (!mbar_test_cta(bar, parity))
+    if ((++n & 1023u) == 0 && globaltimer() - t0 > 10000000000ull) mbar_hang(code, parity);
+}
+template <int BIT>
+__device__ __forceinline__ void lwait_k(unsigned long long* bar, unsigned parity, int code) {
+  if constexpr ((KPP_LEAN_SPIN & BIT) != 0) {
+    if (!mbar_test_cta(bar, parity)) lean_spin_slow(bar, parity, code);
+  } else {
+    lwait(bar, parity, code);
+  }
+}
 
 struct LeanLayout {
   int sp, sl, s4, red, mslz;
@@ -210,7 +240,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     // ---- top: slab + M rows of block t have landed; register tile of the slab
     LM(13);
     if (!early || it == 0) {
-      lwait(bars + 0, ph0, 10);
+      lwait_k<8>(bars + 0, ph0, 10);
       ph0 ^= 1u;
       load_tile(ar);
     }
@@ -252,7 +282,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     unsigned long long* gll = p.ll + (long long)(it & 1) * NQ * s * 2;
     if (warp < nown) {
       // ---- owner warps: cluster partial of my slice -> L2 (LL words) for every cluster
-      if (R > 0) lwait(bars + 2, it & 1u, 12);
+      if (R > 0) lwait_k<4>(bars + 2, it & 1u, 12);
       if constexpr (PROF) TRACE(2);
       LM(3);
       const int row = warp * 32 + lane;
@@ -333,7 +363,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
     if (tid < R)
       for (int cc = 0; cc < C; ++cc) st_async_f64(mapa_u32(la_r + (unsigned)(r0 + tid) * 8u, cc), rv, mapa_u32(lb_r, cc));
     LM(7);
-    lwait(bars + 3, it & 1u, 13);
+    lwait_k<1>(bars + 3, it & 1u, 13);
     LM(8);
     if constexpr (PROF) TRACE(5);
     // ---- row 8 (last warp, beside y): ||r||^2 in a fixed order and the replicated window logic
@@ -373,7 +403,7 @@ __global__ void __launch_bounds__(T2, 1) iterate_lean_kernel(const __grid_consta
       if (row < R && cc < C) st_async_f64(mapa_u32(la_y + (unsigned)(r0 + row) * 8u, cc), v[0], mapa_u32(lb_y, cc));
     }
     LM(9);
-    lwait(bars + 4, it & 1u, 14);
+    lwait_k<2>(bars + 4, it & 1u, 14);
     LM(10);
     if (M1 && pf && tid == 0 && R > 0 && !no_m) {
       // every reader of the M rows of t has sent its y rows (they all arrived): block t+1's rows
