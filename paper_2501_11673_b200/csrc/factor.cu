@@ -575,7 +575,23 @@ void launch_chol_trtri(cudaStream_t st, int batch, double* G, double* X, int s, 
     Operand rpt{R + (long long)k0 * s + c0, s, ss, nullptr, 0, 1};    // logical (i,k) = R[k0+k][c0+i]
     Operand rp{R + (long long)k0 * s + c0, s, ss, nullptr, 0, 0};
     if (prof) cudaEventRecord(e2, st);
-    launch_dgemm(st, batch, tr, tr, kb, rpt, rp, G + (long long)c0 * (s + 1), s, ss, 1, 1, 0, -1.0, 1);
+    // super-steps of two 64-wide steps (s >= 256): the first step updates only the next 64 rows
+    // (G[c0:c0+64, c0:] -= R[k0, c0:c0+64]^T R[k0, c0:]), the second applies both steps' panels to
+    // the rest in one K = 128 update (G[c0:, c0:] -= R[k0-64:k0+64, c0:]^T R[k0-64:k0+64, c0:]):
+    // half the read-modify-write passes over the trailing matrix, twice the K per pass
+    static const bool super = !(getenv("KPP_CHOL_SUPER") && atoi(getenv("KPP_CHOL_SUPER")) == 0);
+    const bool sup = super && s >= 256 && kb == NB;
+    const bool first = sup && ((k0 / NB) & 1) == 0 && tr > NB;
+    const bool second = sup && ((k0 / NB) & 1) == 1;
+    if (first) {
+      launch_dgemm(st, batch, NB, tr, kb, rpt, rp, G + (long long)c0 * (s + 1), s, ss, 1, 1, 0, -1.0, 1);
+    } else if (second) {
+      Operand r2t{R + (long long)(k0 - NB) * s + c0, s, ss, nullptr, 0, 1};
+      Operand r2{R + (long long)(k0 - NB) * s + c0, s, ss, nullptr, 0, 0};
+      launch_dgemm(st, batch, tr, tr, 2 * NB, r2t, r2, G + (long long)c0 * (s + 1), s, ss, 1, 1, 0, -1.0, 1);
+    } else {
+      launch_dgemm(st, batch, tr, tr, kb, rpt, rp, G + (long long)c0 * (s + 1), s, ss, 1, 1, 0, -1.0, 1);
+    }
     if (prof) {
       cudaEventRecord(e3, st);
       cudaEventSynchronize(e3);
