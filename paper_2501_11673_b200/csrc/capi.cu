@@ -1204,6 +1204,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
         q.hist_res = p.hist_res; q.hist_rho = p.hist_rho; q.hist_cap = p.hist_cap;
         q.ygl = 1; q.yll = ctx->d_ll + ctx->ll_bytes / sizeof(unsigned long long) - 4LL * ctx->s;
         q.prof = p.prof;
+        q.dbg_skip = p.dbg_skip;
         // ranks: this one (vcol = all local columns), or vr emulated ones splitting the columns
         q.rank = ctx->rank; q.nranks = ctx->nranks; q.vranks = 1; q.ll_vstride = 0;
         q.vcol[0] = 0; q.vcol[1] = n;

@@ -70,17 +70,21 @@ __host__ __device__ inline Smem cs_layout(int s, int slab, int C) {
 }
 
 // Stream rows of A[S, c0:c0+w] against zv (warps 0..NSW-1): out[k] = sum_j A[S_k, c0+j] zv[j]
-// (fixed order: lane-strided 16-byte chunks, then a butterfly); columns with cmap[j] >= 0 are
-// copied to stash[k][cmap[j]].
+// (fixed order: lane-strided 16-byte chunks, then a butterfly).  The first ns <= STASH columns of the
+// list sl (local columns of S_t in the slab, in list order) are copied to stash[k][i]: lane i loads
+// A[S_k, c0 + sl[i]] beside the row's stream (same sectors: an L1/L2 hit), so the stream itself
+// carries no per-element column test.
 // Row pairs are taken dynamically from *ctr (shared memory), so warps that join late (the chain
 // warps, once the chain of the slot is done) take a share; each row's dot product is computed by
 // one warp in a fixed order, so the result does not depend on which warp takes it.
 __device__ __forceinline__ void stream_pass(const IterParams& p, const int32_t* S, long long c0, int w,
-                                            const double* zv, double* out, const int* cmap, double* stash,
+                                            const double* zv, double* out, const int* sl, int ns, double* stash,
                                             bool vec, int* ctr) {
   const int s = p.s;
   const int lane = threadIdx.x & 31;
   constexpr int UR = 2, UQ = 8;  // a whole 444-column row segment per round: 16 loads in flight per lane
+  const bool stl = lane < ns;
+  const int scol = stl ? sl[lane] : 0;
   for (;;) {
     int kbase = 0;
     if (lane == 0) kbase = atomicAdd(ctr, UR);
@@ -90,6 +94,9 @@ __device__ __forceinline__ void stream_pass(const IterParams& p, const int32_t* 
     const double* rows[UR];
 #pragma unroll
     for (int u = 0; u < UR; ++u) rows[u] = p.A + (long long)S[min(kbase + u, s - 1)] * p.lda + c0;
+    double sv[UR];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) sv[u] = stl ? __ldg(rows[u] + scol) : 0.0;
     if (vec) {
       const int w2 = w >> 1;
       const double2* z2 = reinterpret_cast<const double2*>(zv);
@@ -105,19 +112,6 @@ __device__ __forceinline__ void stream_pass(const IterParams& p, const int32_t* 
         }
 #pragma unroll
         for (int q = 0; q < UQ; ++q) {
-          const int j2 = jb + 32 * q;
-          if (cmap && j2 < w2) {
-            const int2 mm = *reinterpret_cast<const int2*>(cmap + 2 * j2);
-            if ((unsigned)mm.x < (unsigned)STASH || (unsigned)mm.y < (unsigned)STASH) {
-#pragma unroll
-              for (int u = 0; u < UR; ++u) {
-                if (kbase + u < s) {
-                  if ((unsigned)mm.x < (unsigned)STASH) stash[(kbase + u) * STASH + mm.x] = a[u][q].x;
-                  if ((unsigned)mm.y < (unsigned)STASH) stash[(kbase + u) * STASH + mm.y] = a[u][q].y;
-                }
-              }
-            }
-          }
 #pragma unroll
           for (int u = 0; u < UR; ++u) {
             acc[u] = fma(a[u][q].x, zq[q].x, acc[u]);
@@ -127,26 +121,18 @@ __device__ __forceinline__ void stream_pass(const IterParams& p, const int32_t* 
       }
       if ((w & 1) && lane == 0) {
 #pragma unroll
-        for (int u = 0; u < UR; ++u) {
-          const double av = __ldcs(rows[u] + w - 1);
-          if (cmap && (unsigned)cmap[w - 1] < (unsigned)STASH && kbase + u < s) stash[(kbase + u) * STASH + cmap[w - 1]] = av;
-          acc[u] = fma(av, zv[w - 1], acc[u]);
-        }
+        for (int u = 0; u < UR; ++u) acc[u] = fma(__ldcs(rows[u] + w - 1), zv[w - 1], acc[u]);
       }
     } else {
       for (int j = lane; j < w; j += 32) {
         const double zj = zv[j];
-        const int mj = cmap ? cmap[j] : -1;
 #pragma unroll
-        for (int u = 0; u < UR; ++u) {
-          const double av = __ldcs(rows[u] + j);
-          if ((unsigned)mj < (unsigned)STASH && kbase + u < s) stash[(kbase + u) * STASH + mj] = av;
-          acc[u] = fma(av, zj, acc[u]);
-        }
+        for (int u = 0; u < UR; ++u) acc[u] = fma(__ldcs(rows[u] + j), zj, acc[u]);
       }
     }
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
+      if (stl && kbase + u < s) stash[(kbase + u) * STASH + lane] = sv[u];
       const double v = warp_sum(acc[u]);
       if (lane == 0 && kbase + u < s) out[kbase + u] = v;
     }
@@ -294,7 +280,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   if (tid == 0) row_ctr = 0;
   cluster.sync();
   // prologue: D_{t0} = A_{S_{t0}} x_{t0} (no correction: nothing was applied before t0 here)
-  stream_pass(p, S_sh, c0, w, x_sm, dbuf(0), nullptr, stash(0), vec, &row_ctr);
+  stream_pass(p, S_sh, c0, w, x_sm, dbuf(0), nullptr, 0, stash(0), vec, &row_ctr);
   __syncthreads();
 
   const unsigned la_rp = smem_u32(rp_sm), la_r = smem_u32(r_sm);
@@ -375,7 +361,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
 
     if (warp < NSW) {
       // ---- B (streaming warps): D_{t+1} = A[S_{t+1}, slab] z_t, stash A[S_{t+1}, S_t in slab]
-      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf(prv), cmap(cur), stash(prv), vec, &row_ctr);
+      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf(prv), ljb + l0 * L.lcap, min(nl_sh[l0], STASH), stash(prv), vec, &row_ctr);
       CS_MARK(1);  // stream (thread 0)
     } else {
       // ---- B (chain threads): exchange, window logic and projection of iteration t
@@ -455,7 +441,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
       ll_gather_vec<4>(y_sm, ylr + (long long)(it & 1) * s * 2, s, tag, p.err, ct, NCH);
       CS_MARK(5);  // y gathered
       // the chain of t is done: help stream D_{t+1}
-      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf(prv), cmap(cur), stash(prv), vec, &row_ctr);
+      if (pf) stream_pass(p, Sn, c0, w, z_sm, dbuf(prv), ljb + l0 * L.lcap, min(nl_sh[l0], STASH), stash(prv), vec, &row_ctr);
     }
     __syncthreads();
     CS_MARK(6);  // end-of-slot barrier wait
