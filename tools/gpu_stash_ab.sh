@@ -1,5 +1,6 @@
 # CD++ streaming kernel A/B: stash columns loaded by their lanes beside the stream (product) vs the
-# per-element column map (libkpp_old.so), after the CD++ parity tests.
+# per-element column map (libkpp_old.so: the library built from commit 63025a8~2, i.e. before the change),
+# after the CD++ parity tests.
 O=${O:-gpurun_out/r2c}
 mkdir -p $O
 timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -q -k "cdpp or c5 or bell_psd" > $O/pytest_cdpp.log 2>&1
