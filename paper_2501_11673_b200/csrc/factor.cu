@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "kpp_internal.h"
+#include "kernel_common.cuh"
 
 namespace kpp {
 namespace {
@@ -455,6 +456,89 @@ __global__ void __launch_bounds__(256) lmax_kernel(const double* Aall, int s, in
   if (tid == 0) lam_out[blockIdx.x] = lam;
 }
 
+// The same power iteration for s <= 128 with the matrix held in registers: the matrix-based kernel
+// above re-reads G (or X) from L2 on every step (12 x 128 KB per block at s = 128: L2-bandwidth bound,
+// ~0.5 ms per c2 batch of 2108 blocks).  Persistent (one CTA of 512 threads per SM, blocks strided);
+// warp w holds rows w + 16 i (i < 8), lane l columns l + 32 c (c < 4), the tile loaded once per block.
+// Row sums by a warp reduce-scatter (complete within the warp), column sums (mode 1: u = X^T v)
+// through shared memory in a fixed order; same start vector, steps and early exit as lmax_kernel.
+template <int MODE>
+__global__ void __launch_bounds__(512, 1) lmax_reg_kernel(const double* Aall, int B, int s, int iters,
+                                                          double* lam_out, const double* other, double stop) {
+  constexpr int RS = 17;
+  __shared__ double v[128], u[128], wv[128], red[128 * RS];
+  __shared__ double nrm_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    const double* A = Aall + (long long)b * s * s;
+    double a[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = warp + 16 * i;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int col = lane + 32 * c;
+        a[i][c] = (r < s && col < s && (MODE == 0 || col >= r)) ? A[(long long)r * s + col] : 0.0;
+      }
+    }
+    if (tid < 128) v[tid] = tid < s ? 1.0 / sqrt((double)s) : 0.0;
+    __syncthreads();
+    double lam = 0.0;
+    for (int itn = 0; itn < iters; ++itn) {
+      const double* src = v;
+      if (MODE == 1) {  // u = X^T v: column sums of the tile over this warp's rows, then over warps
+        double vr[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vr[i] = v[warp + 16 * i];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double t = 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t = fma(a[i][c], vr[i], t);
+          red[(lane + 32 * c) * RS + warp] = t;
+        }
+        __syncthreads();
+        if (tid < 128) {
+          double t = 0.0;
+#pragma unroll
+          for (int w = 0; w < 16; ++w) t += red[tid * RS + w];
+          u[tid] = t;
+        }
+        __syncthreads();
+        src = u;
+      }
+      // w = A src: row sums (the warp's 8 rows over all 128 columns)
+      double xs[4], q[8];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) xs[c] = src[lane + 32 * c];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        q[i] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[i] = fma(a[i][c], xs[c], q[i]);
+      }
+      itk::warp_reduce_scatter<8>(q, lane);
+      if ((lane & 3) == 0) wv[warp + 16 * itk::rs_row<8>(lane)] = q[0];
+      __syncthreads();
+      if (warp == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t = fma(wv[lane + 32 * i], wv[lane + 32 * i], t);
+        t = itk::warp_sum(t);
+        if (lane == 0) nrm_sh = sqrt(t);
+      }
+      __syncthreads();
+      lam = nrm_sh;
+      if (other && lam * other[b] > stop) break;  // uniform across the CTA
+      const double inv = lam > 0.0 ? 1.0 / lam : 0.0;
+      if (tid < 128) v[tid] = wv[tid] * inv;
+      __syncthreads();
+    }
+    if (tid == 0) lam_out[b] = lam;
+    __syncthreads();  // v / u / wv are reused by the next block
+  }
+}
+
 // list[0..cnt) = blocks whose estimated u * kappa(A_S)^2 = u * lamG * lamM (x safety) exceeds tau
 __global__ void __launch_bounds__(1024) refine_select_kernel(int B, const double* lamG, const double* lamM,
                                                              double thresh, int* list, int* cnt) {
@@ -659,6 +743,20 @@ namespace kpp {
 void launch_lmax(cudaStream_t st, int batch, const double* A, int s, int mode, int iters, double* lam,
                  const double* other, double stop) {
   if (batch <= 0) return;
+  static const bool reg_off = getenv("KPP_LMAX_REG") && atoi(getenv("KPP_LMAX_REG")) == 0;
+  if (s <= 128 && !reg_off) {
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
+    }
+    const int grid = batch < nsm ? batch : nsm;
+    if (mode == 0) lmax_reg_kernel<0><<<grid, 512, 0, st>>>(A, batch, s, iters, lam, other, stop);
+    else lmax_reg_kernel<1><<<grid, 512, 0, st>>>(A, batch, s, iters, lam, other, stop);
+    count_launches(1);
+    return;
+  }
   const size_t sm = 3 * (size_t)s * sizeof(double);
   if (mode == 0) {
     cudaFuncSetAttribute(lmax_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
