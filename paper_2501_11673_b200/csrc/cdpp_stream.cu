@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
       mbar_expect_tx(bars + 3, (unsigned)s * 8u);
       row_ctr = 0;  // read only after the phase-A barrier
     }
-    // ---- phase A (all threads)
+    // ---- phase A (all threads): A1 only -- the stream of t+1 needs z_t; the residual partials of t
+    // (A2) are formed by the chain threads while the stream runs
     // A1: x_t, m_t from w_{t-1} = I_{S_{t-1}}^T y_{t-1} (cmap(prv) holds S_{t-1}'s positions), z_t
     for (int j = tid; j < w; j += T2) {
       double xv = x_sm[j], mv = m_sm[j];
@@ -337,25 +338,6 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
       }
       z_sm[j] = fma(p.eta * c_cur, mv, xv);
     }
-    // A2: partial r_t = D_t - (1 + eta c_{t-1}) A[S_t, S_{t-1} in slab] y_{t-1} -> slice owner
-    {
-      const double* dcur = dbuf(cur);
-      const double* stc = stash(cur);
-      const double g = 1.0 + p.eta * c_prev;
-      for (int k = tid; k < s; k += T2) {
-        double v = dcur[k];
-        if (nprev > 0) {
-          double corr = 0.0;
-          for (int i = 0; i < nprev; ++i) {
-            const double a = i < STASH ? stc[k * STASH + i] : __ldg(p.A + (long long)Sc[k] * p.lda + c0 + ljm[i]);
-            corr = fma(a, yprev[lkm[i]], corr);
-          }
-          v = fma(-g, corr, v);
-        }
-        const int owner = k / sl;
-        st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), v, mapa_u32(lb_rp, owner));
-      }
-    }
     __syncthreads();
     CS_MARK(0);  // phase A
 
@@ -366,6 +348,26 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
     } else {
       // ---- B (chain threads): exchange, window logic and projection of iteration t
       const int ct = tid - CH0;
+      // A2 (chain threads, beside the stream of t+1): partial r_t = D_t - (1 + eta c_{t-1})
+      // A[S_t, S_{t-1} in slab] y_{t-1} -> slice owner
+      {
+        const double* dcur = dbuf(cur);
+        const double* stc = stash(cur);
+        const double g = 1.0 + p.eta * c_prev;
+        for (int k = ct; k < s; k += NCH) {
+          double v = dcur[k];
+          if (nprev > 0) {
+            double corr = 0.0;
+            for (int i = 0; i < nprev; ++i) {
+              const double a = i < STASH ? stc[k * STASH + i] : __ldg(p.A + (long long)Sc[k] * p.lda + c0 + ljm[i]);
+              corr = fma(a, yprev[lkm[i]], corr);
+            }
+            v = fma(-g, corr, v);
+          }
+          const int owner = k / sl;
+          st_async_f64(mapa_u32(la_rp + (unsigned)(c * sl + k - owner * sl) * 8u, owner), v, mapa_u32(lb_rp, owner));
+        }
+      }
       unsigned long long* gll = llr + (long long)(it & 1) * NQ * s * 2;
       if (R > 0) mbar_wait_cluster(bars + 2, it & 1u, 42);
       for (int row = ct; row < R; row += NCH) {
