@@ -112,6 +112,9 @@ struct kpp_ctx {
   size_t cs_smem = 0;
   unsigned long long* d_ll = nullptr;
   size_t ll_bytes = 0;
+  // representation of the CD++ factors in M_pool: 0 = M = X X^T, 1 = Z = X + X^T - diag(X) (the CD++
+  // streaming kernel applies y = X (X^T r) and Phase 1 skips the product X X^T); fixed per cache fill
+  int mrep = 0;
   int* d_err = nullptr;
   long long* d_prof = nullptr;
   long long* d_trace = nullptr;
@@ -429,12 +432,19 @@ kpp_status phase1_batch(kpp_ctx* ctx, long long k0, int B) {
       CKS(allreduce(ctx, G, (size_t)B * ss));
       launch_add_diag(st, B, G, s, ctx->lam);
     }
-    launch_chol_trtri(st, B, G, X1, s, ctx->d_info, W);
-    pp.mark("chol");
-    Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
-    launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 1, 2);  // M = X X^T (X upper): upper tiles
-    launch_mirror_upper(st, B, Mout, s);                          // ... and its mirror image
-    pp.mark("M");
+    if (ctx->mrep) {
+      // the CD++ streaming kernel applies y = X (X^T r): memoize Z = X + X^T - diag(X)
+      launch_chol_trtri(st, B, G, Mout, s, ctx->d_info, W);
+      launch_mirror_upper(st, B, Mout, s);
+      pp.mark("chol");
+    } else {
+      launch_chol_trtri(st, B, G, X1, s, ctx->d_info, W);
+      pp.mark("chol");
+      Operand xa{X1, s, ss, nullptr, 0, 0}, xb{X1, s, ss, nullptr, 0, 1};
+      launch_dgemm(st, B, s, s, s, xa, xb, Mout, s, ss, 1, 1, 2);  // M = X X^T (X upper): upper tiles
+      launch_mirror_upper(st, B, Mout, s);                          // ... and its mirror image
+      pp.mark("M");
+    }
   } else if (ctx->proj == 1) {
     // Alg 6 l.2-5: A_hat = A_S Pi^T (SRHT), R = chol(A_hat A_hat^T + lam I), memoized as X = R^{-1}
     const long long n2 = ctx->lsqr_n2;
@@ -618,6 +628,8 @@ kpp_status phase1(kpp_ctx* ctx, long long k0, long long k1) {
   return KPP_OK;
 }
 
+bool use_cdpp_stream(const kpp_ctx* ctx);
+
 // Schedule for [t0, t0+count) (needs d_nb = fresh count before t0); generates and factors
 // the new blocks.  On return bid[0..count) is valid and every referenced block is ready.
 kpp_status schedule_and_prepare(kpp_ctx* ctx, long long t0, long long count, bool factor) {
@@ -633,6 +645,13 @@ kpp_status schedule_and_prepare(kpp_ctx* ctx, long long t0, long long count, boo
     launch_fresh_blocks(st, ctx->seed, ctx->pop, ctx->s, ctx->nb_gen, nb, ctx->S_pool);
     CK(cudaGetLastError());
     ctx->nb_gen = nb;
+  }
+  // CD++ factors in the form the Phase-2 kernel of this context applies (KPP_CS_M=1: always M)
+  static const bool keep_m = getenv("KPP_CS_M") != nullptr;
+  const int want = (!keep_m && ctx->kind == KIND_CDPP && use_cdpp_stream(ctx)) ? 1 : 0;
+  if (want != ctx->mrep) {
+    ctx->mrep = want;
+    ctx->nb_ready = 0;  // a different memoized representation
   }
   if (factor && nb > ctx->nb_ready) {
     CKS(phase1(ctx, ctx->nb_ready, nb));
@@ -853,7 +872,8 @@ kpp_status setup_common(kpp_ctx* ctx) {
   CKS(plan_cdpp_stream(ctx));
   const long long part_need = std::max<long long>((long long)ctx->grid * ctx->s, 2LL * ctx->num_sms * ctx->s);
   CKS(dalloc(ctx, &ctx->part, (size_t)part_need));
-  ctx->ll_bytes = ((size_t)2 * ctx->num_sms * ctx->s * 2 + 4 * (size_t)ctx->s) * sizeof(unsigned long long);
+  // [2][clusters][s] cluster partials, then [2][s] u (CD++ streaming kernel) and [2][s] y, 2 words each
+  ctx->ll_bytes = ((size_t)2 * ctx->num_sms * ctx->s * 2 + 8 * (size_t)ctx->s) * sizeof(unsigned long long);
   CKS(dalloc(ctx, &ctx->d_ll, ctx->ll_bytes / sizeof(unsigned long long)));
   CKS(dalloc(ctx, &ctx->d_err, 1));
   CK(cudaMemset(ctx->d_err, 0, sizeof(int)));
@@ -1061,7 +1081,7 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
       // per-rank grid-exchange regions: [2][clusters][s] + [2][s] LL words each
       const int gpr = pk_grid / vr / pk_C * pk_C;
       if (gpr < pk_C) return fail(ctx, KPP_EINVAL, "%d emulated ranks do not fit the launch plan", vr);
-      const long long vll = (long long)vr * (4LL * (gpr / pk_C) * ctx->s + 4LL * ctx->s);
+      const long long vll = (long long)vr * (4LL * (gpr / pk_C) * ctx->s + 8LL * ctx->s);
       if (vll > ctx->cs_vll_cap) {
         if (ctx->cs_vll) cudaFree(ctx->cs_vll);
         CK(cudaMalloc((void**)&ctx->cs_vll, (size_t)vll * sizeof(unsigned long long)));
@@ -1203,6 +1223,8 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
         q.adaptive = p.adaptive; q.writer = p.writer; q.ll = p.ll; q.err = p.err; q.st = p.st;
         q.hist_res = p.hist_res; q.hist_rho = p.hist_rho; q.hist_cap = p.hist_cap;
         q.ygl = 1; q.yll = ctx->d_ll + ctx->ll_bytes / sizeof(unsigned long long) - 4LL * ctx->s;
+        q.ull = q.yll - 4LL * ctx->s;
+        q.yx = ctx->mrep;
         q.prof = p.prof;
         q.dbg_skip = p.dbg_skip;
         // ranks: this one (vcol = all local columns), or vr emulated ones splitting the columns
@@ -1221,7 +1243,8 @@ kpp_status solve_impl(kpp_ctx* ctx, const double* b, const double* x0, long long
           for (int r = 0; r < vr; ++r) q.peer_recv[r] = ctx->vpeer + 4LL * vr * ctx->s * r;
           q.ll = ctx->cs_vll;
           q.yll = ctx->cs_vll + 4LL * (gpr / ctx->cs_C) * ctx->s;
-          q.ll_vstride = 4LL * (gpr / ctx->cs_C) * ctx->s + 4LL * ctx->s;
+          q.ull = q.yll + 4LL * ctx->s;
+          q.ll_vstride = 4LL * (gpr / ctx->cs_C) * ctx->s + 8LL * ctx->s;
           CK(cudaMemsetAsync(ctx->cs_vll, 0, (size_t)vr * q.ll_vstride * sizeof(unsigned long long), st));
           cgrid = gpr * vr;
           csmem = cdpp_stream_smem_bytes(q, ctx->cs_C);
@@ -1627,6 +1650,18 @@ kpp_status kpp_get_factor(kpp_ctx* ctx, int64_t block_id, double* M_out) {
   if (!ctx || !M_out || block_id < 0 || block_id >= ctx->nb_ready) return KPP_EINVAL;
   const size_t ss = (size_t)ctx->s * ctx->s;
   CK(cudaMemcpy(M_out, ctx->M_pool + block_id * ss, ss * sizeof(double), cudaMemcpyDeviceToHost));
+  if (ctx->mrep) {
+    // the pool holds Z = X + X^T - diag(X): return M = X X^T (introspection only, not on the path)
+    const long long s = ctx->s;
+    std::vector<double> Z(M_out, M_out + ss);
+    for (long long i = 0; i < s; ++i)
+      for (long long j = i; j < s; ++j) {
+        double v = 0.0;
+        for (long long k = j; k < s; ++k) v += Z[(size_t)(i * s + k)] * Z[(size_t)(j * s + k)];
+        M_out[i * s + j] = v;
+        M_out[j * s + i] = v;
+      }
+  }
   return KPP_OK;
 }
 

@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
   const long long gc0 = p.col_base + c0, gc1 = p.col_base + c1;  // global columns of the slab
   unsigned long long* const llr = p.ll + (long long)vr * p.ll_vstride;   // this rank's grid exchange
   unsigned long long* const ylr = p.yll + (long long)vr * p.ll_vstride;
+  unsigned long long* const ulr = p.yx ? p.ull + (long long)vr * p.ll_vstride : nullptr;
   const bool vec = ((p.lda & 1) == 0) && ((c0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
   const long long ss = (long long)s * s;
   const int yg0 = (int)((long long)gb * s / gpr);
@@ -410,8 +411,8 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
         if (lane == 0) nl_sh[lp] = n;
       }
       tmod = (tmod + 1 == 2 * p.zeta) ? 0 : tmod + 1;
-      // rows [yg0, yg1) of y_t = M_t r_t -> L2 (every element of M_t read once on the GPU)
-      {
+      if (!p.yx) {
+        // rows [yg0, yg1) of y_t = M_t r_t -> L2 (every element of M_t read once on the GPU)
         const double* Mb = p.M_pool + (long long)p.bid[t - p.t0] * ss;
         const int cw = ct >> 5;
         for (int k = yg0 + cw; k < yg1; k += NCH / 32) {
@@ -419,6 +420,36 @@ __global__ void __launch_bounds__(T2, 1) cdpp_stream_kernel(const __grid_constan
           double v = 0.0;
 #pragma unroll 4
           for (int l = lane; l < s; l += 32) v = fma(__ldg(Mrow + l), r_sm[l], v);
+          v = warp_sum(v);
+          if (lane == 0) ll_store_global(ylr + ((long long)(it & 1) * s + k) * 2, v, tag);
+        }
+      } else {
+        // y_t = X_t (X_t^T r_t) with X = R^{-1} upper (M_t = X X^T = (A_SS + lam I)^{-1}, Alg 3 l.8-10
+        // P:754-758), read from Z = X + X^T - diag(X): row k of X^T is Z[k, 0..k], row k of X is
+        // Z[k, k..s).  u rows [yg0, yg1) -> L2, gather u, then y rows [yg0, yg1) -> L2 (the rows are
+        // the same, so the L2 prefetch of block t+1's rows serves both passes).  The chain runs beside
+        // the stream of t+1, so the second exchange round is off the critical path.
+        const double* Zb = p.M_pool + (long long)p.bid[t - p.t0] * ss;
+        // u goes to y_{t-1}'s buffer: every read of y_{t-1} in this slot (phase A, the A2 partials of
+        // this CTA, all sent before r_t could complete) is done.  (A buffer of its own would take c5's
+        // shared memory past the 196 KB carveout, and the smaller L1 slows the stream by a third.)
+        double* u_sm = ybuf(prv);
+        const int cw = ct >> 5;
+        for (int k = yg0 + cw; k < yg1; k += NCH / 32) {
+          const double* Zrow = Zb + (long long)k * s;
+          double v = 0.0;
+#pragma unroll 4
+          for (int l = lane; l <= k; l += 32) v = fma(__ldg(Zrow + l), r_sm[l], v);
+          v = warp_sum(v);
+          if (lane == 0) ll_store_global(ulr + ((long long)(it & 1) * s + k) * 2, v, tag);
+        }
+        ll_gather_vec<4>(u_sm, ulr + (long long)(it & 1) * s * 2, s, tag, p.err, ct, NCH);
+        asm volatile("bar.sync 1, %0;\n" ::"r"(NCH) : "memory");  // u complete (chain threads only)
+        for (int k = yg0 + cw; k < yg1; k += NCH / 32) {
+          const double* Zrow = Zb + (long long)k * s;
+          double v = 0.0;
+#pragma unroll 4
+          for (int l = k + lane; l < s; l += 32) v = fma(__ldg(Zrow + l), u_sm[l], v);
           v = warp_sum(v);
           if (lane == 0) ll_store_global(ylr + ((long long)(it & 1) * s + k) * 2, v, tag);
         }

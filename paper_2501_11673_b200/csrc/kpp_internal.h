@@ -162,6 +162,9 @@ struct alignas(64) IterParams {
   int writer;            // this rank writes the history
   unsigned long long* ll; // [2][clusters][s][2] tagged cluster partials (zeroed before launch)
   unsigned long long* yll; // [2][s][2] tagged y (global-y mode; zeroed before launch)
+  unsigned long long* ull; // [2][s][2] tagged u = X^T r (CD++ streaming kernel with yx = 1; zeroed before launch)
+  int yx;                // CD++ streaming kernel: M_pool holds Z = X + X^T - diag(X), X = R^{-1} upper
+                         // (M = X X^T never formed); y = X (X^T r) in two row passes over Z
   int ygl;               // 1: y computed once on the GPU (CTA-owned rows) and gathered from L2
   int* err;              // set if a spin-wait times out
   DevState* st;
