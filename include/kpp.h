@@ -179,7 +179,9 @@ kpp_status kpp_get_schedule(kpp_ctx* ctx, int64_t t0, int64_t count, int32_t* bl
 kpp_status kpp_get_block(kpp_ctx* ctx, int64_t block_id, int32_t* S_out);
 /* Memoized projection operator of block `block_id` (Phase 1, P:104-109 / P:140 / P:753, DESIGN
    reading R1): M = (A_S A_S^T + lam I)^{-1} (K++) or (A_SS + lam I)^{-1} (CD++), s x s row-major,
-   HOST output.  Requires the factor to exist (run kpp_prepare or a solve first), else KPP_EINVAL. */
+   HOST output.  Requires the factor to exist (run kpp_prepare or a solve first), else KPP_EINVAL.
+   CD++ contexts that run the streaming kernel memoize Z = X + X^T - diag(X) (X = R^{-1}, no M is
+   formed on the GPU); M = X X^T is then formed on the host for this call (introspection only). */
 kpp_status kpp_get_factor(kpp_ctx* ctx, int64_t block_id, double* M_out);
 /* Drop every memoized block (the next solve regenerates and refactors them: a cold solve). */
 kpp_status kpp_clear_cache(kpp_ctx* ctx);
