@@ -4,7 +4,8 @@ cold solve, default window, the input generated on the device exactly as bench.p
 - c1, c2, c3, c5: the first 200 iterations against the oracle run on all host cores (the BJ bar,
   ||x_gpu - x_cpu|| / ||x_cpu|| <= 1e-10), plus the checkpoint residual history;
 - c4: also 200 iterations (~187 fresh blocks, each a 256 x 131072 Householder QR in the oracle: about
-  two minutes on the box's host cores);
+  two minutes on the box's host cores); the same oracle run also checks the Gram + Cholesky route
+  without refinement (KPP_OPT_FACTOR=1) at the same bar;
 - c3 and c5 run to the 1e-8 estimate (Alg 5 l.15 P:1352 / Alg 3 l.15 P:762): the GPU stops at the
   oracle's checkpoint and the final relative residuals ||Ax - b|| / ||b|| agree within 1e-12 absolute
   (the BJ bar, compared at the oracle's stopping iteration, reading Q15), x within 1e-10;
@@ -59,6 +60,16 @@ def test_fullsize_parity(kpp, ora, name, T):
     assert np.array_equal(g_bid.numpy(), bid) and np.array_equal(g_fresh.numpy(), fresh)
     for k in sorted({0, int(bid.max()) // 2, int(bid.max())}):
         assert np.array_equal(ctx.block(k).numpy(), ora.fresh_block(0, pop, cfg.s, k))
+    x_gram = None
+    if name == "c4":
+        # the user's switch for systems like c4 (DESIGN 13 item 2): the literal Gram + Cholesky route
+        # without the CholeskyQR2 refinement, against the same oracle run
+        ctx.destroy()
+        ctx = kpp.kpp_setup(A, cfg.s, cfg.lam, 0)
+        ctx.set_option(kpp.OPT_FACTOR, 1)
+        res1 = ctx.solve(b, max_iters=T)
+        assert res1.iters == T and ctx.stats()["n_refined"] == 0
+        x_gram = res1.x.cpu().numpy()
     An, bn = A.cpu().numpy(), b.cpu().numpy()
     del A
     torch.cuda.empty_cache()
@@ -67,6 +78,8 @@ def test_fullsize_parity(kpp, ora, name, T):
     assert rel(x_gpu, ref.x) <= 1e-10, rel(x_gpu, ref.x)
     if len(ref.hist_res):
         assert np.allclose(res.res_hist.numpy(), ref.hist_res, rtol=1e-6, atol=1e-12)
+    if x_gram is not None:
+        assert rel(x_gram, ref.x) <= 1e-10, rel(x_gram, ref.x)
 
 
 @pytest.mark.parametrize("name", ["c3", "c5"])
